@@ -1,0 +1,212 @@
+"""CPU oracle for the Hawkes log-likelihood and location gradient -- TEST INFRASTRUCTURE ONLY.
+
+Plain fp64 C (``hawkes_oracle.c``) behind ctypes, plus a literal leapfrog
+integrator in numpy.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import this
+package.  The CUDA product path (``paper_2010_02994_b200``) never imports it and
+shares no code with it.
+
+Every function cites /root/reference/PAPER.md as P:L<line>; the formulas are
+restated in the header of ``hawkes_oracle.c``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hawkes_oracle.c")
+_LIB = os.path.join(_HERE, "_build", "liboracle.so")
+
+ORACLE_OK = 0
+
+
+class _Params(ctypes.Structure):
+    # Theta = (mu0, tau_x, tau_t, theta, omega, h)
+    _fields_ = [(n, ctypes.c_double) for n in ("mu0", "tau_x", "tau_t", "theta", "omega", "h")]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with strict IEEE flags (-O2 -ffp-contract=off, OpenMP)."""
+    os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-std=c11", _SRC, "-o", _LIB + ".tmp", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        dp = ctypes.POINTER(ctypes.c_double)
+        pp = ctypes.POINTER(_Params)
+        L, I = ctypes.c_long, ctypes.c_int
+        lib.oracle_rates.argtypes = [L, I, dp, dp, pp, L, L, dp, dp, dp]
+        lib.oracle_Lambda.argtypes = [L, dp, pp, dp]
+        lib.oracle_loglik.argtypes = [L, I, dp, dp, pp, dp, dp, dp]
+        lib.oracle_grad.argtypes = [L, I, dp, dp, pp, dp, L, L, dp, dp]
+        lib.oracle_loglik_complex.argtypes = [L, I, dp, dp, dp, pp, dp, dp]
+        lib.oracle_mu_pair.argtypes = [I, dp, dp, L, L, pp]
+        lib.oracle_mu_pair.restype = ctypes.c_double
+        lib.oracle_xi_pair.argtypes = [I, dp, dp, L, L, pp]
+        lib.oracle_xi_pair.restype = ctypes.c_double
+        lib.oracle_num_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _dptr(a: Optional[np.ndarray]):
+    if a is None:
+        return ctypes.POINTER(ctypes.c_double)()
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _prep(x, t):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    assert x.shape[0] == t.shape[0], "x and t disagree on N"
+    return x, t
+
+
+def _params(theta: Sequence[float]) -> _Params:
+    return _Params(*[float(v) for v in theta])
+
+
+def _check(rc: int, what: str):
+    if rc != ORACLE_OK:
+        raise ValueError(f"oracle {what} failed with status {rc}")
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def mu_pair(x, t, theta, n: int, m: int) -> float:
+    """mu_{nm}, P:L98 (background term of lambda_nm)."""
+    x, t = _prep(x, t)
+    p = _params(theta)
+    return _load().oracle_mu_pair(x.shape[1], _dptr(x), _dptr(t), n, m, ctypes.byref(p))
+
+
+def xi_pair(x, t, theta, n: int, m: int) -> float:
+    """xi_{nm}, P:L99 (self-excitation term of lambda_nm)."""
+    x, t = _prep(x, t)
+    p = _params(theta)
+    return _load().oracle_xi_pair(x.shape[1], _dptr(x), _dptr(t), n, m, ctypes.byref(p))
+
+
+def rates(x, t, theta, rows: Optional[slice] = None):
+    """lambda_n, mu_n = sum_n' mu_nn', xi_n = sum_n' xi_nn' for rows (Eq. 1).
+
+    Returns arrays of length N; rows outside ``rows`` are NaN."""
+    x, t = _prep(x, t)
+    N, D = x.shape
+    r0, r1 = (0, N) if rows is None else (rows.start or 0, N if rows.stop is None else rows.stop)
+    lam = np.full(N, np.nan)
+    mu = np.full(N, np.nan)
+    xi = np.full(N, np.nan)
+    p = _params(theta)
+    _check(_load().oracle_rates(N, D, _dptr(x), _dptr(t), ctypes.byref(p), r0, r1,
+                                _dptr(lam), _dptr(mu), _dptr(xi)), "rates")
+    return lam, mu, xi
+
+
+def Lambda(t, theta) -> np.ndarray:
+    """Lambda_n."""
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    out = np.empty_like(t)
+    p = _params(theta)
+    _check(_load().oracle_Lambda(t.shape[0], _dptr(t), ctypes.byref(p), _dptr(out)), "Lambda")
+    return out
+
+
+def loglik(x, t, theta):
+    """(ell, lambda, Lambda) -- Eq. 1.  ell = -inf if any lambda_n = 0."""
+    x, t = _prep(x, t)
+    N, D = x.shape
+    lam = np.empty(N)
+    Lam = np.empty(N)
+    ll = ctypes.c_double()
+    p = _params(theta)
+    _check(_load().oracle_loglik(N, D, _dptr(x), _dptr(t), ctypes.byref(p), ctypes.byref(ll),
+                                 _dptr(lam), _dptr(Lam)), "loglik")
+    return ll.value, lam, Lam
+
+
+def grad(x, t, theta, lam: Optional[np.ndarray] = None, rows: Optional[slice] = None):
+    """(grad N x D, scale N x D) -- App. A.
+
+    ``lam`` defaults to the oracle's own rates; ``scale[n,d]`` is
+    sum_n' |c_nn' (x_n'd - x_nd)|, the conditioning scale of g[n,d].
+    Raises if some lambda_n = 0 (gradient undefined)."""
+    x, t = _prep(x, t)
+    N, D = x.shape
+    if lam is None:
+        lam, _, _ = rates(x, t, theta)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    if np.any(lam == 0.0):
+        raise ValueError("gradient undefined: some lambda_n = 0 (ell = -inf)")
+    r0, r1 = (0, N) if rows is None else (rows.start or 0, N if rows.stop is None else rows.stop)
+    g = np.full((N, D), np.nan)
+    s = np.full((N, D), np.nan)
+    p = _params(theta)
+    _check(_load().oracle_grad(N, D, _dptr(x), _dptr(t), ctypes.byref(p), _dptr(lam), r0, r1,
+                               _dptr(g), _dptr(s)), "grad")
+    return g, s
+
+
+def loglik_complex(x_re, x_im, t, theta):
+    """Complex-step ell(X_re + i X_im): returns (Re ell, Im ell)."""
+    x_re, t = _prep(x_re, t)
+    x_im = np.ascontiguousarray(x_im, dtype=np.float64).reshape(x_re.shape)
+    N, D = x_re.shape
+    a, b = ctypes.c_double(), ctypes.c_double()
+    p = _params(theta)
+    _check(_load().oracle_loglik_complex(N, D, _dptr(x_re), _dptr(x_im), _dptr(t),
+                                         ctypes.byref(p), ctypes.byref(a), ctypes.byref(b)),
+           "loglik_complex")
+    return a.value, b.value
+
+
+def leapfrog(x, p, t, theta, step: float, n_steps: int, inv_mass=None, box_lo=None, box_hi=None):
+    """Leapfrog trajectory of HMC over locations (Neal 2011, cited there).
+
+    Potential U(X) = -ell(X).  Each step: p += (step/2) grad ell; x += step M^-1 p
+    (reflecting off [box_lo, box_hi] componentwise when given, negating p);
+    p += (step/2) grad ell.  Returns (x, p, ell_end, kinetic_end) with
+    kinetic = 1/2 sum p^2 M^-1."""
+    x = np.array(x, dtype=np.float64, copy=True)
+    p = np.array(p, dtype=np.float64, copy=True)
+    minv = np.ones_like(x) if inv_mass is None else np.asarray(inv_mass, dtype=np.float64)
+    g, _ = grad(x, t, theta)
+    for _ in range(n_steps):
+        p = p + 0.5 * step * g
+        x = x + step * minv * p
+        if box_lo is not None:
+            lo = np.asarray(box_lo, dtype=np.float64)
+            hi = np.asarray(box_hi, dtype=np.float64)
+            for _r in range(64):  # reflect until inside (bounded)
+                below = x < lo
+                above = x > hi
+                if not (below.any() or above.any()):
+                    break
+                x = np.where(below, 2 * lo - x, x)
+                x = np.where(above, 2 * hi - x, x)
+                p = np.where(below | above, -p, p)
+        g, _ = grad(x, t, theta)
+        p = p + 0.5 * step * g
+    ell, _, _ = loglik(x, t, theta)
+    kin = 0.5 * float(np.sum(p * p * minv))
+    return x, p, ell, kin

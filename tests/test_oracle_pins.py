@@ -1,0 +1,270 @@
+"""Pins of the CPU oracle against things other than itself (no GPU needed).
+
+Each test names the passage of PAPER.md (P:L<line>) it checks and what would
+fail if the oracle had a plausible mistake:
+
+  closed forms at N=2 (hand-derived)       -> wrong normalisation, indicator, sign, sigma_x reading
+  N=3 structure of App. A                  -> transposed operand / wrong lambda in the cross term
+  40-digit brute force + mp.diff gradient  -> rounding / summation / indexing, App. A vs d ell/dx
+  complex step, finite differences         -> App. A gradient vs Eq. 1
+  quadrature of the intensity              -> Lambda_n closed form and phi_D normalisation
+  sklearn leave-one-out KDE (theta = 0)    -> background smoother of P:L82
+  invariances, ties, N=1, t_n = t_N        -> indicators, dependence on differences only
+"""
+import json
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import mp_brute
+
+pytestmark = pytest.mark.filterwarnings("ignore::DeprecationWarning")
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+def _mp_eval(expr):
+    with mp.workdps(40):
+        env = {"exp": mp.exp, "pi": mp.pi, "Phi": mp.ncdf}
+        return eval(expr.replace("1/", "mp.mpf(1)/"), {"mp": mp, **env})
+
+
+# ---------------------------------------------------------------- closed forms
+def test_p1_closed_form_n2(golden_dir):
+    """P1: N=2 closed forms (Eq. 1, Lambda P:L92-93, App. A)."""
+    g = _load(golden_dir, "p1_n2.json")
+    x, t, th = np.array(g["x"]), np.array(g["t"]), g["theta"]
+    cf = g["closed_form"]
+    lam1, lam2 = float(_mp_eval(cf["lambda_1"])), float(_mp_eval(cf["lambda_2"]))
+    Lam1, Lam2 = float(_mp_eval(cf["Lambda_1"])), float(_mp_eval(cf["Lambda_2"]))
+    ell_ref = math.log(lam1) + math.log(lam2) - Lam1 - Lam2
+    xi21 = math.exp(-1.5) / (2 * math.pi)
+    c = (1 + lam1 / lam2) / 4 + xi21 / lam2
+
+    ell, lam, Lam = oracle.loglik(x, t, th)
+    np.testing.assert_allclose(lam, [lam1, lam2], rtol=2e-15)
+    np.testing.assert_allclose(Lam, [Lam1, Lam2], rtol=2e-15)
+    assert ell == pytest.approx(ell_ref, rel=2e-15)
+    gr, _ = oracle.grad(x, t, th)
+    np.testing.assert_allclose(gr, [[c, 0.0], [-c, 0.0]], rtol=2e-15, atol=1e-300)
+    # the decomposition into mu and xi
+    _, mu, xi = oracle.rates(x, t, th)
+    np.testing.assert_allclose(mu, [lam1, lam1], rtol=2e-15)
+    np.testing.assert_allclose(xi, [0.0, xi21], rtol=2e-15, atol=0)
+
+
+def test_p2_structure_n3(golden_dir):
+    """P2: App. A's c_nn' is symmetric, so g_2y = g_3x = c_23 and columns sum to 0."""
+    g = _load(golden_dir, "p2_n3.json")
+    x, t, th = np.array(g["x"]), np.array(g["t"]), g["theta"]
+    gr, _ = oracle.grad(x, t, th)
+    assert gr[1, 1] == pytest.approx(gr[2, 0], rel=1e-14)
+    np.testing.assert_allclose(gr.sum(axis=0), 0.0, atol=1e-14 * np.abs(gr).sum())
+    ref = mp_brute.evaluate(g["x"], g["t"], th)
+    np.testing.assert_allclose(gr, np.array([[float(v) for v in r] for r in ref["grad"]]), rtol=1e-13)
+
+
+# --------------------------------------------------------------- brute force
+@pytest.mark.parametrize("N,D,seed", [(4, 2, 0), (7, 2, 1), (6, 3, 2), (8, 1, 3)])
+def test_brute_force_40_digits(N, D, seed):
+    """P3: oracle vs a 40-digit mpmath evaluation; the gradient reference is mp.diff of ell."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0, 1, size=(N, D))
+    t = np.sort(rng.uniform(0, 1, size=N))
+    th = (0.7, 0.4, 0.3, 0.5, 3.0, 0.2)
+    ref = mp_brute.evaluate(x.tolist(), t.tolist(), th)
+    ell, lam, Lam = oracle.loglik(x, t, th)
+    np.testing.assert_allclose(lam, [float(v) for v in ref["lam"]], rtol=1e-14)
+    np.testing.assert_allclose(Lam, [float(v) for v in ref["Lam"]], rtol=1e-14, atol=1e-16)
+    assert ell == pytest.approx(float(ref["ell"]), rel=1e-13)
+    gr, S = oracle.grad(x, t, th)
+    gref = np.array([[float(v) for v in r] for r in ref["grad"]])
+    assert np.all(np.abs(gr - gref) <= 1e-13 * np.maximum(np.abs(gref), S))
+
+
+# --------------------------------------------------------- derivative checks
+def test_complex_step_directional():
+    """P4: <g, V> = Im ell(X + i eps V)/eps (ell analytic in X) at N=60."""
+    c = synth.unit_square(60, config=11)
+    V = np.random.default_rng(5).normal(size=c.x.shape)
+    eps = 1e-30
+    _, im = oracle.loglik_complex(c.x, eps * V, c.t, c.theta)
+    gr, S = oracle.grad(c.x, c.t, c.theta)
+    lhs = float(np.sum(gr * V))
+    assert abs(lhs - im / eps) <= 1e-12 * float(np.sum(np.abs(S * V)))
+
+
+def test_complex_step_components():
+    """P4 per component: d ell/d x_nd = Im ell(X + i eps e_nd)/eps for sampled (n,d)."""
+    c = synth.unit_square(30, config=12)
+    gr, S = oracle.grad(c.x, c.t, c.theta)
+    eps = 1e-30
+    for n, d in [(0, 0), (7, 1), (15, 0), (29, 1)]:
+        E = np.zeros_like(c.x)
+        E[n, d] = eps
+        _, im = oracle.loglik_complex(c.x, E, c.t, c.theta)
+        assert abs(gr[n, d] - im / eps) <= 1e-12 * max(abs(gr[n, d]), S[n, d])
+
+
+def test_finite_differences_spec():
+    """P5: central differences, step 1e-5, relative error < 1e-5."""
+    for seed in range(5):
+        c = synth.unit_square(20, config=13, replicate=seed)
+        gr, S = oracle.grad(c.x, c.t, c.theta)
+        h = 1e-5
+        for n in range(c.N):
+            for d in range(c.D):
+                xp, xm = c.x.copy(), c.x.copy()
+                xp[n, d] += h
+                xm[n, d] -= h
+                fd = (oracle.loglik(xp, c.t, c.theta)[0] - oracle.loglik(xm, c.t, c.theta)[0]) / (2 * h)
+                assert abs(fd - gr[n, d]) <= 1e-5 * max(abs(gr[n, d]), 1e-3 * S[n, d])
+
+
+# ------------------------------------------------------------ Lambda / phi_D
+def test_Lambda_matches_quadrature_of_intensity():
+    """P6: Lambda_n = int_0^{t_N} of the spatially integrated intensity
+    contributed by event n: mu0 phi((t-t_n)/tau_t)/tau_t + theta omega e^{-omega(t-t_n)} I[t>t_n]."""
+    from scipy import integrate
+    c = synth.unit_square(25, config=14)
+    for th in [c.theta, (1.3, 0.2, 0.05, 0.8, 7.0, 0.1)]:
+        mu0, _, tt, tht, om, _ = th
+        Lam = oracle.Lambda(c.t, th)
+        tN = c.t[-1]
+        for n in range(c.N):
+            bg, _ = integrate.quad(lambda s: mu0 * math.exp(-0.5 * ((s - c.t[n]) / tt) ** 2)
+                                   / (tt * math.sqrt(2 * math.pi)), 0, tN, epsabs=0, epsrel=1e-13,
+                                   points=[c.t[n]], limit=200)
+            se, _ = integrate.quad(lambda s: tht * om * math.exp(-om * (s - c.t[n])), c.t[n], tN,
+                                   epsabs=0, epsrel=1e-13, limit=200) if c.t[n] < tN else (0.0, 0)
+            assert Lam[n] == pytest.approx(bg + se, rel=1e-11, abs=1e-14)
+
+
+def test_pair_terms_integrate_to_their_weights():
+    """phi_D normalisation (reading R1): integrating mu_nm over x_n in R^2 leaves
+    mu0 phi(dt/tau_t)/tau_t, and xi_nm leaves theta omega e^{-omega dt}; these are the
+    integrands whose time integrals give Lambda_n."""
+    from scipy import integrate
+    th = (0.9, 0.3, 0.4, 0.6, 2.5, 0.2)
+    t = np.array([0.1, 0.7])
+    dt = t[1] - t[0]
+
+    def f(kind, a, b):
+        x = np.array([[0.3, -0.2], [0.3 + a, -0.2 + b]])
+        return oracle.mu_pair(x, t, th, 1, 0) if kind == "mu" else oracle.xi_pair(x, t, th, 1, 0)
+
+    L = 12.0
+    mu_int, _ = integrate.dblquad(lambda b, a: f("mu", a, b), -L * th[1], L * th[1],
+                                  -L * th[1], L * th[1], epsabs=0, epsrel=1e-10)
+    xi_int, _ = integrate.dblquad(lambda b, a: f("xi", a, b), -L * th[5], L * th[5],
+                                  -L * th[5], L * th[5], epsabs=0, epsrel=1e-10)
+    assert mu_int == pytest.approx(th[0] * math.exp(-0.5 * (dt / th[2]) ** 2)
+                                   / (th[2] * math.sqrt(2 * math.pi)), rel=1e-9)
+    assert xi_int == pytest.approx(th[3] * th[4] * math.exp(-th[4] * dt), rel=1e-9)
+
+
+# -------------------------------------------------------------- KDE (theta=0)
+def test_theta_zero_is_leave_one_out_kde():
+    """P8: with theta = 0, lambda_n is mu0 times the leave-one-out Gaussian product-kernel
+    space-time KDE (the smoother of P:L82), evaluated here by scikit-learn."""
+    from sklearn.neighbors import KernelDensity
+    c = synth.unit_square(200, config=15)
+    th = (0.8, 0.12, 0.07, 0.0, 20.0, 0.03)
+    lam, _, _ = oracle.rates(c.x, c.t, th)
+    z = np.column_stack([c.x / th[1], c.t / th[2]])
+    kde = KernelDensity(kernel="gaussian", bandwidth=1.0, rtol=0.0, atol=0.0).fit(z)
+    dens = np.exp(kde.score_samples(z)) * c.N          # sum_m phi_3(z_n - z_m), self included
+    self_term = (2 * math.pi) ** -1.5
+    ref = th[0] * (dens - self_term) / (th[1] ** 2 * th[2])
+    np.testing.assert_allclose(lam, ref, rtol=1e-9)
+
+
+# ------------------------------------------------------------------ invariants
+def test_invariances_translation_rotation_scaling():
+    """P7: ell depends on X only through differences and norms."""
+    c = synth.unit_square(80, config=16)
+    ell, _, _ = oracle.loglik(c.x, c.t, c.theta)
+    g, S = oracle.grad(c.x, c.t, c.theta)
+    # (i) sum of gradients vanishes (c_nn' symmetric, App. A)
+    assert np.all(np.abs(g.sum(axis=0)) <= 1e-13 * S.sum(axis=0))
+    # (ii) translation
+    ell2, _, _ = oracle.loglik(c.x + np.array([3.7, -11.2]), c.t, c.theta)
+    assert ell2 == pytest.approx(ell, rel=1e-12)
+    # (iii) rotation
+    a = 0.7
+    R = np.array([[math.cos(a), -math.sin(a)], [math.sin(a), math.cos(a)]])
+    xr = c.x @ R.T
+    ell3, _, _ = oracle.loglik(xr, c.t, c.theta)
+    assert ell3 == pytest.approx(ell, rel=1e-12)
+    g3, _ = oracle.grad(xr, c.t, c.theta)
+    assert np.all(np.abs(g3 - g @ R.T) <= 1e-11 * (S + np.abs(g)).max())
+    # (iv) scaling covariance: ell(aX; a tau_x, a h) = ell(X) - N D ln a, g -> g/a
+    s = 3.5
+    th = list(c.theta)
+    th[1] *= s
+    th[5] *= s
+    ell4, _, _ = oracle.loglik(s * c.x, c.t, th)
+    assert ell4 == pytest.approx(ell - c.N * c.D * math.log(s), rel=1e-12)
+    g4, _ = oracle.grad(s * c.x, c.t, th)
+    np.testing.assert_allclose(g4, g / s, rtol=1e-10, atol=1e-12 * np.abs(g).max())
+    # (v) time shift leaves every lambda_n unchanged
+    _, lam, _ = oracle.loglik(c.x, c.t, c.theta)
+    _, lam5, _ = oracle.loglik(c.x, c.t + 0.25, c.theta)
+    np.testing.assert_allclose(lam5, lam, rtol=1e-12)
+
+
+def test_decomposition_sum_of_pairs():
+    """P9: sum_n lambda_n = sum_{n,n'} (mu_nn' + xi_nn')."""
+    c = synth.unit_square(40, config=17)
+    lam, _, _ = oracle.rates(c.x, c.t, c.theta)
+    tot = math.fsum(oracle.mu_pair(c.x, c.t, c.theta, n, m) + oracle.xi_pair(c.x, c.t, c.theta, n, m)
+                    for n in range(c.N) for m in range(c.N))
+    assert lam.sum() == pytest.approx(tot, rel=1e-12)
+
+
+# --------------------------------------------------------- special / edge cases
+def test_single_event_is_minus_infinity():
+    """N=1: both indicators vanish, lambda_1 = 0 -> ell = -inf."""
+    ell, lam, _ = oracle.loglik(np.array([[0.2, 0.3]]), np.array([0.5]), synth.THETA_UNIT)
+    assert lam[0] == 0.0 and ell == -math.inf
+
+
+def test_ties_contribute_nothing():
+    """Equal-time pairs contribute to neither mu nor xi (reading R8)."""
+    c = synth.with_ties(60, 7)
+    for n in range(c.N):
+        for m in range(c.N):
+            if c.t[n] == c.t[m]:
+                assert oracle.mu_pair(c.x, c.t, c.theta, n, m) == 0.0
+                assert oracle.xi_pair(c.x, c.t, c.theta, n, m) == 0.0
+    # all events at one time: every lambda is 0
+    ell, lam, _ = oracle.loglik(c.x, np.full(c.N, 0.5), c.theta)
+    assert np.all(lam == 0.0) and ell == -math.inf
+    # a tied pair far from everything else has zero gradient on the pair's axis
+    x = np.array([[0.0, 0.0], [0.01, 0.0], [5.0, 5.0]])
+    t = np.array([0.2, 0.2, 0.3])
+    g, _ = oracle.grad(x, t, (1.0, 1.0, 1.0, 1.0, 1.0, 1.0))
+    assert np.all(np.isfinite(g))
+    mu01 = oracle.mu_pair(x, t, (1.0, 1.0, 1.0, 1.0, 1.0, 1.0), 0, 1)
+    assert mu01 == 0.0
+
+
+def test_last_event_has_no_self_excitation_integral():
+    """t_n = t_N: the exponential term of Lambda_n is -theta(e^0 - 1) = 0."""
+    th = (0.0, 1.0, 1.0, 2.0, 3.0, 1.0)   # mu0 = 0 isolates the self-excitation term
+    Lam = oracle.Lambda(np.array([0.1, 0.4, 0.9]), th)
+    assert Lam[-1] == 0.0
+    assert Lam[0] == pytest.approx(2.0 * (1 - math.exp(-3.0 * 0.8)), rel=1e-15)
+
+
+def test_unsorted_times_rejected():
+    with pytest.raises(ValueError):
+        oracle.loglik(np.zeros((3, 2)), np.array([0.3, 0.1, 0.2]), synth.THETA_UNIT)
