@@ -1,0 +1,190 @@
+/*
+ * hawkes.h -- C ABI of the B200 (sm_100a) Hawkes log-likelihood + location-gradient library.
+ *
+ * The library evaluates, for a time-sorted catalog of N events (x_n in R^D, t_n >= 0)
+ * and parameters Theta = (mu0, tau_x, tau_t, theta, omega, h):
+ *
+ *   lambda_n = sum_{n'} mu_{nn'} + xi_{nn'}                                  Eq. 1
+ *     mu_{nn'} = mu0/(tau_x^D tau_t) phi_D((x_n-x_n')/tau_x) phi((t_n-t_n')/tau_t) I[t_n != t_n']
+ *                                                                            P:L80-83
+ *     xi_{nn'} = theta omega/h^D e^{-omega (t_n - t_n')} phi_D((x_n-x_n')/h) I[t_n' < t_n]
+ *                                                                            P:L76-79
+ *   Lambda_n = mu0 (Phi((t_N-t_n)/tau_t) - Phi(-t_n/tau_t)) - theta (e^{-omega (t_N-t_n)} - 1)
+ *                                                                            P:L92-93
+ *   ell      = sum_n log lambda_n - Lambda_n                                 Eq. 1
+ *   d ell / d x_n = sum_{n'} (mu_{nn'}/lambda_n + mu_{n'n}/lambda_{n'}) (x_{n'}-x_n)/tau_x^2
+ *                         + (xi_{nn'}/lambda_n + xi_{n'n}/lambda_{n'}) (x_{n'}-x_n)/h^2
+ *                                                                            App. A
+ * (phi_D = D-variate standard normal density; the gradient's sigma_x is the paper's h;
+ * see DESIGN.md "Readings").  One gradient evaluation is the two-pass computation of
+ * Alg. 1/2: a rate pass producing lambda_n, then a gradient pass through
+ * 1/lambda.  hawkes_leapfrog runs the HMC leapfrog integrator over X.
+ *
+ * Conventions (all functions):
+ *  - Every function returns a hawkes_status; no C++ exception crosses this boundary.
+ *    On failure hawkes_last_error(ctx) holds a one-line message.  A CUDA or NCCL error
+ *    is sticky: the context becomes unusable (every later call returns the same status).
+ *  - The context owns all device memory.  set_* functions COPY the caller's arrays; the
+ *    caller keeps ownership of every pointer it passes.  Outputs go to caller buffers.
+ *  - hawkes_mem says where a caller pointer lives: HAWKES_MEM_HOST (pageable or pinned
+ *    host memory) or HAWKES_MEM_DEVICE (device memory on opts.device).
+ *  - Work is stream-ordered on opts.cuda_stream (NULL = legacy default stream).
+ *    Functions that return a host scalar or write host memory synchronise that stream.
+ *  - A context is not re-entrant; distinct contexts are independent.
+ *  - Arrays are row-major: x is N*D doubles (x[n*D + d]), gradients likewise.
+ *  - The library needs an sm_100 device; it fails with HAWKES_ERR_CUDA otherwise.
+ */
+#ifndef HAWKES_B200_H
+#define HAWKES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HAWKES_ABI_VERSION 1
+
+typedef struct hawkes_ctx hawkes_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+  HAWKES_OK = 0,
+  HAWKES_ERR_ARG = -1,            /* null pointer, bad size, bad enum                        */
+  HAWKES_ERR_DIM = -2,            /* unsupported D (supported: 1..HAWKES_MAX_D)             */
+  HAWKES_ERR_UNSORTED = -3,       /* times not non-decreasing                                */
+  HAWKES_ERR_NONFINITE = -4,      /* NaN/Inf, negative time, or |value| > 1e100 in inputs    */
+  HAWKES_ERR_PARAM = -5,          /* Theta not finite / not positive / outside exp range     */
+  HAWKES_ERR_STATE = -6,          /* a required set_* call is missing                        */
+  HAWKES_ERR_GRAD_UNDEFINED = -7, /* some lambda_n = 0 (ell = -inf): gradient undefined      */
+  HAWKES_ERR_CUDA = -8,           /* CUDA runtime failure (sticky)                           */
+  HAWKES_ERR_NCCL = -9,           /* NCCL failure or NCCL unavailable (sticky)               */
+  HAWKES_ERR_OOM = -10            /* device allocation failed                                */
+} hawkes_status;
+
+#define HAWKES_MAX_D 4
+
+typedef enum {
+  HAWKES_FP64 = 0, /* fp64 pair arithmetic and sums (reference precision, reading R13)     */
+  HAWKES_FP32 = 1  /* fp32 pair arithmetic, fp32 in-tile sums promoted to fp64 per tile    */
+} hawkes_precision;
+
+typedef enum { HAWKES_MEM_HOST = 0, HAWKES_MEM_DEVICE = 1 } hawkes_mem;
+
+typedef struct {
+  int32_t device;            /* CUDA device ordinal                                           */
+  void* cuda_stream;         /* cudaStream_t to run on; NULL = default stream                  */
+  int32_t precision;         /* hawkes_precision                                              */
+  int32_t rank, world;       /* row sharding: this process's rank and the number of ranks     */
+  const void* nccl_unique_id;/* world > 1: pointer to a 128-byte ncclUniqueId that every rank
+                                received from rank 0; the library builds its own communicator */
+  int32_t emulate_world;     /* world == 1 only: > 1 runs that many logical row shards one
+                                after another on this GPU, exchanging through device memory
+                                (exercises the sharded path without more GPUs); 0/1 = off      */
+} hawkes_opts;
+
+/* Theta in the paper's order.  sigma_x is the paper's h (Eq. 1 / App. A).
+ * Requirements: tau_x, tau_t, omega, sigma_x finite and > 0; mu0, theta finite and >= 0
+ * (the paper's priors keep them > 0; 0 is allowed for the special cases theta = 0 /
+ * mu0 = 0); the folded kernel constants must stay inside the fp64 exp range
+ * (|log(mu0/(tau_x^(D+2) tau_t))|, |log(theta omega/h^(D+2))| < 600), else HAWKES_ERR_PARAM.
+ * The prior orderings 1/omega < tau_t and h < tau_x are NOT enforced. */
+typedef struct {
+  double mu0, tau_x, tau_t, theta, omega, sigma_x;
+} hawkes_params;
+
+/* Fill opts with defaults: device 0, default stream, FP64, rank 0 of 1, no emulation. */
+int hawkes_default_opts(hawkes_opts* opts);
+
+/* Create a context for N >= 1 events in D dimensions (1 <= D <= HAWKES_MAX_D).
+ * opts may be NULL (defaults).  With world > 1 every rank must call this with identical
+ * N, D and opts (except rank); it is collective (NCCL communicator creation).
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_DIM, HAWKES_ERR_CUDA, HAWKES_ERR_NCCL, HAWKES_ERR_OOM. */
+int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts, hawkes_ctx** out);
+
+/* Release all device memory and the communicator.  NULL is a no-op. */
+int hawkes_destroy(hawkes_ctx* ctx);
+
+/* Event times t[0..N): finite, >= 0 (the integration window starts at 0), and
+ * non-decreasing (the catalog order of P:L84, t_N = last).  Copied.  Synchronous.
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_NONFINITE, HAWKES_ERR_UNSORTED. */
+int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem);
+
+/* Locations x[0..N*D) row-major.  Copied.  Host input is validated immediately
+ * (HAWKES_ERR_NONFINITE); device input is validated on the device and reported by the
+ * next hawkes_loglik / hawkes_grad_locations / hawkes_get_rates call. */
+int hawkes_set_locations(hawkes_ctx* ctx, const double* x, int32_t mem);
+
+/* Parameters; see hawkes_params.  Errors: HAWKES_ERR_ARG, HAWKES_ERR_PARAM. */
+int hawkes_set_params(hawkes_ctx* ctx, const hawkes_params* p);
+
+/* ell (Eq. 1) into *out_loglik (host).  -INFINITY with HAWKES_OK when some lambda_n = 0
+ * (a distinguished value, reading R11).  Needs all three set_* calls (HAWKES_ERR_STATE).
+ * With world > 1 every rank gets the same value. */
+int hawkes_loglik(hawkes_ctx* ctx, double* out_loglik);
+
+/* d ell / d x (App. A) for all N events into out_grad (N*D, row-major, host or device per
+ * mem; with world > 1 every rank receives the full N*D array); ell into *out_loglik when
+ * non-NULL.  A preceding hawkes_loglik with unchanged x and Theta is reused.
+ * Errors: as hawkes_loglik, plus HAWKES_ERR_GRAD_UNDEFINED when ell = -inf. */
+int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double* out_loglik);
+
+/* HMC leapfrog over X (potential U = -ell): starting from (x, p), n_steps steps
+ *   p += (step/2) grad ell(x);  x += step * Minv * p;  [reflect into [box_lo, box_hi]];
+ *   p += (step/2) grad ell(x)
+ * x and p (N*D each, host or device per mem) are read and overwritten with the end state.
+ * inv_mass_diag (N*D, same memory kind) may be NULL (identity mass).  box_lo/box_hi
+ * (N*D, same memory kind) may both be NULL (no box); when given, a coordinate leaving the
+ * box is reflected back (x <- 2 bound - x) and its momentum negated.  On return
+ * *out_loglik_end = ell(x_end) and *out_kinetic_end = 1/2 sum Minv p^2 (host doubles,
+ * each nullable).  The caller does the Metropolis accept/reject.
+ * Errors: as hawkes_grad_locations (HAWKES_ERR_GRAD_UNDEFINED aborts the trajectory). */
+int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double step,
+                    int32_t n_steps, const double* inv_mass_diag, const double* box_lo,
+                    const double* box_hi, double* out_loglik_end, double* out_kinetic_end);
+
+/* Per-event quantities of the last evaluation (computing it if needed): lambda_n,
+ * mu_n = sum_n' mu_nn', xi_n = sum_n' xi_nn' and Lambda_n; each pointer nullable, length N,
+ * host or device per mem.  Full length on every rank. */
+int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, double* Lambda,
+                     int32_t mem);
+
+/* Kernel timing (CUDA events on the context stream around each launch of the two O(N^2)
+ * pass kernels).  enable != 0 starts accumulating from zero.  hawkes_get_kernel_times
+ * synchronises and returns the summed milliseconds and launch counts since enabling;
+ * any pointer may be NULL. */
+int hawkes_enable_timing(hawkes_ctx* ctx, int32_t enable);
+int hawkes_get_kernel_times(hawkes_ctx* ctx, double* rate_ms, int64_t* rate_launches,
+                            double* grad_ms, int64_t* grad_launches, int64_t* total_launches);
+
+/* Rank 0 of a multi-process run calls this to obtain the 128-byte ncclUniqueId that every
+ * rank then passes as opts.nccl_unique_id (the caller distributes it, e.g. with a
+ * torch.distributed broadcast).  out must hold 128 bytes.  Errors: HAWKES_ERR_NCCL. */
+int hawkes_nccl_unique_id(void* out);
+
+/* Row-sharding plan (host only; no device needed): the row tiles rank `rank` of `world`
+ * owns for N events, dealt zig-zag (tile k of each group of 2*world goes to rank k or
+ * 2*world-1-k) to balance the causal self-excitation work; the j-chunk length, which
+ * depends on N only, so every row's summation order is the same for any world.
+ * tiles_out (nullable) receives *n_tiles tile indices; a tile is rows
+ * [k*rows_per_tile, min(N, (k+1)*rows_per_tile)).  Pass tiles_out = NULL to query
+ * *n_tiles first.  Errors: HAWKES_ERR_ARG. */
+int hawkes_plan(int64_t N, int32_t world, int32_t rank, int32_t* tiles_out, int32_t* n_tiles,
+                int32_t* rows_per_tile, int32_t* chunk);
+
+/* Diagnostics (not part of the numerical contract; used by the tests and bench.py):
+ * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak
+ * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */
+int hawkes_diag_exp(const double* a_dev, double* out_dev, int64_t n);
+int hawkes_diag_fp64_peak(double* ops_per_s);
+
+/* One-line description of the last failure on ctx (or of the last failed create when
+ * ctx is NULL).  The string is owned by the library. */
+const char* hawkes_last_error(const hawkes_ctx* ctx);
+
+/* HAWKES_ABI_VERSION. */
+int hawkes_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAWKES_B200_H */

@@ -1,0 +1,1249 @@
+// hawkes_api.cu -- context, C ABI (include/hawkes.h), O(N) kernels and row sharding.
+//
+// One evaluation (ell and d ell/dx) on rank r of W:
+//   pass 1   pass_kernel<PASS=1> over this rank's row tiles x all j chunks
+//            -> per-chunk partials (M', X', G1')                       [rate pass, Alg. 2 step 1]
+//   fin1     fixed-order chunk sum; lambda, rho' = 1/Lambda', Lambda_n (erfc, expm1),
+//            ell_n = log lambda_n - Lambda_n                            [Eq. 1, P:L92-101]
+//   exchange allgather of (rho', ell_n) over NCCL (W > 1)              [S4]
+//   ell      fixed-order reduction of ell_n over all N rows (same on every rank)
+//   pass 2   pass_kernel<PASS=2> -> per-chunk partials G2'             [gradient pass, step 2]
+//   fin2     g_i = rho'_i G1'_i + sum_chunks G2'_i                      [App. A, P:L385]
+//   exchange allgather of gradient rows (W > 1)                        [S6]
+// Row tiles are dealt to ranks zig-zag (tile k of each group of 2W goes to rank k or
+// 2W-1-k) to balance the causal self-excitation work.  Chunk boundaries and per-row
+// summation order do not depend on W, so every output is bitwise identical for any W.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/hawkes.h"
+#include "hawkes_kernels.cuh"
+
+using namespace hk;
+
+namespace {
+
+constexpr int R_ROWS = 2;                    // rows per thread
+constexpr int RT = THREADS * R_ROWS;         // rows per row tile
+constexpr int FIN_THREADS = RT;              // finalize: one thread per row of a tile
+constexpr double TWOM64 = 1.0 / 18446744073709551616.0;
+constexpr double LN2 = 0.693147180559945309417232121458;
+
+thread_local std::string g_create_error;
+
+// ------------------------------------------------------------------ NCCL via dlopen
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    if (!commInitRank || !allGather || !commDestroy || !errStr) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+// --------------------------------------------------------------------- O(N) kernels
+template <int D>
+__global__ void k_pack_x(double* __restrict__ rec, const double* __restrict__ x, int N, int npad,
+                         int* __restrict__ bad) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const int src = min(i, N - 1);   // padding rows replicate the last event (never stored)
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double v = x[(long long)src * D + d];
+    if (!(fabs(v) <= 1e100)) atomicOr(bad, 1);
+    rec[(long long)i * L::REC + d] = v;
+  }
+}
+
+template <int D>
+__global__ void k_pack_t(double* __restrict__ rec, const double* __restrict__ t, int N, int npad) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  rec[(long long)i * L::REC + L::T] = t[min(i, N - 1)];
+  rec[(long long)i * L::REC + L::RHO] = 0.0;
+#pragma unroll
+  for (int k = D + 2; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.0;
+}
+
+struct FinConst {
+  double tx2, h2;         // tau_x^2, h^2
+  double mu0, tau_t, theta, omega, tN;
+};
+
+// Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
+// lambda, rho' and ell_n.  rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda).
+template <int D>
+__global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
+                       const int* __restrict__ tiles, int N, const double* __restrict__ rec,
+                       double* __restrict__ G1, double* __restrict__ rl,
+                       double* __restrict__ rates, FinConst f) {
+  using L = Layout<D>;
+  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
+  if (i >= N) return;
+  double M = 0.0, X = 0.0, G[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* p = part + ((long long)c * npad + i) * L::K1;
+    M += p[0];
+    X += p[1];
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] += p[2 + d];
+  }
+  // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
+  const double mu_s = M * f.tx2, xi_s = X * f.h2;
+  const double Lp = mu_s + xi_s;
+  const double rho = (Lp > 0.0) ? 1.0 / Lp : 0.0;
+  // Lambda_n: mu0 (Phi(a) - Phi(b)) - theta (e^{-omega (t_N - t_n)} - 1),
+  // a = (t_N - t_n)/tau_t >= 0, b = -t_n/tau_t <= 0, Phi(a) - Phi(b) = 1 - Q(a) - Q(-b),
+  // Q(z) = erfc(z/sqrt2)/2 (reading R10: same value without cancellation)
+  const double tn = rec[(long long)i * L::REC + L::T];
+  const double qa = 0.5 * erfc((f.tN - tn) / f.tau_t * 0.70710678118654752440);
+  const double qb = 0.5 * erfc(tn / f.tau_t * 0.70710678118654752440);
+  const double Lam = f.mu0 * ((1.0 - qa) - qb) - f.theta * expm1(-f.omega * (f.tN - tn));
+  const double ell = (Lp > 0.0) ? (log(Lp) - 64.0 * LN2) - Lam : -INFINITY;
+#pragma unroll
+  for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
+  rl[2 * (long long)i] = rho;
+  rl[2 * (long long)i + 1] = ell;
+  rates[4 * (long long)i] = Lp * TWOM64;
+  rates[4 * (long long)i + 1] = mu_s * TWOM64;
+  rates[4 * (long long)i + 2] = xi_s * TWOM64;
+  rates[4 * (long long)i + 3] = Lam;
+}
+
+template <int D>
+__global__ void k_rho_to_rec(double* __restrict__ rec, const double* __restrict__ rl, int N) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  rec[(long long)i * L::REC + L::RHO] = rl[2 * (long long)i];
+}
+
+// sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W
+struct EvalStatus {
+  double ell;
+  int nonfinite;   // device-side input validation failed
+  int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
+  double kinetic;
+};
+
+__global__ void k_ell_reduce(const double* __restrict__ rl, int N, EvalStatus* st) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < N; i += 1024) s += rl[2 * (long long)i + 1];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->ell = sh[0];
+    if (!(sh[0] > -INFINITY)) st->undefined = 1;
+  }
+}
+
+template <int D>
+__global__ void k_fin2(const double* __restrict__ part, long long npad, int nchunks,
+                       const int* __restrict__ tiles, int N, const double* __restrict__ G1,
+                       const double* __restrict__ rl, double* __restrict__ grad) {
+  using L = Layout<D>;
+  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
+  if (i >= N) return;
+  double G[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* p = part + ((long long)c * npad + i) * L::K2;
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] += p[d];
+  }
+  const double rho = rl[2 * (long long)i];
+#pragma unroll
+  for (int d = 0; d < D; ++d) grad[(long long)i * D + d] = fma(rho, G1[(long long)i * D + d], G[d]);
+}
+
+// rows of this rank's tiles -> contiguous send buffer (tile-list order), K values per row
+__global__ void k_pack_rows(const double* __restrict__ src, int K, const int* __restrict__ tiles,
+                            int ntiles, int N, double* __restrict__ dst) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)ntiles * RT * K;
+  if (idx >= total) return;
+  const int k = (int)(idx % K);
+  const long long r = idx / K;
+  const int i = tiles[r / RT] * RT + (int)(r % RT);
+  dst[idx] = (i < N) ? src[(long long)i * K + k] : 0.0;
+}
+
+// gathered buffers of all ranks -> rows (inverse of k_pack_rows for every rank)
+__global__ void k_unpack_rows(const double* __restrict__ src, int K, const int* __restrict__ all_tiles,
+                              int max_tiles, int W, int N, double* __restrict__ dst) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_rank = (long long)max_tiles * RT * K;
+  if (idx >= per_rank * W) return;
+  const int rank = (int)(idx / per_rank);
+  const long long o = idx % per_rank;
+  const int k = (int)(o % K);
+  const long long r = o / K;
+  const int tile = all_tiles[rank * max_tiles + (int)(r / RT)];
+  if (tile < 0) return;
+  const int i = tile * RT + (int)(r % RT);
+  if (i < N) dst[(long long)i * K + k] = src[idx];
+}
+
+// leapfrog pieces: every rank holds the full gradient, so every rank updates all
+// rows identically (no position exchange needed)
+__global__ void k_kick(double* __restrict__ p, const double* __restrict__ g, long long n, double h) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = fma(h, g[i], p[i]);
+}
+
+template <int D>
+__global__ void k_drift(double* __restrict__ x, double* __restrict__ p,
+                        const double* __restrict__ minv, const double* __restrict__ lo,
+                        const double* __restrict__ hi, int N, double eps,
+                        double* __restrict__ rec, int* __restrict__ bad) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const long long k = (long long)i * D + d;
+    double pv = p[k];
+    double xv = fma(eps * (minv ? minv[k] : 1.0), pv, x[k]);
+    if (lo) {
+      const double a = lo[k], b = hi[k];
+      for (int it = 0; it < 64 && (xv < a || xv > b); ++it) {  // one bounce per round
+        xv = (xv < a) ? 2.0 * a - xv : 2.0 * b - xv;
+        pv = -pv;
+      }
+    }
+    if (!(fabs(xv) <= 1e100)) atomicOr(bad, 1);
+    x[k] = xv;
+    p[k] = pv;
+    rec[(long long)i * L::REC + d] = xv;
+  }
+}
+
+__global__ void k_kinetic(const double* __restrict__ p, const double* __restrict__ minv, long long n,
+                          EvalStatus* st) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) {
+    const double v = p[i];
+    s += (minv ? minv[i] : 1.0) * v * v;
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) st->kinetic = 0.5 * sh[0];
+}
+
+// diagnostics: the fast exp on an array (tests pin its accuracy)
+__global__ void k_diag_exp(const double* __restrict__ a, double* __restrict__ out, long long n,
+                           const int2* __restrict__ gtab) {
+  __shared__ int2 tab[32];
+  if (threadIdx.x < 32) tab[threadIdx.x] = gtab[threadIdx.x];
+  __syncthreads();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fexp(a[i], tab);
+}
+
+// diagnostics: dependent-DFMA throughput probe (FP64 pipe peak)
+__global__ void k_diag_dfma(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int k = 0; k < iters; ++k) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace
+
+// ======================================================================= context
+struct hawkes_ctx {
+  int64_t N = 0;
+  int D = 0;
+  int npad = 0;
+  int ntiles = 0;          // row tiles of RT rows
+  int chunk = 0, nchunks = 0;
+  hawkes_opts opts{};
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+  std::string err;
+  int sticky = HAWKES_OK;
+
+  // sharding: logical ranks this process runs (1, or emulate_world), their tile lists
+  int W = 1;               // world size of the row sharding (real or emulated)
+  std::vector<int> my_ranks;
+  std::vector<std::vector<int>> tiles_of;   // per rank
+  int max_tiles = 0;
+  int* d_all_tiles = nullptr;               // [W][max_tiles], -1 padded
+  std::vector<int*> d_tiles;                // per rank (points into d_all_tiles)
+  std::vector<int2*> d_items1, d_items2;    // per rank
+  std::vector<int> n_items;                 // per rank
+  ncclComm_t comm = nullptr;
+
+  // device buffers
+  double* rec = nullptr;   // npad x REC
+  int* gid = nullptr;      // npad
+  double* part1 = nullptr; // nchunks x npad x K1
+  double* part2 = nullptr; // nchunks x npad x K2
+  double* G1 = nullptr;    // npad x D
+  double* rl = nullptr;    // npad x 2 (rho', ell_n)
+  double* rates = nullptr; // npad x 4 (lambda, mu, xi, Lambda)
+  double* grad = nullptr;  // npad x D
+  double* xstage = nullptr;// N x D staging
+  double* sendbuf = nullptr;
+  double* recvbuf = nullptr;
+  int* counters = nullptr; // 2 per logical rank
+  int2* tab = nullptr;     // exp table
+  int* bad = nullptr;      // device-side input validation flag
+  EvalStatus* st = nullptr;
+  EvalStatus* h_st = nullptr;  // pinned
+  // leapfrog state
+  double *lf_x = nullptr, *lf_p = nullptr, *lf_minv = nullptr, *lf_lo = nullptr, *lf_hi = nullptr;
+
+  // state
+  bool have_t = false, have_x = false, have_p = false;
+  bool rates_valid = false;   // pass 1 + exchange done for current (x, t, Theta)
+  bool grad_valid = false;
+  bool rates_exchanged = false;
+  double tN = 0.0;
+  hawkes_params params{};
+  PassConst pc{};
+  FinConst fc{};
+
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_rate, ev_grad;
+  std::vector<cudaEvent_t> ev_pool;
+  double acc_rate_ms = 0, acc_grad_ms = 0;
+  int64_t n_rate = 0, n_grad = 0;
+  int64_t launches = 0;
+
+  int grid1 = 0, grid2 = 0;
+};
+
+namespace {
+
+int set_err(hawkes_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code == HAWKES_ERR_CUDA || code == HAWKES_ERR_NCCL) c->sticky = code;
+  } else {
+    g_create_error = buf;
+  }
+  return code;
+}
+
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_CUDA, "%s failed: %s (%s:%d)", #call,              \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define CHECK_LAUNCH()                                                                  \
+  do {                                                                                  \
+    ++ctx->launches;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_CUDA, "kernel launch failed: %s (%s:%d)",          \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_NCCL, "%s failed: %s", #call, g_nccl.errStr(r_));  \
+  } while (0)
+
+#define ENTER(ctx)                                                                      \
+  do {                                                                                  \
+    if (!(ctx)) return HAWKES_ERR_ARG;                                                  \
+    if ((ctx)->sticky != HAWKES_OK) return (ctx)->sticky;                               \
+    cudaError_t e_ = cudaSetDevice((ctx)->opts.device);                                 \
+    if (e_ != cudaSuccess) return set_err(ctx, HAWKES_ERR_CUDA, "cudaSetDevice: %s",    \
+                                          cudaGetErrorString(e_));                      \
+  } while (0)
+
+template <typename T>
+int dalloc(hawkes_ctx* ctx, T** p, size_t count) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, HAWKES_ERR_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                   cudaGetErrorString(e));
+  }
+  return HAWKES_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    int rc_ = (x);                  \
+    if (rc_ != HAWKES_OK) return rc_; \
+  } while (0)
+
+int K1_of(int D) { return ((D + 3) / 2) * 2; }
+int K2_of(int D) { return ((D + 1) / 2) * 2; }
+int REC_of(int D) { return ((D + 3) / 2) * 2; }
+
+// ---------------------------------------------------------------- dispatch on D
+template <template <int> class F, typename... A>
+int dispatchD(int D, A&&... a) {
+  switch (D) {
+    case 1: return F<1>::run(a...);
+    case 2: return F<2>::run(a...);
+    case 3: return F<3>::run(a...);
+    case 4: return F<4>::run(a...);
+  }
+  return HAWKES_ERR_DIM;
+}
+
+template <int D, int PASS>
+size_t pass_smem() {
+  return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
+         32 * sizeof(int2);
+}
+
+template <int D>
+struct SetupD {
+  static int run(hawkes_ctx* ctx) {
+    auto k1 = pass_kernel<D, 1, R_ROWS>;
+    auto k2 = pass_kernel<D, 2, R_ROWS>;
+    const size_t sm = pass_smem<D, 1>();
+    CU(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CU(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int b1 = 0, b2 = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, THREADS, sm));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
+    ctx->grid1 = std::max(1, b1) * ctx->sms;
+    ctx->grid2 = std::max(1, b2) * ctx->sms;
+    return HAWKES_OK;
+  }
+};
+
+void record_start(hawkes_ctx* ctx, bool rate) {
+  if (!ctx->timing) return;
+  cudaEvent_t a, b;
+  if (ctx->ev_pool.size() >= 2) {
+    a = ctx->ev_pool.back(); ctx->ev_pool.pop_back();
+    b = ctx->ev_pool.back(); ctx->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  cudaEventRecord(a, ctx->stream);
+  (rate ? ctx->ev_rate : ctx->ev_grad).push_back({a, b});
+}
+void record_stop(hawkes_ctx* ctx, bool rate) {
+  if (!ctx->timing) return;
+  cudaEventRecord((rate ? ctx->ev_rate : ctx->ev_grad).back().second, ctx->stream);
+}
+void harvest_events(hawkes_ctx* ctx) {
+  for (int which = 0; which < 2; ++which) {
+    auto& v = which == 0 ? ctx->ev_rate : ctx->ev_grad;
+    for (auto& pr : v) {
+      float ms = 0.f;
+      cudaEventSynchronize(pr.second);
+      cudaEventElapsedTime(&ms, pr.first, pr.second);
+      if (which == 0) { ctx->acc_rate_ms += ms; ++ctx->n_rate; }
+      else { ctx->acc_grad_ms += ms; ++ctx->n_grad; }
+      ctx->ev_pool.push_back(pr.first);
+      ctx->ev_pool.push_back(pr.second);
+    }
+    v.clear();
+  }
+}
+
+template <int D>
+struct PassD {
+  static int run(hawkes_ctx* ctx, int pass, int rank) {
+    PassArgs a;
+    a.rec = ctx->rec;
+    a.gid = ctx->gid;
+    a.items = pass == 1 ? ctx->d_items1[rank] : ctx->d_items2[rank];
+    a.counter = ctx->counters + 2 * rank + (pass - 1);
+    a.part = pass == 1 ? ctx->part1 : ctx->part2;
+    a.tab = ctx->tab;
+    a.npad = ctx->npad;
+    a.N = (int)ctx->N;
+    a.n_items = ctx->n_items[rank];
+    a.chunk = ctx->chunk;
+    a.c = ctx->pc;
+    if (a.n_items == 0) return HAWKES_OK;
+    const size_t sm = pass_smem<D, 1>();
+    const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
+    record_start(ctx, pass == 1);
+    if (pass == 1)
+      pass_kernel<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+    else
+      pass_kernel<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+    CHECK_LAUNCH();
+    record_stop(ctx, pass == 1);
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct Fin1D {
+  static int run(hawkes_ctx* ctx, int rank) {
+    const int nt = (int)ctx->tiles_of[rank].size();
+    if (!nt) return HAWKES_OK;
+    k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part1, ctx->npad, ctx->nchunks,
+                                                   ctx->d_tiles[rank], (int)ctx->N, ctx->rec,
+                                                   ctx->G1, ctx->rl, ctx->rates, ctx->fc);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct Fin2D {
+  static int run(hawkes_ctx* ctx, int rank) {
+    const int nt = (int)ctx->tiles_of[rank].size();
+    if (!nt) return HAWKES_OK;
+    k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nchunks,
+                                                   ctx->d_tiles[rank], (int)ctx->N, ctx->G1,
+                                                   ctx->rl, ctx->grad);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct RhoD {
+  static int run(hawkes_ctx* ctx) {
+    const int n = (int)ctx->N;
+    k_rho_to_rec<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, ctx->rl, n);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct PackXD {
+  static int run(hawkes_ctx* ctx, const double* xdev) {
+    k_pack_x<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, xdev, (int)ctx->N,
+                                                                  ctx->npad, ctx->bad);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct PackTD {
+  static int run(hawkes_ctx* ctx, const double* tdev) {
+    k_pack_t<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, tdev, (int)ctx->N,
+                                                                  ctx->npad);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct DriftD {
+  static int run(hawkes_ctx* ctx, double eps, bool box, bool minv) {
+    const int n = (int)ctx->N;
+    k_drift<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(
+        ctx->lf_x, ctx->lf_p, minv ? ctx->lf_minv : nullptr, box ? ctx->lf_lo : nullptr,
+        box ? ctx->lf_hi : nullptr, n, eps, ctx->rec, ctx->bad);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+// Exchange K values per row: own rows of every logical rank -> all rows everywhere.
+int exchange_rows(hawkes_ctx* ctx, double* rows, int K) {
+  if (ctx->W == 1) return HAWKES_OK;
+  const long long per_rank = (long long)ctx->max_tiles * RT * K;
+  for (int r : ctx->my_ranks) {
+    const int nt = (int)ctx->tiles_of[r].size();
+    const long long tot = (long long)nt * RT * K;
+    if (tot == 0) continue;
+    // with a real communicator the rank packs into its send buffer; emulated ranks pack
+    // directly into their slot of the gather buffer (the loop-back "allgather")
+    double* dst = ctx->comm ? ctx->sendbuf : ctx->recvbuf + r * per_rank;
+    k_pack_rows<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(rows, K, ctx->d_tiles[r], nt,
+                                                                       (int)ctx->N, dst);
+    CHECK_LAUNCH();
+  }
+  if (ctx->comm) {
+    // zero the tail of the send buffer beyond this rank's rows (fixed message size)
+    const int r = ctx->my_ranks[0];
+    const long long tot = (long long)ctx->tiles_of[r].size() * RT * K;
+    if (tot < per_rank)
+      CU(cudaMemsetAsync(ctx->sendbuf + tot, 0, (per_rank - tot) * sizeof(double), ctx->stream));
+    NC(g_nccl.allGather(ctx->sendbuf, ctx->recvbuf, (size_t)per_rank, ncclDouble, ctx->comm,
+                        ctx->stream));
+  }
+  const long long all = per_rank * ctx->W;
+  k_unpack_rows<<<(unsigned)((all + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->recvbuf, K, ctx->d_all_tiles, ctx->max_tiles, ctx->W, (int)ctx->N, rows);
+  CHECK_LAUNCH();
+  return HAWKES_OK;
+}
+
+// rate pass + finalize + exchange + ell reduction (device-side; no host sync)
+int run_rates(hawkes_ctx* ctx) {
+  if (ctx->rates_valid) return HAWKES_OK;
+  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 2 * ctx->W, ctx->stream));
+  for (int r : ctx->my_ranks) {
+    TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
+    TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
+  }
+  TRY(exchange_rows(ctx, ctx->rl, 2));
+  TRY(dispatchD<RhoD>(ctx->D, ctx));
+  k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
+  CHECK_LAUNCH();
+  ctx->rates_valid = true;
+  ctx->rates_exchanged = false;
+  ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+int run_grad(hawkes_ctx* ctx) {
+  TRY(run_rates(ctx));
+  if (ctx->grad_valid) return HAWKES_OK;
+  for (int r : ctx->my_ranks) {
+    TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
+    TRY(dispatchD<Fin2D>(ctx->D, ctx, r));
+  }
+  TRY(exchange_rows(ctx, ctx->grad, ctx->D));
+  ctx->grad_valid = true;
+  return HAWKES_OK;
+}
+
+int fetch_status(hawkes_ctx* ctx) {
+  CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  int bad = 0;
+  CU(cudaMemcpyAsync(&ctx->h_st->nonfinite, ctx->bad, sizeof(int), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  bad = ctx->h_st->nonfinite;
+  if (bad) {
+    ctx->rates_valid = ctx->grad_valid = false;
+    ctx->have_x = false;
+    CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
+    return set_err(ctx, HAWKES_ERR_NONFINITE,
+                   "locations contain NaN/Inf or |x| > 1e100 (device-side validation)");
+  }
+  return HAWKES_OK;
+}
+
+int check_ready(hawkes_ctx* ctx) {
+  if (!ctx->have_t || !ctx->have_x || !ctx->have_p)
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times, set_locations and set_params are all required");
+  return HAWKES_OK;
+}
+
+// ------------------------------------------------------------- sharding plan (host)
+int chunk_of(long long N) {
+  // j chunk: a function of N only (never of W), so per-row sums are W-independent
+  long long c = (N + 63) / 64;
+  c = ((c + TILE_J - 1) / TILE_J) * TILE_J;
+  c = std::max<long long>(4 * TILE_J, std::min<long long>(8192, c));
+  return (int)c;
+}
+
+int owner_of_tile(int k, int W) {
+  const int pos = k % (2 * W);
+  return pos < W ? pos : 2 * W - 1 - pos;
+}
+
+void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
+                std::vector<std::vector<int2>>& it2) {
+  const int W = ctx->W;
+  ctx->tiles_of.assign(W, {});
+  for (int k = 0; k < ctx->ntiles; ++k) ctx->tiles_of[owner_of_tile(k, W)].push_back(k);
+  ctx->max_tiles = 0;
+  for (auto& v : ctx->tiles_of) ctx->max_tiles = std::max<int>(ctx->max_tiles, (int)v.size());
+  it1.assign(W, {});
+  it2.assign(W, {});
+  const int N = (int)ctx->N;
+  for (int r = 0; r < W; ++r) {
+    std::vector<std::pair<long long, int2>> c1, c2;
+    for (int tile : ctx->tiles_of[r]) {
+      const int row0 = tile * RT, row1 = std::min(N, row0 + RT);
+      for (int ck = 0; ck < ctx->nchunks; ++ck) {
+        long long w1 = 0, w2 = 0;
+        const int j0 = ck * ctx->chunk, j1 = std::min(N, j0 + ctx->chunk);
+        for (int jt = j0; jt < j1; jt += TILE_J) {
+          const int je = std::min(j1, jt + TILE_J) - 1;
+          const long long n = (long long)(je - jt + 1);
+          if (je < row0) { w1 += 33 * n; w2 += 20 * n; }        // earlier: pass1 both exps
+          else if (jt > row1 - 1) { w1 += 20 * n; w2 += 32 * n; } // later: pass2 both exps
+          else { w1 += 40 * n; w2 += 40 * n; }
+        }
+        c1.push_back({w1, make_int2(tile, ck)});
+        c2.push_back({w2, make_int2(tile, ck)});
+      }
+    }
+    auto cmp = [](const std::pair<long long, int2>& a, const std::pair<long long, int2>& b) {
+      return a.first > b.first;
+    };
+    std::stable_sort(c1.begin(), c1.end(), cmp);
+    std::stable_sort(c2.begin(), c2.end(), cmp);
+    for (auto& e : c1) it1[r].push_back(e.second);
+    for (auto& e : c2) it2[r].push_back(e.second);
+  }
+}
+
+// Kernel constants for Theta; written to ctx only when every check passes.
+int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
+  const int D = ctx->D;
+  const double two_pi = 6.283185307179586476925286766559;
+  // background weight mu0/((2pi)^{D/2} tau_x^D * sqrt(2pi) tau_t), times alpha = 1/tau_x^2
+  const double lnw_b = log(p.mu0) - 0.5 * (D + 1) * log(two_pi) - D * log(p.tau_x) - log(p.tau_t) -
+                       2.0 * log(p.tau_x);
+  // self-excitation weight theta omega/((2pi)^{D/2} h^D), times beta = 1/h^2
+  const double lnw_s = log(p.theta) + log(p.omega) - 0.5 * D * log(two_pi) - D * log(p.sigma_x) -
+                       2.0 * log(p.sigma_x);
+  if ((p.mu0 > 0 && !(fabs(lnw_b) < 600.0)) || (p.theta > 0 && !(fabs(lnw_s) < 600.0)))
+    return set_err(ctx, HAWKES_ERR_PARAM,
+                   "Theta puts the kernel constants outside the fp64 exp range (|log w| >= 600)");
+  PassConst pc;
+  pc.kx = -0.5 / (p.tau_x * p.tau_x);
+  pc.kt = -0.5 / (p.tau_t * p.tau_t);
+  pc.ks = -0.5 / (p.sigma_x * p.sigma_x);
+  pc.omega = p.omega;
+  pc.lnc_b = p.mu0 > 0 ? lnw_b + 64.0 * LN2 : -INFINITY;
+  pc.lnc_s = p.theta > 0 ? lnw_s + 64.0 * LN2 : -INFINITY;
+  if (!isfinite(pc.kx) || !isfinite(pc.kt) || !isfinite(pc.ks))
+    return set_err(ctx, HAWKES_ERR_PARAM, "bandwidths too small for fp64");
+  FinConst fc;
+  fc.tx2 = p.tau_x * p.tau_x;
+  fc.h2 = p.sigma_x * p.sigma_x;
+  fc.mu0 = p.mu0;
+  fc.tau_t = p.tau_t;
+  fc.theta = p.theta;
+  fc.omega = p.omega;
+  fc.tN = tN;
+  ctx->pc = pc;
+  ctx->fc = fc;
+  return HAWKES_OK;
+}
+
+int copy_in(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     mem == HAWKES_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return HAWKES_OK;
+}
+int copy_out(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     mem == HAWKES_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  return HAWKES_OK;
+}
+
+bool finite_bounded(double v) { return fabs(v) <= 1e100; }
+
+}  // namespace
+
+// ========================================================================== ABI
+extern "C" {
+
+int hawkes_abi_version(void) { return HAWKES_ABI_VERSION; }
+
+int hawkes_default_opts(hawkes_opts* o) {
+  if (!o) return HAWKES_ERR_ARG;
+  memset(o, 0, sizeof *o);
+  o->world = 1;
+  return HAWKES_OK;
+}
+
+const char* hawkes_last_error(const hawkes_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx** out) {
+  hawkes_ctx* ctx = nullptr;
+  if (!out) return set_err(nullptr, HAWKES_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (N < 1 || N > (1LL << 30)) return set_err(nullptr, HAWKES_ERR_ARG, "N must be in [1, 2^30]");
+  if (D < 1 || D > HAWKES_MAX_D) return set_err(nullptr, HAWKES_ERR_DIM, "D must be in [1, %d]", HAWKES_MAX_D);
+  hawkes_opts o;
+  hawkes_default_opts(&o);
+  if (opts_in) o = *opts_in;
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad rank/world");
+  if (o.precision != HAWKES_FP64 && o.precision != HAWKES_FP32)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad precision");
+  if (o.precision == HAWKES_FP32)
+    return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_FP32 is not built in this version");
+  if (o.world > 1 && !o.nccl_unique_id)
+    return set_err(nullptr, HAWKES_ERR_ARG, "world > 1 needs nccl_unique_id");
+  if (o.world > 1 && o.emulate_world > 1)
+    return set_err(nullptr, HAWKES_ERR_ARG, "emulate_world needs world == 1");
+
+  ctx = new hawkes_ctx();
+  ctx->N = N;
+  ctx->D = D;
+  ctx->opts = o;
+  ctx->stream = (cudaStream_t)o.cuda_stream;
+  {
+    cudaError_t e = cudaSetDevice(o.device);
+    if (e != cudaSuccess) {
+      set_err(nullptr, HAWKES_ERR_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
+      delete ctx;
+      return HAWKES_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, o.device);
+    if (e != cudaSuccess || prop.major != 10) {
+      set_err(nullptr, HAWKES_ERR_CUDA, "device %d is not sm_100 (%s)", o.device,
+              e == cudaSuccess ? prop.name : cudaGetErrorString(e));
+      delete ctx;
+      return HAWKES_ERR_CUDA;
+    }
+    ctx->sms = prop.multiProcessorCount;
+  }
+  auto fail = [&](int rc) {
+    if (!ctx->err.empty()) g_create_error = ctx->err;
+    hawkes_destroy(ctx);
+    return rc;
+  };
+  ctx->ntiles = (int)((N + RT - 1) / RT);
+  ctx->npad = ctx->ntiles * RT;
+  ctx->chunk = chunk_of(N);
+  ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
+  ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);
+  if (o.world > 1)
+    ctx->my_ranks = {o.rank};
+  else
+    for (int r = 0; r < ctx->W; ++r) ctx->my_ranks.push_back(r);
+
+  std::vector<std::vector<int2>> it1, it2;
+  build_plan(ctx, it1, it2);
+
+  const int REC = REC_of(D);
+  int rc;
+  if ((rc = dalloc(ctx, &ctx->rec, (size_t)ctx->npad * REC)) ||
+      (rc = dalloc(ctx, &ctx->gid, (size_t)ctx->npad)) ||
+      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nchunks * ctx->npad * K1_of(D))) ||
+      (rc = dalloc(ctx, &ctx->part2, (size_t)ctx->nchunks * ctx->npad * K2_of(D))) ||
+      (rc = dalloc(ctx, &ctx->G1, (size_t)ctx->npad * D)) ||
+      (rc = dalloc(ctx, &ctx->rl, (size_t)ctx->npad * 2)) ||
+      (rc = dalloc(ctx, &ctx->rates, (size_t)ctx->npad * 4)) ||
+      (rc = dalloc(ctx, &ctx->grad, (size_t)ctx->npad * D)) ||
+      (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
+      (rc = dalloc(ctx, &ctx->counters, (size_t)2 * ctx->W)) ||
+      (rc = dalloc(ctx, &ctx->tab, 32)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
+      (rc = dalloc(ctx, &ctx->st, 1)))
+    return fail(rc);
+  if (ctx->W > 1) {
+    const size_t per_rank = (size_t)ctx->max_tiles * RT * std::max(4, D);
+    if ((rc = dalloc(ctx, &ctx->sendbuf, per_rank)) ||
+        (rc = dalloc(ctx, &ctx->recvbuf, per_rank * ctx->W)))
+      return fail(rc);
+  }
+  {
+    cudaError_t e = cudaMallocHost((void**)&ctx->h_st, sizeof(EvalStatus));
+    if (e != cudaSuccess) return fail(set_err(ctx, HAWKES_ERR_OOM, "cudaMallocHost failed"));
+  }
+  // tile lists / items
+  {
+    std::vector<int> all((size_t)ctx->W * std::max(1, ctx->max_tiles), -1);
+    for (int r = 0; r < ctx->W; ++r)
+      for (size_t k = 0; k < ctx->tiles_of[r].size(); ++k) all[(size_t)r * ctx->max_tiles + k] = ctx->tiles_of[r][k];
+    if ((rc = dalloc(ctx, &ctx->d_all_tiles, all.size()))) return fail(rc);
+    if (cudaMemcpy(ctx->d_all_tiles, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of tile lists failed"));
+    ctx->d_tiles.resize(ctx->W);
+    ctx->d_items1.assign(ctx->W, nullptr);
+    ctx->d_items2.assign(ctx->W, nullptr);
+    ctx->n_items.assign(ctx->W, 0);
+    for (int r = 0; r < ctx->W; ++r) {
+      ctx->d_tiles[r] = ctx->d_all_tiles + (size_t)r * ctx->max_tiles;
+      ctx->n_items[r] = (int)it1[r].size();
+      if ((rc = dalloc(ctx, &ctx->d_items1[r], it1[r].size())) ||
+          (rc = dalloc(ctx, &ctx->d_items2[r], it2[r].size())))
+        return fail(rc);
+      if (!it1[r].empty() &&
+          (cudaMemcpy(ctx->d_items1[r], it1[r].data(), it1[r].size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess ||
+           cudaMemcpy(ctx->d_items2[r], it2[r].data(), it2[r].size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess))
+        return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of work items failed"));
+    }
+  }
+  // exp table: T[j] = 2^(j/32) as (low word, high word)
+  {
+    int2 h[32];
+    for (int j = 0; j < 32; ++j) {
+      const double v = (double)exp2l((long double)j / 32.0L);
+      long long b;
+      memcpy(&b, &v, 8);
+      h[j] = make_int2((int)(b & 0xffffffffLL), (int)(b >> 32));
+    }
+    if (cudaMemcpy(ctx->tab, h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of exp table failed"));
+  }
+  if (cudaMemset(ctx->bad, 0, sizeof(int)) != cudaSuccess ||
+      cudaMemset(ctx->st, 0, sizeof(EvalStatus)) != cudaSuccess ||
+      cudaMemset(ctx->rec, 0, (size_t)ctx->npad * REC * sizeof(double)) != cudaSuccess)
+    return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
+  if ((rc = dispatchD<SetupD>(D, ctx))) return fail(rc);
+  if (o.world > 1) {
+    std::string e;
+    if (!g_nccl.load(e)) return fail(set_err(ctx, HAWKES_ERR_NCCL, "%s", e.c_str()));
+    ncclUniqueId id;
+    memcpy(&id, o.nccl_unique_id, sizeof id);
+    ncclResult_t r = g_nccl.commInitRank(&ctx->comm, o.world, id, o.rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      return fail(set_err(ctx, HAWKES_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.errStr(r)));
+    }
+  }
+  *out = ctx;
+  return HAWKES_OK;
+}
+
+int hawkes_destroy(hawkes_ctx* ctx) {
+  if (!ctx) return HAWKES_OK;
+  cudaSetDevice(ctx->opts.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
+  if (ctx->comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->comm);
+  void* bufs[] = {ctx->rec, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
+                  ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
+                  ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
+                  ctx->lf_lo, ctx->lf_hi};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (auto* p : ctx->d_items1) if (p) cudaFree(p);
+  for (auto* p : ctx->d_items2) if (p) cudaFree(p);
+  if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  for (auto& pr : ctx->ev_rate) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto& pr : ctx->ev_grad) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  delete ctx;
+  return HAWKES_OK;
+}
+
+int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
+  ENTER(ctx);
+  if (!t || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_set_times");
+  const int64_t N = ctx->N;
+  std::vector<double> h(N);
+  if (mem == HAWKES_MEM_DEVICE) {
+    CU(cudaMemcpyAsync(h.data(), t, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  } else {
+    memcpy(h.data(), t, N * sizeof(double));
+  }
+  for (int64_t i = 0; i < N; ++i) {
+    if (!finite_bounded(h[i]) || h[i] < 0.0)
+      return set_err(ctx, HAWKES_ERR_NONFINITE, "t[%lld] = %g is not a finite time >= 0", (long long)i, h[i]);
+    if (i && h[i] < h[i - 1])
+      return set_err(ctx, HAWKES_ERR_UNSORTED, "t is not non-decreasing at %lld", (long long)i);
+  }
+  // tie-group ids: first index sharing the time (g_j == g_i <=> t_j == t_i)
+  std::vector<int> g(ctx->npad);
+  for (int64_t i = 0; i < N; ++i) g[i] = (i && h[i] == h[i - 1]) ? g[i - 1] : (int)i;
+  for (int64_t i = N; i < ctx->npad; ++i) g[i] = g[N - 1];
+  CU(cudaMemcpyAsync(ctx->xstage, h.data(), N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->gid, g.data(), ctx->npad * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  TRY(dispatchD<PackTD>(ctx->D, ctx, (const double*)ctx->xstage));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->tN = h[N - 1];
+  ctx->fc.tN = ctx->tN;
+  ctx->have_t = true;
+  ctx->rates_valid = ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+int hawkes_set_locations(hawkes_ctx* ctx, const double* x, int32_t mem) {
+  ENTER(ctx);
+  if (!x || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_set_locations");
+  const size_t n = (size_t)ctx->N * ctx->D;
+  if (mem == HAWKES_MEM_HOST) {
+    for (size_t k = 0; k < n; ++k)
+      if (!finite_bounded(x[k]))
+        return set_err(ctx, HAWKES_ERR_NONFINITE, "x[%zu] = %g is not finite (or |x| > 1e100)", k, x[k]);
+  }
+  TRY(copy_in(ctx, ctx->xstage, x, n, mem));
+  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
+  ctx->have_x = true;
+  ctx->rates_valid = ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+int hawkes_set_params(hawkes_ctx* ctx, const hawkes_params* p) {
+  ENTER(ctx);
+  if (!p) return set_err(ctx, HAWKES_ERR_ARG, "params is NULL");
+  const double v[6] = {p->mu0, p->tau_x, p->tau_t, p->theta, p->omega, p->sigma_x};
+  for (int k = 0; k < 6; ++k)
+    if (!isfinite(v[k]) || v[k] < 0.0)
+      return set_err(ctx, HAWKES_ERR_PARAM, "Theta[%d] = %g is not finite and >= 0", k, v[k]);
+  if (!(p->tau_x > 0 && p->tau_t > 0 && p->omega > 0 && p->sigma_x > 0))
+    return set_err(ctx, HAWKES_ERR_PARAM, "tau_x, tau_t, omega and sigma_x must be > 0");
+  TRY(compute_constants(ctx, *p, ctx->tN));
+  ctx->params = *p;
+  ctx->have_p = true;
+  ctx->rates_valid = ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+int hawkes_loglik(hawkes_ctx* ctx, double* out) {
+  ENTER(ctx);
+  if (!out) return set_err(ctx, HAWKES_ERR_ARG, "out_loglik is NULL");
+  TRY(check_ready(ctx));
+  TRY(run_rates(ctx));
+  TRY(fetch_status(ctx));
+  *out = ctx->h_st->ell;
+  return HAWKES_OK;
+}
+
+int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double* out_ll) {
+  ENTER(ctx);
+  if (!out_grad || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_grad_locations");
+  TRY(check_ready(ctx));
+  TRY(run_rates(ctx));
+  TRY(run_grad(ctx));
+  TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
+  TRY(fetch_status(ctx));
+  if (out_ll) *out_ll = ctx->h_st->ell;
+  if (!(ctx->h_st->ell > -INFINITY))
+    return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "some lambda_n = 0: ell = -inf, gradient undefined");
+  return HAWKES_OK;
+}
+
+int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, double* Lambda,
+                     int32_t mem) {
+  ENTER(ctx);
+  if (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE)
+    return set_err(ctx, HAWKES_ERR_ARG, "bad mem");
+  TRY(check_ready(ctx));
+  TRY(run_rates(ctx));
+  if (!ctx->rates_exchanged) {
+    TRY(exchange_rows(ctx, ctx->rates, 4));
+    ctx->rates_exchanged = true;
+  }
+  const int64_t N = ctx->N;
+  std::vector<double> h((size_t)N * 4);
+  CU(cudaMemcpyAsync(h.data(), ctx->rates, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TRY(fetch_status(ctx));
+  double* outs[4] = {lambda, mu, xi, Lambda};
+  for (int k = 0; k < 4; ++k) {
+    if (!outs[k]) continue;
+    std::vector<double> col(N);
+    for (int64_t i = 0; i < N; ++i) col[i] = h[(size_t)i * 4 + k];
+    if (mem == HAWKES_MEM_HOST)
+      memcpy(outs[k], col.data(), N * sizeof(double));
+    else
+      CU(cudaMemcpy(outs[k], col.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return HAWKES_OK;
+}
+
+int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double step,
+                    int32_t n_steps, const double* inv_mass, const double* box_lo,
+                    const double* box_hi, double* out_ll, double* out_kin) {
+  ENTER(ctx);
+  if (!x || !p || n_steps < 0 || !isfinite(step) ||
+      (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) || ((box_lo == nullptr) != (box_hi == nullptr)))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_leapfrog");
+  if (!ctx->have_t || !ctx->have_p)
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
+  const size_t n = (size_t)ctx->N * ctx->D;
+  if (!ctx->lf_x) {
+    int rc;
+    if ((rc = dalloc(ctx, &ctx->lf_x, n)) || (rc = dalloc(ctx, &ctx->lf_p, n))) return rc;
+  }
+  if (inv_mass && !ctx->lf_minv) TRY(dalloc(ctx, &ctx->lf_minv, n));
+  if (box_lo && !ctx->lf_lo) {
+    TRY(dalloc(ctx, &ctx->lf_lo, n));
+    TRY(dalloc(ctx, &ctx->lf_hi, n));
+  }
+  if (mem == HAWKES_MEM_HOST) {
+    for (size_t k = 0; k < n; ++k)
+      if (!finite_bounded(x[k]) || !finite_bounded(p[k]))
+        return set_err(ctx, HAWKES_ERR_NONFINITE, "x or p not finite at %zu", k);
+  }
+  TRY(copy_in(ctx, ctx->lf_x, x, n, mem));
+  TRY(copy_in(ctx, ctx->lf_p, p, n, mem));
+  if (inv_mass) TRY(copy_in(ctx, ctx->lf_minv, inv_mass, n, mem));
+  if (box_lo) {
+    TRY(copy_in(ctx, ctx->lf_lo, box_lo, n, mem));
+    TRY(copy_in(ctx, ctx->lf_hi, box_hi, n, mem));
+  }
+  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
+  ctx->have_x = true;
+  ctx->rates_valid = ctx->grad_valid = false;
+  TRY(run_grad(ctx));
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  for (int s = 0; s < n_steps; ++s) {
+    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, ctx->grad, (long long)n, 0.5 * step);
+    CHECK_LAUNCH();
+    TRY(dispatchD<DriftD>(ctx->D, ctx, step, box_lo != nullptr, inv_mass != nullptr));
+    ctx->rates_valid = ctx->grad_valid = false;
+    TRY(run_grad(ctx));
+    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, ctx->grad, (long long)n, 0.5 * step);
+    CHECK_LAUNCH();
+  }
+  k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
+  CHECK_LAUNCH();
+  TRY(copy_out(ctx, x, ctx->lf_x, n, mem));
+  TRY(copy_out(ctx, p, ctx->lf_p, n, mem));
+  TRY(fetch_status(ctx));
+  if (out_ll) *out_ll = ctx->h_st->ell;
+  if (out_kin) *out_kin = ctx->h_st->kinetic;
+  if (ctx->h_st->undefined)
+    return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "ell = -inf during the trajectory");
+  return HAWKES_OK;
+}
+
+int hawkes_enable_timing(hawkes_ctx* ctx, int32_t enable) {
+  ENTER(ctx);
+  harvest_events(ctx);
+  ctx->timing = enable != 0;
+  ctx->acc_rate_ms = ctx->acc_grad_ms = 0;
+  ctx->n_rate = ctx->n_grad = 0;
+  ctx->launches = 0;
+  return HAWKES_OK;
+}
+
+int hawkes_get_kernel_times(hawkes_ctx* ctx, double* rate_ms, int64_t* rate_n, double* grad_ms,
+                            int64_t* grad_n, int64_t* total) {
+  ENTER(ctx);
+  harvest_events(ctx);
+  if (rate_ms) *rate_ms = ctx->acc_rate_ms;
+  if (rate_n) *rate_n = ctx->n_rate;
+  if (grad_ms) *grad_ms = ctx->acc_grad_ms;
+  if (grad_n) *grad_n = ctx->n_grad;
+  if (total) *total = ctx->launches;
+  return HAWKES_OK;
+}
+
+int hawkes_plan(int64_t N, int32_t world, int32_t rank, int32_t* tiles_out, int32_t* n_tiles,
+                int32_t* rows_per_tile, int32_t* chunk) {
+  if (N < 1 || N > (1LL << 30) || world < 1 || rank < 0 || rank >= world || !n_tiles)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan");
+  const int nt = (int)((N + RT - 1) / RT);
+  int cnt = 0;
+  for (int k = 0; k < nt; ++k)
+    if (owner_of_tile(k, world) == rank) {
+      if (tiles_out) tiles_out[cnt] = k;
+      ++cnt;
+    }
+  *n_tiles = cnt;
+  if (rows_per_tile) *rows_per_tile = RT;
+  if (chunk) *chunk = chunk_of(N);
+  return HAWKES_OK;
+}
+
+int hawkes_nccl_unique_id(void* out) {
+  if (!out) return set_err(nullptr, HAWKES_ERR_ARG, "out is NULL");
+  std::string e;
+  if (!g_nccl.load(e)) return set_err(nullptr, HAWKES_ERR_NCCL, "%s", e.c_str());
+  auto get = (ncclResult_t(*)(ncclUniqueId*))dlsym(g_nccl.h, "ncclGetUniqueId");
+  if (!get) return set_err(nullptr, HAWKES_ERR_NCCL, "ncclGetUniqueId missing");
+  ncclUniqueId id;
+  ncclResult_t r = get(&id);
+  if (r != ncclSuccess) return set_err(nullptr, HAWKES_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.errStr(r));
+  memcpy(out, &id, sizeof id);
+  return HAWKES_OK;
+}
+
+// ------------------------------------------------------------------ diagnostics
+// Not part of the numerical contract; used by tests and bench.py.
+int hawkes_diag_exp(const double* a_dev, double* out_dev, int64_t n) {
+  hawkes_ctx* ctx = nullptr;
+  int2* tab = nullptr;
+  int2 h[32];
+  for (int j = 0; j < 32; ++j) {
+    const double v = (double)exp2l((long double)j / 32.0L);
+    long long b;
+    memcpy(&b, &v, 8);
+    h[j] = make_int2((int)(b & 0xffffffffLL), (int)(b >> 32));
+  }
+  CU(cudaMalloc(&tab, sizeof h));
+  CU(cudaMemcpy(tab, h, sizeof h, cudaMemcpyHostToDevice));
+  k_diag_exp<<<(unsigned)((n + 255) / 256), 256>>>(a_dev, out_dev, n, tab);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  CU(cudaFree(tab));
+  return HAWKES_OK;
+}
+
+// FP64-pipe probe: returns achieved DFMA lane-ops per second over the whole device.
+int hawkes_diag_fp64_peak(double* ops_per_s) {
+  hawkes_ctx* ctx = nullptr;
+  int dev = 0, sms = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out = nullptr;
+  CU(cudaMalloc(&out, 8));
+  const int iters = 1 << 16, threads = 512, blocks = sms * 4;
+  k_diag_dfma<<<blocks, threads>>>(out, 256);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_diag_dfma<<<blocks, threads>>>(out, iters);
+  cudaEventRecord(b);
+  CU(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  *ops_per_s = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+  return HAWKES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+// hawkes_kernels.cuh -- sm_100a kernels for the O(N^2) Hawkes rate and gradient passes.
+//
+// Math (PAPER.md, see include/hawkes.h for the full statement):
+//   mu_ij = mu0/(tau_x^D tau_t) phi_D(dx/tau_x) phi(dt/tau_t) I[t_i != t_j]
+//   xi_ij = theta omega/h^D e^{-omega dt} phi_D(dx/h) I[t_j < t_i]
+//   lambda_i = sum_j mu_ij + xi_ij
+//   g_i = sum_j [(mu_ij rho_i + mu_ji rho_j)/tau_x^2 + (xi_ij rho_i + xi_ji rho_j)/h^2] (x_j - x_i)
+//                                                                            (App. A)
+// with rho = 1/lambda.  Because mu is symmetric, g_i splits into a part that needs only
+// row-i data (accumulated in the rate pass) and a part weighted by rho_j (gradient pass):
+//   g_i = rho_i * G1_i + G2_i
+//   G1_i = sum_j (mu_ij/tau_x^2 + xi_ij/h^2) dx_ij                  [pass 1, with lambda]
+//   G2_i = sum_j rho_j (mu_ij/tau_x^2 + xi_ji/h^2) dx_ij            [pass 2]
+// so each pass evaluates the background exp for every pair and the self-excitation exp
+// only for the half of the pairs where the relevant indicator can be non-zero.
+//
+// Scaled domain: every pair exponent carries log(alpha*w*2^64) (alpha = 1/tau_x^2 or
+// 1/h^2, w the kernel weight), so the exp returns alpha*mu_ij*2^64 (resp. beta*xi_ij*2^64)
+// directly; sums stay scaled, rho' = 2^-64/lambda, and g_i = rho'_i G1'_i + G2'_i exactly
+// as above.  The 2^64 keeps terms whose true value is subnormal (down to 2^-1086) normal,
+// so the flush-to-zero of the fast exp below matches the oracle's underflow to 0.
+//
+// Layout: each event is one record of REC doubles {x_0..x_{D-1}, t, rho', pad} (32 B for
+// D <= 2); a CTA owns RT = THREADS*R rows (thread k: rows row0 + k + r*THREADS), and
+// streams j-tiles of TILE_J records through shared memory with 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier, STAGES deep).  Every lane reads the same record (broadcast).
+// Work items (row tile, j chunk) are pulled from a global counter by a persistent grid;
+// each item writes its own partial sums, reduced later in a fixed order (deterministic,
+// independent of the number of ranks).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hk {
+
+constexpr int THREADS = 128;
+constexpr int TILE_J = 128;
+constexpr int STAGES = 4;
+
+template <int D>
+struct Layout {
+  static constexpr int REC = ((D + 3) / 2) * 2;   // doubles per event record (even)
+  static constexpr int T = D;                     // offset of t
+  static constexpr int RHO = D + 1;               // offset of rho'
+  static constexpr int K1 = ((D + 3) / 2) * 2;    // pass-1 partial: M', X', G1'[D] (padded)
+  static constexpr int K2 = ((D + 1) / 2) * 2;    // pass-2 partial: G2'[D] (padded)
+};
+
+struct PassConst {
+  double kx, kt, ks;   // -1/(2 tau_x^2), -1/(2 tau_t^2), -1/(2 h^2)
+  double omega;
+  double lnc_b;        // log(mu0/((2pi)^{(D+1)/2} tau_x^D tau_t) / tau_x^2 * 2^64)
+  double lnc_s;        // log(theta omega/((2pi)^{D/2} h^D) / h^2 * 2^64)
+};
+
+// ---------------------------------------------------------------- fast fp64 exp
+// e^a = 2^(k/32) e^r, k = rint(a*32/ln2), r = a - k ln2/32, |r| <= ln2/64.
+// 2^(k/32) = 2^m * T[j] (k = 32m + j, T from a 32-entry shared table, m added to the
+// exponent field with integer ops), e^r - 1 by its degree-5 Taylor polynomial
+// (truncation <= 2.3e-15 relative).  9 FP64-pipe instructions, no branches.
+// Results below 2^-1022 (k < -32704, including a = -inf) are flushed to +0 by a final
+// select (which also discards the NaN a huge |a| makes of the polynomial); the caller
+// keeps arguments below ~700 (validated constants), so there is no overflow path.
+constexpr double EXP_K = 46.166241308446828384;          // 32/ln2
+constexpr double EXP_SHIFT = 6755399441055744.0;          // 1.5 * 2^52
+constexpr double EXP_C = 0.021660849392498290;            // ln2/32
+constexpr long long EXP_YMIN_BITS = 0x4338000000000000LL - 32704;  // bits(SHIFT - 32704)
+
+__device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab) {
+  const double y = fma(a, EXP_K, EXP_SHIFT);
+  const double kf = y - EXP_SHIFT;
+  const double r = fma(kf, -EXP_C, a);
+  const int lo = __double2loint(y);
+  const int2 T = tab[lo & 31];                 // .x = low word, .y = high word of 2^(j/32)
+  const int m = lo >> 5;                       // floor(k/32)
+  double p = fma(1.0 / 120.0, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = p * r;                                   // e^r - 1
+  const double Tm = __hiloint2double(T.y + (int)((unsigned)m << 20), T.x);
+  const double e = fma(Tm, p, Tm);
+  return (__double_as_longlong(y) < EXP_YMIN_BITS) ? 0.0 : e;
+}
+
+// --------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ------------------------------------------------------------------- pair bodies
+enum { KIND_EARLIER = 0, KIND_LATER = 1, KIND_MIXED = 2 };
+
+template <int D>
+struct RowState {
+  double x[D];
+  double t;
+  int g;
+};
+
+// Pass 1 (rate pass + row-local gradient part) for one (i, j) pair.
+//  KIND_EARLIER: every j in the tile is strictly earlier than every row -> mu and xi.
+//  KIND_LATER:   every j strictly later -> mu only (xi_ij = 0).
+//  KIND_MIXED:   per-pair indicators from the tie-group ids g (g_j == g_i <=> t_j == t_i,
+//                g_j < g_i <=> t_j < t_i).
+template <int D, int KIND>
+__device__ __forceinline__ void pair_pass1(const double* __restrict__ rj, int gj,
+                                           const RowState<D>& row, double& M, double& X,
+                                           double (&G)[D], const PassConst& c,
+                                           const int2* __restrict__ tab) {
+  double dx[D];
+  double r2;
+#pragma unroll
+  for (int d = 0; d < D; ++d) dx[d] = rj[d] - row.x[d];
+  r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
+  const double dt = row.t - rj[D];
+  const double ab = fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b));
+  double eb = fexp(ab, tab);
+  if (KIND == KIND_MIXED) eb = (gj == row.g) ? 0.0 : eb;
+  if (KIND == KIND_LATER) {
+    M += eb;
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] = fma(eb, dx[d], G[d]);
+  } else {
+    const double as = fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s));
+    double es = fexp(as, tab);
+    if (KIND == KIND_MIXED) es = (gj < row.g) ? es : 0.0;
+    M += eb;
+    X += es;
+    const double cc = eb + es;
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] = fma(cc, dx[d], G[d]);
+  }
+}
+
+// Pass 2 (gradient pass, terms weighted by rho'_j) for one (i, j) pair.
+//  KIND_EARLIER: xi_ji = 0 -> rho_j mu_ij only.   KIND_LATER: rho_j (mu_ij + xi_ji).
+template <int D, int KIND>
+__device__ __forceinline__ void pair_pass2(const double* __restrict__ rj, int gj,
+                                           const RowState<D>& row, double (&G)[D],
+                                           const PassConst& c, const int2* __restrict__ tab) {
+  double dx[D];
+  double r2;
+#pragma unroll
+  for (int d = 0; d < D; ++d) dx[d] = rj[d] - row.x[d];
+  r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
+  const double dt = row.t - rj[D];
+  const double rho = rj[D + 1];
+  const double ab = fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b));
+  double eb = fexp(ab, tab);
+  if (KIND == KIND_MIXED) eb = (gj == row.g) ? 0.0 : eb;
+  double cc;
+  if (KIND == KIND_EARLIER) {
+    cc = rho * eb;
+  } else {
+    // xi_ji: t_j > t_i, exponent k_s r^2 - omega (t_j - t_i) = k_s r^2 + omega dt
+    const double as = fma(c.ks, r2, fma(c.omega, dt, c.lnc_s));
+    double es = fexp(as, tab);
+    if (KIND == KIND_MIXED) es = (gj > row.g) ? es : 0.0;
+    cc = rho * (eb + es);
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = fma(cc, dx[d], G[d]);
+}
+
+// ------------------------------------------------------------- persistent kernel
+struct PassArgs {
+  const double* rec;     // Npad x REC
+  const int* gid;        // Npad tie-group ids (first index with the same time)
+  const int2* items;     // (row tile, chunk)
+  int* counter;          // work counter, zeroed before launch
+  double* part;          // [chunks][Npad][K]
+  const int2* tab;       // 32-entry exp table in global memory
+  long long npad;
+  int N;
+  int n_items;
+  int chunk;             // events per j chunk (multiple of TILE_J)
+  PassConst c;
+};
+
+template <int D, int PASS, int R>
+__global__ void __launch_bounds__(THREADS, 4) pass_kernel(PassArgs a) {
+  using L = Layout<D>;
+  constexpr int REC = L::REC;
+  constexpr int RT = THREADS * R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage = reinterpret_cast<double*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(double));
+  int2* tab = reinterpret_cast<int2*>(bars + STAGES);
+  __shared__ int s_item;
+
+  const int tid = threadIdx.x;
+  if (tid < 32) tab[tid] = a.tab[tid];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t parity = 0;  // bit s = parity to wait for on stage s
+  const PassConst c = a.c;
+  const int N = a.N;
+
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= a.n_items) break;
+    const int2 w = a.items[it];
+    const int row0 = w.x * RT;
+    const int j0 = w.y * a.chunk;
+    const int j1 = min(N, j0 + a.chunk);
+    const int ntiles = (j1 - j0 + TILE_J - 1) / TILE_J;
+    const int rlast = min(row0 + RT, N) - 1;
+    const int g_first = a.gid[row0];
+    const int g_last = a.gid[rlast];
+
+    RowState<D> row[R];
+    double M[R], X[R], G[R][D];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = min(row0 + tid + r * THREADS, N - 1);
+      const double* ri = a.rec + (long long)i * REC;
+#pragma unroll
+      for (int d = 0; d < D; ++d) row[r].x[d] = ri[d];
+      row[r].t = ri[D];
+      row[r].g = a.gid[i];
+      M[r] = 0.0;
+      X[r] = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) G[r][d] = 0.0;
+    }
+
+    if (tid == 0) {
+      for (int s = 0; s < STAGES && s < ntiles; ++s) {
+        const int jt = j0 + s * TILE_J;
+        const int cnt = min(TILE_J, j1 - jt);
+        tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
+                    (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
+      }
+    }
+
+    for (int tl = 0; tl < ntiles; ++tl) {
+      const int s = tl % STAGES;
+      const int jt = j0 + tl * TILE_J;
+      const int cnt = min(TILE_J, j1 - jt);
+      const int gj_first = a.gid[jt];
+      const int gj_last = a.gid[jt + cnt - 1];
+      mbar_wait(&bars[s], (parity >> s) & 1u);
+      parity ^= (1u << s);
+      const double* st = stage + s * TILE_J * REC;
+      const int kind = (gj_last < g_first) ? KIND_EARLIER
+                                           : ((gj_first > g_last) ? KIND_LATER : KIND_MIXED);
+      if (kind == KIND_EARLIER) {
+#pragma unroll 2
+        for (int jj = 0; jj < cnt; ++jj) {
+          const double* rj = st + jj * REC;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (PASS == 1)
+              pair_pass1<D, KIND_EARLIER>(rj, 0, row[r], M[r], X[r], G[r], c, tab);
+            else
+              pair_pass2<D, KIND_EARLIER>(rj, 0, row[r], G[r], c, tab);
+          }
+        }
+      } else if (kind == KIND_LATER) {
+#pragma unroll 2
+        for (int jj = 0; jj < cnt; ++jj) {
+          const double* rj = st + jj * REC;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (PASS == 1)
+              pair_pass1<D, KIND_LATER>(rj, 0, row[r], M[r], X[r], G[r], c, tab);
+            else
+              pair_pass2<D, KIND_LATER>(rj, 0, row[r], G[r], c, tab);
+          }
+        }
+      } else {
+        for (int jj = 0; jj < cnt; ++jj) {
+          const double* rj = st + jj * REC;
+          const int gj = a.gid[jt + jj];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (PASS == 1)
+              pair_pass1<D, KIND_MIXED>(rj, gj, row[r], M[r], X[r], G[r], c, tab);
+            else
+              pair_pass2<D, KIND_MIXED>(rj, gj, row[r], G[r], c, tab);
+          }
+        }
+      }
+      __syncthreads();  // every lane is done with stage s
+      if (tid == 0 && tl + STAGES < ntiles) {
+        const int jn = j0 + (tl + STAGES) * TILE_J;
+        const int cn = min(TILE_J, j1 - jn);
+        tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
+                    (uint32_t)(cn * REC * sizeof(double)), &bars[s]);
+      }
+    }
+
+    // partial sums of this item
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = row0 + tid + r * THREADS;
+      if (i < N) {
+        if (PASS == 1) {
+          double* o = a.part + ((long long)w.y * a.npad + i) * L::K1;
+          o[0] = M[r];
+          o[1] = X[r];
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[2 + d] = G[r][d];
+        } else {
+          double* o = a.part + ((long long)w.y * a.npad + i) * L::K2;
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[d] = G[r][d];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace hk

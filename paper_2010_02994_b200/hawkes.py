@@ -1,0 +1,178 @@
+"""Python binding of the C ABI (include/hawkes.h): same names, argument marshalling only.
+
+Every step of the computation runs in libhawkes_b200.so; torch is used for device memory
+(tensors passed in / out), the current CUDA stream and the process group that hands the
+NCCL unique id to every rank.
+
+    ctx = HawkesContext(N, D)                 # hawkes_create
+    ctx.set_times(t); ctx.set_locations(x); ctx.set_params(theta)
+    ell = ctx.loglik()                        # Eq. 1
+    g, ell = ctx.grad_locations()             # App. A
+    x, p, ell, kin = ctx.leapfrog(x, p, step, n_steps)   # HMC over X
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import HAWKES_FP32, HAWKES_FP64, HAWKES_MEM_DEVICE, HAWKES_MEM_HOST, HawkesError, check
+
+__all__ = ["HawkesContext", "HawkesError", "nccl_unique_id", "diag_exp", "diag_fp64_peak"]
+
+
+def _ptr_mem(a) -> Tuple[int, int, object]:
+    """(pointer, hawkes_mem, keep-alive) for a float64 torch tensor or numpy array."""
+    if isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64:
+            raise TypeError("arrays must be float64")
+        if not a.is_contiguous():
+            raise ValueError("arrays must be contiguous")
+        return a.data_ptr(), (HAWKES_MEM_DEVICE if a.is_cuda else HAWKES_MEM_HOST), a
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return arr.ctypes.data, HAWKES_MEM_HOST, arr
+
+
+def nccl_unique_id() -> bytes:
+    """hawkes_nccl_unique_id: 128 bytes for opts.nccl_unique_id (rank 0 calls this)."""
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(128)
+    check(lib.hawkes_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+class HawkesContext:
+    """hawkes_create / hawkes_destroy and the calls on one context."""
+
+    def __init__(self, N: int, D: int, device: int = 0, stream: Optional[torch.cuda.Stream] = None,
+                 precision: str = "fp64", rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None, emulate_world: int = 0):
+        self._lib = _lib.load()
+        self.N, self.D, self.device = int(N), int(D), int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        o = _lib.Opts()
+        self._lib.hawkes_default_opts(ctypes.byref(o))
+        o.device = self.device
+        o.cuda_stream = stream.cuda_stream
+        o.precision = {"fp64": HAWKES_FP64, "fp32": HAWKES_FP32}[precision]
+        o.rank, o.world = int(rank), int(world)
+        self._id = None
+        if nccl_id is not None:
+            self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p)
+        o.emulate_world = int(emulate_world)
+        h = ctypes.c_void_p()
+        check(self._lib.hawkes_create(self.N, self.D, ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.hawkes_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- inputs
+    def set_times(self, t):
+        p, mem, keep = _ptr_mem(t)
+        check(self._lib.hawkes_set_times(self._h, p, mem), self._h)
+
+    def set_locations(self, x):
+        p, mem, keep = _ptr_mem(x)
+        check(self._lib.hawkes_set_locations(self._h, p, mem), self._h)
+
+    def set_params(self, theta: Sequence[float]):
+        """Theta = (mu0, tau_x, tau_t, theta, omega, h) in the paper's order."""
+        prm = _lib.Params(*[float(v) for v in theta])
+        check(self._lib.hawkes_set_params(self._h, ctypes.byref(prm)), self._h)
+
+    # -- evaluations
+    def loglik(self) -> float:
+        out = ctypes.c_double()
+        check(self._lib.hawkes_loglik(self._h, ctypes.byref(out)), self._h)
+        return out.value
+
+    def grad_locations(self, out=None) -> Tuple[object, float]:
+        """Returns (gradient N x D, ell).  ``out`` may be a float64 CUDA tensor or a host
+        array/tensor; default: a new CUDA tensor on this context's device."""
+        if out is None:
+            out = torch.empty((self.N, self.D), dtype=torch.float64, device=f"cuda:{self.device}")
+        p, mem, keep = _ptr_mem(out)
+        ll = ctypes.c_double()
+        check(self._lib.hawkes_grad_locations(self._h, p, mem, ctypes.byref(ll)), self._h)
+        return out, ll.value
+
+    def get_rates(self) -> dict:
+        """lambda_n, mu_n, xi_n, Lambda_n of the current state (numpy, host)."""
+        arrs = {k: np.empty(self.N) for k in ("lambda", "mu", "xi", "Lambda")}
+        ptrs = [arrs[k].ctypes.data for k in ("lambda", "mu", "xi", "Lambda")]
+        check(self._lib.hawkes_get_rates(self._h, *ptrs, HAWKES_MEM_HOST), self._h)
+        return arrs
+
+    def leapfrog(self, x, p, step: float, n_steps: int, inv_mass=None, box_lo=None, box_hi=None):
+        """Runs hawkes_leapfrog in place on x and p (same memory kind); returns
+        (x, p, ell_end, kinetic_end)."""
+        px, mem, kx = _ptr_mem(x)
+        pp, memp, kp = _ptr_mem(p)
+        if memp != mem:
+            raise ValueError("x and p must live in the same memory")
+        if kx is not x or kp is not p:
+            raise ValueError("x and p must be contiguous float64 arrays/tensors (updated in place)")
+        extra = []
+        for a in (inv_mass, box_lo, box_hi):
+            if a is None:
+                extra.append((None, None))
+            else:
+                pa, ma, ka = _ptr_mem(a)
+                if ma != mem:
+                    raise ValueError("inv_mass / box arrays must live with x")
+                extra.append((pa, ka))
+        ll, kin = ctypes.c_double(), ctypes.c_double()
+        check(self._lib.hawkes_leapfrog(self._h, px, pp, mem, float(step), int(n_steps),
+                                        extra[0][0], extra[1][0], extra[2][0],
+                                        ctypes.byref(ll), ctypes.byref(kin)), self._h)
+        return x, p, ll.value, kin.value
+
+    # -- timing (CUDA events recorded by the library around the two pass kernels)
+    def enable_timing(self, enable: bool = True):
+        check(self._lib.hawkes_enable_timing(self._h, int(bool(enable))), self._h)
+
+    def kernel_times(self) -> dict:
+        r, g = ctypes.c_double(), ctypes.c_double()
+        nr, ng, tot = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self._lib.hawkes_get_kernel_times(self._h, ctypes.byref(r), ctypes.byref(nr),
+                                                ctypes.byref(g), ctypes.byref(ng),
+                                                ctypes.byref(tot)), self._h)
+        return {"rate_ms": r.value, "rate_launches": nr.value, "grad_ms": g.value,
+                "grad_launches": ng.value, "total_launches": tot.value}
+
+
+def diag_exp(a: torch.Tensor) -> torch.Tensor:
+    """The kernels' fast exp applied to a float64 CUDA tensor (accuracy tests)."""
+    a = a.contiguous()
+    out = torch.empty_like(a)
+    check(_lib.load().hawkes_diag_exp(a.data_ptr(), out.data_ptr(), a.numel()))
+    return out
+
+
+def diag_fp64_peak() -> float:
+    """Measured dependent-DFMA throughput of the current device, FP64 lane-ops/s."""
+    v = ctypes.c_double()
+    check(_lib.load().hawkes_diag_fp64_peak(ctypes.byref(v)))
+    return v.value

@@ -1,0 +1,55 @@
+"""Multi-process plumbing for row sharding; argument marshalling only.
+
+One process per GPU.  torch.distributed hands rank 0's NCCL unique id to every rank;
+the library then builds its own NCCL communicator and does the exchange steps itself
+(allgather of rho' = 1/lambda and ell_n between the passes, allgather of gradient rows).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .hawkes import HawkesContext, nccl_unique_id
+
+
+def plan(N: int, world: int, rank: int) -> Tuple[List[int], int, int]:
+    """hawkes_plan: (row tiles of `rank`, rows per tile, j-chunk length)."""
+    lib = _lib.load()
+    n, rt, ck = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.hawkes_plan(N, world, rank, None, ctypes.byref(n), ctypes.byref(rt),
+                               ctypes.byref(ck)))
+    buf = (ctypes.c_int32 * max(1, n.value))()
+    _lib.check(lib.hawkes_plan(N, world, rank, buf, ctypes.byref(n), None, None))
+    return list(buf[: n.value]), rt.value, ck.value
+
+
+def rows_of(N: int, world: int, rank: int) -> List[int]:
+    tiles, rt, _ = plan(N, world, rank)
+    return [i for k in tiles for i in range(k * rt, min(N, (k + 1) * rt))]
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates an NCCL unique id; every rank returns the same 128 bytes."""
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.cpu().tolist())
+
+
+def init_distributed_context(N: int, D: int, precision: str = "fp64", group=None) -> HawkesContext:
+    """hawkes_create on every rank of an initialised process group (world > 1 shards rows)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.cuda.current_device()
+    if world == 1:
+        return HawkesContext(N, D, device=dev, precision=precision)
+    uid = broadcast_unique_id(group)
+    return HawkesContext(N, D, device=dev, precision=precision, rank=rank, world=world, nccl_id=uid)
