@@ -28,6 +28,7 @@
 
 #include "../../include/hawkes.h"
 #include "hawkes_kernels.cuh"
+#include "hawkes_kernels_f32.cuh"
 
 using namespace hk;
 
@@ -36,7 +37,6 @@ namespace {
 constexpr int R_ROWS = 2;                    // rows per thread
 constexpr int RT = THREADS * R_ROWS;         // rows per row tile
 constexpr int FIN_THREADS = RT;              // finalize: one thread per row of a tile
-constexpr double TWOM64 = 1.0 / 18446744073709551616.0;
 constexpr double LN2 = 0.693147180559945309417232121458;
 
 thread_local std::string g_create_error;
@@ -100,9 +100,38 @@ __global__ void k_pack_t(double* __restrict__ rec, const double* __restrict__ t,
   for (int k = D + 2; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.0;
 }
 
+// fp32 records: hi/lo float splits (v = hi + lo to ~48 bits)
+template <int D>
+__global__ void k_pack_x32(float* __restrict__ rec, const double* __restrict__ x, int N, int npad) {
+  using L = Layout32<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const int src = min(i, N - 1);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double v = x[(long long)src * D + d];
+    const float hi = (float)v;
+    rec[(long long)i * L::REC + L::XH + d] = hi;
+    rec[(long long)i * L::REC + L::XL + d] = (float)(v - (double)hi);
+  }
+}
+
+template <int D>
+__global__ void k_pack_t32(float* __restrict__ rec, const double* __restrict__ t, int N, int npad) {
+  using L = Layout32<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const double v = t[min(i, N - 1)];
+  const float hi = (float)v;
+  rec[(long long)i * L::REC + L::TH] = hi;
+  rec[(long long)i * L::REC + L::TL] = (float)(v - (double)hi);
+  for (int k = L::RHO; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.f;
+}
+
 struct FinConst {
   double tx2, h2;         // tau_x^2, h^2
   double mu0, tau_t, theta, omega, tN;
+  double scale_log2;      // pair sums carry 2^-scale_log2: -64 (fp64 path) or E (fp32 path)
 };
 
 // Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
@@ -129,6 +158,7 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
   const double Lp = mu_s + xi_s;
   const double rho = (Lp > 0.0) ? 1.0 / Lp : 0.0;
+  const double sc = exp2(f.scale_log2);   // exact power of two
   // Lambda_n: mu0 (Phi(a) - Phi(b)) - theta (e^{-omega (t_N - t_n)} - 1),
   // a = (t_N - t_n)/tau_t >= 0, b = -t_n/tau_t <= 0, Phi(a) - Phi(b) = 1 - Q(a) - Q(-b),
   // Q(z) = erfc(z/sqrt2)/2 (reading R10: same value without cancellation)
@@ -136,23 +166,26 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   const double qa = 0.5 * erfc((f.tN - tn) / f.tau_t * 0.70710678118654752440);
   const double qb = 0.5 * erfc(tn / f.tau_t * 0.70710678118654752440);
   const double Lam = f.mu0 * ((1.0 - qa) - qb) - f.theta * expm1(-f.omega * (f.tN - tn));
-  const double ell = (Lp > 0.0) ? (log(Lp) - 64.0 * LN2) - Lam : -INFINITY;
+  const double ell = (Lp > 0.0) ? (log(Lp) + f.scale_log2 * LN2) - Lam : -INFINITY;
 #pragma unroll
   for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
   rl[2 * (long long)i] = rho;
   rl[2 * (long long)i + 1] = ell;
-  rates[4 * (long long)i] = Lp * TWOM64;
-  rates[4 * (long long)i + 1] = mu_s * TWOM64;
-  rates[4 * (long long)i + 2] = xi_s * TWOM64;
+  rates[4 * (long long)i] = Lp * sc;
+  rates[4 * (long long)i + 1] = mu_s * sc;
+  rates[4 * (long long)i + 2] = xi_s * sc;
   rates[4 * (long long)i + 3] = Lam;
 }
 
 template <int D>
-__global__ void k_rho_to_rec(double* __restrict__ rec, const double* __restrict__ rl, int N) {
-  using L = Layout<D>;
+__global__ void k_rho_to_rec(double* __restrict__ rec, float* __restrict__ rec32,
+                             const double* __restrict__ rl, int N) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  rec[(long long)i * L::REC + L::RHO] = rl[2 * (long long)i];
+  if (rec32)
+    rec32[(long long)i * Layout32<D>::REC + Layout32<D>::RHO] = (float)rl[2 * (long long)i];
+  else
+    rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
 }
 
 // sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W
@@ -238,8 +271,7 @@ template <int D>
 __global__ void k_drift(double* __restrict__ x, double* __restrict__ p,
                         const double* __restrict__ minv, const double* __restrict__ lo,
                         const double* __restrict__ hi, int N, double eps,
-                        double* __restrict__ rec, int* __restrict__ bad) {
-  using L = Layout<D>;
+                        int* __restrict__ bad) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
 #pragma unroll
@@ -257,7 +289,6 @@ __global__ void k_drift(double* __restrict__ x, double* __restrict__ p,
     if (!(fabs(xv) <= 1e100)) atomicOr(bad, 1);
     x[k] = xv;
     p[k] = pv;
-    rec[(long long)i * L::REC + d] = xv;
   }
 }
 
@@ -329,6 +360,7 @@ struct hawkes_ctx {
 
   // device buffers
   double* rec = nullptr;   // npad x REC
+  float* rec32 = nullptr;  // npad x REC32 (fp32 path only)
   int* gid = nullptr;      // npad
   double* part1 = nullptr; // nchunks x npad x K1
   double* part2 = nullptr; // nchunks x npad x K2
@@ -355,6 +387,7 @@ struct hawkes_ctx {
   double tN = 0.0;
   hawkes_params params{};
   PassConst pc{};
+  PassConst32 pc32{};
   FinConst fc{};
 
   // timing
@@ -438,6 +471,7 @@ int dalloc(hawkes_ctx* ctx, T** p, size_t count) {
 int K1_of(int D) { return ((D + 3) / 2) * 2; }
 int K2_of(int D) { return ((D + 1) / 2) * 2; }
 int REC_of(int D) { return ((D + 3) / 2) * 2; }
+int Layout32Rec(int D) { return ((2 * D + 3 + 3) / 4) * 4; }
 
 // ---------------------------------------------------------------- dispatch on D
 template <template <int> class F, typename... A>
@@ -458,8 +492,26 @@ size_t pass_smem() {
 }
 
 template <int D>
+size_t pass_smem32() {
+  return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t);
+}
+
+template <int D>
 struct SetupD {
   static int run(hawkes_ctx* ctx) {
+    if (ctx->rec32) {
+      auto k1 = pass_kernel_f32<D, 1, R_ROWS>;
+      auto k2 = pass_kernel_f32<D, 2, R_ROWS>;
+      const size_t sm = pass_smem32<D>();
+      CU(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CU(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int b1 = 0, b2 = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, THREADS, sm));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
+      ctx->grid1 = std::max(1, b1) * ctx->sms;
+      ctx->grid2 = std::max(1, b2) * ctx->sms;
+      return HAWKES_OK;
+    }
     auto k1 = pass_kernel<D, 1, R_ROWS>;
     auto k2 = pass_kernel<D, 2, R_ROWS>;
     const size_t sm = pass_smem<D, 1>();
@@ -510,6 +562,7 @@ void harvest_events(hawkes_ctx* ctx) {
 template <int D>
 struct PassD {
   static int run(hawkes_ctx* ctx, int pass, int rank) {
+    if (ctx->rec32) return run32(ctx, pass, rank);
     PassArgs a;
     a.rec = ctx->rec;
     a.gid = ctx->gid;
@@ -530,6 +583,30 @@ struct PassD {
       pass_kernel<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
     else
       pass_kernel<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+    CHECK_LAUNCH();
+    record_stop(ctx, pass == 1);
+    return HAWKES_OK;
+  }
+  static int run32(hawkes_ctx* ctx, int pass, int rank) {
+    PassArgs32 a;
+    a.rec = ctx->rec32;
+    a.gid = ctx->gid;
+    a.items = pass == 1 ? ctx->d_items1[rank] : ctx->d_items2[rank];
+    a.counter = ctx->counters + 2 * rank + (pass - 1);
+    a.part = pass == 1 ? ctx->part1 : ctx->part2;
+    a.npad = ctx->npad;
+    a.N = (int)ctx->N;
+    a.n_items = ctx->n_items[rank];
+    a.chunk = ctx->chunk;
+    a.c = ctx->pc32;
+    if (a.n_items == 0) return HAWKES_OK;
+    const size_t sm = pass_smem32<D>();
+    const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
+    record_start(ctx, pass == 1);
+    if (pass == 1)
+      pass_kernel_f32<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+    else
+      pass_kernel_f32<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
     CHECK_LAUNCH();
     record_stop(ctx, pass == 1);
     return HAWKES_OK;
@@ -566,7 +643,7 @@ template <int D>
 struct RhoD {
   static int run(hawkes_ctx* ctx) {
     const int n = (int)ctx->N;
-    k_rho_to_rec<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, ctx->rl, n);
+    k_rho_to_rec<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, ctx->rec32, ctx->rl, n);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -578,6 +655,11 @@ struct PackXD {
     k_pack_x<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, xdev, (int)ctx->N,
                                                                   ctx->npad, ctx->bad);
     CHECK_LAUNCH();
+    if (ctx->rec32) {
+      k_pack_x32<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec32, xdev,
+                                                                      (int)ctx->N, ctx->npad);
+      CHECK_LAUNCH();
+    }
     return HAWKES_OK;
   }
 };
@@ -588,6 +670,11 @@ struct PackTD {
     k_pack_t<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, tdev, (int)ctx->N,
                                                                   ctx->npad);
     CHECK_LAUNCH();
+    if (ctx->rec32) {
+      k_pack_t32<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec32, tdev,
+                                                                      (int)ctx->N, ctx->npad);
+      CHECK_LAUNCH();
+    }
     return HAWKES_OK;
   }
 };
@@ -598,9 +685,9 @@ struct DriftD {
     const int n = (int)ctx->N;
     k_drift<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(
         ctx->lf_x, ctx->lf_p, minv ? ctx->lf_minv : nullptr, box ? ctx->lf_lo : nullptr,
-        box ? ctx->lf_hi : nullptr, n, eps, ctx->rec, ctx->bad);
+        box ? ctx->lf_hi : nullptr, n, eps, ctx->bad);
     CHECK_LAUNCH();
-    return HAWKES_OK;
+    return dispatchD<PackXD>(D, ctx, (const double*)ctx->lf_x);
   }
 };
 
@@ -770,6 +857,26 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   fc.theta = p.theta;
   fc.omega = p.omega;
   fc.tN = tN;
+  fc.scale_log2 = -64.0;
+  if (ctx->opts.precision == HAWKES_FP32) {
+    // log2 domain; one power-of-two scale 2^-E puts the largest possible term near 2^20
+    const double L2E = 1.4426950408889634074;
+    const double l2b = p.mu0 > 0 ? lnw_b * L2E : -INFINITY;
+    const double l2s = p.theta > 0 ? lnw_s * L2E : -INFINITY;
+    const double E = floor(std::max(l2b, l2s)) - 20.0;
+    PassConst32 c32;
+    c32.kx = (float)(pc.kx * L2E);
+    c32.kt = (float)(pc.kt * L2E);
+    c32.ks = (float)(pc.ks * L2E);
+    c32.omega = (float)(p.omega * L2E);
+    c32.cb = (float)(l2b - E);
+    c32.cs = (float)(l2s - E);
+    if (!isfinite(c32.kx) || !isfinite(c32.kt) || !isfinite(c32.ks) || !isfinite(c32.omega) ||
+        c32.kx == 0.f || c32.kt == 0.f || c32.ks == 0.f)
+      return set_err(ctx, HAWKES_ERR_PARAM, "Theta outside the fp32 path's range");
+    fc.scale_log2 = E;
+    ctx->pc32 = c32;
+  }
   ctx->pc = pc;
   ctx->fc = fc;
   return HAWKES_OK;
@@ -821,8 +928,6 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     return set_err(nullptr, HAWKES_ERR_ARG, "bad rank/world");
   if (o.precision != HAWKES_FP64 && o.precision != HAWKES_FP32)
     return set_err(nullptr, HAWKES_ERR_ARG, "bad precision");
-  if (o.precision == HAWKES_FP32)
-    return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_FP32 is not built in this version");
   if (o.world > 1 && !o.nccl_unique_id)
     return set_err(nullptr, HAWKES_ERR_ARG, "world > 1 needs nccl_unique_id");
   if (o.world > 1 && o.emulate_world > 1)
@@ -883,6 +988,11 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->tab, 32)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
       (rc = dalloc(ctx, &ctx->st, 1)))
     return fail(rc);
+  if (o.precision == HAWKES_FP32) {
+    if ((rc = dalloc(ctx, &ctx->rec32, (size_t)ctx->npad * Layout32Rec(D)))) return fail(rc);
+    if (cudaMemset(ctx->rec32, 0, (size_t)ctx->npad * Layout32Rec(D) * sizeof(float)) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
+  }
   if (ctx->W > 1) {
     const size_t per_rank = (size_t)ctx->max_tiles * RT * std::max(4, D);
     if ((rc = dalloc(ctx, &ctx->sendbuf, per_rank)) ||
@@ -954,7 +1064,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   cudaSetDevice(ctx->opts.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->comm);
-  void* bufs[] = {ctx->rec, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
+  void* bufs[] = {ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi};

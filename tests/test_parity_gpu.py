@@ -245,3 +245,35 @@ def test_leapfrog_host_buffers_and_box():
     assert np.max(np.abs(x - xr)) <= 1e-9
     assert ell == pytest.approx(ellr, rel=1e-9)
     assert kin == pytest.approx(kr, rel=1e-9)
+
+
+# ----------------------------------------------------------------------- fp32 path
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_fp32_configs(name):
+    """fp32-accumulate variant at the north_star's 1e-4 (normwise per component)."""
+    _check_fp32(synth.config(name), f"fp32 {name}")
+
+
+@pytest.mark.parametrize("N", [3, 257, 1003])
+def test_fp32_ragged_and_ties(N):
+    _check_fp32(synth.unit_square(N, config=25, replicate=N), f"fp32 N={N}")
+    _check_fp32(synth.with_ties(N, max(2, N // 10)), f"fp32 ties N={N}")
+
+
+@pytest.mark.parametrize("D", [1, 3, 4])
+def test_fp32_other_dimensions(D):
+    _check_fp32(synth.unit_square(700, config=26, D=D), f"fp32 D={D}")
+
+
+def test_fp32_emulated_world_bitwise():
+    c = synth.unit_square(2000, config=27)
+    e1, g1, r1 = gpu_eval(c.x, c.t, c.theta, precision="fp32")
+    e4, g4, r4 = gpu_eval(c.x, c.t, c.theta, precision="fp32", emulate_world=4)
+    assert e1 == e4 and np.array_equal(g1, g4) and np.array_equal(r1["lambda"], r4["lambda"])
+
+
+def _check_fp32(c, what):
+    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision="fp32")
+    ell_ref, lam_ref, Lam_ref, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    np.testing.assert_allclose(rates["lambda"], lam_ref, rtol=1e-4, err_msg=what)
+    return assert_parity(ell, g, ell_ref, g_ref, S, precision="fp32", what=what)
