@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HAWKES_ABI_VERSION 1
+#define HAWKES_ABI_VERSION 2
 
 typedef struct hawkes_ctx hawkes_ctx; /* opaque; owns all device memory */
 
@@ -70,6 +70,17 @@ typedef enum {
 
 typedef enum { HAWKES_MEM_HOST = 0, HAWKES_MEM_DEVICE = 1 } hawkes_mem;
 
+/* Work decomposition of the two O(N^2) passes (both compute the same quantities):
+ *  ROWS  -- ordered pairs: every row i sums over all j (3 exps per ordered pair over both
+ *           passes); W > 1 shards row tiles and allgathers (1/lambda, ell_n) between the
+ *           passes; results are bitwise identical for every W.
+ *  PAIRS -- unordered pairs: chunk pairs (a < b) evaluate each pair's two exps once and
+ *           feed both events (2 exps per ordered pair over both
+ *           passes); W > 1 shards chunk pairs and allreduces per-event partial sums;
+ *           results are deterministic for a fixed W.  fp64 only in this version.
+ *  AUTO  -- PAIRS for fp64, ROWS for fp32. */
+typedef enum { HAWKES_ALGO_AUTO = 0, HAWKES_ALGO_ROWS = 1, HAWKES_ALGO_PAIRS = 2 } hawkes_algorithm;
+
 typedef struct {
   int32_t device;            /* CUDA device ordinal                                           */
   void* cuda_stream;         /* cudaStream_t to run on; NULL = default stream                  */
@@ -80,6 +91,7 @@ typedef struct {
   int32_t emulate_world;     /* world == 1 only: > 1 runs that many logical row shards one
                                 after another on this GPU, exchanging through device memory
                                 (exercises the sharded path without more GPUs); 0/1 = off      */
+  int32_t algorithm;         /* hawkes_algorithm                                              */
 } hawkes_opts;
 
 /* Theta in the paper's order.  sigma_x is the paper's h (Eq. 1 / App. A).
@@ -92,7 +104,8 @@ typedef struct {
   double mu0, tau_x, tau_t, theta, omega, sigma_x;
 } hawkes_params;
 
-/* Fill opts with defaults: device 0, default stream, FP64, rank 0 of 1, no emulation. */
+/* Fill opts with defaults: device 0, default stream, FP64, rank 0 of 1, no emulation,
+ * HAWKES_ALGO_AUTO. */
 int hawkes_default_opts(hawkes_opts* opts);
 
 /* Create a context for N >= 1 events in D dimensions (1 <= D <= HAWKES_MAX_D).
@@ -170,6 +183,14 @@ int hawkes_nccl_unique_id(void* out);
  * *n_tiles first.  Errors: HAWKES_ERR_ARG. */
 int hawkes_plan(int64_t N, int32_t world, int32_t rank, int32_t* tiles_out, int32_t* n_tiles,
                 int32_t* rows_per_tile, int32_t* chunk);
+
+/* Work plan of HAWKES_ALGO_PAIRS (host only): the chunk length (a function of N only) and
+ * the chunk pairs (a, b), a <= b, that rank `rank` of `world` evaluates (a == b: the pairs
+ * inside chunk a).  items_out (nullable) receives 2 * *n_items int32 (a, b).  Chunk pairs
+ * are dealt to ranks by greedy longest-processing-time on their pair counts.
+ * Errors: HAWKES_ERR_ARG. */
+int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out,
+                      int32_t* n_items, int32_t* chunk);
 
 /* Diagnostics (not part of the numerical contract; used by the tests and bench.py):
  * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak

@@ -19,13 +19,14 @@ STATUS = {
 }
 HAWKES_FP64, HAWKES_FP32 = 0, 1
 HAWKES_MEM_HOST, HAWKES_MEM_DEVICE = 0, 1
+ALGORITHMS = {"auto": 0, "rows": 1, "pairs": 2}
 
 # every symbol include/hawkes.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
     "hawkes_leapfrog", "hawkes_get_rates", "hawkes_enable_timing", "hawkes_get_kernel_times",
-    "hawkes_plan", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_last_error",
+    "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_last_error",
     "hawkes_abi_version",
 )
 
@@ -33,7 +34,8 @@ EXPORTS = (
 class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("precision", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("emulate_world", ctypes.c_int32)]
+                ("nccl_unique_id", ctypes.c_void_p), ("emulate_world", ctypes.c_int32),
+                ("algorithm", ctypes.c_int32)]
 
 
 class Params(ctypes.Structure):
@@ -76,6 +78,7 @@ def load() -> ctypes.CDLL:
                                             P(i64), P(i64)]
     lib.hawkes_nccl_unique_id.argtypes = [vp]
     lib.hawkes_plan.argtypes = [i64, i32, i32, P(i32), P(i32), P(i32), P(i32)]
+    lib.hawkes_plan_pairs.argtypes = [i64, i32, i32, P(i32), P(i32), P(i32)]
     lib.hawkes_diag_exp.argtypes = [dp, dp, i64]
     lib.hawkes_diag_fp64_peak.argtypes = [P(ctypes.c_double)]
     lib.hawkes_last_error.argtypes = [vp]

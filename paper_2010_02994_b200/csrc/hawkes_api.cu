@@ -29,6 +29,7 @@
 #include "../../include/hawkes.h"
 #include "hawkes_kernels.cuh"
 #include "hawkes_kernels_f32.cuh"
+#include "hawkes_kernels_sym.cuh"
 
 using namespace hk;
 
@@ -47,6 +48,8 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
   bool load(std::string& err) {
@@ -63,8 +66,9 @@ struct NcclApi {
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
     allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    if (!commInitRank || !allGather || !commDestroy || !errStr) {
+    if (!commInitRank || !allGather || !allReduce || !commDestroy || !errStr) {
       err = "libnccl.so.2 lacks required symbols";
       return false;
     }
@@ -126,6 +130,33 @@ __global__ void k_pack_t32(float* __restrict__ rec, const double* __restrict__ t
   rec[(long long)i * L::REC + L::TH] = hi;
   rec[(long long)i * L::REC + L::TL] = (float)(v - (double)hi);
   for (int k = L::RHO; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.f;
+}
+
+// PAIRS with W > 1: per event, fixed-order sum of the partial slots this rank computed.
+// Slot s of event i (chunk c) comes from chunk pair (min(s, c), max(s, c)).
+__global__ void k_slot_sum(const double* __restrict__ part, long long npad, int nchunks, int chunk,
+                           int K, const int* __restrict__ own, int rank, int N,
+                           double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)N * K) return;
+  const int i = (int)(idx / K), k = (int)(idx % K);
+  const int c = i / chunk;
+  double v = 0.0;
+  for (int sl = 0; sl < nchunks; ++sl) {
+    const int a = min(sl, c), b = max(sl, c);
+    if (own[a * nchunks + b] == rank) v += part[((long long)sl * npad + i) * K + k];
+  }
+  out[idx] = v;
+}
+
+// emulated ranks: the "allreduce" of their per-event sums, in rank order
+__global__ void k_sum_ranks(const double* __restrict__ in, long long stride, int W, long long n,
+                            double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  double v = in[idx];
+  for (int r = 1; r < W; ++r) v += in[r * stride + idx];
+  out[idx] = v;
 }
 
 struct FinConst {
@@ -357,6 +388,14 @@ struct hawkes_ctx {
   std::vector<int2*> d_items1, d_items2;    // per rank
   std::vector<int> n_items;                 // per rank
   ncclComm_t comm = nullptr;
+  // HAWKES_ALGO_PAIRS
+  bool pairs = false;
+  std::vector<int2*> d_sym;                 // per rank: off-diagonal chunk pairs
+  std::vector<int> n_sym;
+  int* d_own = nullptr;                     // [nchunks][nchunks] owner rank of pair (a <= b)
+  int* d_every_tile = nullptr;              // all row tiles 0..ntiles-1
+  double* sums1 = nullptr;                  // W > 1: [W or 1][npad][K1] per-event sums
+  double* sums2 = nullptr;                  // W > 1: [W or 1][npad][K2]
 
   // device buffers
   double* rec = nullptr;   // npad x REC
@@ -371,7 +410,7 @@ struct hawkes_ctx {
   double* xstage = nullptr;// N x D staging
   double* sendbuf = nullptr;
   double* recvbuf = nullptr;
-  int* counters = nullptr; // 2 per logical rank
+  int* counters = nullptr; // 4 per logical rank
   int2* tab = nullptr;     // exp table
   int* bad = nullptr;      // device-side input validation flag
   EvalStatus* st = nullptr;
@@ -399,6 +438,7 @@ struct hawkes_ctx {
   int64_t launches = 0;
 
   int grid1 = 0, grid2 = 0;
+  int grid_s1 = 0, grid_s2 = 0;
 };
 
 namespace {
@@ -491,6 +531,13 @@ size_t pass_smem() {
          32 * sizeof(int2);
 }
 
+template <int D, int PASS>
+size_t sym_smem() {
+  const int KR = PASS == 1 ? 1 + D : D;
+  return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
+         32 * sizeof(int2) + (size_t)4 * SYM_RT * KR * sizeof(double);
+}
+
 template <int D>
 size_t pass_smem32() {
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t);
@@ -522,6 +569,16 @@ struct SetupD {
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
     ctx->grid1 = std::max(1, b1) * ctx->sms;
     ctx->grid2 = std::max(1, b2) * ctx->sms;
+    if (ctx->pairs) {
+      auto s1 = sym_kernel<D, 1>;
+      auto s2 = sym_kernel<D, 2>;
+      CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 1>()));
+      CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 2>()));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym_smem<D, 1>()));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym_smem<D, 2>()));
+      ctx->grid_s1 = std::max(1, b1) * ctx->sms;
+      ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+    }
     return HAWKES_OK;
   }
 };
@@ -567,7 +624,7 @@ struct PassD {
     a.rec = ctx->rec;
     a.gid = ctx->gid;
     a.items = pass == 1 ? ctx->d_items1[rank] : ctx->d_items2[rank];
-    a.counter = ctx->counters + 2 * rank + (pass - 1);
+    a.counter = ctx->counters + 4 * rank + (pass - 1);
     a.part = pass == 1 ? ctx->part1 : ctx->part2;
     a.tab = ctx->tab;
     a.npad = ctx->npad;
@@ -575,15 +632,36 @@ struct PassD {
     a.n_items = ctx->n_items[rank];
     a.chunk = ctx->chunk;
     a.c = ctx->pc;
-    if (a.n_items == 0) return HAWKES_OK;
-    const size_t sm = pass_smem<D, 1>();
-    const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
     record_start(ctx, pass == 1);
-    if (pass == 1)
-      pass_kernel<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
-    else
-      pass_kernel<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
-    CHECK_LAUNCH();
+    if (a.n_items > 0) {
+      const size_t sm = pass_smem<D, 1>();
+      const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
+      if (pass == 1)
+        pass_kernel<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+      else
+        pass_kernel<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+      CHECK_LAUNCH();
+    }
+    if (ctx->pairs && ctx->n_sym[rank] > 0) {
+      SymArgs b;
+      b.rec = ctx->rec;
+      b.gid = ctx->gid;
+      b.items = ctx->d_sym[rank];
+      b.counter = ctx->counters + 4 * rank + 2 + (pass - 1);
+      b.part = pass == 1 ? ctx->part1 : ctx->part2;
+      b.tab = ctx->tab;
+      b.npad = ctx->npad;
+      b.N = (int)ctx->N;
+      b.n_items = ctx->n_sym[rank];
+      b.chunk = ctx->chunk;
+      b.c = ctx->pc;
+      const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+      if (pass == 1)
+        sym_kernel<D, 1><<<grid, THREADS, sym_smem<D, 1>(), ctx->stream>>>(b);
+      else
+        sym_kernel<D, 2><<<grid, THREADS, sym_smem<D, 2>(), ctx->stream>>>(b);
+      CHECK_LAUNCH();
+    }
     record_stop(ctx, pass == 1);
     return HAWKES_OK;
   }
@@ -592,7 +670,7 @@ struct PassD {
     a.rec = ctx->rec32;
     a.gid = ctx->gid;
     a.items = pass == 1 ? ctx->d_items1[rank] : ctx->d_items2[rank];
-    a.counter = ctx->counters + 2 * rank + (pass - 1);
+    a.counter = ctx->counters + 4 * rank + (pass - 1);
     a.part = pass == 1 ? ctx->part1 : ctx->part2;
     a.npad = ctx->npad;
     a.N = (int)ctx->N;
@@ -615,12 +693,17 @@ struct PassD {
 
 template <int D>
 struct Fin1D {
+  // ROWS: this rank's row tiles from the chunk partials.  PAIRS: every row, from the chunk
+  // partials (W == 1) or from the exchanged per-event sums (W > 1).
   static int run(hawkes_ctx* ctx, int rank) {
-    const int nt = (int)ctx->tiles_of[rank].size();
+    const bool all = ctx->pairs;
+    const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
-    k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part1, ctx->npad, ctx->nchunks,
-                                                   ctx->d_tiles[rank], (int)ctx->N, ctx->rec,
-                                                   ctx->G1, ctx->rl, ctx->rates, ctx->fc);
+    const bool sums = all && ctx->W > 1;
+    k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
+        sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nchunks,
+        all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1, ctx->rl,
+        ctx->rates, ctx->fc);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -629,11 +712,13 @@ struct Fin1D {
 template <int D>
 struct Fin2D {
   static int run(hawkes_ctx* ctx, int rank) {
-    const int nt = (int)ctx->tiles_of[rank].size();
+    const bool all = ctx->pairs;
+    const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
-    k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nchunks,
-                                                   ctx->d_tiles[rank], (int)ctx->N, ctx->G1,
-                                                   ctx->rl, ctx->grad);
+    const bool sums = all && ctx->W > 1;
+    k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
+        sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nchunks,
+        all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->G1, ctx->rl, ctx->grad);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -723,14 +808,41 @@ int exchange_rows(hawkes_ctx* ctx, double* rows, int K) {
 }
 
 // rate pass + finalize + exchange + ell reduction (device-side; no host sync)
+// PAIRS, W > 1: per-event sums over this process's chunk pairs, then the exchange
+// (NCCL allreduce, or the rank-ordered sum of the emulated ranks' buffers)
+int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int K) {
+  const long long n = (long long)ctx->N * K;
+  const long long stride = (long long)ctx->npad * K;
+  for (int r : ctx->my_ranks) {
+    double* out = ctx->comm ? sums : sums + (1 + r) * stride;
+    k_slot_sum<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        part, ctx->npad, ctx->nchunks, ctx->chunk, K, ctx->d_own, r, (int)ctx->N, out);
+    CHECK_LAUNCH();
+  }
+  if (ctx->comm) {
+    NC(g_nccl.allReduce(sums, sums, (size_t)n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  } else {
+    k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(sums + stride, stride, ctx->W,
+                                                                     n, sums);
+    CHECK_LAUNCH();
+  }
+  return HAWKES_OK;
+}
+
 int run_rates(hawkes_ctx* ctx) {
   if (ctx->rates_valid) return HAWKES_OK;
-  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 2 * ctx->W, ctx->stream));
-  for (int r : ctx->my_ranks) {
-    TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
-    TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
+  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
+  if (ctx->pairs) {
+    for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
+    if (ctx->W > 1) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1_of(ctx->D)));
+    TRY(dispatchD<Fin1D>(ctx->D, ctx, 0));
+  } else {
+    for (int r : ctx->my_ranks) {
+      TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
+      TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
+    }
+    TRY(exchange_rows(ctx, ctx->rl, 2));
   }
-  TRY(exchange_rows(ctx, ctx->rl, 2));
   TRY(dispatchD<RhoD>(ctx->D, ctx));
   k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
   CHECK_LAUNCH();
@@ -743,11 +855,17 @@ int run_rates(hawkes_ctx* ctx) {
 int run_grad(hawkes_ctx* ctx) {
   TRY(run_rates(ctx));
   if (ctx->grad_valid) return HAWKES_OK;
-  for (int r : ctx->my_ranks) {
-    TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
-    TRY(dispatchD<Fin2D>(ctx->D, ctx, r));
+  if (ctx->pairs) {
+    for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
+    if (ctx->W > 1) TRY(reduce_pair_partials(ctx, ctx->part2, ctx->sums2, K2_of(ctx->D)));
+    TRY(dispatchD<Fin2D>(ctx->D, ctx, 0));
+  } else {
+    for (int r : ctx->my_ranks) {
+      TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
+      TRY(dispatchD<Fin2D>(ctx->D, ctx, r));
+    }
+    TRY(exchange_rows(ctx, ctx->grad, ctx->D));
   }
-  TRY(exchange_rows(ctx, ctx->grad, ctx->D));
   ctx->grad_valid = true;
   return HAWKES_OK;
 }
@@ -784,9 +902,78 @@ int chunk_of(long long N) {
   return (int)c;
 }
 
+// PAIRS chunk: a multiple of the ordered kernel's 256-row tile, ~N/138 so that the
+// C(C-1)/2 chunk pairs give >= ~16 work items per CTA slot while the [C][Npad][K] partial
+// arrays stay ~C*N*48 bytes.  A function of N only.
+int chunk_pairs_of(long long N) {
+  long long c = (N + 137) / 138;
+  c = ((c + RT - 1) / RT) * RT;
+  return (int)std::max<long long>(RT, c);
+}
+
+// Chunk pairs (a <= b) dealt to ranks by greedy longest-processing-time on their cost.
+std::vector<int> pair_owners(long long N, int chunk, int W) {
+  const int C = (int)((N + chunk - 1) / chunk);
+  struct It { double cost; int a, b; };
+  std::vector<It> items;
+  for (int a = 0; a < C; ++a)
+    for (int b = a; b < C; ++b) {
+      const double na = (double)std::min<long long>(chunk, N - (long long)a * chunk);
+      const double nb = (double)std::min<long long>(chunk, N - (long long)b * chunk);
+      items.push_back({a == b ? na * na * 26.5 : na * nb * 36.0, a, b});
+    }
+  std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) { return x.cost > y.cost; });
+  std::vector<double> load(W, 0.0);
+  std::vector<int> own((size_t)C * C, -1);
+  for (const It& it : items) {
+    int r = 0;
+    for (int q = 1; q < W; ++q)
+      if (load[q] < load[r]) r = q;
+    load[r] += it.cost;
+    own[(size_t)it.a * C + it.b] = r;
+  }
+  return own;
+}
+
 int owner_of_tile(int k, int W) {
   const int pos = k % (2 * W);
   return pos < W ? pos : 2 * W - 1 - pos;
+}
+
+void build_plan_pairs(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
+                      std::vector<std::vector<int2>>& it2, std::vector<std::vector<int2>>& sym,
+                      std::vector<int>& own) {
+  const int W = ctx->W, C = ctx->nchunks, N = (int)ctx->N;
+  own = pair_owners(N, ctx->chunk, W);
+  ctx->tiles_of.assign(W, {});
+  ctx->max_tiles = 0;
+  it1.assign(W, {});
+  it2.assign(W, {});
+  sym.assign(W, {});
+  const int tiles_per_chunk = ctx->chunk / RT;
+  for (int r = 0; r < W; ++r) {
+    std::vector<std::pair<long long, int2>> off;
+    for (int a = 0; a < C; ++a)
+      for (int b = a; b < C; ++b) {
+        if (own[(size_t)a * C + b] != r) continue;
+        if (a == b) {
+          for (int k = 0; k < tiles_per_chunk; ++k) {
+            const int tile = a * tiles_per_chunk + k;
+            if (tile * RT >= N) break;
+            it1[r].push_back(make_int2(tile, a));
+            it2[r].push_back(make_int2(tile, a));
+          }
+        } else {
+          const long long nb = std::min<long long>(ctx->chunk, (long long)N - (long long)b * ctx->chunk);
+          off.push_back({nb, make_int2(a, b)});
+        }
+      }
+    std::stable_sort(off.begin(), off.end(),
+                     [](const std::pair<long long, int2>& x, const std::pair<long long, int2>& y) {
+                       return x.first > y.first;
+                     });
+    for (auto& e : off) sym[r].push_back(e.second);
+  }
 }
 
 void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
@@ -962,7 +1149,17 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   };
   ctx->ntiles = (int)((N + RT - 1) / RT);
   ctx->npad = ctx->ntiles * RT;
-  ctx->chunk = chunk_of(N);
+  if (o.algorithm < HAWKES_ALGO_AUTO || o.algorithm > HAWKES_ALGO_PAIRS) {
+    delete ctx;
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad algorithm");
+  }
+  if (o.algorithm == HAWKES_ALGO_PAIRS && o.precision == HAWKES_FP32) {
+    delete ctx;
+    return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_ALGO_PAIRS is fp64-only in this version");
+  }
+  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS ||
+               (o.algorithm == HAWKES_ALGO_AUTO && o.precision == HAWKES_FP64);
+  ctx->chunk = ctx->pairs ? chunk_pairs_of(N) : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
   ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);
   if (o.world > 1)
@@ -970,8 +1167,12 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   else
     for (int r = 0; r < ctx->W; ++r) ctx->my_ranks.push_back(r);
 
-  std::vector<std::vector<int2>> it1, it2;
-  build_plan(ctx, it1, it2);
+  std::vector<std::vector<int2>> it1, it2, sym;
+  std::vector<int> own;
+  if (ctx->pairs)
+    build_plan_pairs(ctx, it1, it2, sym, own);
+  else
+    build_plan(ctx, it1, it2);
 
   const int REC = REC_of(D);
   int rc;
@@ -984,7 +1185,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->rates, (size_t)ctx->npad * 4)) ||
       (rc = dalloc(ctx, &ctx->grad, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
-      (rc = dalloc(ctx, &ctx->counters, (size_t)2 * ctx->W)) ||
+      (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W)) ||
       (rc = dalloc(ctx, &ctx->tab, 32)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
       (rc = dalloc(ctx, &ctx->st, 1)))
     return fail(rc);
@@ -993,7 +1194,31 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     if (cudaMemset(ctx->rec32, 0, (size_t)ctx->npad * Layout32Rec(D) * sizeof(float)) != cudaSuccess)
       return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   }
-  if (ctx->W > 1) {
+  if (ctx->pairs) {
+    std::vector<int> every(ctx->ntiles);
+    for (int k = 0; k < ctx->ntiles; ++k) every[k] = k;
+    if ((rc = dalloc(ctx, &ctx->d_every_tile, every.size())) ||
+        (rc = dalloc(ctx, &ctx->d_own, own.size())))
+      return fail(rc);
+    if (cudaMemcpy(ctx->d_every_tile, every.data(), every.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->d_own, own.data(), own.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair plan failed"));
+    ctx->d_sym.assign(ctx->W, nullptr);
+    ctx->n_sym.assign(ctx->W, 0);
+    for (int r = 0; r < ctx->W; ++r) {
+      ctx->n_sym[r] = (int)sym[r].size();
+      if ((rc = dalloc(ctx, &ctx->d_sym[r], sym[r].size()))) return fail(rc);
+      if (!sym[r].empty() &&
+          cudaMemcpy(ctx->d_sym[r], sym[r].data(), sym[r].size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair items failed"));
+    }
+    if (ctx->W > 1) {
+      const size_t copies = o.world > 1 ? 1 : (size_t)ctx->W + 1;
+      if ((rc = dalloc(ctx, &ctx->sums1, copies * ctx->npad * K1_of(D))) ||
+          (rc = dalloc(ctx, &ctx->sums2, copies * ctx->npad * K2_of(D))))
+        return fail(rc);
+    }
+  } else if (ctx->W > 1) {
     const size_t per_rank = (size_t)ctx->max_tiles * RT * std::max(4, D);
     if ((rc = dalloc(ctx, &ctx->sendbuf, per_rank)) ||
         (rc = dalloc(ctx, &ctx->recvbuf, per_rank * ctx->W)))
@@ -1006,6 +1231,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   // tile lists / items
   {
     std::vector<int> all((size_t)ctx->W * std::max(1, ctx->max_tiles), -1);
+    if (all.empty()) all.push_back(-1);
     for (int r = 0; r < ctx->W; ++r)
       for (size_t k = 0; k < ctx->tiles_of[r].size(); ++k) all[(size_t)r * ctx->max_tiles + k] = ctx->tiles_of[r][k];
     if ((rc = dalloc(ctx, &ctx->d_all_tiles, all.size()))) return fail(rc);
@@ -1067,11 +1293,12 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   void* bufs[] = {ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
-                  ctx->lf_lo, ctx->lf_hi};
+                  ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto* p : ctx->d_items1) if (p) cudaFree(p);
   for (auto* p : ctx->d_items2) if (p) cudaFree(p);
+  for (auto* p : ctx->d_sym) if (p) cudaFree(p);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   for (auto& pr : ctx->ev_rate) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto& pr : ctx->ev_grad) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -1178,7 +1405,7 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
     return set_err(ctx, HAWKES_ERR_ARG, "bad mem");
   TRY(check_ready(ctx));
   TRY(run_rates(ctx));
-  if (!ctx->rates_exchanged) {
+  if (!ctx->rates_exchanged && !ctx->pairs) {
     TRY(exchange_rows(ctx, ctx->rates, 4));
     ctx->rates_exchanged = true;
   }
@@ -1293,6 +1520,28 @@ int hawkes_plan(int64_t N, int32_t world, int32_t rank, int32_t* tiles_out, int3
   *n_tiles = cnt;
   if (rows_per_tile) *rows_per_tile = RT;
   if (chunk) *chunk = chunk_of(N);
+  return HAWKES_OK;
+}
+
+int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out,
+                      int32_t* n_items, int32_t* chunk) {
+  if (N < 1 || N > (1LL << 30) || world < 1 || rank < 0 || rank >= world || !n_items)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan_pairs");
+  const int ck = chunk_pairs_of(N);
+  const int C = (int)((N + ck - 1) / ck);
+  const std::vector<int> own = pair_owners(N, ck, world);
+  int cnt = 0;
+  for (int a = 0; a < C; ++a)
+    for (int b = a; b < C; ++b)
+      if (own[(size_t)a * C + b] == rank) {
+        if (items_out) {
+          items_out[2 * cnt] = a;
+          items_out[2 * cnt + 1] = b;
+        }
+        ++cnt;
+      }
+  *n_items = cnt;
+  if (chunk) *chunk = ck;
   return HAWKES_OK;
 }
 

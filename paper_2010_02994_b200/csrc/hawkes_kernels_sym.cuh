@@ -1,0 +1,327 @@
+// hawkes_kernels_sym.cuh -- unordered-pair ("symmetric") pass kernels, fp64 (sm_100a).
+//
+// SURVEY.md §8(f) NEXT-1.  mu_ij = mu_ji, and for t_i < t_j only xi_ji is non-zero
+// (P:L98-99), so one evaluation of the two exps of an unordered pair {i, j} (i earlier)
+// serves both events:
+//   pass 1  row i: M += mu'                 G1_i += mu' dx            (xi_ij = 0)
+//           col j: M += mu', X += xi'       G1_j -= (mu' + xi') dx
+//   pass 2  row i: G2_i += rho'_j (mu' + xi') dx
+//           col j: G2_j -= rho'_i mu' dx
+// with dx = x_j - x_i and the scaled-domain terms of hawkes_kernels.cuh (mu' = alpha mu 2^64,
+// xi' = beta xi_ji 2^64).  Work items are chunk pairs (a, b), a < b (every event of chunk a
+// precedes every event of chunk b in the time-sorted catalog); pairs inside one chunk go
+// through the ordered kernel (pass_kernel).  An item writes the row partial of chunk a's
+// events into slot b and the column partial of chunk b's events into slot a of the same
+// [chunks][Npad][K] partial array the ordered kernel uses, so every (slot, event) is
+// written exactly once and the fixed-order finalize is unchanged.
+//
+// Mapping: a CTA (4 warps) holds a row tile of 32*R events (lane l owns rows l + 32r, all
+// four warps hold the same rows) and streams column tiles of 128 events via TMA; warp w
+// takes columns [32w, 32w+32) of each tile.  Lane l loads column l of its group, then in
+// step s = 0..31 pairs its R rows with column (l + s) mod 32, obtained by warp shuffle,
+// while the column's accumulators rotate one lane down per step: after 32 steps every
+// row has met every column and lane l again holds column l's sums.  Row sums stay in
+// registers across the column tiles and are reduced over the 4 warps in a fixed order.
+#pragma once
+#include "hawkes_kernels.cuh"
+
+namespace hk {
+
+constexpr int SYM_R = 4;                  // rows per lane
+constexpr int SYM_RT = 32 * SYM_R;        // rows per row tile
+
+struct SymArgs {
+  const double* rec;
+  const int* gid;
+  const int2* items;     // (a, b) chunk pairs, a < b
+  int* counter;
+  double* part;          // [chunks][Npad][K]
+  const int2* tab;
+  long long npad;
+  int N;
+  int n_items;
+  int chunk;
+  PassConst c;
+};
+
+template <int D>
+struct SymRow {
+  double x[D];
+  double t;
+  double rho;
+  int g;
+};
+
+// one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
+template <int D, bool MASK>
+__device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
+                                          bool dead, double& rM, double (&rG)[D], double& cM,
+                                          double& cX, double (&cG)[D], const PassConst& c,
+                                          const int2* __restrict__ tab) {
+  double dx[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) dx[d] = cx[d] - row.x[d];
+  double r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
+  const double dt = ct - row.t;   // >= 0: the column is the later event
+  double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
+  double es = fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab);
+  if (MASK) {
+    eb = dead ? 0.0 : eb;
+    es = dead ? 0.0 : es;
+  }
+  rM += eb;
+  cM += eb;
+  cX += es;
+  const double cc = eb + es;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    rG[d] = fma(eb, dx[d], rG[d]);
+    cG[d] = fma(-cc, dx[d], cG[d]);
+  }
+}
+
+template <int D, bool MASK>
+__device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
+                                          double crho, bool dead, double (&rG)[D],
+                                          double (&cG)[D], const PassConst& c,
+                                          const int2* __restrict__ tab) {
+  double dx[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) dx[d] = cx[d] - row.x[d];
+  double r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
+  const double dt = ct - row.t;
+  double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
+  double es = fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab);
+  if (MASK) {
+    eb = dead ? 0.0 : eb;
+    es = dead ? 0.0 : es;
+  }
+  const double cr = crho * (eb + es);
+  const double cc = row.rho * eb;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    rG[d] = fma(cr, dx[d], rG[d]);
+    cG[d] = fma(-cc, dx[d], cG[d]);
+  }
+}
+
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
+template <int D, int PASS, bool MASK>
+__device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double (&cx0)[D],
+                                          double ct0, double crho0, int cg0, bool cvalid0,
+                                          double (&rM)[SYM_R], double (&rG)[SYM_R][D],
+                                          double (&cacc)[2 + D], const PassConst& c,
+                                          const int2* __restrict__ tab) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int s = 0; s < 32; ++s) {
+    const int src = (lane + s) & 31;
+    double cx[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cx[d] = shfl(cx0[d], src);
+    const double ct = shfl(ct0, src);
+    double crho = 0.0;
+    if (PASS == 2) crho = shfl(crho0, src);
+    int cg = 0;
+    bool cv = true;
+    if (MASK) {
+      cg = __shfl_sync(0xffffffffu, cg0, src);
+      cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
+    }
+    if (PASS == 1) {
+      double cG[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
+#pragma unroll
+      for (int r = 0; r < SYM_R; ++r)
+        sym_pair1<D, MASK>(row[r], cx, ct, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
+                           cacc[1], cG, c, tab);
+#pragma unroll
+      for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
+    } else {
+      double cG[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
+#pragma unroll
+      for (int r = 0; r < SYM_R; ++r)
+        sym_pair2<D, MASK>(row[r], cx, ct, crho, MASK && (!cv || cg == row[r].g), rG[r], cG, c, tab);
+#pragma unroll
+      for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
+    }
+    // rotate the column sums one lane down: lane l now holds column (l + s + 1) mod 32
+    const int nxt = (lane + 1) & 31;
+    if (PASS == 1) {
+      cacc[0] = shfl(cacc[0], nxt);
+      cacc[1] = shfl(cacc[1], nxt);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) cacc[2 + d] = shfl(cacc[2 + d], nxt);
+  }
+}
+
+template <int D, int PASS>
+__global__ void __launch_bounds__(THREADS, 3) sym_kernel(SymArgs a) {
+  using L = Layout<D>;
+  constexpr int REC = L::REC;
+  constexpr int K = PASS == 1 ? L::K1 : L::K2;
+  constexpr int KR = PASS == 1 ? 1 + D : D;   // row sums reduced over warps: (M, G) or G
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage = reinterpret_cast<double*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(double));
+  int2* tab = reinterpret_cast<int2*>(bars + STAGES);
+  double* red = reinterpret_cast<double*>(tab + 32);   // [4 warps][SYM_RT][KR]
+  __shared__ int s_item;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 32) tab[tid] = a.tab[tid];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  const PassConst c = a.c;
+  const int N = a.N;
+
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= a.n_items) break;
+    const int2 w = a.items[it];
+    const int r0 = w.x * a.chunk;                 // chunk a: rows (always a full chunk)
+    const int c0 = w.y * a.chunk;                 // chunk b: columns (may be ragged)
+    const int c1 = min(N, c0 + a.chunk);
+    const int n_rt = a.chunk / SYM_RT;
+    const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
+    const int total = n_rt * n_ct;                // tiles streamed: (row tile, col tile)
+
+    if (tid == 0) {
+      for (int s = 0; s < STAGES && s < total; ++s) {
+        const int jt = c0 + (s % n_ct) * TILE_J;
+        const int cnt = min(TILE_J, c1 - jt);
+        tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
+                    (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
+      }
+    }
+
+    int k = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      const int row0 = r0 + rt * SYM_RT;
+      SymRow<D> row[SYM_R];
+      double rM[SYM_R], rG[SYM_R][D];
+#pragma unroll
+      for (int r = 0; r < SYM_R; ++r) {
+        const int i = row0 + lane + 32 * r;
+        const double* ri = a.rec + (long long)i * REC;
+#pragma unroll
+        for (int d = 0; d < D; ++d) row[r].x[d] = ri[d];
+        row[r].t = ri[D];
+        row[r].rho = ri[D + 1];
+        row[r].g = a.gid[i];
+        rM[r] = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
+      }
+      const int g_rlast = a.gid[row0 + SYM_RT - 1];
+
+      for (int ct = 0; ct < n_ct; ++ct, ++k) {
+        const int s = k % STAGES;
+        const int jt = c0 + ct * TILE_J;
+        const int cnt = min(TILE_J, c1 - jt);
+        mbar_wait(&bars[s], (parity >> s) & 1u);
+        parity ^= (1u << s);
+        const double* st = stage + s * TILE_J * REC;
+        // this lane's column in its warp's group
+        const int cl = warp * 32 + lane;
+        const bool cvalid = cl < cnt;
+        const int cj = jt + min(cl, cnt - 1);
+        double cx[D];
+        const double* rc = st + min(cl, cnt - 1) * REC;
+#pragma unroll
+        for (int d = 0; d < D; ++d) cx[d] = rc[d];
+        const double ctm = rc[D];
+        const double crho = rc[D + 1];
+        const int cg = a.gid[cj];
+        // column sums: slot a of the partial array, accumulated over this item's row tiles
+        double* cpart = a.part + ((long long)w.x * a.npad + cj) * K;
+        double cacc[2 + D];
+        if (rt == 0 || !cvalid) {
+#pragma unroll
+          for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.0;
+        } else if (PASS == 1) {
+#pragma unroll
+          for (int q = 0; q < 2 + D; ++q) cacc[q] = cpart[q];
+        } else {
+          cacc[0] = cacc[1] = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) cacc[2 + d] = cpart[d];
+        }
+        const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
+        if (strict)
+          sym_group<D, PASS, false>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+        else
+          sym_group<D, PASS, true>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+        if (cvalid) {
+          if (PASS == 1) {
+#pragma unroll
+            for (int q = 0; q < 2 + D; ++q) cpart[q] = cacc[q];
+          } else {
+#pragma unroll
+            for (int d = 0; d < D; ++d) cpart[d] = cacc[2 + d];
+          }
+        }
+        __syncthreads();   // stage s fully consumed
+        if (tid == 0 && k + STAGES < total) {
+          const int kn = k + STAGES;
+          const int jn = c0 + (kn % n_ct) * TILE_J;
+          const int cn = min(TILE_J, c1 - jn);
+          tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
+                      (uint32_t)(cn * REC * sizeof(double)), &bars[s]);
+        }
+      }
+      // row sums of this row tile: reduce the 4 warps' partials in a fixed order
+#pragma unroll
+      for (int r = 0; r < SYM_R; ++r) {
+        double* o = red + ((long long)warp * SYM_RT + lane + 32 * r) * KR;
+        if (PASS == 1) {
+          o[0] = rM[r];
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[1 + d] = rG[r][d];
+        } else {
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[d] = rG[r][d];
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < SYM_RT * KR; q += THREADS) {
+        const int rr = q / KR, kk = q % KR;
+        double v = red[(0 * SYM_RT + rr) * KR + kk];
+        v += red[(1 * SYM_RT + rr) * KR + kk];
+        v += red[(2 * SYM_RT + rr) * KR + kk];
+        v += red[(3 * SYM_RT + rr) * KR + kk];
+        double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;   // slot b
+        if (PASS == 1) {
+          if (kk == 0) {
+            o[0] = v;      // M
+            o[1] = 0.0;    // X: xi_ij = 0 for a later j
+          } else {
+            o[1 + kk] = v; // G
+          }
+        } else {
+          o[kk] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace hk

@@ -49,7 +49,8 @@ class HawkesContext:
 
     def __init__(self, N: int, D: int, device: int = 0, stream: Optional[torch.cuda.Stream] = None,
                  precision: str = "fp64", rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None, emulate_world: int = 0):
+                 nccl_id: Optional[bytes] = None, emulate_world: int = 0,
+                 algorithm: str = "auto"):
         self._lib = _lib.load()
         self.N, self.D, self.device = int(N), int(D), int(device)
         if stream is None:
@@ -66,6 +67,8 @@ class HawkesContext:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p)
         o.emulate_world = int(emulate_world)
+        o.algorithm = _lib.ALGORITHMS[algorithm]
+        self.algorithm = algorithm
         h = ctypes.c_void_p()
         check(self._lib.hawkes_create(self.N, self.D, ctypes.byref(o), ctypes.byref(h)))
         self._h = h

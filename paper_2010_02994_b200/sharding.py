@@ -27,6 +27,16 @@ def plan(N: int, world: int, rank: int) -> Tuple[List[int], int, int]:
     return list(buf[: n.value]), rt.value, ck.value
 
 
+def plan_pairs(N: int, world: int, rank: int) -> Tuple[List[Tuple[int, int]], int]:
+    """hawkes_plan_pairs: (chunk pairs (a, b), a <= b, of `rank`; chunk length)."""
+    lib = _lib.load()
+    n, ck = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.hawkes_plan_pairs(N, world, rank, None, ctypes.byref(n), ctypes.byref(ck)))
+    buf = (ctypes.c_int32 * max(2, 2 * n.value))()
+    _lib.check(lib.hawkes_plan_pairs(N, world, rank, buf, ctypes.byref(n), None))
+    return [(buf[2 * k], buf[2 * k + 1]) for k in range(n.value)], ck.value
+
+
 def rows_of(N: int, world: int, rank: int) -> List[int]:
     tiles, rt, _ = plan(N, world, rank)
     return [i for k in tiles for i in range(k * rt, min(N, (k + 1) * rt))]
@@ -44,12 +54,14 @@ def broadcast_unique_id(group=None) -> bytes:
     return bytes(buf.cpu().tolist())
 
 
-def init_distributed_context(N: int, D: int, precision: str = "fp64", group=None) -> HawkesContext:
+def init_distributed_context(N: int, D: int, precision: str = "fp64", group=None,
+                             algorithm: str = "auto") -> HawkesContext:
     """hawkes_create on every rank of an initialised process group (world > 1 shards rows)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = torch.cuda.current_device()
     if world == 1:
-        return HawkesContext(N, D, device=dev, precision=precision)
+        return HawkesContext(N, D, device=dev, precision=precision, algorithm=algorithm)
     uid = broadcast_unique_id(group)
-    return HawkesContext(N, D, device=dev, precision=precision, rank=rank, world=world, nccl_id=uid)
+    return HawkesContext(N, D, device=dev, precision=precision, rank=rank, world=world, nccl_id=uid,
+                         algorithm=algorithm)

@@ -22,7 +22,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(lib, s)]
     assert not missing, missing
     assert set(declared) == set(_lib.EXPORTS)
-    assert lib.hawkes_abi_version() == 1
+    assert lib.hawkes_abi_version() == 2
 
 
 def test_library_is_sm100a():
@@ -83,3 +83,32 @@ def test_nccl_unique_id_is_fresh():
     from paper_2010_02994_b200 import nccl_unique_id
     a, b = nccl_unique_id(), nccl_unique_id()
     assert len(a) == 128 and a != b
+
+
+@pytest.mark.parametrize("N", [1, 300, 5000, 100_000, 1_000_000])
+@pytest.mark.parametrize("W", [1, 2, 3, 8])
+def test_pair_plan_covers_every_pair_once(N, W):
+    """HAWKES_ALGO_PAIRS: the chunk pairs (a <= b) of all ranks cover each unordered chunk
+    pair exactly once, and the LPT deal balances pair counts within a few percent."""
+    from paper_2010_02994_b200 import sharding
+    seen = set()
+    loads = []
+    chunk = None
+    for r in range(W):
+        items, ck = sharding.plan_pairs(N, W, r)
+        chunk = ck if chunk is None else chunk
+        assert ck == chunk
+        load = 0
+        for a, b in items:
+            assert a <= b and (a, b) not in seen
+            seen.add((a, b))
+            na = min(ck, N - a * ck)
+            nb = min(ck, N - b * ck)
+            load += na * na if a == b else 2 * na * nb
+        loads.append(load)
+    C = (N + chunk - 1) // chunk
+    assert seen == {(a, b) for a in range(C) for b in range(a, C)}
+    assert sum(loads) == N * N
+    assert chunk % 256 == 0
+    if N >= 100_000:
+        assert max(loads) / (sum(loads) / W) < 1.03

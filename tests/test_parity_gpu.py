@@ -41,7 +41,7 @@ def test_c1_unit_square_seeds(rep):
     _check(synth.config("C1", replicate=rep), f"C1 rep {rep}")
 
 
-@pytest.mark.parametrize("N", [2, 3, 127, 128, 255, 256, 257, 511, 513, 1003, 4097])
+@pytest.mark.parametrize("N", [2, 3, 127, 128, 255, 256, 257, 511, 513, 1003, 4097, 35_584, 35_841])
 def test_ragged_sizes(N):
     """Tile edges: row tiles of 256, j tiles of 128, chunks >= 512."""
     _check(synth.unit_square(N, config=21, replicate=N), f"N={N}")
@@ -136,20 +136,49 @@ def test_abi_errors():
 
 
 def test_bitwise_determinism_and_emulated_world():
-    """Repeat runs and W = 2, 3, 8 logical row shards give bit-identical ell, lambda, g
-    (per-row summation order does not depend on W)."""
+    """ROWS: repeat runs and W = 2, 3, 8 logical row shards give bit-identical ell, lambda, g
+    (per-row summation order does not depend on W).  PAIRS: repeat runs
+    are bit-identical; W logical shards (allreduce of per-event sums) agree to rounding."""
     c = synth.unit_square(3000, config=24)
-    ell1, g1, r1 = gpu_eval(c.x, c.t, c.theta)
-    ell1b, g1b, r1b = gpu_eval(c.x, c.t, c.theta)
+    ell_ref, lam_ref, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    ell1, g1, r1 = gpu_eval(c.x, c.t, c.theta, algorithm="rows")
+    ell1b, g1b, r1b = gpu_eval(c.x, c.t, c.theta, algorithm="rows")
     assert ell1 == ell1b and np.array_equal(g1, g1b) and np.array_equal(r1["lambda"], r1b["lambda"])
     for W in (2, 3, 8):
-        ellw, gw, rw = gpu_eval(c.x, c.t, c.theta, emulate_world=W)
+        ellw, gw, rw = gpu_eval(c.x, c.t, c.theta, emulate_world=W, algorithm="rows")
         assert ellw == ell1, W
         assert np.array_equal(gw, g1), W
         for k in ("lambda", "mu", "xi", "Lambda"):
             assert np.array_equal(rw[k], r1[k]), (W, k)
-    ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
-    assert_parity(ell1, g1, ell_ref, g_ref, S, what="W-sweep reference")
+    assert_parity(ell1, g1, ell_ref, g_ref, S, what="ROWS W-sweep reference")
+    ep, gp, rp = gpu_eval(c.x, c.t, c.theta, algorithm="pairs")
+    ep2, gp2, rp2 = gpu_eval(c.x, c.t, c.theta, algorithm="pairs")
+    assert ep == ep2 and np.array_equal(gp, gp2) and np.array_equal(rp["lambda"], rp2["lambda"])
+    assert_parity(ep, gp, ell_ref, g_ref, S, what="PAIRS")
+    for W in (2, 3, 8):
+        ew, gw, rw = gpu_eval(c.x, c.t, c.theta, emulate_world=W, algorithm="pairs")
+        assert abs(ew - ep) <= 1e-13 * abs(ep), W
+        assert np.all(np.abs(gw - gp) <= 1e-13 * (np.abs(gp) + S)), W
+        np.testing.assert_allclose(rw["lambda"], rp["lambda"], rtol=1e-14)
+        assert_parity(ew, gw, ell_ref, g_ref, S, what=f"PAIRS W={W}")
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_rows_algorithm_configs(name):
+    """The ordered-pair (ROWS) decomposition on the small configs."""
+    c = synth.config(name)
+    ell, g, rates = gpu_eval(c.x, c.t, c.theta, algorithm="rows")
+    ell_ref, lam_ref, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    np.testing.assert_allclose(rates["lambda"], lam_ref, rtol=1e-11)
+    assert_parity(ell, g, ell_ref, g_ref, S, what=f"ROWS {name}")
+
+
+@pytest.mark.parametrize("N", [257, 1003, 5000])
+def test_rows_algorithm_ragged_and_ties(N):
+    for c in (synth.unit_square(N, config=28, replicate=N), synth.with_ties(N, max(2, N // 7))):
+        ell, g, _ = gpu_eval(c.x, c.t, c.theta, algorithm="rows")
+        ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+        assert_parity(ell, g, ell_ref, g_ref, S, what=f"ROWS {c.name}")
 
 
 def test_full_size_c4_sampled_rows_and_properties():
