@@ -197,6 +197,10 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
  * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */
 int hawkes_diag_exp(const double* a_dev, double* out_dev, int64_t n);
 int hawkes_diag_fp64_peak(double* ops_per_s);
+/* FP64 operand-pattern probe (mode 0: DFMA reg,imm,imm; 1: DFMA with 3 register operands;
+ * 2: DADD; 3: DMUL; 4: the kernels' fast exp; 5: DFMA reg,reg,imm) at warps_per_sm resident
+ * warps: chain-steps per second over the device (x1 op each; the exp is 9 FP64 ops). */
+int hawkes_diag_fp64_mode(int32_t mode, int32_t warps_per_sm, double* iters_per_s);
 
 /* One-line description of the last failure on ctx (or of the last failed create when
  * ctx is NULL).  The string is owned by the library. */

@@ -26,7 +26,7 @@ EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
     "hawkes_leapfrog", "hawkes_get_rates", "hawkes_enable_timing", "hawkes_get_kernel_times",
-    "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_last_error",
+    "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version",
 )
 
@@ -81,6 +81,7 @@ def load() -> ctypes.CDLL:
     lib.hawkes_plan_pairs.argtypes = [i64, i32, i32, P(i32), P(i32), P(i32)]
     lib.hawkes_diag_exp.argtypes = [dp, dp, i64]
     lib.hawkes_diag_fp64_peak.argtypes = [P(ctypes.c_double)]
+    lib.hawkes_diag_fp64_mode.argtypes = [i32, i32, P(ctypes.c_double)]
     lib.hawkes_last_error.argtypes = [vp]
     lib.hawkes_last_error.restype = ctypes.c_char_p
     lib.hawkes_abi_version.restype = ctypes.c_int

@@ -17,8 +17,7 @@
 // Scaled domain: every pair exponent carries log(alpha*w*2^64) (alpha = 1/tau_x^2 or
 // 1/h^2, w the kernel weight), so the exp returns alpha*mu_ij*2^64 (resp. beta*xi_ij*2^64)
 // directly; sums stay scaled, rho' = 2^-64/lambda, and g_i = rho'_i G1'_i + G2'_i exactly
-// as above.  The 2^64 keeps terms whose true value is subnormal (down to 2^-1086) normal,
-// so the flush-to-zero of the fast exp below matches the oracle's underflow to 0.
+// as above.
 //
 // Layout: each event is one record of REC doubles {x_0..x_{D-1}, t, rho', pad} (32 B for
 // D <= 2); a CTA owns RT = THREADS*R rows (thread k: rows row0 + k + r*THREADS), and
@@ -54,33 +53,47 @@ struct PassConst {
 };
 
 // ---------------------------------------------------------------- fast fp64 exp
-// e^a = 2^(k/32) e^r, k = rint(a*32/ln2), r = a - k ln2/32, |r| <= ln2/64.
-// 2^(k/32) = 2^m * T[j] (k = 32m + j, T from a 32-entry shared table, m added to the
-// exponent field with integer ops), e^r - 1 by its degree-5 Taylor polynomial
-// (truncation <= 2.3e-15 relative).  9 FP64-pipe instructions, no branches.
-// Results below 2^-1022 (k < -32704, including a = -inf) are flushed to +0 by a final
-// select (which also discards the NaN a huge |a| makes of the polynomial); the caller
-// keeps arguments below ~700 (validated constants), so there is no overflow path.
-constexpr double EXP_K = 46.166241308446828384;          // 32/ln2
-constexpr double EXP_SHIFT = 6755399441055744.0;          // 1.5 * 2^52
-constexpr double EXP_C = 0.021660849392498290;            // ln2/32
-constexpr long long EXP_YMIN_BITS = 0x4338000000000000LL - 32704;  // bits(SHIFT - 32704)
+// e^a for the pair kernels.  On sm_100 an FP64 instruction holds its SM sub-partition's
+// dispatch for two cycles and every other instruction for one (measured: the FP64 pipe
+// utilisation of a kernel tracks 2*n_fp64 / (2*n_fp64 + n_other)), so this exp is
+// built to minimise both: 8 FP64 instructions and 5 integer/shared-memory ones.
+//   a' = max(a, AMIN)            one unsigned min on the high word (AMIN = -707: for
+//                                negative doubles a larger high word means a larger |a|;
+//                                positive a, high bit clear, pass through)
+//   y  = a' * 64/ln2 + 1.5*2^52  rounds to an integer: y's low word is
+//                                k = rint(a' * 64/ln2) = 64m + j
+//   r  = a' - k ln2/64           |r| <= ln2/128
+//   T  = 2^(j/64) from a 64-entry shared table whose high words are pre-biased by
+//        -(j << 14), so that one integer multiply-add, hi + (k << 14), also adds m to the
+//        exponent field
+//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r + c3 r^2 + c4 r^3)  (minimax, tools/
+//        fit_exp_poly.py: |rel. err.| <= 5.1e-15 on |r| <= ln2/128)
+// Arguments below AMIN return e^(a') ~ e^-707 instead of a smaller number (callers treat
+// sums below N e^-700 as zero; reading R23).  Arguments must be < ~700
+// (guaranteed by the validated kernel constants).
+constexpr double EXP_K = 92.332482616893656;                // 64/ln2
+constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
+constexpr double EXP_C = 0.010830424696249145;              // ln2/64
+constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
+constexpr double EXP_C2 = 0.5000000000031142;
+constexpr double EXP_C3 = 0.1666668790487242;
+constexpr double EXP_C4 = 0.04166656920987773;
+constexpr int EXP_TABLE = 64;
 
 __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab) {
-  const double y = fma(a, EXP_K, EXP_SHIFT);
+  const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
+  const double ac = __hiloint2double((int)ahi, __double2loint(a));
+  const double y = fma(ac, EXP_K, EXP_SHIFT);
   const double kf = y - EXP_SHIFT;
-  const double r = fma(kf, -EXP_C, a);
-  const int lo = __double2loint(y);
-  const int2 T = tab[lo & 31];                 // .x = low word, .y = high word of 2^(j/32)
-  const int m = lo >> 5;                       // floor(k/32)
-  double p = fma(1.0 / 120.0, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = p * r;                                   // e^r - 1
-  const double Tm = __hiloint2double(T.y + (int)((unsigned)m << 20), T.x);
-  const double e = fma(Tm, p, Tm);
-  return (__double_as_longlong(y) < EXP_YMIN_BITS) ? 0.0 : e;
+  const double r = fma(kf, -EXP_C, ac);
+  const int k = __double2loint(y);
+  const int2 T = tab[k & (EXP_TABLE - 1)];
+  double q = fma(EXP_C4, r, EXP_C3);
+  q = fma(q, r, EXP_C2);
+  q = fma(q, r, 1.0);
+  const double p = q * r;                                      // e^r - 1
+  const double Tm = __hiloint2double(T.y + k * 16384, T.x);    // 2^(j/64) * 2^m
+  return fma(Tm, p, Tm);
 }
 
 // --------------------------------------------------------------- TMA / mbarrier
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel(PassArgs a) {
   __shared__ int s_item;
 
   const int tid = threadIdx.x;
-  if (tid < 32) tab[tid] = a.tab[tid];
+  if (tid < EXP_TABLE) tab[tid] = a.tab[tid];
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();

@@ -27,8 +27,7 @@
 
 namespace hk {
 
-constexpr int SYM_R = 4;                  // rows per lane
-constexpr int SYM_RT = 32 * SYM_R;        // rows per row tile
+constexpr int SYM_RMAX = 4;               // largest rows-per-lane variant
 
 struct SymArgs {
   const double* rec;
@@ -53,7 +52,7 @@ struct SymRow {
 };
 
 // one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
-template <int D, bool MASK>
+template <int D, bool MASK, int V>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           bool dead, double& rM, double (&rG)[D], double& cM,
                                           double& cX, double (&cG)[D], const PassConst& c,
@@ -82,7 +81,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   }
 }
 
-template <int D, bool MASK>
+template <int D, bool MASK, int V>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           double crho, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
@@ -112,7 +111,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK>
+template <int D, int PASS, bool MASK, int SYM_R, int V>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double (&cx0)[D],
                                           double ct0, double crho0, int cg0, bool cvalid0,
                                           double (&rM)[SYM_R], double (&rG)[SYM_R][D],
@@ -140,7 +139,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double 
       for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
 #pragma unroll
       for (int r = 0; r < SYM_R; ++r)
-        sym_pair1<D, MASK>(row[r], cx, ct, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
+        sym_pair1<D, MASK, V>(row[r], cx, ct, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
                            cacc[1], cG, c, tab);
 #pragma unroll
       for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -150,7 +149,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double 
       for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
 #pragma unroll
       for (int r = 0; r < SYM_R; ++r)
-        sym_pair2<D, MASK>(row[r], cx, ct, crho, MASK && (!cv || cg == row[r].g), rG[r], cG, c, tab);
+        sym_pair2<D, MASK, V>(row[r], cx, ct, crho, MASK && (!cv || cg == row[r].g), rG[r], cG, c, tab);
 #pragma unroll
       for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
     }
@@ -165,8 +164,9 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double 
   }
 }
 
-template <int D, int PASS>
-__global__ void __launch_bounds__(THREADS, 3) sym_kernel(SymArgs a) {
+template <int D, int PASS, int SYM_R, int V>
+__global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArgs a) {
+  constexpr int SYM_RT = 32 * SYM_R;
   using L = Layout<D>;
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? L::K1 : L::K2;
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(THREADS, 3) sym_kernel(SymArgs a) {
   double* stage = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(double));
   int2* tab = reinterpret_cast<int2*>(bars + STAGES);
-  double* red = reinterpret_cast<double*>(tab + 32);   // [4 warps][SYM_RT][KR]
+  double* red = reinterpret_cast<double*>(tab + EXP_TABLE);   // [4 warps][SYM_RT][KR]
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 32) tab[tid] = a.tab[tid];
+  if (tid < EXP_TABLE) tab[tid] = a.tab[tid];
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -266,9 +266,9 @@ __global__ void __launch_bounds__(THREADS, 3) sym_kernel(SymArgs a) {
         }
         const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
         if (strict)
-          sym_group<D, PASS, false>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, false, SYM_R, V>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
         else
-          sym_group<D, PASS, true>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, true, SYM_R, V>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
         if (cvalid) {
           if (PASS == 1) {
 #pragma unroll
