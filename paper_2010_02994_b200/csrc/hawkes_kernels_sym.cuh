@@ -112,21 +112,24 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
 template <int D, int PASS, bool MASK, int SYM_R, int V>
-__device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R], double (&cx0)[D],
-                                          double ct0, double crho0, int cg0, bool cvalid0,
+__device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
+                                          const double* __restrict__ grp, int cg0, bool cvalid0,
                                           double (&rM)[SYM_R], double (&rG)[SYM_R][D],
                                           double (&cacc)[2 + D], const PassConst& c,
                                           const int2* __restrict__ tab) {
+  constexpr int REC = Layout<D>::REC;
   const int lane = threadIdx.x & 31;
 #pragma unroll 1
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
+    // column (l + s) mod 32 of this warp's group, straight from the staged tile
+    const double* rc = grp + src * REC;
     double cx[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) cx[d] = shfl(cx0[d], src);
-    const double ct = shfl(ct0, src);
+    for (int d = 0; d < D; ++d) cx[d] = rc[d];
+    const double ct = rc[D];
     double crho = 0.0;
-    if (PASS == 2) crho = shfl(crho0, src);
+    if (PASS == 2) crho = rc[D + 1];
     int cg = 0;
     bool cv = true;
     if (MASK) {
@@ -239,16 +242,11 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
         mbar_wait(&bars[s], (parity >> s) & 1u);
         parity ^= (1u << s);
         const double* st = stage + s * TILE_J * REC;
-        // this lane's column in its warp's group
+        // this lane's column in its warp's group (padding columns of a ragged tile read
+        // stale stage data and are masked out)
         const int cl = warp * 32 + lane;
         const bool cvalid = cl < cnt;
         const int cj = jt + min(cl, cnt - 1);
-        double cx[D];
-        const double* rc = st + min(cl, cnt - 1) * REC;
-#pragma unroll
-        for (int d = 0; d < D; ++d) cx[d] = rc[d];
-        const double ctm = rc[D];
-        const double crho = rc[D + 1];
         const int cg = a.gid[cj];
         // column sums: slot a of the partial array, accumulated over this item's row tiles
         double* cpart = a.part + ((long long)w.x * a.npad + cj) * K;
@@ -266,9 +264,9 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
         }
         const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
         if (strict)
-          sym_group<D, PASS, false, SYM_R, V>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, false, SYM_R, V>(row, st + warp * 32 * REC, cg, cvalid, rM, rG, cacc, c, tab);
         else
-          sym_group<D, PASS, true, SYM_R, V>(row, cx, ctm, crho, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, true, SYM_R, V>(row, st + warp * 32 * REC, cg, cvalid, rM, rG, cacc, c, tab);
         if (cvalid) {
           if (PASS == 1) {
 #pragma unroll
