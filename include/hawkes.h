@@ -77,8 +77,8 @@ typedef enum { HAWKES_MEM_HOST = 0, HAWKES_MEM_DEVICE = 1 } hawkes_mem;
  *  PAIRS -- unordered pairs: chunk pairs (a < b) evaluate each pair's two exps once and
  *           feed both events (2 exps per ordered pair over both
  *           passes); W > 1 shards chunk pairs and allreduces per-event partial sums;
- *           results are deterministic for a fixed W.  fp64 only in this version.
- *  AUTO  -- PAIRS for fp64, ROWS for fp32. */
+ *           results are deterministic for a fixed W.
+ *  AUTO  -- PAIRS. */
 typedef enum { HAWKES_ALGO_AUTO = 0, HAWKES_ALGO_ROWS = 1, HAWKES_ALGO_PAIRS = 2 } hawkes_algorithm;
 
 typedef struct {

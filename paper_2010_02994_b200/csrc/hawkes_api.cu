@@ -640,6 +640,14 @@ int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
   return pass ? SymOps<D, 4, 0>::launch(ctx, pass, *b) : SymOps<D, 4, 0>::setup(ctx);
 }
 
+constexpr int SYM32_R = 4;
+template <int D, int PASS>
+size_t sym32_smem() {
+  const int KR = PASS == 1 ? 1 + D : D;
+  return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t) +
+         (size_t)4 * 32 * SYM32_R * KR * sizeof(double);
+}
+
 template <int D>
 size_t pass_smem32() {
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t);
@@ -659,6 +667,16 @@ struct SetupD {
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
       ctx->grid1 = std::max(1, b1) * ctx->sms;
       ctx->grid2 = std::max(1, b2) * ctx->sms;
+      if (ctx->pairs) {
+        auto s1 = sym_kernel_f32<D, 1, SYM32_R>;
+        auto s2 = sym_kernel_f32<D, 2, SYM32_R>;
+        CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1>()));
+        CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2>()));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1>()));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2>()));
+        ctx->grid_s1 = std::max(1, b1) * ctx->sms;
+        ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+      }
       return HAWKES_OK;
     }
     auto k1 = pass_kernel<D, 1, R_ROWS>;
@@ -766,14 +784,35 @@ struct PassD {
     a.chunk = ctx->chunk;
     a.c = ctx->pc32;
     if (a.n_items == 0) return HAWKES_OK;
-    const size_t sm = pass_smem32<D>();
-    const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
     record_start(ctx, pass == 1);
-    if (pass == 1)
-      pass_kernel_f32<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
-    else
-      pass_kernel_f32<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
-    CHECK_LAUNCH();
+    if (a.n_items > 0) {
+      const size_t sm = pass_smem32<D>();
+      const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
+      if (pass == 1)
+        pass_kernel_f32<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+      else
+        pass_kernel_f32<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
+      CHECK_LAUNCH();
+    }
+    if (ctx->pairs && ctx->n_sym[rank] > 0) {
+      SymArgs32 b;
+      b.rec = ctx->rec32;
+      b.gid = ctx->gid;
+      b.items = ctx->d_sym[rank];
+      b.counter = ctx->counters + 4 * rank + 2 + (pass - 1);
+      b.part = pass == 1 ? ctx->part1 : ctx->part2;
+      b.npad = ctx->npad;
+      b.N = (int)ctx->N;
+      b.n_items = ctx->n_sym[rank];
+      b.chunk = ctx->chunk;
+      b.c = ctx->pc32;
+      const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+      if (pass == 1)
+        sym_kernel_f32<D, 1, SYM32_R><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
+      else
+        sym_kernel_f32<D, 2, SYM32_R><<<grid, THREADS, sym32_smem<D, 2>(), ctx->stream>>>(b);
+      CHECK_LAUNCH();
+    }
     record_stop(ctx, pass == 1);
     return HAWKES_OK;
   }
@@ -1255,13 +1294,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     delete ctx;
     return set_err(nullptr, HAWKES_ERR_ARG, "bad algorithm");
   }
-  if (o.algorithm == HAWKES_ALGO_PAIRS && o.precision == HAWKES_FP32) {
-    delete ctx;
-    return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_ALGO_PAIRS is fp64-only in this version");
-  }
   if (const char* v = getenv("HAWKES_SYM_VARIANT")) ctx->sym_variant = atoi(v);
-  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS ||
-               (o.algorithm == HAWKES_ALGO_AUTO && o.precision == HAWKES_FP64);
+  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || o.algorithm == HAWKES_ALGO_AUTO;
   ctx->chunk = ctx->pairs ? chunk_pairs_of(N) : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
   ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);

@@ -271,3 +271,268 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel_f32(PassArgs32 a) {
 }
 
 }  // namespace hk
+
+// --------------------------------------------------------------------------------------
+// fp32 unordered-pair kernel: hawkes_kernels_sym.cuh's chunk-pair mapping (R rows per lane,
+// 32-step skewed column schedule, column sums rotating through warp shuffles) with the
+// fp32 pair arithmetic above.  Row sums are fp32 over one 128-column tile and promoted to
+// fp64 after it; column sums are fp32 over the 128 rows of a row tile and promoted when
+// they are added to the fp64 partial slot.
+#include "hawkes_kernels_sym.cuh"
+
+namespace hk {
+
+template <int D>
+struct SymRow32 {
+  float xh[D], xl[D];
+  float th, tl, rho;
+  int g;
+};
+
+template <int D, int PASS, bool MASK>
+__device__ __forceinline__ void sym32_pair(const SymRow32<D>& row, const float* __restrict__ rc,
+                                           bool dead, float& rM, float (&rG)[D], float& cM,
+                                           float& cX, float (&cG)[D], const PassConst32& c) {
+  using L = Layout32<D>;
+  float dx[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) dx[d] = (rc[L::XH + d] - row.xh[d]) + (rc[L::XL + d] - row.xl[d]);
+  float r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = fmaf(dx[d], dx[d], r2);
+  const float dt = (rc[L::TH] - row.th) + (rc[L::TL] - row.tl);   // >= 0
+  float eb = ex2f(fmaf(c.kx, r2, fmaf(c.kt * dt, dt, c.cb)));
+  float es = ex2f(fmaf(c.ks, r2, fmaf(-c.omega, dt, c.cs)));
+  if (MASK) {
+    eb = dead ? 0.f : eb;
+    es = dead ? 0.f : es;
+  }
+  if (PASS == 1) {
+    rM += eb;
+    cM += eb;
+    cX += es;
+    const float cc = eb + es;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      rG[d] = fmaf(eb, dx[d], rG[d]);
+      cG[d] = fmaf(-cc, dx[d], cG[d]);
+    }
+  } else {
+    const float cr = rc[L::RHO] * (eb + es);
+    const float cc = row.rho * eb;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      rG[d] = fmaf(cr, dx[d], rG[d]);
+      cG[d] = fmaf(-cc, dx[d], cG[d]);
+    }
+  }
+}
+
+template <int D, int PASS, bool MASK, int SR>
+__device__ __forceinline__ void sym32_group(const SymRow32<D> (&row)[SR],
+                                            const float* __restrict__ grp, int cg0, bool cvalid0,
+                                            float (&rM)[SR], float (&rG)[SR][D],
+                                            float (&cacc)[2 + D], const PassConst32& c) {
+  constexpr int REC = Layout32<D>::REC;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 2
+  for (int s = 0; s < 32; ++s) {
+    const int src = (lane + s) & 31;
+    const float* rc = grp + src * REC;
+    int cg = 0;
+    bool cv = true;
+    if (MASK) {
+      cg = __shfl_sync(0xffffffffu, cg0, src);
+      cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
+    }
+    float cG[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
+#pragma unroll
+    for (int r = 0; r < SR; ++r)
+      sym32_pair<D, PASS, MASK>(row[r], rc, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
+                                cacc[1], cG, c);
+#pragma unroll
+    for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
+    const int nxt = (lane + 1) & 31;
+    if (PASS == 1) {
+      cacc[0] = __shfl_sync(0xffffffffu, cacc[0], nxt);
+      cacc[1] = __shfl_sync(0xffffffffu, cacc[1], nxt);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) cacc[2 + d] = __shfl_sync(0xffffffffu, cacc[2 + d], nxt);
+  }
+}
+
+struct SymArgs32 {
+  const float* rec;
+  const int* gid;
+  const int2* items;
+  int* counter;
+  double* part;
+  long long npad;
+  int N;
+  int n_items;
+  int chunk;
+  PassConst32 c;
+};
+
+template <int D, int PASS, int SR>
+__global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
+  constexpr int SRT = 32 * SR;
+  using L = Layout32<D>;
+  using L64 = Layout<D>;
+  constexpr int REC = L::REC;
+  constexpr int K = PASS == 1 ? L64::K1 : L64::K2;
+  constexpr int KR = PASS == 1 ? 1 + D : D;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
+  double* red = reinterpret_cast<double*>(bars + STAGES);   // [4 warps][SRT][KR]
+  __shared__ int s_item;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  const PassConst32 c = a.c;
+  const int N = a.N;
+
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= a.n_items) break;
+    const int2 w = a.items[it];
+    const int r0 = w.x * a.chunk;
+    const int c0 = w.y * a.chunk;
+    const int c1 = min(N, c0 + a.chunk);
+    const int n_rt = a.chunk / SRT;
+    const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
+    const int total = n_rt * n_ct;
+
+    if (tid == 0) {
+      for (int s = 0; s < STAGES && s < total; ++s) {
+        const int jt = c0 + (s % n_ct) * TILE_J;
+        const int cnt = min(TILE_J, c1 - jt);
+        tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
+                    (uint32_t)(cnt * REC * sizeof(float)), &bars[s]);
+      }
+    }
+
+    int k = 0;
+    for (int rt = 0; rt < n_rt; ++rt) {
+      const int row0 = r0 + rt * SRT;
+      SymRow32<D> row[SR];
+      double rM[SR], rG[SR][D];
+#pragma unroll
+      for (int r = 0; r < SR; ++r) {
+        const int i = row0 + lane + 32 * r;
+        const float* ri = a.rec + (long long)i * REC;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          row[r].xh[d] = ri[L::XH + d];
+          row[r].xl[d] = ri[L::XL + d];
+        }
+        row[r].th = ri[L::TH];
+        row[r].tl = ri[L::TL];
+        row[r].rho = ri[L::RHO];
+        row[r].g = a.gid[i];
+        rM[r] = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
+      }
+      const int g_rlast = a.gid[row0 + SRT - 1];
+
+      for (int ct = 0; ct < n_ct; ++ct, ++k) {
+        const int s = k % STAGES;
+        const int jt = c0 + ct * TILE_J;
+        const int cnt = min(TILE_J, c1 - jt);
+        mbar_wait(&bars[s], (parity >> s) & 1u);
+        parity ^= (1u << s);
+        const float* st = stage + s * TILE_J * REC;
+        const int cl = warp * 32 + lane;
+        const bool cvalid = cl < cnt;
+        const int cj = jt + min(cl, cnt - 1);
+        const int cg = a.gid[cj];
+        double* cpart = a.part + ((long long)w.x * a.npad + cj) * K;
+        float cacc[2 + D];
+#pragma unroll
+        for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.f;
+        float rM32[SR], rG32[SR][D];
+#pragma unroll
+        for (int r = 0; r < SR; ++r) {
+          rM32[r] = 0.f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) rG32[r][d] = 0.f;
+        }
+        const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
+        if (strict)
+          sym32_group<D, PASS, false, SR>(row, st + warp * 32 * REC, cg, cvalid, rM32, rG32, cacc, c);
+        else
+          sym32_group<D, PASS, true, SR>(row, st + warp * 32 * REC, cg, cvalid, rM32, rG32, cacc, c);
+#pragma unroll
+        for (int r = 0; r < SR; ++r) {
+          rM[r] += (double)rM32[r];
+#pragma unroll
+          for (int d = 0; d < D; ++d) rG[r][d] += (double)rG32[r][d];
+        }
+        if (cvalid) {
+          if (PASS == 1) {
+#pragma unroll
+            for (int q = 0; q < 2 + D; ++q) cpart[q] = (rt ? cpart[q] : 0.0) + (double)cacc[q];
+          } else {
+#pragma unroll
+            for (int d = 0; d < D; ++d) cpart[d] = (rt ? cpart[d] : 0.0) + (double)cacc[2 + d];
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && k + STAGES < total) {
+          const int kn = k + STAGES;
+          const int jn = c0 + (kn % n_ct) * TILE_J;
+          const int cn = min(TILE_J, c1 - jn);
+          tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
+                      (uint32_t)(cn * REC * sizeof(float)), &bars[s]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < SR; ++r) {
+        double* o = red + ((long long)warp * SRT + lane + 32 * r) * KR;
+        if (PASS == 1) {
+          o[0] = rM[r];
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[1 + d] = rG[r][d];
+        } else {
+#pragma unroll
+          for (int d = 0; d < D; ++d) o[d] = rG[r][d];
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < SRT * KR; q += THREADS) {
+        const int rr = q / KR, kk = q % KR;
+        double v = red[(0 * SRT + rr) * KR + kk];
+        v += red[(1 * SRT + rr) * KR + kk];
+        v += red[(2 * SRT + rr) * KR + kk];
+        v += red[(3 * SRT + rr) * KR + kk];
+        double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;
+        if (PASS == 1) {
+          if (kk == 0) {
+            o[0] = v;
+            o[1] = 0.0;
+          } else {
+            o[1 + kk] = v;
+          }
+        } else {
+          o[kk] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace hk

@@ -294,11 +294,25 @@ def test_fp32_other_dimensions(D):
     _check_fp32(synth.unit_square(700, config=26, D=D), f"fp32 D={D}")
 
 
-def test_fp32_emulated_world_bitwise():
+def test_fp32_emulated_world():
+    """fp32: ROWS is bitwise W-independent; PAIRS agrees across W to fp64 rounding of the
+    exchanged per-event sums and stays within the fp32 tolerance."""
     c = synth.unit_square(2000, config=27)
-    e1, g1, r1 = gpu_eval(c.x, c.t, c.theta, precision="fp32")
-    e4, g4, r4 = gpu_eval(c.x, c.t, c.theta, precision="fp32", emulate_world=4)
+    e1, g1, r1 = gpu_eval(c.x, c.t, c.theta, precision="fp32", algorithm="rows")
+    e4, g4, r4 = gpu_eval(c.x, c.t, c.theta, precision="fp32", emulate_world=4, algorithm="rows")
     assert e1 == e4 and np.array_equal(g1, g4) and np.array_equal(r1["lambda"], r4["lambda"])
+    ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    for W in (1, 3):
+        ew, gw, _ = gpu_eval(c.x, c.t, c.theta, precision="fp32", emulate_world=W, algorithm="pairs")
+        assert_parity(ew, gw, ell_ref, g_ref, S, precision="fp32", what=f"fp32 PAIRS W={W}")
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_fp32_rows_algorithm(name):
+    c = synth.config(name)
+    ell, g, _ = gpu_eval(c.x, c.t, c.theta, precision="fp32", algorithm="rows")
+    ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    assert_parity(ell, g, ell_ref, g_ref, S, precision="fp32", what=f"fp32 ROWS {name}")
 
 
 def _check_fp32(c, what):
