@@ -346,7 +346,7 @@ __global__ void k_kinetic(const double* __restrict__ p, const double* __restrict
 __global__ void k_diag_exp(const double* __restrict__ a, double* __restrict__ out, long long n,
                            const int2* __restrict__ gtab) {
   __shared__ int2 tab[EXP_TABLE];
-  if (threadIdx.x < EXP_TABLE) tab[threadIdx.x] = gtab[threadIdx.x];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
   __syncthreads();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = fexp(a[i], tab);
@@ -368,7 +368,7 @@ __global__ void k_diag_dfma(double* out, int iters) {
 // diagnostics: FP64-pipe throughput for several operand patterns (ops per thread per iter = 8)
 __global__ void k_diag_mode(double* out, int iters, int mode, const int2* __restrict__ gtab) {
   __shared__ int2 tab[EXP_TABLE];
-  if (threadIdx.x < EXP_TABLE) tab[threadIdx.x] = gtab[threadIdx.x];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
   __syncthreads();
   double a[8], b[8];
 #pragma unroll
@@ -1214,14 +1214,14 @@ int copy_out(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem)
 
 bool finite_bounded(double v) { return fabs(v) <= 1e100; }
 
-// fexp's table: T[j] = 2^(j/64) as (low word, high word - (j << 14)) (the bias lets one
-// integer multiply-add insert the binary exponent; see hawkes_kernels.cuh)
+// fexp's table: T[j] = 2^(j/EXP_TABLE) as (low word, high word - (j << EXP_BIAS_SHIFT))
+// (the bias lets one integer multiply-add insert the binary exponent; hawkes_kernels.cuh)
 void make_exp_table(int2* h) {
   for (int j = 0; j < EXP_TABLE; ++j) {
     const double v = (double)exp2l((long double)j / (long double)EXP_TABLE);
     long long b;
     memcpy(&b, &v, 8);
-    h[j] = make_int2((int)(b & 0xffffffffLL), (int)(b >> 32) - (j << 14));
+    h[j] = make_int2((int)(b & 0xffffffffLL), (int)(b >> 32) - (j << EXP_BIAS_SHIFT));
   }
 }
 

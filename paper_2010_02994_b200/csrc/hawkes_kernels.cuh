@@ -56,29 +56,29 @@ struct PassConst {
 // e^a for the pair kernels.  On sm_100 an FP64 instruction holds its SM sub-partition's
 // dispatch for two cycles and every other instruction for one (measured: the FP64 pipe
 // utilisation of a kernel tracks 2*n_fp64 / (2*n_fp64 + n_other)), so this exp is
-// built to minimise both: 8 FP64 instructions and 5 integer/shared-memory ones.
+// built to minimise both: 7 FP64 instructions and 5 integer/shared-memory ones.
 //   a' = max(a, AMIN)            one unsigned min on the high word (AMIN = -707: for
 //                                negative doubles a larger high word means a larger |a|;
 //                                positive a, high bit clear, pass through)
-//   y  = a' * 64/ln2 + 1.5*2^52  rounds to an integer: y's low word is
-//                                k = rint(a' * 64/ln2) = 64m + j
-//   r  = a' - k ln2/64           |r| <= ln2/128
-//   T  = 2^(j/64) from a 64-entry shared table whose high words are pre-biased by
-//        -(j << 14), so that one integer multiply-add, hi + (k << 14), also adds m to the
-//        exponent field
-//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r + c3 r^2 + c4 r^3)  (minimax, tools/
-//        fit_exp_poly.py: |rel. err.| <= 5.1e-15 on |r| <= ln2/128)
+//   y  = a' * 256/ln2 + 1.5*2^52 rounds to an integer: y's low word is
+//                                k = rint(a' * 256/ln2) = 256m + j
+//   r  = a' - k ln2/256          |r| <= ln2/512
+//   T  = 2^(j/256) from a 256-entry (2 KB) shared table whose high words are pre-biased
+//        by -(j << 12), so that one integer multiply-add, hi + (k << 12), also adds m to
+//        the exponent field
+//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r + c3 r^2)  (minimax, tools/
+//        fit_exp_poly.py 256 3: |rel. err.| <= 2.4e-14 on |r| <= ln2/512)
 // Arguments below AMIN return e^(a') ~ e^-707 instead of a smaller number (callers treat
 // sums below N e^-700 as zero; reading R23).  Arguments must be < ~700
 // (guaranteed by the validated kernel constants).
-constexpr double EXP_K = 92.332482616893656;                // 64/ln2
+constexpr double EXP_K = 369.3299304675746;                // 256/ln2
 constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
-constexpr double EXP_C = 0.010830424696249145;              // ln2/64
+constexpr double EXP_C = 0.0027076061740622863;            // ln2/256
 constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
-constexpr double EXP_C2 = 0.5000000000031142;
-constexpr double EXP_C3 = 0.1666668790487242;
-constexpr double EXP_C4 = 0.04166656920987773;
-constexpr int EXP_TABLE = 64;
+constexpr double EXP_C2 = 0.5000000632802307;
+constexpr double EXP_C3 = 0.1666666688540192;
+constexpr int EXP_TABLE = 256;
+constexpr int EXP_BIAS_SHIFT = 12;                          // 20 - log2(EXP_TABLE)
 
 __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab) {
   const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
@@ -88,11 +88,9 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab) {
   const double r = fma(kf, -EXP_C, ac);
   const int k = __double2loint(y);
   const int2 T = tab[k & (EXP_TABLE - 1)];
-  double q = fma(EXP_C4, r, EXP_C3);
-  q = fma(q, r, EXP_C2);
-  q = fma(q, r, 1.0);
+  const double q = fma(fma(EXP_C3, r, EXP_C2), r, 1.0);
   const double p = q * r;                                      // e^r - 1
-  const double Tm = __hiloint2double(T.y + k * 16384, T.x);    // 2^(j/64) * 2^m
+  const double Tm = __hiloint2double(T.y + k * (1 << EXP_BIAS_SHIFT), T.x);   // 2^(j/256) 2^m
   return fma(Tm, p, Tm);
 }
 
@@ -234,7 +232,7 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel(PassArgs a) {
   __shared__ int s_item;
 
   const int tid = threadIdx.x;
-  if (tid < EXP_TABLE) tab[tid] = a.tab[tid];
+  for (int q = tid; q < EXP_TABLE; q += THREADS) tab[q] = a.tab[q];
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < EXP_TABLE) tab[tid] = a.tab[tid];
+  for (int q = tid; q < EXP_TABLE; q += THREADS) tab[q] = a.tab[q];
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();

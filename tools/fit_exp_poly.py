@@ -1,9 +1,16 @@
-"""Minimax (Remez) fit of e^r - 1 = r (1 + c2 r + c3 r^2 + c4 r^3) on |r| <= ln2/128 (+margin),
-relative error, at 60 digits; prints the coefficients used by fexp in hawkes_kernels.cuh."""
+"""Minimax (Remez) fit of e^r - 1 = r (1 + c2 r + ... ) on |r| <= ln2/(2*TABLE) (+margin),
+relative error, at 60 digits; prints the coefficients used by fexp in hawkes_kernels.cuh.
+
+    python tools/fit_exp_poly.py [TABLE] [DEGREE]      (current kernels: 256 3)
+"""
+import sys
+
 import mpmath as mp
 
 mp.mp.dps = 60
-R = mp.log(2) / 128 * (1 + mp.mpf("1e-6"))
+TABLE = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+DEG = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+R = mp.log(2) / (2 * TABLE) * (1 + mp.mpf("1e-6"))
 
 
 def fit(deg=3):
@@ -37,7 +44,7 @@ def fit(deg=3):
     return cs, maxerr
 
 
-cs, e = fit()
+cs, e = fit(DEG - 1)
 print("max rel err", mp.nstr(e, 5))
 for j, c in enumerate(cs):
     print(f"c{j+2} = {mp.nstr(c, 20)}  double: {float(c).hex()}  {float(c)!r}")
