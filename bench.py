@@ -258,6 +258,40 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_val = e2e_steps / (float(e2e_ms.item()) * 1e-3)
 
+    # ---- C5 (BASELINE configs[4]): one 20-step HMC leapfrog trajectory at N = 50k through
+    # hawkes_leapfrog (device buffers; 21 gradient evaluations per trajectory)
+    hmc = None
+    if not args.no_hmc:
+        c5 = synth.config("C5")
+        if world > 1:
+            hctx = init_distributed_context(c5.N, D, precision=args.precision, algorithm=args.algorithm)
+        else:
+            hctx = HawkesContext(c5.N, D, device=local, precision=args.precision,
+                                 algorithm=args.algorithm)
+        hctx.set_times(torch.from_numpy(c5.t).to(dev))
+        hctx.set_params(c5.theta)
+        x5 = torch.from_numpy(c5.x).to(dev)
+        p5 = torch.from_numpy(synth.momenta(c5.N, D, seed=5)).to(dev)
+        xs, ps = x5.clone(), p5.clone()
+        hctx.leapfrog(xs, ps, 1e-4, 2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        xs.copy_(x5)
+        ps.copy_(p5)
+        h0.record(hctx.stream)
+        _, _, ell5, kin5 = hctx.leapfrog(xs, ps, 1e-4, 20)
+        h1.record(hctx.stream)
+        torch.cuda.synchronize()
+        hms = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(hms, op=dist.ReduceOp.MAX)
+        hmc = {"config": "C5 N=50000 D=2, 20 leapfrog steps, step 1e-4, identity mass",
+               "ms_per_trajectory": float(hms.item()), "trajectories_per_s": 1e3 / float(hms.item()),
+               "grad_evals_per_s": 21e3 / float(hms.item()), "ell_end": ell5, "kinetic_end": kin5}
+        hctx.close()
+
     # ---- roofline of the dominant pass (FP64 pipe), from the library's own CUDA events
     rate_avg = kt["rate_ms"] / max(1, kt["rate_launches"])
     grad_avg = kt["grad_ms"] / max(1, kt["grad_launches"])
@@ -311,6 +345,7 @@ def run_ours(args):
                      "executed_frac": achieved_exec / peak, "measured_dfma_peak": dfma_peak},
         "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": N * D * 8,
                 "d2h_bytes_per_step": N * D * 8 + 8},
+        "hmc": hmc,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline()
@@ -337,6 +372,7 @@ def main():
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--algorithm", choices=["auto", "rows", "pairs"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hmc", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
