@@ -135,6 +135,7 @@ __global__ void k_pack_t32(float* __restrict__ rec, const double* __restrict__ t
 
 // PAIRS with W > 1: per event, fixed-order sum of the partial slots this rank computed.
 // Slot s of event i (chunk c) comes from chunk pair (min(s, c), max(s, c)).
+// Slot nchunks (the diagonal items' column role) comes from pair (c, c).
 __global__ void k_slot_sum(const double* __restrict__ part, long long npad, int nchunks, int chunk,
                            int K, const int* __restrict__ own, int rank, int N,
                            double* __restrict__ out) {
@@ -143,8 +144,8 @@ __global__ void k_slot_sum(const double* __restrict__ part, long long npad, int 
   const int i = (int)(idx / K), k = (int)(idx % K);
   const int c = i / chunk;
   double v = 0.0;
-  for (int sl = 0; sl < nchunks; ++sl) {
-    const int a = min(sl, c), b = max(sl, c);
+  for (int sl = 0; sl <= nchunks; ++sl) {
+    const int a = sl == nchunks ? c : min(sl, c), b = sl == nchunks ? c : max(sl, c);
     if (own[a * nchunks + b] == rank) v += part[((long long)sl * npad + i) * K + k];
   }
   out[idx] = v;
@@ -167,16 +168,25 @@ struct FinConst {
   double zero_floor;      // Lambda' at or below this is lambda = 0 (fexp clamps at e^-707)
 };
 
+// kernel constants live in device memory so captured CUDA graphs survive set_params
+struct DevConsts {
+  PassConst pc;
+  PassConst32 pc32;
+  FinConst fc;
+};
+
 // Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
 // lambda, rho' and ell_n.  rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda).
 template <int D>
 __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
                        const int* __restrict__ tiles, int N, const double* __restrict__ rec,
                        double* __restrict__ G1, double* __restrict__ rl,
-                       double* __restrict__ rates, FinConst f) {
+                       double* __restrict__ rates, const FinConst* __restrict__ fcp,
+                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho) {
   using L = Layout<D>;
   const int i = tiles[blockIdx.x] * RT + threadIdx.x;
   if (i >= N) return;
+  const FinConst f = *fcp;
   double M = 0.0, X = 0.0, G[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) G[d] = 0.0;
@@ -204,6 +214,9 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
   rl[2 * (long long)i] = rho;
   rl[2 * (long long)i + 1] = ell;
+  // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
+  if (rec_rho) rec_rho[(long long)i * L::REC] = rho;
+  if (rec32_rho) rec32_rho[(long long)i * Layout32<D>::REC] = (float)rho;
   rates[4 * (long long)i] = Lp * sc;
   rates[4 * (long long)i + 1] = mu_s * sc;
   rates[4 * (long long)i + 2] = xi_s * sc;
@@ -433,7 +446,7 @@ struct hawkes_ctx {
   int D = 0;
   int npad = 0;
   int ntiles = 0;          // row tiles of RT rows
-  int chunk = 0, nchunks = 0;
+  int chunk = 0, nchunks = 0, nslots = 0;
   hawkes_opts opts{};
   cudaStream_t stream = nullptr;
   int sms = 0;
@@ -501,6 +514,14 @@ struct hawkes_ctx {
 
   int grid1 = 0, grid2 = 0;
   int grid_s1 = 0, grid_s2 = 0;
+  DevConsts* d_consts = nullptr;
+  // CUDA graphs of one evaluation (single process, W = 1, timing off)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};   // rates, rates+grad, grad only
+  bool graphs = false;
+  bool capturing = false;
+  int64_t graph_launches[3] = {0, 0, 0};
   int sym_variant = 40;     // 10 * rows-per-lane + exp scheme (tuning knob HAWKES_SYM_VARIANT)
 };
 
@@ -629,14 +650,6 @@ struct SymOps {
 
 template <int D>
 int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
-  if constexpr (D == 2) {
-    switch (ctx->sym_variant) {
-      case 41: return pass ? SymOps<D, 4, 1>::launch(ctx, pass, *b) : SymOps<D, 4, 1>::setup(ctx);
-      case 20: return pass ? SymOps<D, 2, 0>::launch(ctx, pass, *b) : SymOps<D, 2, 0>::setup(ctx);
-      case 21: return pass ? SymOps<D, 2, 1>::launch(ctx, pass, *b) : SymOps<D, 2, 1>::setup(ctx);
-      default: break;
-    }
-  }
   return pass ? SymOps<D, 4, 0>::launch(ctx, pass, *b) : SymOps<D, 4, 0>::setup(ctx);
 }
 
@@ -742,7 +755,7 @@ struct PassD {
     a.N = (int)ctx->N;
     a.n_items = ctx->n_items[rank];
     a.chunk = ctx->chunk;
-    a.c = ctx->pc;
+    a.c = &ctx->d_consts->pc;
     record_start(ctx, pass == 1);
     if (a.n_items > 0) {
       const size_t sm = pass_smem<D, 1>();
@@ -765,7 +778,8 @@ struct PassD {
       b.N = (int)ctx->N;
       b.n_items = ctx->n_sym[rank];
       b.chunk = ctx->chunk;
-      b.c = ctx->pc;
+      b.nchunks = ctx->nchunks;
+      b.c = &ctx->d_consts->pc;
       TRY(sym_call<D>(ctx, pass, &b));
     }
     record_stop(ctx, pass == 1);
@@ -782,8 +796,7 @@ struct PassD {
     a.N = (int)ctx->N;
     a.n_items = ctx->n_items[rank];
     a.chunk = ctx->chunk;
-    a.c = ctx->pc32;
-    if (a.n_items == 0) return HAWKES_OK;
+    a.c = &ctx->d_consts->pc32;
     record_start(ctx, pass == 1);
     if (a.n_items > 0) {
       const size_t sm = pass_smem32<D>();
@@ -805,7 +818,8 @@ struct PassD {
       b.N = (int)ctx->N;
       b.n_items = ctx->n_sym[rank];
       b.chunk = ctx->chunk;
-      b.c = ctx->pc32;
+      b.nchunks = ctx->nchunks;
+      b.c = &ctx->d_consts->pc32;
       const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
       if (pass == 1)
         sym_kernel_f32<D, 1, SYM32_R><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
@@ -827,10 +841,13 @@ struct Fin1D {
     const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->W > 1;
+    const bool final_here = all || ctx->W == 1;   // else rho' is exchanged first
     k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
-        sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nchunks,
+        sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1, ctx->rl,
-        ctx->rates, ctx->fc);
+        ctx->rates, &ctx->d_consts->fc,
+        final_here && !ctx->rec32 ? ctx->rec + Layout<D>::RHO : nullptr,
+        final_here && ctx->rec32 ? ctx->rec32 + Layout32<D>::RHO : nullptr);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -844,7 +861,7 @@ struct Fin2D {
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->W > 1;
     k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
-        sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nchunks,
+        sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->G1, ctx->rl, ctx->grad);
     CHECK_LAUNCH();
     return HAWKES_OK;
@@ -956,8 +973,68 @@ int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int 
   return HAWKES_OK;
 }
 
+int run_rates(hawkes_ctx* ctx);
+int run_grad(hawkes_ctx* ctx);
+
+bool use_graph(const hawkes_ctx* ctx) { return ctx->graphs && !ctx->timing && !ctx->capturing; }
+
+// Capture one evaluation sequence (0: rate pass; 1: rate + gradient pass; 2: gradient pass
+// with cached rates) on the context's own stream and instantiate it.
+int capture(hawkes_ctx* ctx, int which) {
+  cudaStream_t user = ctx->stream;
+  const bool rv = ctx->rates_valid, gv = ctx->grad_valid;
+  const int64_t l0 = ctx->launches;
+  ctx->stream = ctx->gstream;
+  ctx->capturing = true;
+  int rc = HAWKES_OK;
+  cudaError_t e = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    ctx->rates_valid = which == 2;
+    ctx->grad_valid = false;
+    rc = which == 0 ? run_rates(ctx) : run_grad(ctx);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->gstream, &g);
+  ctx->stream = user;
+  ctx->capturing = false;
+  ctx->rates_valid = rv;
+  ctx->grad_valid = gv;
+  if (rc != HAWKES_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return set_err(ctx, HAWKES_ERR_CUDA, "graph capture failed: %s",
+                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+  cudaError_t e3 = cudaGraphInstantiate(&ctx->gexec[which], g, 0);
+  cudaGraphDestroy(g);
+  if (e3 != cudaSuccess)
+    return set_err(ctx, HAWKES_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e3));
+  ctx->graph_launches[which] = ctx->launches - l0;
+  ctx->launches = l0;
+  return HAWKES_OK;
+}
+
+int replay(hawkes_ctx* ctx, int which) {
+  if (!ctx->gexec[which]) TRY(capture(ctx, which));
+  CU(cudaEventRecord(ctx->ev_in, ctx->stream));
+  CU(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
+  CU(cudaGraphLaunch(ctx->gexec[which], ctx->gstream));
+  CU(cudaEventRecord(ctx->ev_out, ctx->gstream));
+  CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
+  ctx->launches += ctx->graph_launches[which];
+  return HAWKES_OK;
+}
+
 int run_rates(hawkes_ctx* ctx) {
   if (ctx->rates_valid) return HAWKES_OK;
+  if (use_graph(ctx)) {
+    TRY(replay(ctx, 0));
+    ctx->rates_valid = true;
+    ctx->rates_exchanged = false;
+    ctx->grad_valid = false;
+    return HAWKES_OK;
+  }
   CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
@@ -969,8 +1046,8 @@ int run_rates(hawkes_ctx* ctx) {
       TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
     }
     TRY(exchange_rows(ctx, ctx->rl, 2));
+    if (ctx->W > 1) TRY(dispatchD<RhoD>(ctx->D, ctx));
   }
-  TRY(dispatchD<RhoD>(ctx->D, ctx));
   k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
   CHECK_LAUNCH();
   ctx->rates_valid = true;
@@ -980,8 +1057,14 @@ int run_rates(hawkes_ctx* ctx) {
 }
 
 int run_grad(hawkes_ctx* ctx) {
-  TRY(run_rates(ctx));
   if (ctx->grad_valid) return HAWKES_OK;
+  if (use_graph(ctx)) {
+    TRY(replay(ctx, ctx->rates_valid ? 2 : 1));
+    if (!ctx->rates_valid) ctx->rates_exchanged = false;
+    ctx->rates_valid = ctx->grad_valid = true;
+    return HAWKES_OK;
+  }
+  TRY(run_rates(ctx));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
     if (ctx->W > 1) TRY(reduce_pair_partials(ctx, ctx->part2, ctx->sums2, K2_of(ctx->D)));
@@ -1029,13 +1112,14 @@ int chunk_of(long long N) {
   return (int)c;
 }
 
-// PAIRS chunk: a multiple of the ordered kernel's 256-row tile, ~N/138 so that the
-// C(C-1)/2 chunk pairs give >= ~16 work items per CTA slot while the [C][Npad][K] partial
-// arrays stay ~C*N*48 bytes.  A function of N only.
+// PAIRS chunk: a multiple of the sym kernel's 128-event tile, ~N/138 so that the C(C+1)/2
+// chunk pairs give >= ~16 work items per CTA slot while the [C+1][Npad][K] partial arrays
+// stay ~C*N*48 bytes; 128 for N <= ~17k (latency: small catalogs still fill the GPU).
+// A function of N only.
 int chunk_pairs_of(long long N) {
   long long c = (N + 137) / 138;
-  c = ((c + RT - 1) / RT) * RT;
-  return (int)std::max<long long>(RT, c);
+  c = ((c + TILE_J - 1) / TILE_J) * TILE_J;
+  return (int)std::max<long long>(TILE_J, c);
 }
 
 // Chunk pairs (a <= b) dealt to ranks by greedy longest-processing-time on their cost.
@@ -1047,7 +1131,7 @@ std::vector<int> pair_owners(long long N, int chunk, int W) {
     for (int b = a; b < C; ++b) {
       const double na = (double)std::min<long long>(chunk, N - (long long)a * chunk);
       const double nb = (double)std::min<long long>(chunk, N - (long long)b * chunk);
-      items.push_back({a == b ? na * na * 26.5 : na * nb * 36.0, a, b});
+      items.push_back({a == b ? 0.5 * na * na : na * nb, a, b});
     }
   std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) { return x.cost > y.cost; });
   std::vector<double> load(W, 0.0);
@@ -1077,29 +1161,20 @@ void build_plan_pairs(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
   it1.assign(W, {});
   it2.assign(W, {});
   sym.assign(W, {});
-  const int tiles_per_chunk = ctx->chunk / RT;
   for (int r = 0; r < W; ++r) {
-    std::vector<std::pair<long long, int2>> off;
+    std::vector<std::pair<double, int2>> items;   // (pair count, (a, b)); heaviest first
     for (int a = 0; a < C; ++a)
       for (int b = a; b < C; ++b) {
         if (own[(size_t)a * C + b] != r) continue;
-        if (a == b) {
-          for (int k = 0; k < tiles_per_chunk; ++k) {
-            const int tile = a * tiles_per_chunk + k;
-            if (tile * RT >= N) break;
-            it1[r].push_back(make_int2(tile, a));
-            it2[r].push_back(make_int2(tile, a));
-          }
-        } else {
-          const long long nb = std::min<long long>(ctx->chunk, (long long)N - (long long)b * ctx->chunk);
-          off.push_back({nb, make_int2(a, b)});
-        }
+        const double na = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)a * ctx->chunk);
+        const double nb = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)b * ctx->chunk);
+        items.push_back({a == b ? 0.5 * na * na : na * nb, make_int2(a, b)});
       }
-    std::stable_sort(off.begin(), off.end(),
-                     [](const std::pair<long long, int2>& x, const std::pair<long long, int2>& y) {
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<double, int2>& x, const std::pair<double, int2>& y) {
                        return x.first > y.first;
                      });
-    for (auto& e : off) sym[r].push_back(e.second);
+    for (auto& e : items) sym[r].push_back(e.second);
   }
 }
 
@@ -1139,6 +1214,15 @@ void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
     for (auto& e : c1) it1[r].push_back(e.second);
     for (auto& e : c2) it2[r].push_back(e.second);
   }
+}
+
+int upload_consts(hawkes_ctx* ctx) {
+  DevConsts h;
+  h.pc = ctx->pc;
+  h.pc32 = ctx->pc32;
+  h.fc = ctx->fc;
+  CU(cudaMemcpyAsync(ctx->d_consts, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  return HAWKES_OK;
 }
 
 // Kernel constants for Theta; written to ctx only when every check passes.
@@ -1196,7 +1280,7 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   }
   ctx->pc = pc;
   ctx->fc = fc;
-  return HAWKES_OK;
+  return upload_consts(ctx);
 }
 
 int copy_in(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem) {
@@ -1298,6 +1382,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || o.algorithm == HAWKES_ALGO_AUTO;
   ctx->chunk = ctx->pairs ? chunk_pairs_of(N) : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
+  ctx->nslots = ctx->nchunks + (ctx->pairs ? 1 : 0);   // PAIRS: + diagonal column slot
   ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);
   if (o.world > 1)
     ctx->my_ranks = {o.rank};
@@ -1315,8 +1400,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   int rc;
   if ((rc = dalloc(ctx, &ctx->rec, (size_t)ctx->npad * REC)) ||
       (rc = dalloc(ctx, &ctx->gid, (size_t)ctx->npad)) ||
-      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nchunks * ctx->npad * K1_of(D))) ||
-      (rc = dalloc(ctx, &ctx->part2, (size_t)ctx->nchunks * ctx->npad * K2_of(D))) ||
+      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nslots * ctx->npad * K1_of(D))) ||
+      (rc = dalloc(ctx, &ctx->part2, (size_t)ctx->nslots * ctx->npad * K2_of(D))) ||
       (rc = dalloc(ctx, &ctx->G1, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->rl, (size_t)ctx->npad * 2)) ||
       (rc = dalloc(ctx, &ctx->rates, (size_t)ctx->npad * 4)) ||
@@ -1324,8 +1409,15 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
       (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W)) ||
       (rc = dalloc(ctx, &ctx->tab, EXP_TABLE)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
-      (rc = dalloc(ctx, &ctx->st, 1)))
+      (rc = dalloc(ctx, &ctx->st, 1)) || (rc = dalloc(ctx, &ctx->d_consts, 1)))
     return fail(rc);
+  if (o.world == 1 && ctx->W == 1 && !getenv("HAWKES_NO_GRAPHS")) {
+    if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "stream/event creation failed"));
+    ctx->graphs = true;
+  }
   if (o.precision == HAWKES_FP32) {
     if ((rc = dalloc(ctx, &ctx->rec32, (size_t)ctx->npad * Layout32Rec(D)))) return fail(rc);
     if (cudaMemset(ctx->rec32, 0, (size_t)ctx->npad * Layout32Rec(D) * sizeof(float)) != cudaSuccess)
@@ -1421,7 +1513,15 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   cudaSetDevice(ctx->opts.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->comm);
-  void* bufs[] = {ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
+  for (auto& ge : ctx->gexec)
+    if (ge) cudaGraphExecDestroy(ge);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+  if (ctx->gstream) {
+    cudaStreamSynchronize(ctx->gstream);
+    cudaStreamDestroy(ctx->gstream);
+  }
+  void* bufs[] = {ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
@@ -1466,6 +1566,7 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->tN = h[N - 1];
   ctx->fc.tN = ctx->tN;
+  TRY(upload_consts(ctx));
   ctx->have_t = true;
   ctx->rates_valid = ctx->grad_valid = false;
   return HAWKES_OK;

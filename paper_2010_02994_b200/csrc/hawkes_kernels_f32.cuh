@@ -109,7 +109,7 @@ struct PassArgs32 {
   int N;
   int n_items;
   int chunk;
-  PassConst32 c;
+  const PassConst32* c; // device memory
 };
 
 template <int D, int PASS, int R>
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel_f32(PassArgs32 a) {
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst32 c = a.c;
+  const PassConst32 c = *a.c;
   const int N = a.N;
 
   for (;;) {
@@ -331,6 +331,7 @@ __device__ __forceinline__ void sym32_pair(const SymRow32<D>& row, const float* 
 template <int D, int PASS, bool MASK, int SR>
 __device__ __forceinline__ void sym32_group(const SymRow32<D> (&row)[SR],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
+                                            int ridx0, int cidx0, bool diag,
                                             float (&rM)[SR], float (&rG)[SR][D],
                                             float (&cacc)[2 + D], const PassConst32& c) {
   constexpr int REC = Layout32<D>::REC;
@@ -349,9 +350,11 @@ __device__ __forceinline__ void sym32_group(const SymRow32<D> (&row)[SR],
 #pragma unroll
     for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
 #pragma unroll
-    for (int r = 0; r < SR; ++r)
-      sym32_pair<D, PASS, MASK>(row[r], rc, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
-                                cacc[1], cG, c);
+    for (int r = 0; r < SR; ++r) {
+      const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
+                                 (diag && cidx0 + src <= ridx0 + 32 * r));
+      sym32_pair<D, PASS, MASK>(row[r], rc, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c);
+    }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
     const int nxt = (lane + 1) & 31;
@@ -374,11 +377,13 @@ struct SymArgs32 {
   int N;
   int n_items;
   int chunk;
-  PassConst32 c;
+  int nchunks;
+  const PassConst32* c; // device memory
 };
 
 template <int D, int PASS, int SR>
 __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
+  static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
   using L = Layout32<D>;
   using L64 = Layout<D>;
@@ -398,7 +403,7 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst32 c = a.c;
+  const PassConst32 c = *a.c;
   const int N = a.N;
 
   for (;;) {
@@ -408,16 +413,19 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
     __syncthreads();
     if (it >= a.n_items) break;
     const int2 w = a.items[it];
+    const bool diag = w.x == w.y;
     const int r0 = w.x * a.chunk;
+    const int r1 = min(N, r0 + a.chunk);
     const int c0 = w.y * a.chunk;
     const int c1 = min(N, c0 + a.chunk);
-    const int n_rt = a.chunk / SRT;
+    const int n_rt = (r1 - r0 + SRT - 1) / SRT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
-    const int total = n_rt * n_ct;
+    const int cslot = diag ? a.nchunks : w.x;
 
+    TileWalk prod{0, 0};
     if (tid == 0) {
-      for (int s = 0; s < STAGES && s < total; ++s) {
-        const int jt = c0 + (s % n_ct) * TILE_J;
+      for (int s = 0; s < STAGES && prod.rt < n_rt; ++s, prod.next(n_ct, diag)) {
+        const int jt = c0 + prod.ct * TILE_J;
         const int cnt = min(TILE_J, c1 - jt);
         tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
                     (uint32_t)(cnt * REC * sizeof(float)), &bars[s]);
@@ -427,12 +435,13 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
     int k = 0;
     for (int rt = 0; rt < n_rt; ++rt) {
       const int row0 = r0 + rt * SRT;
+      const bool rows_full = row0 + SRT <= r1;
       SymRow32<D> row[SR];
       double rM[SR], rG[SR][D];
 #pragma unroll
       for (int r = 0; r < SR; ++r) {
         const int i = row0 + lane + 32 * r;
-        const float* ri = a.rec + (long long)i * REC;
+        const float* ri = a.rec + (long long)min(i, N - 1) * REC;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           row[r].xh[d] = ri[L::XH + d];
@@ -441,14 +450,14 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
         row[r].th = ri[L::TH];
         row[r].tl = ri[L::TL];
         row[r].rho = ri[L::RHO];
-        row[r].g = a.gid[i];
+        row[r].g = i < N ? a.gid[i] : -1;
         rM[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
       }
-      const int g_rlast = a.gid[row0 + SRT - 1];
+      const int g_rlast = a.gid[min(row0 + SRT, r1) - 1];
 
-      for (int ct = 0; ct < n_ct; ++ct, ++k) {
+      for (int ct = diag ? rt : 0; ct < n_ct; ++ct, ++k) {
         const int s = k % STAGES;
         const int jt = c0 + ct * TILE_J;
         const int cnt = min(TILE_J, c1 - jt);
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
         const bool cvalid = cl < cnt;
         const int cj = jt + min(cl, cnt - 1);
         const int cg = a.gid[cj];
-        double* cpart = a.part + ((long long)w.x * a.npad + cj) * K;
+        double* cpart = a.part + ((long long)cslot * a.npad + cj) * K;
         float cacc[2 + D];
 #pragma unroll
         for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.f;
@@ -470,11 +479,14 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
 #pragma unroll
           for (int d = 0; d < D; ++d) rG32[r][d] = 0.f;
         }
-        const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
+        const bool diag_tile = diag && ct == rt;
+        const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
         if (strict)
-          sym32_group<D, PASS, false, SR>(row, st + warp * 32 * REC, cg, cvalid, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                          jt + warp * 32, false, rM32, rG32, cacc, c);
         else
-          sym32_group<D, PASS, true, SR>(row, st + warp * 32 * REC, cg, cvalid, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, true, SR>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                         jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
 #pragma unroll
         for (int r = 0; r < SR; ++r) {
           rM[r] += (double)rM32[r];
@@ -491,12 +503,12 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
           }
         }
         __syncthreads();
-        if (tid == 0 && k + STAGES < total) {
-          const int kn = k + STAGES;
-          const int jn = c0 + (kn % n_ct) * TILE_J;
+        if (tid == 0 && prod.rt < n_rt) {
+          const int jn = c0 + prod.ct * TILE_J;
           const int cn = min(TILE_J, c1 - jn);
           tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
                       (uint32_t)(cn * REC * sizeof(float)), &bars[s]);
+          prod.next(n_ct, diag);
         }
       }
 #pragma unroll
@@ -514,6 +526,7 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
       __syncthreads();
       for (int q = tid; q < SRT * KR; q += THREADS) {
         const int rr = q / KR, kk = q % KR;
+        if (row0 + rr >= N) continue;
         double v = red[(0 * SRT + rr) * KR + kk];
         v += red[(1 * SRT + rr) * KR + kk];
         v += red[(2 * SRT + rr) * KR + kk];

@@ -8,12 +8,13 @@
 //   pass 2  row i: G2_i += rho'_j (mu' + xi') dx
 //           col j: G2_j -= rho'_i mu' dx
 // with dx = x_j - x_i and the scaled-domain terms of hawkes_kernels.cuh (mu' = alpha mu 2^64,
-// xi' = beta xi_ji 2^64).  Work items are chunk pairs (a, b), a < b (every event of chunk a
-// precedes every event of chunk b in the time-sorted catalog); pairs inside one chunk go
-// through the ordered kernel (pass_kernel).  An item writes the row partial of chunk a's
-// events into slot b and the column partial of chunk b's events into slot a of the same
-// [chunks][Npad][K] partial array the ordered kernel uses, so every (slot, event) is
-// written exactly once and the fixed-order finalize is unchanged.
+// xi' = beta xi_ji 2^64).  Work items are chunk pairs (a, b), a <= b.  For a < b every event
+// of chunk a precedes every event of chunk b in the time-sorted catalog; a diagonal item
+// (a, a) visits only the upper triangle of its tile pairs and masks j <= i (by index, which
+// is time order) on the diagonal tiles.  An item writes the row partial of chunk a's events
+// into slot b and the column partial of chunk b's events into slot a (slot C for diagonal
+// items) of a [C + 1][Npad][K] array, so every (slot, event) is written exactly once and
+// the fixed-order finalize sums C + 1 slots.
 //
 // Mapping: a CTA (4 warps) holds a row tile of 32*R events (lane l owns rows l + 32r, all
 // four warps hold the same rows) and streams column tiles of 128 events via TMA; warp w
@@ -40,7 +41,8 @@ struct SymArgs {
   int N;
   int n_items;
   int chunk;
-  PassConst c;
+  int nchunks;           // slot nchunks holds the column-role sums of diagonal items
+  const PassConst* c;   // device memory (graph-stable across set_params)
 };
 
 template <int D>
@@ -111,9 +113,10 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R, int V>
+template <int D, int PASS, bool MASK, int SYM_R>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp, int cg0, bool cvalid0,
+                                          int ridx0, int cidx0, bool diag,
                                           double (&rM)[SYM_R], double (&rG)[SYM_R][D],
                                           double (&cacc)[2 + D], const PassConst& c,
                                           const int2* __restrict__ tab) {
@@ -136,26 +139,22 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       cg = __shfl_sync(0xffffffffu, cg0, src);
       cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
     }
-    if (PASS == 1) {
-      double cG[D];
+    double cG[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
+    for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
 #pragma unroll
-      for (int r = 0; r < SYM_R; ++r)
-        sym_pair1<D, MASK, V>(row[r], cx, ct, MASK && (!cv || cg == row[r].g), rM[r], rG[r], cacc[0],
-                           cacc[1], cG, c, tab);
-#pragma unroll
-      for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
-    } else {
-      double cG[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
-#pragma unroll
-      for (int r = 0; r < SYM_R; ++r)
-        sym_pair2<D, MASK, V>(row[r], cx, ct, crho, MASK && (!cv || cg == row[r].g), rG[r], cG, c, tab);
-#pragma unroll
-      for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
+    for (int r = 0; r < SYM_R; ++r) {
+      // masked tiles: padding column or row, equal times, and (diagonal tiles) the
+      // lower triangle j <= i, which the transposed tile pair covers
+      const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
+                                 (diag && cidx0 + src <= ridx0 + 32 * r));
+      if (PASS == 1)
+        sym_pair1<D, MASK, 0>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
+      else
+        sym_pair2<D, MASK, 0>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
     }
+#pragma unroll
+    for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
     // rotate the column sums one lane down: lane l now holds column (l + s + 1) mod 32
     const int nxt = (lane + 1) & 31;
     if (PASS == 1) {
@@ -167,8 +166,21 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
   }
 }
 
+// Tile walk of one item: row tiles rt = 0..n_rt-1, column tiles ct = (diag ? rt : 0)..n_ct-1
+// (a diagonal item (a, a) visits only the upper triangle of its tile pairs).
+struct TileWalk {
+  int rt, ct;
+  __device__ __forceinline__ void next(int n_ct, bool diag) {
+    if (++ct == n_ct) {
+      ++rt;
+      ct = diag ? rt : 0;
+    }
+  }
+};
+
 template <int D, int PASS, int SYM_R, int V>
 __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArgs a) {
+  static_assert(32 * SYM_R == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SYM_RT = 32 * SYM_R;
   using L = Layout<D>;
   constexpr int REC = L::REC;
@@ -189,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst c = a.c;
+  const PassConst c = *a.c;
   const int N = a.N;
 
   for (;;) {
@@ -199,16 +211,19 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
     __syncthreads();
     if (it >= a.n_items) break;
     const int2 w = a.items[it];
-    const int r0 = w.x * a.chunk;                 // chunk a: rows (always a full chunk)
-    const int c0 = w.y * a.chunk;                 // chunk b: columns (may be ragged)
+    const bool diag = w.x == w.y;
+    const int r0 = w.x * a.chunk;                 // chunk a: rows
+    const int r1 = min(N, r0 + a.chunk);
+    const int c0 = w.y * a.chunk;                 // chunk b: columns
     const int c1 = min(N, c0 + a.chunk);
-    const int n_rt = a.chunk / SYM_RT;
+    const int n_rt = (r1 - r0 + SYM_RT - 1) / SYM_RT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
-    const int total = n_rt * n_ct;                // tiles streamed: (row tile, col tile)
+    const int cslot = diag ? a.nchunks : w.x;     // column-role slot of this item
 
+    TileWalk prod{0, 0};
     if (tid == 0) {
-      for (int s = 0; s < STAGES && s < total; ++s) {
-        const int jt = c0 + (s % n_ct) * TILE_J;
+      for (int s = 0; s < STAGES && prod.rt < n_rt; ++s, prod.next(n_ct, diag)) {
+        const int jt = c0 + prod.ct * TILE_J;
         const int cnt = min(TILE_J, c1 - jt);
         tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
                     (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
@@ -218,24 +233,25 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
     int k = 0;
     for (int rt = 0; rt < n_rt; ++rt) {
       const int row0 = r0 + rt * SYM_RT;
+      const bool rows_full = row0 + SYM_RT <= r1;
       SymRow<D> row[SYM_R];
       double rM[SYM_R], rG[SYM_R][D];
 #pragma unroll
       for (int r = 0; r < SYM_R; ++r) {
         const int i = row0 + lane + 32 * r;
-        const double* ri = a.rec + (long long)i * REC;
+        const double* ri = a.rec + (long long)min(i, N - 1) * REC;
 #pragma unroll
         for (int d = 0; d < D; ++d) row[r].x[d] = ri[d];
         row[r].t = ri[D];
         row[r].rho = ri[D + 1];
-        row[r].g = a.gid[i];
+        row[r].g = i < N ? a.gid[i] : -1;   // -1: padding row (masked)
         rM[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
       }
-      const int g_rlast = a.gid[row0 + SYM_RT - 1];
+      const int g_rlast = a.gid[min(row0 + SYM_RT, r1) - 1];
 
-      for (int ct = 0; ct < n_ct; ++ct, ++k) {
+      for (int ct = diag ? rt : 0; ct < n_ct; ++ct, ++k) {
         const int s = k % STAGES;
         const int jt = c0 + ct * TILE_J;
         const int cnt = min(TILE_J, c1 - jt);
@@ -248,10 +264,11 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
         const bool cvalid = cl < cnt;
         const int cj = jt + min(cl, cnt - 1);
         const int cg = a.gid[cj];
-        // column sums: slot a of the partial array, accumulated over this item's row tiles
-        double* cpart = a.part + ((long long)w.x * a.npad + cj) * K;
+        // column sums: accumulated over this item's row tiles in its own slot
+        double* cpart = a.part + ((long long)cslot * a.npad + cj) * K;
+        const bool first = rt == 0;   // every column tile is first visited by row tile 0
         double cacc[2 + D];
-        if (rt == 0 || !cvalid) {
+        if (first || !cvalid) {
 #pragma unroll
           for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.0;
         } else if (PASS == 1) {
@@ -262,11 +279,14 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
 #pragma unroll
           for (int d = 0; d < D; ++d) cacc[2 + d] = cpart[d];
         }
-        const bool strict = g_rlast < a.gid[jt] && cnt == TILE_J;
+        const bool diag_tile = diag && ct == rt;
+        const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
         if (strict)
-          sym_group<D, PASS, false, SYM_R, V>(row, st + warp * 32 * REC, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, false, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                           jt + warp * 32, false, rM, rG, cacc, c, tab);
         else
-          sym_group<D, PASS, true, SYM_R, V>(row, st + warp * 32 * REC, cg, cvalid, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, true, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                          jt + warp * 32, diag_tile, rM, rG, cacc, c, tab);
         if (cvalid) {
           if (PASS == 1) {
 #pragma unroll
@@ -277,12 +297,12 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
           }
         }
         __syncthreads();   // stage s fully consumed
-        if (tid == 0 && k + STAGES < total) {
-          const int kn = k + STAGES;
-          const int jn = c0 + (kn % n_ct) * TILE_J;
+        if (tid == 0 && prod.rt < n_rt) {
+          const int jn = c0 + prod.ct * TILE_J;
           const int cn = min(TILE_J, c1 - jn);
           tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
                       (uint32_t)(cn * REC * sizeof(double)), &bars[s]);
+          prod.next(n_ct, diag);
         }
       }
       // row sums of this row tile: reduce the 4 warps' partials in a fixed order
@@ -301,6 +321,7 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
       __syncthreads();
       for (int q = tid; q < SYM_RT * KR; q += THREADS) {
         const int rr = q / KR, kk = q % KR;
+        if (row0 + rr >= N) continue;
         double v = red[(0 * SYM_RT + rr) * KR + kk];
         v += red[(1 * SYM_RT + rr) * KR + kk];
         v += red[(2 * SYM_RT + rr) * KR + kk];

@@ -109,6 +109,6 @@ def test_pair_plan_covers_every_pair_once(N, W):
     C = (N + chunk - 1) // chunk
     assert seen == {(a, b) for a in range(C) for b in range(a, C)}
     assert sum(loads) == N * N
-    assert chunk % 256 == 0
+    assert chunk % 128 == 0
     if N >= 100_000:
         assert max(loads) / (sum(loads) / W) < 1.03
