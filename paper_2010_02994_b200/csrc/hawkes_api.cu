@@ -522,6 +522,7 @@ struct hawkes_ctx {
   bool graphs = false;
   bool capturing = false;
   int64_t graph_launches[3] = {0, 0, 0};
+  int evals_same_consts = 0;   // evaluations since the last constants change
   int sym_variant = 40;     // 10 * rows-per-lane + exp scheme (tuning knob HAWKES_SYM_VARIANT)
 };
 
@@ -755,7 +756,7 @@ struct PassD {
     a.N = (int)ctx->N;
     a.n_items = ctx->n_items[rank];
     a.chunk = ctx->chunk;
-    a.c = &ctx->d_consts->pc;
+    a.c = ctx->pc;
     record_start(ctx, pass == 1);
     if (a.n_items > 0) {
       const size_t sm = pass_smem<D, 1>();
@@ -779,7 +780,7 @@ struct PassD {
       b.n_items = ctx->n_sym[rank];
       b.chunk = ctx->chunk;
       b.nchunks = ctx->nchunks;
-      b.c = &ctx->d_consts->pc;
+      b.c = ctx->pc;
       TRY(sym_call<D>(ctx, pass, &b));
     }
     record_stop(ctx, pass == 1);
@@ -796,7 +797,7 @@ struct PassD {
     a.N = (int)ctx->N;
     a.n_items = ctx->n_items[rank];
     a.chunk = ctx->chunk;
-    a.c = &ctx->d_consts->pc32;
+    a.c = ctx->pc32;
     record_start(ctx, pass == 1);
     if (a.n_items > 0) {
       const size_t sm = pass_smem32<D>();
@@ -819,7 +820,7 @@ struct PassD {
       b.n_items = ctx->n_sym[rank];
       b.chunk = ctx->chunk;
       b.nchunks = ctx->nchunks;
-      b.c = &ctx->d_consts->pc32;
+      b.c = ctx->pc32;
       const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
       if (pass == 1)
         sym_kernel_f32<D, 1, SYM32_R><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
@@ -976,7 +977,22 @@ int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int 
 int run_rates(hawkes_ctx* ctx);
 int run_grad(hawkes_ctx* ctx);
 
-bool use_graph(const hawkes_ctx* ctx) { return ctx->graphs && !ctx->timing && !ctx->capturing; }
+// Graphs bake the kernel constants in (they are kernel parameters, so the FP64 instructions
+// read them from the constant bank); set_params / set_times drop the graphs, and a graph is
+// captured only at the second evaluation with unchanged constants, so MCMC moves that
+// change Theta every step never pay for a capture.
+bool use_graph(const hawkes_ctx* ctx) {
+  return ctx->graphs && !ctx->timing && !ctx->capturing && ctx->evals_same_consts >= 2;
+}
+
+void drop_graphs(hawkes_ctx* ctx) {
+  for (auto& ge : ctx->gexec)
+    if (ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
+  ctx->evals_same_consts = 0;
+}
 
 // Capture one evaluation sequence (0: rate pass; 1: rate + gradient pass; 2: gradient pass
 // with cached rates) on the context's own stream and instantiate it.
@@ -1028,6 +1044,7 @@ int replay(hawkes_ctx* ctx, int which) {
 
 int run_rates(hawkes_ctx* ctx) {
   if (ctx->rates_valid) return HAWKES_OK;
+  if (!ctx->capturing) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, 0));
     ctx->rates_valid = true;
@@ -1058,6 +1075,7 @@ int run_rates(hawkes_ctx* ctx) {
 
 int run_grad(hawkes_ctx* ctx) {
   if (ctx->grad_valid) return HAWKES_OK;
+  if (!ctx->capturing && !ctx->rates_valid) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, ctx->rates_valid ? 2 : 1));
     if (!ctx->rates_valid) ctx->rates_exchanged = false;
@@ -1216,7 +1234,10 @@ void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
   }
 }
 
+void drop_graphs(hawkes_ctx* ctx);
+
 int upload_consts(hawkes_ctx* ctx) {
+  drop_graphs(ctx);
   DevConsts h;
   h.pc = ctx->pc;
   h.pc32 = ctx->pc32;

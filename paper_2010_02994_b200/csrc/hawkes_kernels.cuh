@@ -217,7 +217,7 @@ struct PassArgs {
   int N;
   int n_items;
   int chunk;             // events per j chunk (multiple of TILE_J)
-  const PassConst* c;   // device memory (graph-stable across set_params)
+  PassConst c;          // by value: DFMA constant-bank operands
 };
 
 template <int D, int PASS, int R>
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel(PassArgs a) {
   }
   __syncthreads();
   uint32_t parity = 0;  // bit s = parity to wait for on stage s
-  const PassConst c = *a.c;
+  const PassConst c = a.c;
   const int N = a.N;
 
   for (;;) {

@@ -109,7 +109,7 @@ struct PassArgs32 {
   int N;
   int n_items;
   int chunk;
-  const PassConst32* c; // device memory
+  PassConst32 c;
 };
 
 template <int D, int PASS, int R>
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(THREADS, 4) pass_kernel_f32(PassArgs32 a) {
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst32 c = *a.c;
+  const PassConst32 c = a.c;
   const int N = a.N;
 
   for (;;) {
@@ -378,7 +378,7 @@ struct SymArgs32 {
   int n_items;
   int chunk;
   int nchunks;
-  const PassConst32* c; // device memory
+  PassConst32 c;
 };
 
 template <int D, int PASS, int SR>
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst32 c = *a.c;
+  const PassConst32 c = a.c;
   const int N = a.N;
 
   for (;;) {

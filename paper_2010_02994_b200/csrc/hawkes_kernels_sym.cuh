@@ -42,7 +42,7 @@ struct SymArgs {
   int n_items;
   int chunk;
   int nchunks;           // slot nchunks holds the column-role sums of diagonal items
-  const PassConst* c;   // device memory (graph-stable across set_params)
+  PassConst c;          // by value: DFMA constant-bank operands
 };
 
 template <int D>
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
   }
   __syncthreads();
   uint32_t parity = 0;
-  const PassConst c = *a.c;
+  const PassConst c = a.c;
   const int N = a.N;
 
   for (;;) {
