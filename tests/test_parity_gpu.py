@@ -320,3 +320,37 @@ def _check_fp32(c, what):
     ell_ref, lam_ref, Lam_ref, g_ref, S = oracle_eval(c.x, c.t, c.theta)
     np.testing.assert_allclose(rates["lambda"], lam_ref, rtol=1e-4, err_msg=what)
     return assert_parity(ell, g, ell_ref, g_ref, S, precision="fp32", what=what)
+
+
+def test_graph_replay_matches_fresh_contexts():
+    """Repeated evaluations replay a captured CUDA graph; changing Theta or x between them
+    must give bit-identical results to a fresh context (small-N latency)."""
+    from paper_2010_02994_b200 import HawkesContext
+    c = synth.unit_square(1500, config=29)
+    th2 = (0.5, 0.12, 0.08, 0.5, 15.0, 0.04)
+    x2 = c.x + 0.001
+
+    def fresh(x, th):
+        with HawkesContext(c.N, c.D) as f:
+            f.set_times(c.t)
+            f.set_locations(x)
+            f.set_params(th)
+            g, e = f.grad_locations()
+            return e, g.cpu().numpy()
+
+    with HawkesContext(c.N, c.D) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_params(c.theta)
+        seq = [(c.x, c.theta), (c.x, c.theta), (x2, c.theta), (x2, c.theta), (x2, th2),
+               (x2, th2), (c.x, th2), (c.x, c.theta)]
+        prev_th = c.theta
+        for x, th in seq:
+            if th is not prev_th:
+                ctx.set_params(th)
+                prev_th = th
+            ctx.set_locations(torch.from_numpy(np.ascontiguousarray(x)).cuda())
+            ell_l = ctx.loglik()
+            g, e = ctx.grad_locations()
+            ef, gf = fresh(x, th)
+            assert e == ef and ell_l == ef
+            assert np.array_equal(g.cpu().numpy(), gf)
