@@ -161,6 +161,21 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
 int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, double* Lambda,
                      int32_t mem);
 
+/* Block Metropolis-Hastings over locations.
+ * hawkes_propose_move returns in *out_delta = ell(X') - ell(X) for X' = X with the k events
+ * idx[0..k) (host array, distinct, 1 <= k <= 256) moved to new_x (k*D row-major, host or
+ * device per mem).  Lambda_n does not depend on x, so only the lambda_n change: the cost is
+ * O(k N) given the rates of the current state, which are computed on demand (one full
+ * evaluation) and then kept up to date by hawkes_accept_move.  The proposal stays pending
+ * until hawkes_accept_move commits it (the context's locations and cached rates become
+ * those of X'), or until another proposal, set_* or leapfrog call discards it.  IEEE
+ * semantics: -inf when some lambda_n' = 0.  Accepted moves update the cached rates
+ * incrementally; a hawkes_loglik / hawkes_grad_locations call recomputes everything.
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_NONFINITE, HAWKES_ERR_STATE. */
+int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const double* new_x,
+                        int32_t mem, double* out_delta);
+int hawkes_accept_move(hawkes_ctx* ctx);
+
 /* Kernel timing (CUDA events on the context stream around each launch of the two O(N^2)
  * pass kernels).  enable != 0 starts accumulating from zero.  hawkes_get_kernel_times
  * synchronises and returns the summed milliseconds and launch counts since enabling;

@@ -25,7 +25,7 @@ ALGORITHMS = {"auto": 0, "rows": 1, "pairs": 2}
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
-    "hawkes_leapfrog", "hawkes_get_rates", "hawkes_enable_timing", "hawkes_get_kernel_times",
+    "hawkes_leapfrog", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move", "hawkes_enable_timing", "hawkes_get_kernel_times",
     "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version",
 )
@@ -73,6 +73,8 @@ def load() -> ctypes.CDLL:
     lib.hawkes_leapfrog.argtypes = [vp, dp, dp, i32, ctypes.c_double, i32, dp, dp, dp,
                                     P(ctypes.c_double), P(ctypes.c_double)]
     lib.hawkes_get_rates.argtypes = [vp, dp, dp, dp, dp, i32]
+    lib.hawkes_propose_move.argtypes = [vp, i32, P(i32), dp, i32, P(ctypes.c_double)]
+    lib.hawkes_accept_move.argtypes = [vp]
     lib.hawkes_enable_timing.argtypes = [vp, i32]
     lib.hawkes_get_kernel_times.argtypes = [vp, P(ctypes.c_double), P(i64), P(ctypes.c_double),
                                             P(i64), P(i64)]

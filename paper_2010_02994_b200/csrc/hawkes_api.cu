@@ -31,6 +31,7 @@
 #include "hawkes_kernels.cuh"
 #include "hawkes_kernels_f32.cuh"
 #include "hawkes_kernels_sym.cuh"
+#include "hawkes_moves.cuh"
 
 using namespace hk;
 
@@ -240,7 +241,96 @@ struct EvalStatus {
   int nonfinite;   // device-side input validation failed
   int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
   double kinetic;
+  double dell;     // Delta ell of the pending block move
 };
+
+// Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
+// events [256 b, 256 b + 256) in a fixed tree, k_sum_partials adds the block sums in order.
+// rates[n] = (lambda, mu, xi, Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.
+__global__ void k_move_terms(const double* __restrict__ rates, const double* __restrict__ delta,
+                             const double* __restrict__ rows, const int* __restrict__ slot_of,
+                             int N, double tx2, double h2, double floor_, double* __restrict__ part) {
+  __shared__ double sh[256];
+  const double S = 18446744073709551616.0;   // 2^64
+  const int n = blockIdx.x * 256 + threadIdx.x;
+  double term = 0.0;
+  if (n < N) {
+    const double L0 = rates[4 * (long long)n] * S;
+    const int q = slot_of[n];
+    if (q < 0) {
+      const double d = fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2);
+      term = (d == 0.0) ? 0.0 : ((L0 + d > floor_) ? log1p(d / L0) : -INFINITY);
+    } else {
+      const double L1 = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2);
+      term = ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
+    }
+  }
+  sh[threadIdx.x] = term;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// Commit an accepted move: cached rates, ell and the moved events' records.
+template <int D>
+__global__ void k_move_commit(double* __restrict__ rates, const double* __restrict__ delta,
+                              const double* __restrict__ rows, const int* __restrict__ slot_of,
+                              const int* __restrict__ idx, const double* __restrict__ new_x, int k,
+                              int N, double tx2, double h2, double* __restrict__ rec,
+                              float* __restrict__ rec32, EvalStatus* st) {
+  const double S1 = 1.0 / 18446744073709551616.0;   // 2^-64
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n == 0) st->ell += st->dell;
+  if (n < N) {
+    const int q = slot_of[n];
+    double mu, xi;
+    if (q < 0) {
+      mu = rates[4 * (long long)n + 1] + delta[2 * (long long)n] * tx2 * S1;
+      xi = rates[4 * (long long)n + 2] + delta[2 * (long long)n + 1] * h2 * S1;
+      rates[4 * (long long)n] += fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2) * S1;
+    } else {
+      mu = rows[2 * q] * tx2 * S1;
+      xi = rows[2 * q + 1] * h2 * S1;
+      rates[4 * (long long)n] = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2) * S1;
+    }
+    rates[4 * (long long)n + 1] = mu;
+    rates[4 * (long long)n + 2] = xi;
+  }
+  if (n < k) {
+    const int m = idx[n];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double v = new_x[n * D + d];
+      rec[(long long)m * Layout<D>::REC + d] = v;
+      if (rec32) {
+        const float hi = (float)v;
+        rec32[(long long)m * Layout32<D>::REC + Layout32<D>::XH + d] = hi;
+        rec32[(long long)m * Layout32<D>::REC + Layout32<D>::XL + d] = (float)(v - (double)hi);
+      }
+    }
+  }
+}
+
+__global__ void k_scatter_slots(int* __restrict__ slot_of, const int* __restrict__ idx, int k, int set) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < k) slot_of[idx[q]] = set ? q : -1;
+}
 
 __global__ void k_ell_reduce(const double* __restrict__ rl, int N, EvalStatus* st) {
   __shared__ double sh[1024];
@@ -523,6 +613,16 @@ struct hawkes_ctx {
   bool capturing = false;
   int64_t graph_launches[3] = {0, 0, 0};
   int evals_same_consts = 0;   // evaluations since the last constants change
+  // block moves (hawkes_propose_move / hawkes_accept_move)
+  int* d_slot_of = nullptr;    // N, -1 or the event's index in the pending proposal
+  int* d_move_idx = nullptr;   // MOVE_MAX
+  double* d_move_x = nullptr;  // MOVE_MAX x D
+  double* d_move_delta = nullptr;  // Npad x 2
+  double* d_move_rows = nullptr;   // MOVE_MAX x 2
+  double* d_move_part = nullptr;   // ceil(N/256) block sums
+  double* d_move_rows_part = nullptr;  // MOVE_MAX x ceil(N/MOVE_SPLIT) x 2
+  bool lam_valid = false;      // rates[][] hold lambda of the current state (all rows)
+  int move_k = 0;              // pending proposal size (0: none)
   int sym_variant = 40;     // 10 * rows-per-lane + exp scheme (tuning knob HAWKES_SYM_VARIANT)
 };
 
@@ -910,6 +1010,51 @@ struct PackTD {
 };
 
 template <int D>
+struct MoveD {
+  static int run(hawkes_ctx* ctx, int k) {
+    MoveArgs<D> a;
+    a.rec = ctx->rec;
+    a.gid = ctx->gid;
+    a.slot_of = ctx->d_slot_of;
+    a.idx = ctx->d_move_idx;
+    a.new_x = ctx->d_move_x;
+    a.k = k;
+    a.N = (int)ctx->N;
+    a.c = ctx->pc;
+    a.tab = ctx->tab;
+    k_move_delta<D><<<(unsigned)((ctx->N + 255) / 256), 256, 0, ctx->stream>>>(a, ctx->tab, ctx->d_move_delta);
+    CHECK_LAUNCH();
+    const int nsplit = (int)((ctx->N + MOVE_SPLIT - 1) / MOVE_SPLIT);
+    k_move_rows<D><<<dim3(k, nsplit), 256, 0, ctx->stream>>>(a, ctx->tab, ctx->d_move_rows_part);
+    CHECK_LAUNCH();
+    k_move_rows_combine<<<(k + 127) / 128, 128, 0, ctx->stream>>>(ctx->d_move_rows_part, k, nsplit,
+                                                                  ctx->d_move_rows);
+    CHECK_LAUNCH();
+    const int nb = (int)((ctx->N + 255) / 256);
+    k_move_terms<<<nb, 256, 0, ctx->stream>>>(ctx->rates, ctx->d_move_delta, ctx->d_move_rows,
+                                              ctx->d_slot_of, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2,
+                                              ctx->fc.zero_floor, ctx->d_move_part);
+    CHECK_LAUNCH();
+    k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_move_part, nb, &ctx->st->dell);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct CommitD {
+  static int run(hawkes_ctx* ctx) {
+    const int n = (int)std::max<int64_t>(ctx->N, ctx->move_k);
+    k_move_commit<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(
+        ctx->rates, ctx->d_move_delta, ctx->d_move_rows, ctx->d_slot_of, ctx->d_move_idx,
+        ctx->d_move_x, ctx->move_k, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2, ctx->rec, ctx->rec32,
+        ctx->st);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
 struct DriftD {
   static int run(hawkes_ctx* ctx, double eps, bool box, bool minv) {
     const int n = (int)ctx->N;
@@ -1050,6 +1195,7 @@ int run_rates(hawkes_ctx* ctx) {
     ctx->rates_valid = true;
     ctx->rates_exchanged = false;
     ctx->grad_valid = false;
+    ctx->lam_valid = true;
     return HAWKES_OK;
   }
   CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
@@ -1070,6 +1216,7 @@ int run_rates(hawkes_ctx* ctx) {
   ctx->rates_valid = true;
   ctx->rates_exchanged = false;
   ctx->grad_valid = false;
+  ctx->lam_valid = true;
   return HAWKES_OK;
 }
 
@@ -1080,6 +1227,7 @@ int run_grad(hawkes_ctx* ctx) {
     TRY(replay(ctx, ctx->rates_valid ? 2 : 1));
     if (!ctx->rates_valid) ctx->rates_exchanged = false;
     ctx->rates_valid = ctx->grad_valid = true;
+    ctx->lam_valid = true;
     return HAWKES_OK;
   }
   TRY(run_rates(ctx));
@@ -1111,6 +1259,17 @@ int fetch_status(hawkes_ctx* ctx) {
     CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
     return set_err(ctx, HAWKES_ERR_NONFINITE,
                    "locations contain NaN/Inf or |x| > 1e100 (device-side validation)");
+  }
+  return HAWKES_OK;
+}
+
+// drop a pending block move (restores the event -> proposal-slot map)
+int clear_move(hawkes_ctx* ctx) {
+  if (ctx->move_k > 0) {
+    k_scatter_slots<<<(ctx->move_k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx,
+                                                                        ctx->move_k, 0);
+    CHECK_LAUNCH();
+    ctx->move_k = 0;
   }
   return HAWKES_OK;
 }
@@ -1430,8 +1589,16 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
       (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W)) ||
       (rc = dalloc(ctx, &ctx->tab, EXP_TABLE)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
-      (rc = dalloc(ctx, &ctx->st, 1)) || (rc = dalloc(ctx, &ctx->d_consts, 1)))
+      (rc = dalloc(ctx, &ctx->st, 1)) || (rc = dalloc(ctx, &ctx->d_consts, 1)) ||
+      (rc = dalloc(ctx, &ctx->d_slot_of, (size_t)N)) || (rc = dalloc(ctx, &ctx->d_move_idx, MOVE_MAX)) ||
+      (rc = dalloc(ctx, &ctx->d_move_x, (size_t)MOVE_MAX * D)) ||
+      (rc = dalloc(ctx, &ctx->d_move_delta, (size_t)ctx->npad * 2)) ||
+      (rc = dalloc(ctx, &ctx->d_move_rows, (size_t)MOVE_MAX * 2)) ||
+      (rc = dalloc(ctx, &ctx->d_move_part, (size_t)(N + 255) / 256)) ||
+      (rc = dalloc(ctx, &ctx->d_move_rows_part, (size_t)MOVE_MAX * 2 * ((N + MOVE_SPLIT - 1) / MOVE_SPLIT))))
     return fail(rc);
+  if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess)
+    return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   if (o.world == 1 && ctx->W == 1 && !getenv("HAWKES_NO_GRAPHS")) {
     if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
@@ -1542,7 +1709,8 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
   }
-  void* bufs[] = {ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
+  void* bufs[] = {ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
+                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
@@ -1589,7 +1757,8 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   ctx->fc.tN = ctx->tN;
   TRY(upload_consts(ctx));
   ctx->have_t = true;
-  ctx->rates_valid = ctx->grad_valid = false;
+  ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+  TRY(clear_move(ctx));
   return HAWKES_OK;
 }
 
@@ -1606,7 +1775,8 @@ int hawkes_set_locations(hawkes_ctx* ctx, const double* x, int32_t mem) {
   TRY(copy_in(ctx, ctx->xstage, x, n, mem));
   TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
   ctx->have_x = true;
-  ctx->rates_valid = ctx->grad_valid = false;
+  ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+  TRY(clear_move(ctx));
   return HAWKES_OK;
 }
 
@@ -1622,7 +1792,8 @@ int hawkes_set_params(hawkes_ctx* ctx, const hawkes_params* p) {
   TRY(compute_constants(ctx, *p, ctx->tN));
   ctx->params = *p;
   ctx->have_p = true;
-  ctx->rates_valid = ctx->grad_valid = false;
+  ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+  TRY(clear_move(ctx));
   return HAWKES_OK;
 }
 
@@ -1711,6 +1882,7 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
     TRY(copy_in(ctx, ctx->lf_hi, box_hi, n, mem));
   }
   CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+  TRY(clear_move(ctx));
   TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
   ctx->have_x = true;
   ctx->rates_valid = ctx->grad_valid = false;
@@ -1734,6 +1906,64 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
   if (out_kin) *out_kin = ctx->h_st->kinetic;
   if (ctx->h_st->undefined)
     return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "ell = -inf during the trajectory");
+  return HAWKES_OK;
+}
+
+int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const double* new_x,
+                        int32_t mem, double* out_delta) {
+  ENTER(ctx);
+  if (!idx || !new_x || !out_delta || k < 1 || k > MOVE_MAX ||
+      (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_propose_move (1 <= k <= %d)", MOVE_MAX);
+  TRY(check_ready(ctx));
+  const int D = ctx->D;
+  std::vector<int> hidx(idx, idx + k);
+  {
+    std::vector<int> sorted = hidx;
+    std::sort(sorted.begin(), sorted.end());
+    for (int q = 0; q < k; ++q)
+      if (sorted[q] < 0 || sorted[q] >= ctx->N || (q && sorted[q] == sorted[q - 1]))
+        return set_err(ctx, HAWKES_ERR_ARG, "move indices must be distinct and in [0, N)");
+  }
+  std::vector<double> hx((size_t)k * D);
+  if (mem == HAWKES_MEM_DEVICE) {
+    CU(cudaMemcpyAsync(hx.data(), new_x, hx.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  } else {
+    memcpy(hx.data(), new_x, hx.size() * sizeof(double));
+  }
+  for (double v : hx)
+    if (!finite_bounded(v)) return set_err(ctx, HAWKES_ERR_NONFINITE, "proposed location not finite");
+  TRY(clear_move(ctx));
+  if (!ctx->lam_valid) {
+    ctx->rates_valid = false;
+    TRY(run_rates(ctx));
+    if (!ctx->pairs && !ctx->rates_exchanged) {
+      TRY(exchange_rows(ctx, ctx->rates, 4));
+      ctx->rates_exchanged = true;
+    }
+  }
+  CU(cudaMemcpyAsync(ctx->d_move_idx, hidx.data(), k * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_move_x, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 1);
+  CHECK_LAUNCH();
+  ctx->move_k = k;
+  TRY(dispatchD<MoveD>(D, ctx, k));
+  TRY(fetch_status(ctx));
+  *out_delta = ctx->h_st->dell;
+  return HAWKES_OK;
+}
+
+int hawkes_accept_move(hawkes_ctx* ctx) {
+  ENTER(ctx);
+  if (ctx->move_k <= 0) return set_err(ctx, HAWKES_ERR_STATE, "no pending move");
+  TRY(dispatchD<CommitD>(ctx->D, ctx));
+  TRY(clear_move(ctx));
+  ctx->rates_valid = ctx->grad_valid = false;   // rho', G1 and ell_n of the old state
+  ctx->rates_exchanged = true;                  // every rank updated every row
+  ctx->lam_valid = true;
+  CU(cudaStreamSynchronize(ctx->stream));
   return HAWKES_OK;
 }
 

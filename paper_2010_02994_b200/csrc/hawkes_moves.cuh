@@ -1,0 +1,149 @@
+// hawkes_moves.cuh -- block Metropolis-Hastings over locations: Delta ell for moving k events.
+//
+// The paper's DC and Alaska samplers update locations with "a Metropolis-Hastings kernel
+// with block-wise updates over sets of individual location variables".  Moving
+// the events S to new positions leaves every Lambda_n unchanged (P:L92-93 has no x) and
+// changes lambda_n only through the pairs that touch S:
+//   n not in S:  lambda_n' = lambda_n + sum_{m in S} [lambda_nm(x_m') - lambda_nm(x_m)]
+//   n in S:      lambda_n' = sum_j lambda_nj(X')            (full row, O(N))
+//   Delta ell = sum_n log(lambda_n' / lambda_n)              (Eq. 1)
+// so a proposal costs O(k N) instead of the O(N^2) of a fresh evaluation.  Pair terms use
+// the same scaled-domain exps as the pass kernels (alpha mu 2^64, beta xi 2^64).
+#pragma once
+#include "hawkes_kernels.cuh"
+
+namespace hk {
+
+constexpr int MOVE_MAX = 256;   // events per proposal (one shared-memory batch)
+
+template <int D>
+struct MoveArgs {
+  const double* rec;       // event records (x, t, ...)
+  const int* gid;
+  const int* slot_of;      // N: index into the proposal, or -1
+  const int* idx;          // k moved events
+  const double* new_x;     // k x D proposed locations
+  int k, N;
+  PassConst c;
+  const int2* tab;
+};
+
+// pair term parts (scaled) for event n at xn against event m at xm, times/ties from records
+template <int D>
+__device__ __forceinline__ void move_pair(const double* xn, double tn, int gn, const double* xm,
+                                          double tm, int gm, const PassConst& c,
+                                          const int2* __restrict__ tab, double& eb, double& es) {
+  double r2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double dx = xm[d] - xn[d];
+    r2 = fma(dx, dx, r2);
+  }
+  const double dt = tn - tm;
+  eb = gm == gn ? 0.0 : fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
+  es = gm < gn ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
+}
+
+// rows not in S: (delta M', delta X') from the k moved events
+template <int D>
+__global__ void k_move_delta(MoveArgs<D> a, const int2* __restrict__ gtab, double* __restrict__ dout) {
+  using L = Layout<D>;
+  __shared__ int2 tab[EXP_TABLE];
+  __shared__ double sx_old[MOVE_MAX * D], sx_new[MOVE_MAX * D], st[MOVE_MAX];
+  __shared__ int sg[MOVE_MAX];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  for (int q = threadIdx.x; q < a.k; q += blockDim.x) {
+    const int m = a.idx[q];
+    const double* rm = a.rec + (long long)m * L::REC;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      sx_old[q * D + d] = rm[d];
+      sx_new[q * D + d] = a.new_x[q * D + d];
+    }
+    st[q] = rm[D];
+    sg[q] = a.gid[m];
+  }
+  __syncthreads();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.N) return;
+  double dM = 0.0, dX = 0.0;
+  if (a.slot_of[n] < 0) {
+    const double* rn = a.rec + (long long)n * L::REC;
+    double xn[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) xn[d] = rn[d];
+    const double tn = rn[D];
+    const int gn = a.gid[n];
+    for (int q = 0; q < a.k; ++q) {
+      double eb0, es0, eb1, es1;
+      move_pair<D>(xn, tn, gn, sx_old + q * D, st[q], sg[q], a.c, tab, eb0, es0);
+      move_pair<D>(xn, tn, gn, sx_new + q * D, st[q], sg[q], a.c, tab, eb1, es1);
+      dM += eb1 - eb0;
+      dX += es1 - es0;
+    }
+  }
+  dout[2 * (long long)n] = dM;
+  dout[2 * (long long)n + 1] = dX;
+}
+
+// rows in S: full (M', X') at the proposed configuration.  Block (q, s) sums the j range
+// [s*MOVE_SPLIT, (s+1)*MOVE_SPLIT) for moved event q (strided per thread, fixed tree);
+// k_move_rows_combine adds the split partials in order.
+constexpr int MOVE_SPLIT = 4096;
+
+template <int D>
+__global__ void k_move_rows(MoveArgs<D> a, const int2* __restrict__ gtab, double* __restrict__ rows_part) {
+  using L = Layout<D>;
+  __shared__ int2 tab[EXP_TABLE];
+  __shared__ double shM[256], shX[256];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  __syncthreads();
+  const int q = blockIdx.x;
+  const int n = a.idx[q];
+  double xn[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) xn[d] = a.new_x[q * D + d];
+  const double tn = a.rec[(long long)n * L::REC + D];
+  const int gn = a.gid[n];
+  const int j0 = blockIdx.y * MOVE_SPLIT, j1 = min(a.N, j0 + MOVE_SPLIT);
+  double M = 0.0, X = 0.0;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    const double* rj = a.rec + (long long)j * L::REC;
+    const int sj = a.slot_of[j];
+    const double* xj = sj >= 0 ? a.new_x + sj * D : rj;
+    double eb, es;
+    move_pair<D>(xn, tn, gn, xj, rj[D], a.gid[j], a.c, tab, eb, es);
+    M += eb;
+    X += es;
+  }
+  shM[threadIdx.x] = M;
+  shX[threadIdx.x] = X;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      shM[threadIdx.x] += shM[threadIdx.x + w];
+      shX[threadIdx.x] += shX[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const long long o = 2 * ((long long)q * gridDim.y + blockIdx.y);
+    rows_part[o] = shM[0];
+    rows_part[o + 1] = shX[0];
+  }
+}
+
+__global__ void k_move_rows_combine(const double* __restrict__ rows_part, int k, int nsplit,
+                                    double* __restrict__ rows) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= k) return;
+  double M = 0.0, X = 0.0;
+  for (int s = 0; s < nsplit; ++s) {
+    M += rows_part[2 * ((long long)q * nsplit + s)];
+    X += rows_part[2 * ((long long)q * nsplit + s) + 1];
+  }
+  rows[2 * q] = M;
+  rows[2 * q + 1] = X;
+}
+
+}  // namespace hk

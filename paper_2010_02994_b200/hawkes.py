@@ -152,6 +152,21 @@ class HawkesContext:
                                         ctypes.byref(ll), ctypes.byref(kin)), self._h)
         return x, p, ll.value, kin.value
 
+    # -- block Metropolis-Hastings moves
+    def propose_move(self, idx, new_x) -> float:
+        """hawkes_propose_move: ell(X') - ell(X) for events idx moved to new_x (k x D)."""
+        idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1)
+        p, mem, keep = _ptr_mem(new_x)
+        out = ctypes.c_double()
+        check(self._lib.hawkes_propose_move(self._h, int(idx.size),
+                                            idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                            p, mem, ctypes.byref(out)), self._h)
+        return out.value
+
+    def accept_move(self):
+        """hawkes_accept_move: commit the pending proposal."""
+        check(self._lib.hawkes_accept_move(self._h), self._h)
+
     # -- timing (CUDA events recorded by the library around the two pass kernels)
     def enable_timing(self, enable: bool = True):
         check(self._lib.hawkes_enable_timing(self._h, int(bool(enable))), self._h)
