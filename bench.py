@@ -298,8 +298,7 @@ def run_ours(args):
     pairs_alg = pairs / world                   # each rank's launches cover 1/W of the pairs
     unordered = ctx.algorithm in ("auto", "pairs") and args.precision == "fp64"
     if unordered:
-        names = ("rate pass: sym_kernel<2,1> + pass_kernel<2,1> (diagonal chunks)",
-                 "gradient pass: sym_kernel<2,2> + pass_kernel<2,2> (diagonal chunks)")
+        names = ("rate pass: sym_kernel<2,1,4,0>", "gradient pass: sym_kernel<2,2,4,0>")
         executed = (17.0, 17.0)                 # FP64 instructions per ordered pair (SASS)
     else:
         names = ("rate pass: pass_kernel<2,1>", "gradient pass: pass_kernel<2,2>")
