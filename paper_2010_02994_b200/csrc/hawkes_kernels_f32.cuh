@@ -328,35 +328,107 @@ __device__ __forceinline__ void sym32_pair(const SymRow32<D>& row, const float* 
   }
 }
 
+// Two rows of one lane against one column, packed into f32x2 instructions (sm_100
+// FADD2/FMUL2/FFMA2): every FP32 instruction serves two pairs; the two exps stay on MUFU.
+// Row data are stored negated (nxh = -x_hi, ...) so differences are packed adds.
+template <int D>
+struct RowPair32 {
+  float2 nxh[D], nxl[D];
+  float2 nth, ntl, rho;
+  int ga, gb;
+};
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+template <int D, int PASS, bool MASK>
+__device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float (&cxh)[D],
+                                            const float (&cxl)[D], float cth, float ctl,
+                                            float crho, bool dead_a, bool dead_b, float2& rM,
+                                            float2 (&rG)[D], float2& cM, float2& cX,
+                                            float2 (&cG)[D], const PassConst32& c) {
+  float2 dx[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    dx[d] = __fadd2_rn(__fadd2_rn(f2(cxh[d]), rp.nxh[d]), __fadd2_rn(f2(cxl[d]), rp.nxl[d]));
+  float2 r2 = __fmul2_rn(dx[0], dx[0]);
+#pragma unroll
+  for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
+  const float2 dt = __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
+  const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
+  const float2 as = __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), dt, f2(c.cs)));
+  float2 eb = make_float2(ex2f(ab.x), ex2f(ab.y));
+  float2 es = make_float2(ex2f(as.x), ex2f(as.y));
+  if (MASK) {
+    eb.x = dead_a ? 0.f : eb.x;
+    es.x = dead_a ? 0.f : es.x;
+    eb.y = dead_b ? 0.f : eb.y;
+    es.y = dead_b ? 0.f : es.y;
+  }
+  if (PASS == 1) {
+    rM = __fadd2_rn(rM, eb);
+    cM = __fadd2_rn(cM, eb);
+    cX = __fadd2_rn(cX, es);
+    const float2 ncc = __fadd2_rn(make_float2(-eb.x, -eb.y), make_float2(-es.x, -es.y));
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      rG[d] = __ffma2_rn(eb, dx[d], rG[d]);
+      cG[d] = __ffma2_rn(ncc, dx[d], cG[d]);
+    }
+  } else {
+    const float2 cr = __fmul2_rn(f2(crho), __fadd2_rn(eb, es));
+    const float2 ncc = __fmul2_rn(make_float2(-rp.rho.x, -rp.rho.y), eb);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      rG[d] = __ffma2_rn(cr, dx[d], rG[d]);
+      cG[d] = __ffma2_rn(ncc, dx[d], cG[d]);
+    }
+  }
+}
+
 template <int D, int PASS, bool MASK, int SR>
-__device__ __forceinline__ void sym32_group(const SymRow32<D> (&row)[SR],
+__device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag,
-                                            float (&rM)[SR], float (&rG)[SR][D],
+                                            float2 (&rM)[SR / 2], float2 (&rG)[SR / 2][D],
                                             float (&cacc)[2 + D], const PassConst32& c) {
-  constexpr int REC = Layout32<D>::REC;
+  using L = Layout32<D>;
+  constexpr int REC = L::REC;
   const int lane = threadIdx.x & 31;
 #pragma unroll 2
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
     const float* rc = grp + src * REC;
+    float cxh[D], cxl[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      cxh[d] = rc[L::XH + d];
+      cxl[d] = rc[L::XL + d];
+    }
+    const float cth = rc[L::TH], ctl = rc[L::TL];
+    const float crho = PASS == 2 ? rc[L::RHO] : 0.f;
     int cg = 0;
     bool cv = true;
     if (MASK) {
       cg = __shfl_sync(0xffffffffu, cg0, src);
       cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
     }
-    float cG[D];
+    float2 cM = make_float2(cacc[0], 0.f), cX = make_float2(cacc[1], 0.f), cG[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) cG[d] = cacc[2 + d];
+    for (int d = 0; d < D; ++d) cG[d] = make_float2(cacc[2 + d], 0.f);
 #pragma unroll
-    for (int r = 0; r < SR; ++r) {
-      const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
-                                 (diag && cidx0 + src <= ridx0 + 32 * r));
-      sym32_pair<D, PASS, MASK>(row[r], rc, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c);
+    for (int h = 0; h < SR / 2; ++h) {
+      bool da = false, db = false;
+      if (MASK) {
+        const int ia = ridx0 + 32 * (2 * h), ib = ridx0 + 32 * (2 * h + 1);
+        da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
+        db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
+      }
+      sym32_pair2<D, PASS, MASK>(rp[h], cxh, cxl, cth, ctl, crho, da, db, rM[h], rG[h], cM, cX, cG, c);
     }
+    cacc[0] = cM.x + cM.y;
+    cacc[1] = cX.x + cX.y;
 #pragma unroll
-    for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
+    for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d].x + cG[d].y;
     const int nxt = (lane + 1) & 31;
     if (PASS == 1) {
       cacc[0] = __shfl_sync(0xffffffffu, cacc[0], nxt);
@@ -436,21 +508,26 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
     for (int rt = 0; rt < n_rt; ++rt) {
       const int row0 = r0 + rt * SRT;
       const bool rows_full = row0 + SRT <= r1;
-      SymRow32<D> row[SR];
+      RowPair32<D> rp[SR / 2];
       double rM[SR], rG[SR][D];
 #pragma unroll
-      for (int r = 0; r < SR; ++r) {
-        const int i = row0 + lane + 32 * r;
-        const float* ri = a.rec + (long long)min(i, N - 1) * REC;
+      for (int h = 0; h < SR / 2; ++h) {
+        const int ia = row0 + lane + 32 * (2 * h), ib = ia + 32;
+        const float* ra = a.rec + (long long)min(ia, N - 1) * REC;
+        const float* rb = a.rec + (long long)min(ib, N - 1) * REC;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          row[r].xh[d] = ri[L::XH + d];
-          row[r].xl[d] = ri[L::XL + d];
+          rp[h].nxh[d] = make_float2(-ra[L::XH + d], -rb[L::XH + d]);
+          rp[h].nxl[d] = make_float2(-ra[L::XL + d], -rb[L::XL + d]);
         }
-        row[r].th = ri[L::TH];
-        row[r].tl = ri[L::TL];
-        row[r].rho = ri[L::RHO];
-        row[r].g = i < N ? a.gid[i] : -1;
+        rp[h].nth = make_float2(-ra[L::TH], -rb[L::TH]);
+        rp[h].ntl = make_float2(-ra[L::TL], -rb[L::TL]);
+        rp[h].rho = make_float2(ra[L::RHO], rb[L::RHO]);
+        rp[h].ga = ia < N ? a.gid[ia] : -1;
+        rp[h].gb = ib < N ? a.gid[ib] : -1;
+      }
+#pragma unroll
+      for (int r = 0; r < SR; ++r) {
         rM[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
@@ -472,26 +549,30 @@ __global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
         float cacc[2 + D];
 #pragma unroll
         for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.f;
-        float rM32[SR], rG32[SR][D];
+        float2 rM32[SR / 2], rG32[SR / 2][D];
 #pragma unroll
-        for (int r = 0; r < SR; ++r) {
-          rM32[r] = 0.f;
+        for (int h = 0; h < SR / 2; ++h) {
+          rM32[h] = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int d = 0; d < D; ++d) rG32[r][d] = 0.f;
+          for (int d = 0; d < D; ++d) rG32[h][d] = make_float2(0.f, 0.f);
         }
         const bool diag_tile = diag && ct == rt;
         const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
         if (strict)
-          sym32_group<D, PASS, false, SR>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+          sym32_group<D, PASS, false, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
                                           jt + warp * 32, false, rM32, rG32, cacc, c);
         else
-          sym32_group<D, PASS, true, SR>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+          sym32_group<D, PASS, true, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
                                          jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
 #pragma unroll
-        for (int r = 0; r < SR; ++r) {
-          rM[r] += (double)rM32[r];
+        for (int h = 0; h < SR / 2; ++h) {
+          rM[2 * h] += (double)rM32[h].x;
+          rM[2 * h + 1] += (double)rM32[h].y;
 #pragma unroll
-          for (int d = 0; d < D; ++d) rG[r][d] += (double)rG32[r][d];
+          for (int d = 0; d < D; ++d) {
+            rG[2 * h][d] += (double)rG32[h][d].x;
+            rG[2 * h + 1][d] += (double)rG32[h][d].y;
+          }
         }
         if (cvalid) {
           if (PASS == 1) {

@@ -354,3 +354,26 @@ def test_graph_replay_matches_fresh_contexts():
             ef, gf = fresh(x, th)
             assert e == ef and ell_l == ef
             assert np.array_equal(g.cpu().numpy(), gf)
+
+
+def test_full_size_c4_gradient_rows_vs_oracle():
+    """BASELINE configs[3] at N = 100k in the bench's launch configuration: the oracle's
+    rates for all events (O(N^2), ~30 s on the host cores), then its App. A gradient for
+    sampled rows, against the GPU gradient under the fp64 tolerance rule."""
+    c = synth.config("C4")
+    from paper_2010_02994_b200 import HawkesContext
+    with HawkesContext(c.N, 2) as ctx:
+        ctx.set_times(torch.from_numpy(c.t).cuda())
+        ctx.set_params(c.theta)
+        ctx.set_locations(torch.from_numpy(c.x).cuda())
+        g, ell = ctx.grad_locations()
+        g = g.cpu().numpy()
+    lam, _, _ = oracle.rates(c.x, c.t, c.theta)
+    Lam = oracle.Lambda(c.t, c.theta)
+    ell_ref = math.fsum(np.log(lam) - Lam)
+    assert abs(ell - ell_ref) <= 1e-9 * abs(ell_ref)
+    rows = np.unique(np.concatenate([np.arange(0, c.N, 997), [c.N - 1, 127, 128, 767, 768]]))
+    for r in rows[::8]:
+        gr, S = oracle.grad(c.x, c.t, c.theta, lam=lam, rows=slice(int(r), int(r) + 1))
+        bound = 1e-9 * np.maximum(np.abs(gr[r]), 1e-3 * S[r])
+        assert np.all(np.abs(g[r] - gr[r]) <= bound), (r, g[r], gr[r])
