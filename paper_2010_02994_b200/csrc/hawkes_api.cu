@@ -1289,13 +1289,14 @@ int chunk_of(long long N) {
   return (int)c;
 }
 
-// PAIRS chunk: a multiple of the sym kernel's 128-event tile, ~N/138 so that the C(C+1)/2
-// chunk pairs give >= ~16 work items per CTA slot while the [C+1][Npad][K] partial arrays
-// stay ~C*N*48 bytes; 128 for N <= ~17k (latency: small catalogs still fill the GPU).
-// A function of N only.
-int chunk_pairs_of(long long N) {
-  long long c = (N + 137) / 138;
-  c = ((c + TILE_J - 1) / TILE_J) * TILE_J;
+// PAIRS chunk: a multiple of the sym kernel's 128-event tile, ~N/(138 sqrt(W)) so that the
+// C(C+1)/2 chunk pairs give every rank >= ~16 work items per CTA slot (tail < ~5 %) while
+// the [C+1][Npad][K] partial arrays stay ~C*N*48 bytes; 128 for small N (latency: small
+// catalogs still fill the GPU).  PAIRS sums are not bitwise W-independent anyway (the
+// per-event partials meet in an allreduce), so the chunk may depend on W.
+int chunk_pairs_of(long long N, int W) {
+  const double C = 138.0 * sqrt((double)std::max(1, W));
+  long long c = (long long)llround((double)N / C / TILE_J) * TILE_J;   // nearest multiple
   return (int)std::max<long long>(TILE_J, c);
 }
 
@@ -1560,7 +1561,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   }
   if (const char* v = getenv("HAWKES_SYM_VARIANT")) ctx->sym_variant = atoi(v);
   ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || o.algorithm == HAWKES_ALGO_AUTO;
-  ctx->chunk = ctx->pairs ? chunk_pairs_of(N) : chunk_of(N);
+  ctx->chunk = ctx->pairs ? chunk_pairs_of(N, o.world > 1 ? o.world : std::max(1, o.emulate_world))
+                           : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
   ctx->nslots = ctx->nchunks + (ctx->pairs ? 1 : 0);   // PAIRS: + diagonal column slot
   ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);
@@ -2010,7 +2012,7 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
                       int32_t* n_items, int32_t* chunk) {
   if (N < 1 || N > (1LL << 30) || world < 1 || rank < 0 || rank >= world || !n_items)
     return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan_pairs");
-  const int ck = chunk_pairs_of(N);
+  const int ck = chunk_pairs_of(N, world);
   const int C = (int)((N + ck - 1) / ck);
   const std::vector<int> own = pair_owners(N, ck, world);
   int cnt = 0;
