@@ -61,7 +61,7 @@ typedef enum {
   HAWKES_ERR_OOM = -10            /* device allocation failed                                */
 } hawkes_status;
 
-#define HAWKES_MAX_D 4
+#define HAWKES_MAX_D 8
 
 typedef enum {
   HAWKES_FP64 = 0, /* fp64 pair arithmetic and sums (reference precision, reading R13)     */
@@ -77,8 +77,8 @@ typedef enum { HAWKES_MEM_HOST = 0, HAWKES_MEM_DEVICE = 1 } hawkes_mem;
  *  PAIRS -- unordered pairs: chunk pairs (a < b) evaluate each pair's two exps once and
  *           feed both events (2 exps per ordered pair over both
  *           passes); W > 1 shards chunk pairs and allreduces per-event partial sums;
- *           results are deterministic for a fixed W.
- *  AUTO  -- PAIRS. */
+ *           results are deterministic for a fixed W.  D <= 4.
+ *  AUTO  -- PAIRS for D <= 4, ROWS for D = 5..8. */
 typedef enum { HAWKES_ALGO_AUTO = 0, HAWKES_ALGO_ROWS = 1, HAWKES_ALGO_PAIRS = 2 } hawkes_algorithm;
 
 typedef struct {

@@ -38,6 +38,7 @@ using namespace hk;
 namespace {
 
 constexpr int R_ROWS = 2;                    // rows per thread
+constexpr int SYM_MAX_D = 4;                 // unordered-pair kernels: register tile of 4 rows
 constexpr int RT = THREADS * R_ROWS;         // rows per row tile
 constexpr int FIN_THREADS = RT;              // finalize: one thread per row of a tile
 constexpr double LN2 = 0.693147180559945309417232121458;
@@ -706,6 +707,10 @@ int dispatchD(int D, A&&... a) {
     case 2: return F<2>::run(a...);
     case 3: return F<3>::run(a...);
     case 4: return F<4>::run(a...);
+    case 5: return F<5>::run(a...);
+    case 6: return F<6>::run(a...);
+    case 7: return F<7>::run(a...);
+    case 8: return F<8>::run(a...);
   }
   return HAWKES_ERR_DIM;
 }
@@ -781,7 +786,7 @@ struct SetupD {
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
       ctx->grid1 = std::max(1, b1) * ctx->sms;
       ctx->grid2 = std::max(1, b2) * ctx->sms;
-      if (ctx->pairs) {
+      if constexpr (D <= SYM_MAX_D) if (ctx->pairs) {
         auto s1 = sym_kernel_f32<D, 1, SYM32_R>;
         auto s2 = sym_kernel_f32<D, 2, SYM32_R>;
         CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1>()));
@@ -803,7 +808,7 @@ struct SetupD {
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
     ctx->grid1 = std::max(1, b1) * ctx->sms;
     ctx->grid2 = std::max(1, b2) * ctx->sms;
-    if (ctx->pairs) TRY(sym_call<D>(ctx, 0, nullptr));
+    if constexpr (D <= SYM_MAX_D) if (ctx->pairs) TRY(sym_call<D>(ctx, 0, nullptr));
     return HAWKES_OK;
   }
 };
@@ -867,7 +872,7 @@ struct PassD {
         pass_kernel<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
       CHECK_LAUNCH();
     }
-    if (ctx->pairs && ctx->n_sym[rank] > 0) {
+    if constexpr (D <= SYM_MAX_D) if (ctx->pairs && ctx->n_sym[rank] > 0) {
       SymArgs b;
       b.rec = ctx->rec;
       b.gid = ctx->gid;
@@ -908,7 +913,7 @@ struct PassD {
         pass_kernel_f32<D, 2, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
       CHECK_LAUNCH();
     }
-    if (ctx->pairs && ctx->n_sym[rank] > 0) {
+    if constexpr (D <= SYM_MAX_D) if (ctx->pairs && ctx->n_sym[rank] > 0) {
       SymArgs32 b;
       b.rec = ctx->rec32;
       b.gid = ctx->gid;
@@ -1560,7 +1565,11 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     return set_err(nullptr, HAWKES_ERR_ARG, "bad algorithm");
   }
   if (const char* v = getenv("HAWKES_SYM_VARIANT")) ctx->sym_variant = atoi(v);
-  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || o.algorithm == HAWKES_ALGO_AUTO;
+  if (o.algorithm == HAWKES_ALGO_PAIRS && D > SYM_MAX_D) {
+    delete ctx;
+    return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_ALGO_PAIRS supports D <= %d", SYM_MAX_D);
+  }
+  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || (o.algorithm == HAWKES_ALGO_AUTO && D <= SYM_MAX_D);
   ctx->chunk = ctx->pairs ? chunk_pairs_of(N, o.world > 1 ? o.world : std::max(1, o.emulate_world))
                            : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);

@@ -221,7 +221,7 @@ struct PassArgs {
 };
 
 template <int D, int PASS, int R>
-__global__ void __launch_bounds__(THREADS, 4) pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(THREADS, D <= 4 ? 4 : 3) pass_kernel(PassArgs a) {
   using L = Layout<D>;
   constexpr int REC = L::REC;
   constexpr int RT = THREADS * R;

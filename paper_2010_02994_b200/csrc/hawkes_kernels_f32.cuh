@@ -113,7 +113,7 @@ struct PassArgs32 {
 };
 
 template <int D, int PASS, int R>
-__global__ void __launch_bounds__(THREADS, 4) pass_kernel_f32(PassArgs32 a) {
+__global__ void __launch_bounds__(THREADS, D <= 4 ? 4 : 3) pass_kernel_f32(PassArgs32 a) {
   using L = Layout32<D>;
   using L64 = Layout<D>;
   constexpr int REC = L::REC;
@@ -454,7 +454,7 @@ struct SymArgs32 {
 };
 
 template <int D, int PASS, int SR>
-__global__ void __launch_bounds__(THREADS, 4) sym_kernel_f32(SymArgs32 a) {
+__global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArgs32 a) {
   static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
   using L = Layout32<D>;

@@ -63,8 +63,9 @@ def test_ties(N, k):
     _check(synth.with_ties(N, k), f"ties N={N} k={k}")
 
 
-@pytest.mark.parametrize("D", [1, 3, 4])
+@pytest.mark.parametrize("D", [1, 3, 4, 5, 6, 8])
 def test_other_dimensions(D):
+    """D = 1..8 (the flu model's latent space uses D up to 8); D > 4 runs ROWS."""
     _check(synth.unit_square(900, config=22, D=D), f"D={D}")
 
 
@@ -289,7 +290,7 @@ def test_fp32_ragged_and_ties(N):
     _check_fp32(synth.with_ties(N, max(2, N // 10)), f"fp32 ties N={N}")
 
 
-@pytest.mark.parametrize("D", [1, 3, 4])
+@pytest.mark.parametrize("D", [1, 3, 4, 6, 8])
 def test_fp32_other_dimensions(D):
     _check_fp32(synth.unit_square(700, config=26, D=D), f"fp32 D={D}")
 
