@@ -96,23 +96,32 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(power) if power else None}
 
 
-def cpu_baseline(n_rows_target_s: float = 12.0):
+def _oracle_eval(c):
+    import oracle
+    ll, lam, _ = oracle.loglik(c.x, c.t, c.theta)
+    oracle.grad(c.x, c.t, c.theta, lam=lam)
+
+
+def _oracle_rate():
+    """Ordered pairs per second of one oracle ell + gradient evaluation on this host
+    (warm-up at N=500, then a probe at N=3000)."""
+    import synth
+    _oracle_eval(synth.unit_square(500, config=4))
+    c = synth.unit_square(3000, config=4)
+    t0 = time.perf_counter()
+    _oracle_eval(c)
+    return 3000 * 2999 / (time.perf_counter() - t0)
+
+
+def cpu_baseline(target_s: float = 12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
     full ell + gradient evaluation of the C4 generator at a smaller N chosen for ~10-15 s."""
-    import numpy as np
     import oracle
     import synth
-    c = synth.unit_square(1000, config=4)
-    t0 = time.perf_counter()
-    ll, lam, _ = oracle.loglik(c.x, c.t, c.theta)
-    oracle.grad(c.x, c.t, c.theta, lam=lam)
-    dt = time.perf_counter() - t0
-    per_pair = dt / (1000 * 999)
-    Ns = int(min(100_000, max(1000, (n_rows_target_s / per_pair) ** 0.5)))
+    Ns = int(min(100_000, max(1000, (target_s * _oracle_rate()) ** 0.5)))
     c = synth.unit_square(Ns, config=4)
     t0 = time.perf_counter()
-    ll, lam, _ = oracle.loglik(c.x, c.t, c.theta)
-    oracle.grad(c.x, c.t, c.theta, lam=lam)
+    _oracle_eval(c)
     dt = time.perf_counter() - t0
     pairs = Ns * (Ns - 1)
     return {"pairs_per_s": pairs / dt, "Ns": Ns, "seconds": dt, "cores": oracle.num_threads()}
@@ -126,14 +135,12 @@ def run_reference(args):
     import oracle
     import synth
     N = args.n
-    # size each step for ~3 s of oracle work
-    probe = cpu_baseline(n_rows_target_s=0.5)
-    Ns = int(min(N, max(1000, (3.0 / (1.0 / probe["pairs_per_s"])) ** 0.5)))
+    # each step: a full oracle evaluation sized for ~4 s on this host
+    Ns = int(min(N, max(1000, (4.0 * _oracle_rate()) ** 0.5)))
     c = synth.unit_square(Ns, config=4)
 
     def step():
-        ll, lam, _ = oracle.loglik(c.x, c.t, c.theta)
-        oracle.grad(c.x, c.t, c.theta, lam=lam)
+        _oracle_eval(c)
 
     for _ in range(args.warmup):
         step()
