@@ -61,6 +61,9 @@ def _load():
         lib.oracle_xi_pair.argtypes = [I, dp, dp, L, L, pp]
         lib.oracle_xi_pair.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_bmds.argtypes = [L, I, dp, dp, ctypes.c_double, dp, dp, dp]
+        lib.oracle_bmds_pair.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        lib.oracle_bmds_pair.restype = ctypes.c_double
         _lib = lib
     return _lib
 
@@ -210,3 +213,26 @@ def leapfrog(x, p, t, theta, step: float, n_steps: int, inv_mass=None, box_lo=No
     ell, _, _ = loglik(x, t, theta)
     kin = 0.5 * float(np.sum(p * p * minv))
     return x, p, ell, kin
+
+
+def bmds(x, Y, sigma: float, with_grad: bool = True, with_scale: bool = False):
+    """BMDS log density of the dissimilarities Y given locations x (Eq. bmdsLikelihood,
+    P:L158-184, normal constant kept) and its gradient in x.  Returns (logp, grad or None)
+    or, with_scale, (logp, grad, scale) with scale[n,d] = sum_n' |term_{nn'd}|."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    N, D = x.shape
+    assert Y.shape == (N, N)
+    lp = ctypes.c_double()
+    g = np.empty((N, D)) if (with_grad or with_scale) else None
+    sc = np.empty((N, D)) if with_scale else None
+    _check(_load().oracle_bmds(N, D, _dptr(x), _dptr(Y), float(sigma), ctypes.byref(lp), _dptr(g),
+                               _dptr(sc)), "bmds")
+    return (lp.value, g, sc) if with_scale else (lp.value, g)
+
+
+def bmds_pair(y: float, delta: float, sigma: float) -> float:
+    """r_{nn'} of Eq. bmdsLikelihood plus the normal constant 1/2 log(2 pi sigma^2)."""
+    return _load().oracle_bmds_pair(float(y), float(delta), float(sigma))

@@ -162,3 +162,37 @@ def config(name: str, N: Optional[int] = None, replicate: int = 0) -> Catalog:
 def momenta(N: int, D: int, seed: int = 7) -> np.ndarray:
     """Standard normal momenta for HMC tests / benches (Philox)."""
     return np.random.Generator(np.random.Philox(seed)).normal(size=(N, D))
+
+
+def bmds_dissimilarities(x: np.ndarray, sigma: float, seed: int = 0) -> np.ndarray:
+    """Synthetic BMDS data for latent locations x (N x D): y_nn' ~ N(|x_n - x_n'|, sigma^2)
+    truncated to y > 0 (rejection), symmetric, zero diagonal (P:L171-173 data model)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    N = x.shape[0]
+    diff = x[:, None, :] - x[None, :, :]
+    delta = np.sqrt(np.sum(diff * diff, axis=-1))
+    Y = np.zeros((N, N))
+    iu = np.triu_indices(N, 1)
+    d = delta[iu]
+    y = d + sigma * rng.normal(size=d.shape)
+    bad = y <= 0
+    while bad.any():
+        y[bad] = d[bad] + sigma * rng.normal(size=int(bad.sum()))
+        bad = y <= 0
+    Y[iu] = y
+    Y[(iu[1], iu[0])] = y
+    return Y
+
+
+def flu_shaped(N: int = 4733, D: int = 6, sigma: float = 0.3, replicate: int = 0):
+    """Flu-shaped synthetic BMDS + Hawkes workload (N = 4733 cases, latent D = 6):
+    latent locations from a 64-country Gaussian mixture in R^D, days over 12 years, and
+    dissimilarities drawn from the BMDS data model.  Returns (Catalog, Y, sigma)."""
+    rng, seed = _rng(6, replicate)
+    centres = rng.normal(0.0, 3.0, size=(64, D))
+    pick = rng.integers(0, 64, size=N)
+    x = centres[pick] + rng.normal(0.0, 0.5, size=(N, D))
+    t = np.sort(rng.uniform(0.0, 4383.0, size=N))
+    theta = (0.5, 2.0, 60.0, 0.5, 0.1, 0.5)
+    Y = bmds_dissimilarities(x, sigma, seed=seed)
+    return Catalog(np.ascontiguousarray(x), t, theta, f"flu_shaped_N{N}_D{D}", seed), Y, sigma

@@ -268,3 +268,64 @@ def test_last_event_has_no_self_excitation_integral():
 def test_unsorted_times_rejected():
     with pytest.raises(ValueError):
         oracle.loglik(np.zeros((3, 2)), np.array([0.3, 0.1, 0.2]), synth.THETA_UNIT)
+
+
+# ------------------------------------------------------------------- BMDS oracle
+def test_bmds_two_points_is_a_truncated_normal():
+    """N=2: the BMDS density of Eq. bmdsLikelihood is the density of one
+    N(delta, sigma^2) variate truncated to y > 0 (scipy.stats.truncnorm)."""
+    from scipy.stats import truncnorm
+    x = np.array([[0.3, -0.2, 1.1], [1.0, 0.4, 0.2]])
+    delta = float(np.linalg.norm(x[0] - x[1]))
+    for y, s in [(1.1, 0.3), (0.2, 0.9), (4.0, 2.0)]:
+        Y = np.array([[0.0, y], [y, 0.0]])
+        lp, _ = oracle.bmds(x, Y, s)
+        ref = truncnorm.logpdf(y, a=-delta / s, b=np.inf, loc=delta, scale=s)
+        assert lp == pytest.approx(ref, rel=1e-13)
+
+
+@pytest.mark.parametrize("N,D", [(4, 2), (5, 6)])
+def test_bmds_brute_force_40_digits(N, D):
+    """mpmath transcription of Eq. bmdsLikelihood; its gradient by mp.diff (so the hand-
+    derived gradient in the oracle is pinned to the density)."""
+    rng = np.random.default_rng(N + D)
+    x = rng.normal(size=(N, D))
+    Y = synth.bmds_dissimilarities(x, 0.4, seed=N)
+    s = 0.4
+    with mp.workdps(40):
+        def logp(X):
+            tot = mp.mpf(0)
+            for n in range(N):
+                for m in range(n):
+                    d = mp.sqrt(sum((X[n][k] - X[m][k]) ** 2 for k in range(D)))
+                    tot += -mp.log(2 * mp.pi * s * s) / 2 - (mp.mpf(Y[n, m]) - d) ** 2 / (2 * s * s) \
+                        - mp.log(mp.ncdf(d / s))
+            return tot
+        X = [[mp.mpf(v) for v in row] for row in x]
+        ref = logp(X)
+        gref = []
+        for n in range(N):
+            for k in range(D):
+                def f(v, n=n, k=k):
+                    Xv = [list(r) for r in X]
+                    Xv[n][k] = v
+                    return logp(Xv)
+                gref.append(float(mp.diff(f, X[n][k])))
+    lp, g, S = oracle.bmds(x, Y, s, with_scale=True)
+    assert lp == pytest.approx(float(ref), rel=1e-13)
+    np.testing.assert_allclose(g.reshape(-1), gref, rtol=0, atol=1e-12 * S.max())
+
+
+def test_bmds_gradient_invariances_and_differences():
+    c, Y, s = synth.flu_shaped(60, 3)
+    lp, g, S = oracle.bmds(c.x, Y, s, with_scale=True)
+    assert np.all(np.abs(g.sum(axis=0)) <= 1e-12 * S.sum(axis=0))
+    shifted, _ = oracle.bmds(c.x + 5.0, Y, s)
+    assert shifted == pytest.approx(lp, rel=1e-12)
+    h = 1e-6
+    for n, d in [(0, 0), (17, 2), (59, 1)]:
+        xp, xm = c.x.copy(), c.x.copy()
+        xp[n, d] += h
+        xm[n, d] -= h
+        fd = (oracle.bmds(xp, Y, s, with_grad=False)[0] - oracle.bmds(xm, Y, s, with_grad=False)[0]) / (2 * h)
+        assert abs(fd - g[n, d]) <= 1e-6 * max(abs(g[n, d]), S[n, d])
