@@ -161,6 +161,28 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
 int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, double* Lambda,
                      int32_t mem);
 
+/* Bayesian MDS: the flu application's second O(N^2)
+ * term.  hawkes_set_bmds copies the N*N row-major dissimilarity matrix Y (host or device per
+ * mem; only the lower triangle y[n*N + n'], n > n', is read, as in Eq. bmdsLikelihood) and
+ * sigma > 0 (the paper's mdsSD).  Every y_{nn'} (n > n') must be finite and > 0 (the
+ * truncated-normal support), else HAWKES_ERR_NONFINITE (host input: now; device input: at
+ * the next evaluation).  The context then holds 8 N^2 bytes of device memory.
+ * hawkes_bmds_logdensity writes
+ *   log p(Y | X) = sum_{n > n'} [-1/2 log(2 pi sigma^2) - (y - delta)^2/(2 sigma^2)
+ *                                - log Phi(delta/sigma)],   delta = |x_n - x_n'|
+ * (Eq. bmdsLikelihood with the normal constant kept) to *out_logp and, when out_grad is
+ * non-NULL, its gradient in x (N*D, host or device per mem) at the context's current
+ * locations.  A coincident pair (delta = 0) contributes no gradient (reading R25).
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_PARAM (sigma), HAWKES_ERR_STATE (no Y / no x). */
+int hawkes_set_bmds(hawkes_ctx* ctx, const double* Y, int32_t mem, double sigma);
+int hawkes_bmds_logdensity(hawkes_ctx* ctx, double* out_grad, int32_t mem, double* out_logp);
+
+/* Which log densities hawkes_leapfrog's potential U = -(sum) includes: a bit mask of
+ * HAWKES_POTENTIAL_HAWKES (ell, the default) and HAWKES_POTENTIAL_BMDS (log p(Y | X));
+ * both = the flu model's HMC over X.  out_loglik_end then reports the sum. */
+typedef enum { HAWKES_POTENTIAL_HAWKES = 1, HAWKES_POTENTIAL_BMDS = 2 } hawkes_potential;
+int hawkes_set_potential(hawkes_ctx* ctx, int32_t flags);
+
 /* Block Metropolis-Hastings over locations.
  * hawkes_propose_move returns in *out_delta = ell(X') - ell(X) for X' = X with the k events
  * idx[0..k) (host array, distinct, 1 <= k <= 256) moved to new_x (k*D row-major, host or

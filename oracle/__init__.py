@@ -183,17 +183,28 @@ def loglik_complex(x_re, x_im, t, theta):
     return a.value, b.value
 
 
-def leapfrog(x, p, t, theta, step: float, n_steps: int, inv_mass=None, box_lo=None, box_hi=None):
+def leapfrog(x, p, t, theta, step: float, n_steps: int, inv_mass=None, box_lo=None, box_hi=None,
+             bmds_data=None, hawkes: bool = True):
     """Leapfrog trajectory of HMC over locations (Neal 2011, cited there).
 
-    Potential U(X) = -ell(X).  Each step: p += (step/2) grad ell; x += step M^-1 p
+    Potential U(X) = -ell(X) [- log p(Y | X) with bmds_data = (Y, sigma): the flu model's
+    joint density; hawkes=False drops ell].  Each step: p += (step/2) grad ell; x += step M^-1 p
     (reflecting off [box_lo, box_hi] componentwise when given, negating p);
     p += (step/2) grad ell.  Returns (x, p, ell_end, kinetic_end) with
     kinetic = 1/2 sum p^2 M^-1."""
     x = np.array(x, dtype=np.float64, copy=True)
     p = np.array(p, dtype=np.float64, copy=True)
     minv = np.ones_like(x) if inv_mass is None else np.asarray(inv_mass, dtype=np.float64)
-    g, _ = grad(x, t, theta)
+
+    def grad(xx):
+        gg = np.zeros_like(xx)
+        if hawkes:
+            gg = gg + globals()["grad"](xx, t, theta)[0]
+        if bmds_data is not None:
+            gg = gg + bmds(xx, bmds_data[0], bmds_data[1])[1]
+        return gg
+
+    g = grad(x)
     for _ in range(n_steps):
         p = p + 0.5 * step * g
         x = x + step * minv * p
@@ -208,9 +219,11 @@ def leapfrog(x, p, t, theta, step: float, n_steps: int, inv_mass=None, box_lo=No
                 x = np.where(below, 2 * lo - x, x)
                 x = np.where(above, 2 * hi - x, x)
                 p = np.where(below | above, -p, p)
-        g, _ = grad(x, t, theta)
+        g = grad(x)
         p = p + 0.5 * step * g
-    ell, _, _ = loglik(x, t, theta)
+    ell = loglik(x, t, theta)[0] if hawkes else 0.0
+    if bmds_data is not None:
+        ell += bmds(x, bmds_data[0], bmds_data[1], with_grad=False)[0]
     kin = 0.5 * float(np.sum(p * p * minv))
     return x, p, ell, kin
 

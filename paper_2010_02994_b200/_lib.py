@@ -20,12 +20,14 @@ STATUS = {
 HAWKES_FP64, HAWKES_FP32 = 0, 1
 HAWKES_MEM_HOST, HAWKES_MEM_DEVICE = 0, 1
 ALGORITHMS = {"auto": 0, "rows": 1, "pairs": 2}
+POTENTIAL_HAWKES, POTENTIAL_BMDS = 1, 2
 
 # every symbol include/hawkes.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
-    "hawkes_leapfrog", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move", "hawkes_enable_timing", "hawkes_get_kernel_times",
+    "hawkes_leapfrog", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move",
+    "hawkes_set_bmds", "hawkes_bmds_logdensity", "hawkes_set_potential", "hawkes_enable_timing", "hawkes_get_kernel_times",
     "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version",
 )
@@ -75,6 +77,9 @@ def load() -> ctypes.CDLL:
     lib.hawkes_get_rates.argtypes = [vp, dp, dp, dp, dp, i32]
     lib.hawkes_propose_move.argtypes = [vp, i32, P(i32), dp, i32, P(ctypes.c_double)]
     lib.hawkes_accept_move.argtypes = [vp]
+    lib.hawkes_set_bmds.argtypes = [vp, dp, i32, ctypes.c_double]
+    lib.hawkes_bmds_logdensity.argtypes = [vp, dp, i32, P(ctypes.c_double)]
+    lib.hawkes_set_potential.argtypes = [vp, i32]
     lib.hawkes_enable_timing.argtypes = [vp, i32]
     lib.hawkes_get_kernel_times.argtypes = [vp, P(ctypes.c_double), P(i64), P(ctypes.c_double),
                                             P(i64), P(i64)]

@@ -32,6 +32,7 @@
 #include "hawkes_kernels_f32.cuh"
 #include "hawkes_kernels_sym.cuh"
 #include "hawkes_moves.cuh"
+#include "hawkes_bmds.cuh"
 
 using namespace hk;
 
@@ -243,6 +244,7 @@ struct EvalStatus {
   int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
   double kinetic;
   double dell;     // Delta ell of the pending block move
+  double bmds;     // BMDS log density of the last BMDS evaluation
 };
 
 // Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
@@ -294,7 +296,7 @@ __global__ void k_move_commit(double* __restrict__ rates, const double* __restri
                               const double* __restrict__ rows, const int* __restrict__ slot_of,
                               const int* __restrict__ idx, const double* __restrict__ new_x, int k,
                               int N, double tx2, double h2, double* __restrict__ rec,
-                              float* __restrict__ rec32, EvalStatus* st) {
+                              float* __restrict__ rec32, double* __restrict__ xcur, EvalStatus* st) {
   const double S1 = 1.0 / 18446744073709551616.0;   // 2^-64
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n == 0) st->ell += st->dell;
@@ -319,6 +321,7 @@ __global__ void k_move_commit(double* __restrict__ rates, const double* __restri
     for (int d = 0; d < D; ++d) {
       const double v = new_x[n * D + d];
       rec[(long long)m * Layout<D>::REC + d] = v;
+      xcur[(long long)m * D + d] = v;
       if (rec32) {
         const float hi = (float)v;
         rec32[(long long)m * Layout32<D>::REC + Layout32<D>::XH + d] = hi;
@@ -399,9 +402,13 @@ __global__ void k_unpack_rows(const double* __restrict__ src, int K, const int* 
 
 // leapfrog pieces: every rank holds the full gradient, so every rank updates all
 // rows identically (no position exchange needed)
-__global__ void k_kick(double* __restrict__ p, const double* __restrict__ g, long long n, double h) {
+// p += h (g1 + g2): the potential's gradient is the sum of the selected log densities'
+__global__ void k_kick(double* __restrict__ p, const double* __restrict__ g1,
+                       const double* __restrict__ g2, long long n, double h) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = fma(h, g[i], p[i]);
+  if (i >= n) return;
+  const double g = (g1 ? g1[i] : 0.0) + (g2 ? g2[i] : 0.0);
+  p[i] = fma(h, g, p[i]);
 }
 
 template <int D>
@@ -623,6 +630,13 @@ struct hawkes_ctx {
   double* d_move_part = nullptr;   // ceil(N/256) block sums
   double* d_move_rows_part = nullptr;  // MOVE_MAX x ceil(N/MOVE_SPLIT) x 2
   bool lam_valid = false;      // rates[][] hold lambda of the current state (all rows)
+  // BMDS (hawkes_set_bmds / hawkes_bmds_logdensity / hawkes_set_potential)
+  double* d_Y = nullptr;       // N x N, lower triangle mirrored into the upper
+  double* d_bgrad = nullptr;   // N x D
+  double* d_brow = nullptr;    // N per-row values
+  BmdsConst bc{};
+  bool have_bmds = false;
+  int potential = HAWKES_POTENTIAL_HAWKES;
   int move_k = 0;              // pending proposal size (0: none)
   int sym_variant = 40;     // 10 * rows-per-lane + exp scheme (tuning knob HAWKES_SYM_VARIANT)
 };
@@ -1053,7 +1067,20 @@ struct CommitD {
     k_move_commit<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(
         ctx->rates, ctx->d_move_delta, ctx->d_move_rows, ctx->d_slot_of, ctx->d_move_idx,
         ctx->d_move_x, ctx->move_k, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2, ctx->rec, ctx->rec32,
-        ctx->st);
+        ctx->xstage, ctx->st);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct BmdsD {
+  static int run(hawkes_ctx* ctx, const double* x) {
+    const long long threads = ctx->N * 32;
+    k_bmds<D><<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N,
+                                                                          ctx->bc, ctx->d_bgrad, ctx->d_brow);
+    CHECK_LAUNCH();
+    k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_brow, (int)ctx->N, &ctx->st->bmds);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -1259,9 +1286,14 @@ int fetch_status(hawkes_ctx* ctx) {
   CU(cudaStreamSynchronize(ctx->stream));
   bad = ctx->h_st->nonfinite;
   if (bad) {
-    ctx->rates_valid = ctx->grad_valid = false;
-    ctx->have_x = false;
     CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
+    if (bad & 2) {
+      ctx->have_bmds = false;
+      return set_err(ctx, HAWKES_ERR_NONFINITE,
+                     "BMDS dissimilarities must be finite and > 0 below the diagonal");
+    }
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+    ctx->have_x = false;
     return set_err(ctx, HAWKES_ERR_NONFINITE,
                    "locations contain NaN/Inf or |x| > 1e100 (device-side validation)");
   }
@@ -1720,7 +1752,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
   }
-  void* bufs[] = {ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
+  void* bufs[] = {ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
@@ -1760,9 +1792,10 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   std::vector<int> g(ctx->npad);
   for (int64_t i = 0; i < N; ++i) g[i] = (i && h[i] == h[i - 1]) ? g[i - 1] : (int)i;
   for (int64_t i = N; i < ctx->npad; ++i) g[i] = g[N - 1];
-  CU(cudaMemcpyAsync(ctx->xstage, h.data(), N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  // stage t in the (rho', ell_n) buffer: xstage keeps the current locations
+  CU(cudaMemcpyAsync(ctx->rl, h.data(), N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyAsync(ctx->gid, g.data(), ctx->npad * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  TRY(dispatchD<PackTD>(ctx->D, ctx, (const double*)ctx->xstage));
+  TRY(dispatchD<PackTD>(ctx->D, ctx, (const double*)ctx->rl));
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->tN = h[N - 1];
   ctx->fc.tN = ctx->tN;
@@ -1868,7 +1901,7 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
   if (!x || !p || n_steps < 0 || !isfinite(step) ||
       (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) || ((box_lo == nullptr) != (box_hi == nullptr)))
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_leapfrog");
-  if (!ctx->have_t || !ctx->have_p)
+  if ((ctx->potential & HAWKES_POTENTIAL_HAWKES) && (!ctx->have_t || !ctx->have_p))
     return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
   const size_t n = (size_t)ctx->N * ctx->D;
   if (!ctx->lf_x) {
@@ -1897,23 +1930,34 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
   TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
   ctx->have_x = true;
   ctx->rates_valid = ctx->grad_valid = false;
-  TRY(run_grad(ctx));
+  const bool use_h = ctx->potential & HAWKES_POTENTIAL_HAWKES;
+  const bool use_b = (ctx->potential & HAWKES_POTENTIAL_BMDS) != 0;
+  if (use_b && !ctx->have_bmds) return set_err(ctx, HAWKES_ERR_STATE, "BMDS potential without hawkes_set_bmds");
+  auto potential_grad = [&]() -> int {
+    if (use_h) TRY(run_grad(ctx));
+    if (use_b) TRY(dispatchD<BmdsD>(ctx->D, ctx, (const double*)ctx->lf_x));
+    return HAWKES_OK;
+  };
+  const double* g1 = use_h ? ctx->grad : nullptr;
+  const double* g2 = use_b ? ctx->d_bgrad : nullptr;
+  TRY(potential_grad());
   const unsigned nb = (unsigned)((n + 255) / 256);
   for (int s = 0; s < n_steps; ++s) {
-    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, ctx->grad, (long long)n, 0.5 * step);
+    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, g1, g2, (long long)n, 0.5 * step);
     CHECK_LAUNCH();
     TRY(dispatchD<DriftD>(ctx->D, ctx, step, box_lo != nullptr, inv_mass != nullptr));
     ctx->rates_valid = ctx->grad_valid = false;
-    TRY(run_grad(ctx));
-    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, ctx->grad, (long long)n, 0.5 * step);
+    TRY(potential_grad());
+    k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, g1, g2, (long long)n, 0.5 * step);
     CHECK_LAUNCH();
   }
+  CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
   CHECK_LAUNCH();
   TRY(copy_out(ctx, x, ctx->lf_x, n, mem));
   TRY(copy_out(ctx, p, ctx->lf_p, n, mem));
   TRY(fetch_status(ctx));
-  if (out_ll) *out_ll = ctx->h_st->ell;
+  if (out_ll) *out_ll = (use_h ? ctx->h_st->ell : 0.0) + (use_b ? ctx->h_st->bmds : 0.0);
   if (out_kin) *out_kin = ctx->h_st->kinetic;
   if (ctx->h_st->undefined)
     return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "ell = -inf during the trajectory");
@@ -1975,6 +2019,56 @@ int hawkes_accept_move(hawkes_ctx* ctx) {
   ctx->rates_exchanged = true;                  // every rank updated every row
   ctx->lam_valid = true;
   CU(cudaStreamSynchronize(ctx->stream));
+  return HAWKES_OK;
+}
+
+int hawkes_set_bmds(hawkes_ctx* ctx, const double* Y, int32_t mem, double sigma) {
+  ENTER(ctx);
+  if (!Y || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_set_bmds");
+  if (!(sigma > 0.0) || !isfinite(sigma) || !isfinite(1.0 / (sigma * sigma)))
+    return set_err(ctx, HAWKES_ERR_PARAM, "sigma must be finite and > 0");
+  const long long N = ctx->N;
+  if (mem == HAWKES_MEM_HOST)
+    for (long long nn = 1; nn < N; ++nn)
+      for (long long m = 0; m < nn; ++m) {
+        const double y = Y[nn * N + m];
+        if (!(y > 0.0) || !finite_bounded(y))
+          return set_err(ctx, HAWKES_ERR_NONFINITE, "Y[%lld, %lld] = %g: need finite y > 0 below the diagonal", nn, m, y);
+      }
+  if (!ctx->d_Y) {
+    TRY(dalloc(ctx, &ctx->d_Y, (size_t)(N * N)));
+    TRY(dalloc(ctx, &ctx->d_bgrad, (size_t)N * ctx->D));
+    TRY(dalloc(ctx, &ctx->d_brow, (size_t)N));
+  }
+  TRY(copy_in(ctx, ctx->d_Y, Y, (size_t)(N * N), mem));
+  k_bmds_mirror<<<(unsigned)((N * N + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_Y, (int)N, ctx->bad);
+  CHECK_LAUNCH();
+  ctx->bc.inv_s = 1.0 / sigma;
+  ctx->bc.inv_s2 = 1.0 / (sigma * sigma);
+  ctx->bc.half_log = 0.5 * log(2.0 * 3.14159265358979323846 * sigma * sigma);
+  ctx->have_bmds = true;
+  return HAWKES_OK;
+}
+
+int hawkes_bmds_logdensity(hawkes_ctx* ctx, double* out_grad, int32_t mem, double* out_logp) {
+  ENTER(ctx);
+  if (!out_logp || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_bmds_logdensity");
+  if (!ctx->have_bmds || !ctx->have_x)
+    return set_err(ctx, HAWKES_ERR_STATE, "hawkes_set_bmds and hawkes_set_locations are required");
+  TRY(dispatchD<BmdsD>(ctx->D, ctx, (const double*)ctx->xstage));
+  if (out_grad) TRY(copy_out(ctx, out_grad, ctx->d_bgrad, (size_t)ctx->N * ctx->D, mem));
+  TRY(fetch_status(ctx));
+  *out_logp = ctx->h_st->bmds;
+  return HAWKES_OK;
+}
+
+int hawkes_set_potential(hawkes_ctx* ctx, int32_t flags) {
+  ENTER(ctx);
+  if (flags <= 0 || flags > (HAWKES_POTENTIAL_HAWKES | HAWKES_POTENTIAL_BMDS))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad potential flags");
+  ctx->potential = flags;
   return HAWKES_OK;
 }
 

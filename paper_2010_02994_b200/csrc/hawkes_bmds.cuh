@@ -1,0 +1,92 @@
+// hawkes_bmds.cuh -- Bayesian MDS log density and location gradient (sm_100a, fp64).
+//
+// The flu application models observed dissimilarities y_{nn'} ~ N(delta_{nn'}, sigma^2)
+// truncated to y > 0, delta_{nn'} = |x_n - x_n'|, so (Eq. bmdsLikelihood,
+// P:L176-180, with the normal constant kept)
+//   log p(Y | X) = sum_{n > n'} -1/2 log(2 pi sigma^2) - (y - delta)^2 / (2 sigma^2)
+//                              - log Phi(delta / sigma)
+//   d log p / d x_n = - sum_{n' != n} r'(delta) (x_n - x_n') / delta,
+//   r'(delta) = -(y - delta)/sigma^2 + phi(delta/sigma) / (sigma Phi(delta/sigma)).
+// HMC over X needs this gradient next to the Hawkes one.  One warp per event n:
+// lanes stride over n' (row n of Y is contiguous, so the loads coalesce), the D gradient
+// components and the value (pairs n' < n only, so each pair counts once) are reduced over
+// the warp in a fixed order.  Per pair: one sqrt, one erfc, one exp, one log1p (libdevice).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hk {
+
+struct BmdsConst {
+  double inv_s;        // 1/sigma
+  double inv_s2;       // 1/sigma^2
+  double half_log;     // 1/2 log(2 pi sigma^2)
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bmds(const double* __restrict__ x, const double* __restrict__ Y,
+                                              int N, BmdsConst c, double* __restrict__ grad,
+                                              double* __restrict__ row_value) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  const int n = warp;
+  double xn[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) xn[d] = x[(long long)n * D + d];
+  const double* yrow = Y + (long long)n * N;
+  double g[D], v = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) g[d] = 0.0;
+  for (int m = lane; m < N; m += 32) {
+    if (m == n) continue;
+    double u[D], r2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      u[d] = xn[d] - x[(long long)m * D + d];
+      r2 = fma(u[d], u[d], r2);
+    }
+    // hawkes_set_bmds mirrored the lower triangle (Eq. bmdsLikelihood's n > n') into the
+    // upper one, so row n holds y_{nn'} for every n' and the loads coalesce
+    const double y = yrow[m];
+    const double delta = sqrt(r2);
+    const double z = delta * c.inv_s;
+    const double q = 0.5 * erfc(z * 0.70710678118654752440);   // 1 - Phi(z), z >= 0
+    if (m < n) {
+      const double e = y - delta;
+      v -= c.half_log + 0.5 * e * e * c.inv_s2 + log1p(-q);
+    }
+    if (delta > 0.0) {
+      const double phi = exp(-0.5 * z * z) * 0.39894228040143267794;
+      const double drdd = -(y - delta) * c.inv_s2 + phi * c.inv_s / (1.0 - q);
+      const double s = -drdd / delta;
+#pragma unroll
+      for (int d = 0; d < D; ++d) g[d] = fma(s, u[d], g[d]);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) g[d] += __shfl_down_sync(0xffffffffu, g[d], off);
+    v += __shfl_down_sync(0xffffffffu, v, off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) grad[(long long)n * D + d] = g[d];
+    row_value[n] = v;
+  }
+}
+
+// mirror the lower triangle into the upper one (device copy of Y), flag bad entries
+__global__ void k_bmds_mirror(double* __restrict__ Y, int N, int* __restrict__ bad) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)N * N) return;
+  const int n = (int)(idx / N), m = (int)(idx % N);
+  if (n > m) {
+    const double y = Y[idx];
+    if (!(y > 0.0) || !(y <= 1e100)) atomicOr(bad, 2);
+    Y[(long long)m * N + n] = y;
+  }
+}
+
+}  // namespace hk

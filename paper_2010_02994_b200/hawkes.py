@@ -152,6 +152,29 @@ class HawkesContext:
                                         ctypes.byref(ll), ctypes.byref(kin)), self._h)
         return x, p, ll.value, kin.value
 
+    # -- Bayesian MDS and the HMC potential
+    def set_bmds(self, Y, sigma: float):
+        """hawkes_set_bmds: N x N dissimilarities (lower triangle read) and sigma."""
+        p, mem, keep = _ptr_mem(Y)
+        check(self._lib.hawkes_set_bmds(self._h, p, mem, float(sigma)), self._h)
+
+    def bmds_logdensity(self, grad: bool = True, out=None):
+        """hawkes_bmds_logdensity: (log p(Y | X), gradient N x D or None)."""
+        lp = ctypes.c_double()
+        if grad and out is None:
+            out = torch.empty((self.N, self.D), dtype=torch.float64, device=f"cuda:{self.device}")
+        if grad:
+            p, mem, keep = _ptr_mem(out)
+        else:
+            p, mem = None, HAWKES_MEM_DEVICE
+        check(self._lib.hawkes_bmds_logdensity(self._h, p, mem, ctypes.byref(lp)), self._h)
+        return lp.value, (out if grad else None)
+
+    def set_potential(self, hawkes: bool = True, bmds: bool = False):
+        """hawkes_set_potential: which log densities the leapfrog potential includes."""
+        flags = (_lib.POTENTIAL_HAWKES if hawkes else 0) | (_lib.POTENTIAL_BMDS if bmds else 0)
+        check(self._lib.hawkes_set_potential(self._h, flags), self._h)
+
     # -- block Metropolis-Hastings moves (P:L245)
     def propose_move(self, idx, new_x) -> float:
         """hawkes_propose_move: ell(X') - ell(X) for events idx moved to new_x (k x D)."""
