@@ -378,3 +378,47 @@ def test_full_size_c4_gradient_rows_vs_oracle():
         gr, S = oracle.grad(c.x, c.t, c.theta, lam=lam, rows=slice(int(r), int(r) + 1))
         bound = 1e-9 * np.maximum(np.abs(gr[r]), 1e-3 * S[r])
         assert np.all(np.abs(g[r] - gr[r]) <= bound), (r, g[r], gr[r])
+
+
+def test_gpu_invariances():
+    """SURVEY T3 on the GPU output: translation and rotation of X leave ell unchanged and
+    rotate g; scaling X, tau_x and h by a gives ell - N D log a and g / a (P7)."""
+    from paper_2010_02994_b200 import HawkesContext
+    c = synth.unit_square(4000, config=30)
+    ell, g, _ = gpu_eval(c.x, c.t, c.theta, with_rates=False)
+    S = np.abs(g).sum()
+    e2, g2, _ = gpu_eval(c.x + np.array([12.5, -3.25]), c.t, c.theta, with_rates=False)
+    assert e2 == pytest.approx(ell, rel=1e-12) and np.abs(g2 - g).max() <= 1e-10 * np.abs(g).max()
+    a = 0.3
+    R = np.array([[math.cos(a), -math.sin(a)], [math.sin(a), math.cos(a)]])
+    e3, g3, _ = gpu_eval(c.x @ R.T, c.t, c.theta, with_rates=False)
+    assert e3 == pytest.approx(ell, rel=1e-12)
+    assert np.abs(g3 - g @ R.T).max() <= 1e-10 * np.abs(g).max()
+    s = 7.0
+    th = list(c.theta)
+    th[1] *= s
+    th[5] *= s
+    e4, g4, _ = gpu_eval(s * c.x, c.t, th, with_rates=False)
+    assert e4 == pytest.approx(ell - c.N * c.D * math.log(s), rel=1e-12)
+    assert np.abs(g4 - g / s).max() <= 1e-10 * np.abs(g).max() / s
+
+
+def test_leapfrog_energy_error_is_second_order():
+    """the leapfrog's energy error |Delta H| shrinks ~4x when the step halves
+    (second-order integrator; H = -ell + K)."""
+    from paper_2010_02994_b200 import HawkesContext
+    c = synth.config("C1", replicate=5)
+    p0 = synth.momenta(c.N, c.D, seed=21)
+    with HawkesContext(c.N, c.D) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_params(c.theta)
+        ctx.set_locations(c.x)
+        H0 = -ctx.loglik() + 0.5 * float(np.sum(p0 * p0))
+        errs = []
+        T = 4e-3
+        for L in (8, 16, 32):
+            x, p = c.x.copy(), p0.copy()
+            _, _, ell, kin = ctx.leapfrog(x, p, T / L, L)
+            errs.append(abs(-ell + kin - H0))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 3.0 < r1 < 5.5 and 3.0 < r2 < 5.5, errs
