@@ -36,6 +36,7 @@ def _nccl_include() -> str:
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                  + glob.glob(os.path.join(CSRC, "*.h"))
                   + [os.path.join(ROOT, "include", "hawkes.h")])
 
 

@@ -1,0 +1,477 @@
+// hawkes_ops.cuh -- the O(N) device kernels around the two O(N^2) passes: staging of the
+// event records, the finalize steps (chunk-slot reductions, lambda, rho', Lambda_n, ell_n),
+// exchange packing, block-move bookkeeping, leapfrog updates, deterministic reductions and
+// the FP64 / exp diagnostics.  Included by hawkes_api.cu only (one translation unit).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "hawkes_kernels.cuh"
+#include "hawkes_kernels_f32.cuh"
+
+namespace hk {
+
+constexpr int R_ROWS = 2;                    // rows per thread
+constexpr int SYM_MAX_D = 4;                 // unordered-pair kernels: register tile of 4 rows
+constexpr int RT = THREADS * R_ROWS;         // rows per row tile
+constexpr int FIN_THREADS = RT;              // finalize: one thread per row of a tile
+constexpr double LN2 = 0.693147180559945309417232121458;
+
+// --------------------------------------------------------------------- O(N) kernels
+template <int D>
+__global__ void k_pack_x(double* __restrict__ rec, const double* __restrict__ x, int N, int npad,
+                         int* __restrict__ bad) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const int src = min(i, N - 1);   // padding rows replicate the last event (never stored)
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double v = x[(long long)src * D + d];
+    if (!(fabs(v) <= 1e100)) atomicOr(bad, 1);
+    rec[(long long)i * L::REC + d] = v;
+  }
+}
+
+template <int D>
+__global__ void k_pack_t(double* __restrict__ rec, const double* __restrict__ t, int N, int npad) {
+  using L = Layout<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  rec[(long long)i * L::REC + L::T] = t[min(i, N - 1)];
+  rec[(long long)i * L::REC + L::RHO] = 0.0;
+#pragma unroll
+  for (int k = D + 2; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.0;
+}
+
+// fp32 records: hi/lo float splits (v = hi + lo to ~48 bits)
+template <int D>
+__global__ void k_pack_x32(float* __restrict__ rec, const double* __restrict__ x, int N, int npad) {
+  using L = Layout32<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const int src = min(i, N - 1);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double v = x[(long long)src * D + d];
+    const float hi = (float)v;
+    rec[(long long)i * L::REC + L::XH + d] = hi;
+    rec[(long long)i * L::REC + L::XL + d] = (float)(v - (double)hi);
+  }
+}
+
+template <int D>
+__global__ void k_pack_t32(float* __restrict__ rec, const double* __restrict__ t, int N, int npad) {
+  using L = Layout32<D>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  const double v = t[min(i, N - 1)];
+  const float hi = (float)v;
+  rec[(long long)i * L::REC + L::TH] = hi;
+  rec[(long long)i * L::REC + L::TL] = (float)(v - (double)hi);
+  for (int k = L::RHO; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.f;
+}
+
+// PAIRS with W > 1: per event, fixed-order sum of the partial slots this rank computed.
+// Slot s of event i (chunk c) comes from chunk pair (min(s, c), max(s, c)).
+// Slot nchunks (the diagonal items' column role) comes from pair (c, c).
+__global__ void k_slot_sum(const double* __restrict__ part, long long npad, int nchunks, int chunk,
+                           int K, const int* __restrict__ own, int rank, int N,
+                           double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)N * K) return;
+  const int i = (int)(idx / K), k = (int)(idx % K);
+  const int c = i / chunk;
+  double v = 0.0;
+  for (int sl = 0; sl <= nchunks; ++sl) {
+    const int a = sl == nchunks ? c : min(sl, c), b = sl == nchunks ? c : max(sl, c);
+    if (own[a * nchunks + b] == rank) v += part[((long long)sl * npad + i) * K + k];
+  }
+  out[idx] = v;
+}
+
+// emulated ranks: the "allreduce" of their per-event sums, in rank order
+__global__ void k_sum_ranks(const double* __restrict__ in, long long stride, int W, long long n,
+                            double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  double v = in[idx];
+  for (int r = 1; r < W; ++r) v += in[r * stride + idx];
+  out[idx] = v;
+}
+
+struct FinConst {
+  double tx2, h2;         // tau_x^2, h^2
+  double mu0, tau_t, theta, omega, tN;
+  double scale_log2;      // pair sums carry 2^-scale_log2: -64 (fp64 path) or E (fp32 path)
+  double zero_floor;      // Lambda' at or below this is lambda = 0 (fexp clamps at e^-707)
+};
+
+// kernel constants live in device memory so captured CUDA graphs survive set_params
+struct DevConsts {
+  PassConst pc;
+  PassConst32 pc32;
+  FinConst fc;
+};
+
+// Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
+// lambda, rho' and ell_n.  rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda).
+template <int D>
+__global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
+                       const int* __restrict__ tiles, int N, const double* __restrict__ rec,
+                       double* __restrict__ G1, double* __restrict__ rl,
+                       double* __restrict__ rates, const FinConst* __restrict__ fcp,
+                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho) {
+  using L = Layout<D>;
+  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
+  if (i >= N) return;
+  const FinConst f = *fcp;
+  double M = 0.0, X = 0.0, G[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* p = part + ((long long)c * npad + i) * L::K1;
+    M += p[0];
+    X += p[1];
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] += p[2 + d];
+  }
+  // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
+  const double mu_s = M * f.tx2, xi_s = X * f.h2;
+  const double Lp = (mu_s + xi_s > f.zero_floor) ? mu_s + xi_s : 0.0;
+  const double rho = (Lp > 0.0) ? 1.0 / Lp : 0.0;
+  const double sc = exp2(f.scale_log2);   // exact power of two
+  // Lambda_n: mu0 (Phi(a) - Phi(b)) - theta (e^{-omega (t_N - t_n)} - 1),
+  // a = (t_N - t_n)/tau_t >= 0, b = -t_n/tau_t <= 0, Phi(a) - Phi(b) = 1 - Q(a) - Q(-b),
+  // Q(z) = erfc(z/sqrt2)/2 (reading R10: same value without cancellation)
+  const double tn = rec[(long long)i * L::REC + L::T];
+  const double qa = 0.5 * erfc((f.tN - tn) / f.tau_t * 0.70710678118654752440);
+  const double qb = 0.5 * erfc(tn / f.tau_t * 0.70710678118654752440);
+  const double Lam = f.mu0 * ((1.0 - qa) - qb) - f.theta * expm1(-f.omega * (f.tN - tn));
+  const double ell = (Lp > 0.0) ? (log(Lp) + f.scale_log2 * LN2) - Lam : -INFINITY;
+#pragma unroll
+  for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
+  rl[2 * (long long)i] = rho;
+  rl[2 * (long long)i + 1] = ell;
+  // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
+  if (rec_rho) rec_rho[(long long)i * L::REC] = rho;
+  if (rec32_rho) rec32_rho[(long long)i * Layout32<D>::REC] = (float)rho;
+  rates[4 * (long long)i] = Lp * sc;
+  rates[4 * (long long)i + 1] = mu_s * sc;
+  rates[4 * (long long)i + 2] = xi_s * sc;
+  rates[4 * (long long)i + 3] = Lam;
+}
+
+template <int D>
+__global__ void k_rho_to_rec(double* __restrict__ rec, float* __restrict__ rec32,
+                             const double* __restrict__ rl, int N) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  if (rec32)
+    rec32[(long long)i * Layout32<D>::REC + Layout32<D>::RHO] = (float)rl[2 * (long long)i];
+  else
+    rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
+}
+
+// sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W
+struct EvalStatus {
+  double ell;
+  int nonfinite;   // device-side input validation failed
+  int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
+  double kinetic;
+  double dell;     // Delta ell of the pending block move
+  double bmds;     // BMDS log density of the last BMDS evaluation
+};
+
+// Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
+// events [256 b, 256 b + 256) in a fixed tree, k_sum_partials adds the block sums in order.
+// rates[n] = (lambda, mu, xi, Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.
+__global__ void k_move_terms(const double* __restrict__ rates, const double* __restrict__ delta,
+                             const double* __restrict__ rows, const int* __restrict__ slot_of,
+                             int N, double tx2, double h2, double floor_, double* __restrict__ part) {
+  __shared__ double sh[256];
+  const double S = 18446744073709551616.0;   // 2^64
+  const int n = blockIdx.x * 256 + threadIdx.x;
+  double term = 0.0;
+  if (n < N) {
+    const double L0 = rates[4 * (long long)n] * S;
+    const int q = slot_of[n];
+    if (q < 0) {
+      const double d = fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2);
+      term = (d == 0.0) ? 0.0 : ((L0 + d > floor_) ? log1p(d / L0) : -INFINITY);
+    } else {
+      const double L1 = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2);
+      term = ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
+    }
+  }
+  sh[threadIdx.x] = term;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// Commit an accepted move: cached rates, ell and the moved events' records.
+template <int D>
+__global__ void k_move_commit(double* __restrict__ rates, const double* __restrict__ delta,
+                              const double* __restrict__ rows, const int* __restrict__ slot_of,
+                              const int* __restrict__ idx, const double* __restrict__ new_x, int k,
+                              int N, double tx2, double h2, double* __restrict__ rec,
+                              float* __restrict__ rec32, double* __restrict__ xcur, EvalStatus* st) {
+  const double S1 = 1.0 / 18446744073709551616.0;   // 2^-64
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n == 0) st->ell += st->dell;
+  if (n < N) {
+    const int q = slot_of[n];
+    double mu, xi;
+    if (q < 0) {
+      mu = rates[4 * (long long)n + 1] + delta[2 * (long long)n] * tx2 * S1;
+      xi = rates[4 * (long long)n + 2] + delta[2 * (long long)n + 1] * h2 * S1;
+      rates[4 * (long long)n] += fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2) * S1;
+    } else {
+      mu = rows[2 * q] * tx2 * S1;
+      xi = rows[2 * q + 1] * h2 * S1;
+      rates[4 * (long long)n] = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2) * S1;
+    }
+    rates[4 * (long long)n + 1] = mu;
+    rates[4 * (long long)n + 2] = xi;
+  }
+  if (n < k) {
+    const int m = idx[n];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double v = new_x[n * D + d];
+      rec[(long long)m * Layout<D>::REC + d] = v;
+      xcur[(long long)m * D + d] = v;
+      if (rec32) {
+        const float hi = (float)v;
+        rec32[(long long)m * Layout32<D>::REC + Layout32<D>::XH + d] = hi;
+        rec32[(long long)m * Layout32<D>::REC + Layout32<D>::XL + d] = (float)(v - (double)hi);
+      }
+    }
+  }
+}
+
+__global__ void k_scatter_slots(int* __restrict__ slot_of, const int* __restrict__ idx, int k, int set) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < k) slot_of[idx[q]] = set ? q : -1;
+}
+
+__global__ void k_ell_reduce(const double* __restrict__ rl, int N, EvalStatus* st) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < N; i += 1024) s += rl[2 * (long long)i + 1];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->ell = sh[0];
+    if (!(sh[0] > -INFINITY)) st->undefined = 1;
+  }
+}
+
+template <int D>
+__global__ void k_fin2(const double* __restrict__ part, long long npad, int nchunks,
+                       const int* __restrict__ tiles, int N, const double* __restrict__ G1,
+                       const double* __restrict__ rl, double* __restrict__ grad) {
+  using L = Layout<D>;
+  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
+  if (i >= N) return;
+  double G[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* p = part + ((long long)c * npad + i) * L::K2;
+#pragma unroll
+    for (int d = 0; d < D; ++d) G[d] += p[d];
+  }
+  const double rho = rl[2 * (long long)i];
+#pragma unroll
+  for (int d = 0; d < D; ++d) grad[(long long)i * D + d] = fma(rho, G1[(long long)i * D + d], G[d]);
+}
+
+// rows of this rank's tiles -> contiguous send buffer (tile-list order), K values per row
+__global__ void k_pack_rows(const double* __restrict__ src, int K, const int* __restrict__ tiles,
+                            int ntiles, int N, double* __restrict__ dst) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)ntiles * RT * K;
+  if (idx >= total) return;
+  const int k = (int)(idx % K);
+  const long long r = idx / K;
+  const int i = tiles[r / RT] * RT + (int)(r % RT);
+  dst[idx] = (i < N) ? src[(long long)i * K + k] : 0.0;
+}
+
+// gathered buffers of all ranks -> rows (inverse of k_pack_rows for every rank)
+__global__ void k_unpack_rows(const double* __restrict__ src, int K, const int* __restrict__ all_tiles,
+                              int max_tiles, int W, int N, double* __restrict__ dst) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_rank = (long long)max_tiles * RT * K;
+  if (idx >= per_rank * W) return;
+  const int rank = (int)(idx / per_rank);
+  const long long o = idx % per_rank;
+  const int k = (int)(o % K);
+  const long long r = o / K;
+  const int tile = all_tiles[rank * max_tiles + (int)(r / RT)];
+  if (tile < 0) return;
+  const int i = tile * RT + (int)(r % RT);
+  if (i < N) dst[(long long)i * K + k] = src[idx];
+}
+
+// leapfrog pieces: every rank holds the full gradient, so every rank updates all
+// rows identically (no position exchange needed)
+// p += h (g1 + g2): the potential's gradient is the sum of the selected log densities'
+__global__ void k_kick(double* __restrict__ p, const double* __restrict__ g1,
+                       const double* __restrict__ g2, long long n, double h) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double g = (g1 ? g1[i] : 0.0) + (g2 ? g2[i] : 0.0);
+  p[i] = fma(h, g, p[i]);
+}
+
+template <int D>
+__global__ void k_drift(double* __restrict__ x, double* __restrict__ p,
+                        const double* __restrict__ minv, const double* __restrict__ lo,
+                        const double* __restrict__ hi, int N, double eps,
+                        int* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const long long k = (long long)i * D + d;
+    double pv = p[k];
+    double xv = fma(eps * (minv ? minv[k] : 1.0), pv, x[k]);
+    if (lo) {
+      const double a = lo[k], b = hi[k];
+      for (int it = 0; it < 64 && (xv < a || xv > b); ++it) {  // one bounce per round
+        xv = (xv < a) ? 2.0 * a - xv : 2.0 * b - xv;
+        pv = -pv;
+      }
+    }
+    if (!(fabs(xv) <= 1e100)) atomicOr(bad, 1);
+    x[k] = xv;
+    p[k] = pv;
+  }
+}
+
+__global__ void k_kinetic(const double* __restrict__ p, const double* __restrict__ minv, long long n,
+                          EvalStatus* st) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) {
+    const double v = p[i];
+    s += (minv ? minv[i] : 1.0) * v * v;
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) st->kinetic = 0.5 * sh[0];
+}
+
+// diagnostics: the fast exp on an array (tests pin its accuracy)
+__global__ void k_diag_exp(const double* __restrict__ a, double* __restrict__ out, long long n,
+                           const int2* __restrict__ gtab) {
+  __shared__ int2 tab[EXP_TABLE];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  __syncthreads();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fexp(a[i], tab);
+}
+
+// diagnostics: dependent-DFMA throughput probe (FP64 pipe peak)
+__global__ void k_diag_dfma(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int k = 0; k < iters; ++k) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[0] = s;
+}
+
+// diagnostics: FP64-pipe throughput for several operand patterns (ops per thread per iter = 8)
+__global__ void k_diag_mode(double* out, int iters, int mode, const int2* __restrict__ gtab) {
+  __shared__ int2 tab[EXP_TABLE];
+  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  __syncthreads();
+  double a[8], b[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    a[q] = 1e-3 * (threadIdx.x + q);
+    b[q] = 0.5 + 1e-4 * q;
+  }
+  const double m = 0.999999, c = 1e-7;
+  if (mode == 0) {
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fma(a[q], m, c);
+  } else if (mode == 1) {      // three distinct register operands
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b[q], b[(q + 1) & 7]);
+  } else if (mode == 2) {      // DADD of two registers
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = a[q] + b[q];
+  } else if (mode == 3) {      // DMUL of two registers
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = a[q] * b[q];
+  } else if (mode == 4) {      // fast exp, 8 independent chains (9 FP64 ops each)
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = -fexp(-a[q] * 1e-3, tab);
+  } else if (mode == 5) {      // two-register DFMA with one constant
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b[q], c);
+  } else if (mode == 6) {      // alternating DFMA / DADD
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = (q & 1) ? a[q] + b[q] : fma(a[q], b[q], c);
+  } else if (mode == 10) {     // alternating DFMA / DMUL
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = (q & 1) ? a[q] * b[q] : fma(a[q], b[q], c);
+  } else if (mode == 11) {     // alternating DFMA / (DADD written as DFMA with a runtime 1.0)
+    const double one = gtab ? 1.0 + 0.0 * (double)iters : 1.0;
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = (q & 1) ? fma(a[q], one, b[q]) : fma(a[q], b[q], c);
+  } else if (mode == 9) {      // one dependent DFMA chain per thread (latency probe)
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[0] = fma(a[0], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == 12345.678) out[0] = s;
+}
+
+
+}  // namespace hk
