@@ -618,9 +618,8 @@ struct CommitD {
 template <int D>
 struct BmdsD {
   static int run(hawkes_ctx* ctx, const double* x) {
-    const long long threads = ctx->N * 32;
-    k_bmds<D><<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N,
-                                                                          ctx->bc, ctx->d_bgrad, ctx->d_brow);
+    k_bmds<D><<<(unsigned)ctx->N, BMDS_THREADS, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N, ctx->bc,
+                                                                   ctx->d_bgrad, ctx->d_brow);
     CHECK_LAUNCH();
     k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_brow, (int)ctx->N, &ctx->st->bmds);
     CHECK_LAUNCH();

@@ -7,10 +7,11 @@
 //                              - log Phi(delta / sigma)
 //   d log p / d x_n = - sum_{n' != n} r'(delta) (x_n - x_n') / delta,
 //   r'(delta) = -(y - delta)/sigma^2 + phi(delta/sigma) / (sigma Phi(delta/sigma)).
-// HMC over X needs this gradient next to the Hawkes one.  One warp per event n:
-// lanes stride over n' (row n of Y is contiguous, so the loads coalesce), the D gradient
-// components and the value (pairs n' < n only, so each pair counts once) are reduced over
-// the warp in a fixed order.  Per pair: one sqrt, one erfc, one exp, one log1p (libdevice).
+// HMC over X needs this gradient next to the Hawkes one.  One 128-thread CTA per
+// event n: threads stride over n' (row n of Y is contiguous, so the loads coalesce), the D
+// gradient components and the value (pairs n' < n only, so each pair counts once) are
+// reduced over the CTA in a fixed tree.  Per pair: one sqrt, one erfc, one exp, one log1p
+// (libdevice); the per-pair chain is long and dependent, so the kernel needs many warps.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,14 +24,16 @@ struct BmdsConst {
   double half_log;     // 1/2 log(2 pi sigma^2)
 };
 
+constexpr int BMDS_THREADS = 128;
+
 template <int D>
-__global__ void __launch_bounds__(256) k_bmds(const double* __restrict__ x, const double* __restrict__ Y,
-                                              int N, BmdsConst c, double* __restrict__ grad,
-                                              double* __restrict__ row_value) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= N) return;
-  const int n = warp;
+__global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict__ x,
+                                                       const double* __restrict__ Y, int N,
+                                                       BmdsConst c, double* __restrict__ grad,
+                                                       double* __restrict__ row_value) {
+  __shared__ double red[BMDS_THREADS][D + 1];
+  const int n = blockIdx.x;
+  const int tid = threadIdx.x;
   double xn[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) xn[d] = x[(long long)n * D + d];
@@ -38,7 +41,8 @@ __global__ void __launch_bounds__(256) k_bmds(const double* __restrict__ x, cons
   double g[D], v = 0.0;
 #pragma unroll
   for (int d = 0; d < D; ++d) g[d] = 0.0;
-  for (int m = lane; m < N; m += 32) {
+#pragma unroll 2
+  for (int m = tid; m < N; m += BMDS_THREADS) {
     if (m == n) continue;
     double u[D], r2 = 0.0;
 #pragma unroll
@@ -64,16 +68,22 @@ __global__ void __launch_bounds__(256) k_bmds(const double* __restrict__ x, cons
       for (int d = 0; d < D; ++d) g[d] = fma(s, u[d], g[d]);
     }
   }
+  // fixed-order tree over the CTA
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
+  for (int d = 0; d < D; ++d) red[tid][d] = g[d];
+  red[tid][D] = v;
+  __syncthreads();
+  for (int w = BMDS_THREADS / 2; w > 0; w >>= 1) {
+    if (tid < w) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) g[d] += __shfl_down_sync(0xffffffffu, g[d], off);
-    v += __shfl_down_sync(0xffffffffu, v, off);
+      for (int d = 0; d <= D; ++d) red[tid][d] += red[tid + w][d];
+    }
+    __syncthreads();
   }
-  if (lane == 0) {
+  if (tid == 0) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) grad[(long long)n * D + d] = g[d];
-    row_value[n] = v;
+    for (int d = 0; d < D; ++d) grad[(long long)n * D + d] = red[0][d];
+    row_value[n] = red[0][D];
   }
 }
 
