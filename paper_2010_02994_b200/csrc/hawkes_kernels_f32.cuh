@@ -340,7 +340,7 @@ struct RowPair32 {
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
-template <int D, int PASS, bool MASK>
+template <int D, int PASS, bool MASK, bool SELF>
 __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float (&cxh)[D],
                                             const float (&cxl)[D], float cth, float ctl,
                                             float crho, bool dead_a, bool dead_b, float2& rM,
@@ -355,9 +355,10 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
   const float2 dt = __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
   const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
-  const float2 as = __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), dt, f2(c.cs)));
+  const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), dt, f2(c.cs)))
+                         : make_float2(0.f, 0.f);
   float2 eb = make_float2(ex2f(ab.x), ex2f(ab.y));
-  float2 es = make_float2(ex2f(as.x), ex2f(as.y));
+  float2 es = SELF ? make_float2(ex2f(as.x), ex2f(as.y)) : make_float2(0.f, 0.f);
   if (MASK) {
     eb.x = dead_a ? 0.f : eb.x;
     es.x = dead_a ? 0.f : es.x;
@@ -367,15 +368,16 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   if (PASS == 1) {
     rM = __fadd2_rn(rM, eb);
     cM = __fadd2_rn(cM, eb);
-    cX = __fadd2_rn(cX, es);
-    const float2 ncc = __fadd2_rn(make_float2(-eb.x, -eb.y), make_float2(-es.x, -es.y));
+    if (SELF) cX = __fadd2_rn(cX, es);
+    const float2 ncc = SELF ? __fadd2_rn(make_float2(-eb.x, -eb.y), make_float2(-es.x, -es.y))
+                            : make_float2(-eb.x, -eb.y);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       rG[d] = __ffma2_rn(eb, dx[d], rG[d]);
       cG[d] = __ffma2_rn(ncc, dx[d], cG[d]);
     }
   } else {
-    const float2 cr = __fmul2_rn(f2(crho), __fadd2_rn(eb, es));
+    const float2 cr = __fmul2_rn(f2(crho), SELF ? __fadd2_rn(eb, es) : eb);
     const float2 ncc = __fmul2_rn(make_float2(-rp.rho.x, -rp.rho.y), eb);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -385,7 +387,7 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR>
+template <int D, int PASS, bool MASK, int SR, bool SELF = true>
 __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag,
@@ -423,7 +425,8 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
         da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
         db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
       }
-      sym32_pair2<D, PASS, MASK>(rp[h], cxh, cxl, cth, ctl, crho, da, db, rM[h], rG[h], cM, cX, cG, c);
+      sym32_pair2<D, PASS, MASK, SELF>(rp[h], cxh, cxl, cth, ctl, crho, da, db, rM[h], rG[h], cM, cX,
+                                       cG, c);
     }
     cacc[0] = cM.x + cM.y;
     cacc[1] = cX.x + cX.y;
@@ -532,7 +535,10 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArg
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
       }
-      const int g_rlast = a.gid[min(row0 + SRT, r1) - 1];
+      const int rlast = min(row0 + SRT, r1) - 1;
+      const int g_rlast = a.gid[rlast];
+      const float th_rlast = a.rec[(long long)rlast * REC + L::TH];
+      const float tl_rlast = a.rec[(long long)rlast * REC + L::TL];
 
       for (int ct = diag ? rt : 0; ct < n_ct; ++ct, ++k) {
         const int s = k % STAGES;
@@ -558,12 +564,20 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArg
         }
         const bool diag_tile = diag && ct == rt;
         const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
-        if (strict)
-          sym32_group<D, PASS, false, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                          jt + warp * 32, false, rM32, rG32, cacc, c);
-        else
+        // temporal culling as in the fp64 kernel, in the log2 domain: ex2.approx.ftz
+        // returns 0 below 2^-126 (with the 2^-E scale already folded into cb, cs)
+        const float dtmin = fmaxf((st[L::TH] - th_rlast) + (st[L::TL] - tl_rlast), 0.f);
+        const bool self_live = c.cs - c.omega * dtmin > -127.f;
+        const bool bg_live = fmaf(c.kt * dtmin, dtmin, c.cb) > -127.f;
+        if (!strict)
           sym32_group<D, PASS, true, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
                                          jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
+        else if (self_live)
+          sym32_group<D, PASS, false, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                          jt + warp * 32, false, rM32, rG32, cacc, c);
+        else if (bg_live)
+          sym32_group<D, PASS, false, SR, false>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                                 jt + warp * 32, false, rM32, rG32, cacc, c);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;

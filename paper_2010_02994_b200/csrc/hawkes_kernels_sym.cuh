@@ -29,6 +29,9 @@
 namespace hk {
 
 constexpr int SYM_RMAX = 4;               // largest rows-per-lane variant
+// a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
+// treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
+constexpr double CULL_EXPONENT = -708.0;
 
 struct SymArgs {
   const double* rec;
@@ -54,7 +57,7 @@ struct SymRow {
 };
 
 // one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
-template <int D, bool MASK, int V>
+template <int D, bool MASK, bool SELF>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           bool dead, double& rM, double (&rG)[D], double& cM,
                                           double& cX, double (&cG)[D], const PassConst& c,
@@ -67,15 +70,15 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;   // >= 0: the column is the later event
   double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
-  double es = fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab);
+  double es = SELF ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
   }
   rM += eb;
   cM += eb;
-  cX += es;
-  const double cc = eb + es;
+  if (SELF) cX += es;
+  const double cc = SELF ? eb + es : eb;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     rG[d] = fma(eb, dx[d], rG[d]);
@@ -83,7 +86,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   }
 }
 
-template <int D, bool MASK, int V>
+template <int D, bool MASK, bool SELF>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           double crho, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
@@ -96,12 +99,12 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;
   double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
-  double es = fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab);
+  double es = SELF ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
   }
-  const double cr = crho * (eb + es);
+  const double cr = crho * (SELF ? eb + es : eb);
   const double cc = row.rho * eb;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -113,7 +116,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R>
+template <int D, int PASS, bool MASK, int SYM_R, bool SELF = true>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp, int cg0, bool cvalid0,
                                           int ridx0, int cidx0, bool diag,
@@ -149,9 +152,9 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
                                  (diag && cidx0 + src <= ridx0 + 32 * r));
       if (PASS == 1)
-        sym_pair1<D, MASK, 0>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
+        sym_pair1<D, MASK, SELF>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
       else
-        sym_pair2<D, MASK, 0>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
+        sym_pair2<D, MASK, SELF>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -249,7 +252,9 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
       }
-      const int g_rlast = a.gid[min(row0 + SYM_RT, r1) - 1];
+      const int rlast = min(row0 + SYM_RT, r1) - 1;
+      const int g_rlast = a.gid[rlast];
+      const double t_rlast = a.rec[(long long)rlast * REC + D];
 
       for (int ct = diag ? rt : 0; ct < n_ct; ++ct, ++k) {
         const int s = k % STAGES;
@@ -281,12 +286,22 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
         }
         const bool diag_tile = diag && ct == rt;
         const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
-        if (strict)
-          sym_group<D, PASS, false, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                           jt + warp * 32, false, rM, rG, cacc, c, tab);
-        else
+        // temporal culling (NEXT-2 on time-compact tiles): with dt >= dtmin for every pair
+        // of this tile pair, the self-excitation exponent is <= lnc_s - omega dtmin and the
+        // background one <= lnc_b + k_t dtmin^2; below the exp's clamp they add nothing
+        const double dtmin = fmax(st[D] - t_rlast, 0.0);
+        const bool self_live = c.lnc_s - c.omega * dtmin > CULL_EXPONENT;
+        const bool bg_live = fma(c.kt * dtmin, dtmin, c.lnc_b) > CULL_EXPONENT;
+        if (!strict)
           sym_group<D, PASS, true, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
                                           jt + warp * 32, diag_tile, rM, rG, cacc, c, tab);
+        else if (self_live)
+          sym_group<D, PASS, false, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                           jt + warp * 32, false, rM, rG, cacc, c, tab);
+        else if (bg_live)
+          sym_group<D, PASS, false, SYM_R, false>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
+                                                  jt + warp * 32, false, rM, rG, cacc, c, tab);
+        // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {
 #pragma unroll
