@@ -265,8 +265,9 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_val = e2e_steps / (float(e2e_ms.item()) * 1e-3)
 
-    # ---- C5 (BASELINE configs[4]): one 20-step HMC leapfrog trajectory at N = 50k through
-    # hawkes_leapfrog (device buffers; 21 gradient evaluations per trajectory)
+    # ---- C5 (BASELINE configs[4]): full HMC transitions over X at N = 50k through
+    # hawkes_hmc_step -- on-device Philox momenta, a 20-step leapfrog, the Metropolis decision;
+    # an accepted transition leaves the end-point gradient cached for the next one
     hmc = None
     if not args.no_hmc:
         c5 = synth.config("C5")
@@ -277,26 +278,28 @@ def run_ours(args):
                                  algorithm=args.algorithm)
         hctx.set_times(torch.from_numpy(c5.t).to(dev))
         hctx.set_params(c5.theta)
-        x5 = torch.from_numpy(c5.x).to(dev)
-        p5 = torch.from_numpy(synth.momenta(c5.N, D, seed=5)).to(dev)
-        xs, ps = x5.clone(), p5.clone()
-        hctx.leapfrog(xs, ps, 1e-4, 2)
+        hctx.set_locations(torch.from_numpy(c5.x).to(dev))
+        hstep, hL, hK = 1e-4, 20, 5
+        hctx.hmc_step(2010, 0, hstep, 2)            # warm-up (graph capture)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        xs.copy_(x5)
-        ps.copy_(p5)
         h0.record(hctx.stream)
-        _, _, ell5, kin5 = hctx.leapfrog(xs, ps, 1e-4, 20)
+        accs, las = [], []
+        for it in range(1, hK + 1):
+            acc, la = hctx.hmc_step(2010, it, hstep, hL)
+            accs.append(acc)
+            las.append(la)
         h1.record(hctx.stream)
         torch.cuda.synchronize()
-        hms = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+        hms = torch.tensor([h0.elapsed_time(h1) / hK], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(hms, op=dist.ReduceOp.MAX)
-        hmc = {"config": "C5 N=50000 D=2, 20 leapfrog steps, step 1e-4, identity mass",
-               "ms_per_trajectory": float(hms.item()), "trajectories_per_s": 1e3 / float(hms.item()),
-               "grad_evals_per_s": 21e3 / float(hms.item()), "ell_end": ell5, "kinetic_end": kin5}
+        hmc = {"config": f"C5 N=50000 D=2, {hK} HMC transitions of {hL} leapfrog steps, step {hstep}, "
+                         "identity mass, Philox momenta + Metropolis on the device",
+               "ms_per_transition": float(hms.item()), "transitions_per_s": 1e3 / float(hms.item()),
+               "acceptance": sum(accs) / hK, "log_alpha": las}
         hctx.close()
 
     # ---- roofline of the dominant pass (FP64 pipe), from the library's own CUDA events

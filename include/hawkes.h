@@ -155,6 +155,30 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
                     int32_t n_steps, const double* inv_mass_diag, const double* box_lo,
                     const double* box_hi, double* out_loglik_end, double* out_kinetic_end);
 
+/* One HMC transition over X (Neal 2011, "MCMC using Hamiltonian dynamics") from the
+ * context's current locations x0, every random number drawn on the device:
+ *   p0 = Minv^{-1/2} z, z_e ~ N(0,1) for element e (row-major N*D) = Box-Muller of the two
+ *       53-bit uniforms u1 = words (0,1), u2 = words (2,3) of the Philox-4x32-10 block
+ *       (Salmon et al. 2011) with counter (it_lo, it_hi, e/2, 0) and key (seed_lo, seed_hi):
+ *       z_{2q} = sqrt(-2 log u1) cos(2 pi u2), z_{2q+1} = sqrt(-2 log u1) sin(2 pi u2),
+ *       u = ((w_a >> 5) 2^26 + (w_b >> 6) + 1/2) / 2^53;
+ *   (x1, p1) = hawkes_leapfrog's trajectory (n_steps, step, inv_mass_diag, box) from (x0, p0);
+ *   accept iff log u < log alpha = H(x0, p0) - H(x1, p1), H = U + 1/2 sum Minv p^2 with U the
+ *       potential of hawkes_set_potential, u from the block with counter
+ *       (it_lo, it_hi, 0xffffffff, 1), words (0,1).
+ * A trajectory that leaves the support (ell = -inf) or diverges (|x| > 1e100, NaN) has
+ * log alpha = -inf and is rejected (not an error).  The chain's state becomes x1 (accepted;
+ * its rates and gradient stay cached, so the next step's first gradient is free) or stays
+ * x0.  The random stream depends on (seed, iteration) only: the same transition for any
+ * world size.  inv_mass_diag (> 0), box_lo, box_hi: as hawkes_leapfrog, host or device per
+ * mem, nullable.  x_out (nullable, N*D per mem) receives the new state; *out_accepted
+ * (0/1) and *out_log_alpha are host, nullable.  One host synchronisation per call.
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_STATE, HAWKES_ERR_GRAD_UNDEFINED (ell(x0) = -inf). */
+int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double step,
+                    int32_t n_steps, const double* inv_mass_diag, const double* box_lo,
+                    const double* box_hi, int32_t mem, double* x_out, int32_t* out_accepted,
+                    double* out_log_alpha);
+
 /* Per-event quantities of the last evaluation (computing it if needed): lambda_n,
  * mu_n = sum_n' mu_nn', xi_n = sum_n' xi_nn' and Lambda_n; each pointer nullable, length N,
  * host or device per mem.  Full length on every rank. */
@@ -233,6 +257,9 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
  * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak
  * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */
 int hawkes_diag_exp(const double* a_dev, double* out_dev, int64_t n);
+/* the standard normals z_0..z_{n-1} hawkes_hmc_step draws for (seed, iteration), into n
+ * device doubles (tests pin the device Philox stream against the oracle's) */
+int hawkes_diag_normals(uint64_t seed, uint64_t iteration, double* out_dev, int64_t n);
 int hawkes_diag_fp64_peak(double* ops_per_s);
 /* FP64 operand-pattern probe (mode 0: DFMA reg,imm,imm; 1: DFMA with 3 register operands;
  * 2: DADD; 3: DMUL; 4: the kernels' fast exp; 5: DFMA reg,reg,imm) at warps_per_sm resident

@@ -12,6 +12,7 @@ restated in the header of ``hawkes_oracle.c``.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from typing import Optional, Sequence
@@ -62,6 +63,11 @@ def _load():
         lib.oracle_xi_pair.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
         lib.oracle_bmds.argtypes = [L, I, dp, dp, ctypes.c_double, dp, dp, dp]
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        lib.oracle_philox4x32_10.argtypes = [u32p, u32p, u32p]
+        lib.oracle_hmc_normals.argtypes = [ctypes.c_uint64, ctypes.c_uint64, L, dp]
+        lib.oracle_hmc_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        lib.oracle_hmc_uniform.restype = ctypes.c_double
         lib.oracle_bmds_pair.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double]
         lib.oracle_bmds_pair.restype = ctypes.c_double
         _lib = lib
@@ -249,3 +255,45 @@ def bmds(x, Y, sigma: float, with_grad: bool = True, with_scale: bool = False):
 def bmds_pair(y: float, delta: float, sigma: float) -> float:
     """r_{nn'} of Eq. bmdsLikelihood plus the normal constant 1/2 log(2 pi sigma^2)."""
     return _load().oracle_bmds_pair(float(y), float(delta), float(sigma))
+
+
+def philox4x32_10(ctr, key):
+    """Philox-4x32-10 block (Salmon et al. 2011) of counter ctr (4 x uint32), key (2 x uint32)."""
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    _load().oracle_philox4x32_10(c, k, o)
+    return list(o)
+
+
+def hmc_normals(seed: int, it: int, n: int) -> np.ndarray:
+    """The HMC step's standard normals for iteration it (hawkes_hmc_step's stream)."""
+    z = np.empty(n)
+    _load().oracle_hmc_normals(seed, it, n, _dptr(z))
+    return z
+
+
+def hmc_uniform(seed: int, it: int) -> float:
+    return _load().oracle_hmc_uniform(seed, it)
+
+
+def hmc_step(x, t, theta, seed: int, it: int, step: float, n_steps: int, inv_mass=None,
+             box_lo=None, box_hi=None, bmds_data=None, hawkes: bool = True):
+    """One HMC transition (Neal 2011): p = z / sqrt(Minv) with z from the Philox
+    stream, leapfrog, accept iff log u < H0 - H1, H = -logpost + 1/2 sum Minv p^2.
+    Returns (x_next, accepted, log_alpha)."""
+    x = np.asarray(x, dtype=np.float64)
+    minv = np.ones_like(x) if inv_mass is None else np.asarray(inv_mass, dtype=np.float64)
+    p0 = hmc_normals(seed, it, x.size).reshape(x.shape) / np.sqrt(minv)
+    lp0 = (loglik(x, t, theta)[0] if hawkes else 0.0) + \
+        (bmds(x, bmds_data[0], bmds_data[1], with_grad=False)[0] if bmds_data is not None else 0.0)
+    H0 = -lp0 + 0.5 * float(np.sum(minv * p0 * p0))
+    with np.errstate(all="ignore"):
+        x1, p1, lp1, k1 = leapfrog(x, p0, t, theta, step, n_steps, inv_mass=inv_mass,
+                                   box_lo=box_lo, box_hi=box_hi, bmds_data=bmds_data,
+                                   hawkes=hawkes)
+    H1 = -lp1 + k1
+    # a trajectory that leaves the support or diverges has H1 = +inf (rejected)
+    log_alpha = H0 - H1 if (np.isfinite(H1) and np.all(np.abs(x1) <= 1e100)) else -math.inf
+    acc = math.log(hmc_uniform(seed, it)) < log_alpha
+    return (x1 if acc else x.copy()), acc, log_alpha

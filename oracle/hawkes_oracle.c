@@ -305,3 +305,56 @@ int oracle_bmds(long N, int D, const double* x, const double* Y, double sigma, d
   free(rows);
   return ORACLE_OK;
 }
+
+/* ---- HMC transition (Neal 2011) with counter-based random numbers ----------
+ * Philox-4x32-10 (Salmon et al. 2011, "Parallel random numbers: as easy as 1, 2, 3"):
+ * 10 rounds of (L, R) <- (mulhi(R0,M0) ^ k0 ^ R1, lo(R0 M0), ...) with the Weyl key
+ * schedule.  The HMC step draws, for momentum element e (row-major N*D) and iteration it,
+ * one block with counter (it_lo, it_hi, e/2, 0) and key (seed_lo, seed_hi); two 53-bit
+ * uniforms from its four words, and Box-Muller gives the normals of elements 2q, 2q+1.
+ * The accept uniform uses counter (it_lo, it_hi, 0xffffffff, 1).                      */
+static void philox_round(uint32_t* c, const uint32_t* k) {
+  const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+  const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+  const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+  const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+  const uint32_t n0 = hi1 ^ c[1] ^ k[0];
+  const uint32_t n2 = hi0 ^ c[3] ^ k[1];
+  c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+  uint32_t k[2] = {key[0], key[1]};
+  for (int r = 0; r < 10; ++r) {
+    philox_round(c, k);
+    k[0] += 0x9E3779B9u;
+    k[1] += 0xBB67AE85u;
+  }
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+static double u53(uint32_t a, uint32_t b) {   /* (0, 1), 53 bits */
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) / 9007199254740992.0;
+}
+
+void oracle_hmc_normals(uint64_t seed, uint64_t it, long n, double* z) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (long q = 0; 2 * q < n; ++q) {
+    const uint32_t ctr[4] = {(uint32_t)it, (uint32_t)(it >> 32), (uint32_t)q, 0u};
+    uint32_t w[4];
+    oracle_philox4x32_10(ctr, key, w);
+    const double u1 = u53(w[0], w[1]), u2 = u53(w[2], w[3]);
+    const double rad = sqrt(-2.0 * log(u1)), ang = 2.0 * ORACLE_PI * u2;
+    z[2 * q] = rad * cos(ang);
+    if (2 * q + 1 < n) z[2 * q + 1] = rad * sin(ang);
+  }
+}
+
+double oracle_hmc_uniform(uint64_t seed, uint64_t it) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const uint32_t ctr[4] = {(uint32_t)it, (uint32_t)(it >> 32), 0xffffffffu, 1u};
+  uint32_t w[4];
+  oracle_philox4x32_10(ctr, key, w);
+  return u53(w[0], w[1]);
+}

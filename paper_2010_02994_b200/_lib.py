@@ -26,9 +26,9 @@ POTENTIAL_HAWKES, POTENTIAL_BMDS = 1, 2
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
-    "hawkes_leapfrog", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move",
+    "hawkes_leapfrog", "hawkes_hmc_step", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move",
     "hawkes_set_bmds", "hawkes_bmds_logdensity", "hawkes_set_potential", "hawkes_enable_timing", "hawkes_get_kernel_times",
-    "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
+    "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_normals", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version",
 )
 
@@ -74,6 +74,10 @@ def load() -> ctypes.CDLL:
     lib.hawkes_grad_locations.argtypes = [vp, dp, i32, P(ctypes.c_double)]
     lib.hawkes_leapfrog.argtypes = [vp, dp, dp, i32, ctypes.c_double, i32, dp, dp, dp,
                                     P(ctypes.c_double), P(ctypes.c_double)]
+    u64 = ctypes.c_uint64
+    lib.hawkes_hmc_step.argtypes = [vp, u64, u64, ctypes.c_double, i32, dp, dp, dp, i32, dp,
+                                    P(i32), P(ctypes.c_double)]
+    lib.hawkes_diag_normals.argtypes = [u64, u64, dp, i64]
     lib.hawkes_get_rates.argtypes = [vp, dp, dp, dp, dp, i32]
     lib.hawkes_propose_move.argtypes = [vp, i32, P(i32), dp, i32, P(ctypes.c_double)]
     lib.hawkes_accept_move.argtypes = [vp]

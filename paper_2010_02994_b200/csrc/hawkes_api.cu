@@ -1386,15 +1386,10 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
   return HAWKES_OK;
 }
 
-int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double step,
-                    int32_t n_steps, const double* inv_mass, const double* box_lo,
-                    const double* box_hi, double* out_ll, double* out_kin) {
-  ENTER(ctx);
-  if (!x || !p || n_steps < 0 || !isfinite(step) ||
-      (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) || ((box_lo == nullptr) != (box_hi == nullptr)))
-    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_leapfrog");
-  if ((ctx->potential & HAWKES_POTENTIAL_HAWKES) && (!ctx->have_t || !ctx->have_p))
-    return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
+extern "C++" {
+// leapfrog buffers + the optional diagonal inverse mass and box, copied in (per mem)
+static int lf_prepare(hawkes_ctx* ctx, int32_t mem, const double* inv_mass, const double* box_lo,
+                      const double* box_hi) {
   const size_t n = (size_t)ctx->N * ctx->D;
   if (!ctx->lf_x) {
     int rc;
@@ -1405,26 +1400,23 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
     TRY(dalloc(ctx, &ctx->lf_lo, n));
     TRY(dalloc(ctx, &ctx->lf_hi, n));
   }
-  if (mem == HAWKES_MEM_HOST) {
-    for (size_t k = 0; k < n; ++k)
-      if (!finite_bounded(x[k]) || !finite_bounded(p[k]))
-        return set_err(ctx, HAWKES_ERR_NONFINITE, "x or p not finite at %zu", k);
-  }
-  TRY(copy_in(ctx, ctx->lf_x, x, n, mem));
-  TRY(copy_in(ctx, ctx->lf_p, p, n, mem));
   if (inv_mass) TRY(copy_in(ctx, ctx->lf_minv, inv_mass, n, mem));
   if (box_lo) {
     TRY(copy_in(ctx, ctx->lf_lo, box_lo, n, mem));
     TRY(copy_in(ctx, ctx->lf_hi, box_hi, n, mem));
   }
-  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
-  TRY(clear_move(ctx));
-  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
-  ctx->have_x = true;
-  ctx->rates_valid = ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+// n_steps leapfrog steps from (lf_x, lf_p), whose positions the records already hold.
+// on_start runs after the potential's gradient at the start point is available (the HMC
+// step snapshots U(x0) there).  Ends with k_kinetic of the final momenta in st->kinetic.
+template <class F>
+static int lf_core(hawkes_ctx* ctx, double step, int32_t n_steps, bool has_minv, bool has_box,
+                   F on_start) {
+  const size_t n = (size_t)ctx->N * ctx->D;
   const bool use_h = ctx->potential & HAWKES_POTENTIAL_HAWKES;
   const bool use_b = (ctx->potential & HAWKES_POTENTIAL_BMDS) != 0;
-  if (use_b && !ctx->have_bmds) return set_err(ctx, HAWKES_ERR_STATE, "BMDS potential without hawkes_set_bmds");
   auto potential_grad = [&]() -> int {
     if (use_h) TRY(run_grad(ctx));
     if (use_b) TRY(dispatchD<BmdsD>(ctx->D, ctx, (const double*)ctx->lf_x));
@@ -1433,19 +1425,51 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
   const double* g1 = use_h ? ctx->grad : nullptr;
   const double* g2 = use_b ? ctx->d_bgrad : nullptr;
   TRY(potential_grad());
+  TRY(on_start());
   const unsigned nb = (unsigned)((n + 255) / 256);
   for (int s = 0; s < n_steps; ++s) {
     k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, g1, g2, (long long)n, 0.5 * step);
     CHECK_LAUNCH();
-    TRY(dispatchD<DriftD>(ctx->D, ctx, step, box_lo != nullptr, inv_mass != nullptr));
+    TRY(dispatchD<DriftD>(ctx->D, ctx, step, has_box, has_minv));
     ctx->rates_valid = ctx->grad_valid = false;
     TRY(potential_grad());
     k_kick<<<nb, 256, 0, ctx->stream>>>(ctx->lf_p, g1, g2, (long long)n, 0.5 * step);
     CHECK_LAUNCH();
   }
-  CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-  k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
+  k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, has_minv ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
   CHECK_LAUNCH();
+  return HAWKES_OK;
+}
+}  // extern "C++"
+
+int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double step,
+                    int32_t n_steps, const double* inv_mass, const double* box_lo,
+                    const double* box_hi, double* out_ll, double* out_kin) {
+  ENTER(ctx);
+  if (!x || !p || n_steps < 0 || !isfinite(step) ||
+      (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) || ((box_lo == nullptr) != (box_hi == nullptr)))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_leapfrog");
+  if ((ctx->potential & HAWKES_POTENTIAL_HAWKES) && (!ctx->have_t || !ctx->have_p))
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
+  const bool use_h = ctx->potential & HAWKES_POTENTIAL_HAWKES;
+  const bool use_b = (ctx->potential & HAWKES_POTENTIAL_BMDS) != 0;
+  if (use_b && !ctx->have_bmds) return set_err(ctx, HAWKES_ERR_STATE, "BMDS potential without hawkes_set_bmds");
+  const size_t n = (size_t)ctx->N * ctx->D;
+  if (mem == HAWKES_MEM_HOST) {
+    for (size_t k = 0; k < n; ++k)
+      if (!finite_bounded(x[k]) || !finite_bounded(p[k]))
+        return set_err(ctx, HAWKES_ERR_NONFINITE, "x or p not finite at %zu", k);
+  }
+  TRY(lf_prepare(ctx, mem, inv_mass, box_lo, box_hi));
+  TRY(copy_in(ctx, ctx->lf_x, x, n, mem));
+  TRY(copy_in(ctx, ctx->lf_p, p, n, mem));
+  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+  TRY(clear_move(ctx));
+  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
+  ctx->have_x = true;
+  ctx->rates_valid = ctx->grad_valid = false;
+  TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [] { return HAWKES_OK; }));
+  CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   TRY(copy_out(ctx, x, ctx->lf_x, n, mem));
   TRY(copy_out(ctx, p, ctx->lf_p, n, mem));
   TRY(fetch_status(ctx));
@@ -1453,6 +1477,76 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
   if (out_kin) *out_kin = ctx->h_st->kinetic;
   if (ctx->h_st->undefined)
     return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "ell = -inf during the trajectory");
+  return HAWKES_OK;
+}
+
+int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double step, int32_t n_steps,
+                    const double* inv_mass, const double* box_lo, const double* box_hi, int32_t mem,
+                    double* x_out, int32_t* out_accepted, double* out_log_alpha) {
+  ENTER(ctx);
+  if (n_steps < 0 || !isfinite(step) || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) ||
+      ((box_lo == nullptr) != (box_hi == nullptr)))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_hmc_step");
+  const bool use_h = ctx->potential & HAWKES_POTENTIAL_HAWKES;
+  const bool use_b = (ctx->potential & HAWKES_POTENTIAL_BMDS) != 0;
+  if (!ctx->have_x) return set_err(ctx, HAWKES_ERR_STATE, "hawkes_set_locations is required");
+  if (use_h && (!ctx->have_t || !ctx->have_p))
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
+  if (use_b && !ctx->have_bmds) return set_err(ctx, HAWKES_ERR_STATE, "BMDS potential without hawkes_set_bmds");
+  if (inv_mass && mem == HAWKES_MEM_HOST) {
+    const size_t n = (size_t)ctx->N * ctx->D;
+    for (size_t k = 0; k < n; ++k)
+      if (!(inv_mass[k] > 0.0) || !(inv_mass[k] < INFINITY))
+        return set_err(ctx, HAWKES_ERR_ARG, "inv_mass_diag must be finite and > 0");
+  }
+  TRY(fetch_status(ctx));   // surface a pending device-side validation failure of x0
+  const size_t n = (size_t)ctx->N * ctx->D;
+  TRY(lf_prepare(ctx, mem, inv_mass, box_lo, box_hi));
+  TRY(clear_move(ctx));
+  const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
+  // x0 = the context's state (records already hold it, so a cached gradient is reused)
+  CU(cudaMemcpyAsync(ctx->lf_x, ctx->xstage, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+  const unsigned nq = (unsigned)((n + 1) / 2);
+  k_hmc_momenta<<<(nq + 255) / 256, 256, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr,
+                                                           (long long)n, key, iteration, 0);
+  CHECK_LAUNCH();
+  k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
+  CHECK_LAUNCH();
+  TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [&]() -> int {
+    k_hmc_begin<<<1, 1, 0, ctx->stream>>>(ctx->st, use_h, use_b);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }));
+  k_hmc_decide<<<1, 1, 0, ctx->stream>>>(ctx->st, ctx->bad, use_h, use_b, key, iteration);
+  CHECK_LAUNCH();
+  k_hmc_select<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->xstage, ctx->lf_x, (long long)n,
+                                                                      ctx->st);
+  CHECK_LAUNCH();
+  TRY(fetch_status(ctx));
+  const bool acc = ctx->h_st->accepted != 0;
+  if (ctx->h_st->undef0) {
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+    return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "ell = -inf at the chain's current state");
+  }
+  if (!acc) {   // back to x0: the records and cached rates were those of the trajectory
+    TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+  }
+  if (x_out) TRY(copy_out(ctx, x_out, ctx->xstage, n, mem));
+  if (out_accepted) *out_accepted = acc ? 1 : 0;
+  if (out_log_alpha) *out_log_alpha = ctx->h_st->log_alpha;
+  return HAWKES_OK;
+}
+
+int hawkes_diag_normals(uint64_t seed, uint64_t iteration, double* out_dev, int64_t n) {
+  if (!out_dev || n < 0) return HAWKES_ERR_ARG;
+  if (n == 0) return HAWKES_OK;
+  const long long nq = (n + 1) / 2;
+  k_hmc_momenta<<<(unsigned)((nq + 255) / 256), 256>>>(out_dev, nullptr, (long long)n,
+                                                        make_uint2((unsigned)seed, (unsigned)(seed >> 32)),
+                                                        iteration, 1);
+  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return HAWKES_ERR_CUDA;
   return HAWKES_OK;
 }
 

@@ -182,6 +182,12 @@ struct EvalStatus {
   double kinetic;
   double dell;     // Delta ell of the pending block move
   double bmds;     // BMDS log density of the last BMDS evaluation
+  // HMC transition (hawkes_hmc_step)
+  double lp0;      // log density at the chain's current state
+  double kin0;     // 1/2 sum Minv p0^2
+  double log_alpha;
+  int accepted;
+  int undef0;      // ell(x0) = -inf: the chain's state has zero density
 };
 
 // Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
@@ -388,6 +394,79 @@ __global__ void k_kinetic(const double* __restrict__ p, const double* __restrict
     __syncthreads();
   }
   if (threadIdx.x == 0) st->kinetic = 0.5 * sh[0];
+}
+
+// ---- HMC transition (Neal 2011): counter-based random numbers on the device.
+// Philox-4x32-10 (Salmon et al. 2011): 10 rounds of the two 32x32->64 multiplies with the
+// Weyl key schedule; the counter is (iteration lo, hi, block, lane) and the key the seed, so
+// every rank (and every world size) draws the same numbers without any state.
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// 53-bit uniform in (0, 1) from two words (high 27 bits of a, high 26 of b)
+__device__ __forceinline__ double u53(unsigned a, unsigned b) {
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) * (1.0 / 9007199254740992.0);
+}
+
+// standard normals z[2q], z[2q+1] from block (it, q): Box-Muller of (u1, u2)
+__device__ __forceinline__ double2 hmc_normal_pair(uint2 key, unsigned long long it, unsigned q) {
+  const uint4 w = philox10(make_uint4((unsigned)it, (unsigned)(it >> 32), q, 0u), key);
+  const double u1 = u53(w.x, w.y), u2 = u53(w.z, w.w);
+  const double rad = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  return make_double2(rad * c, rad * s);
+}
+
+// p = Minv^{-1/2} z (Minv = nullptr: identity), or z itself into p when raw != 0
+__global__ void k_hmc_momenta(double* __restrict__ p, const double* __restrict__ minv, long long n,
+                              uint2 key, unsigned long long it, int raw) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * q >= n) return;
+  const double2 z = hmc_normal_pair(key, it, (unsigned)q);
+  const long long e = 2 * q;
+  p[e] = (minv && !raw) ? z.x * rsqrt(minv[e]) : z.x;
+  if (e + 1 < n) p[e + 1] = (minv && !raw) ? z.y * rsqrt(minv[e + 1]) : z.y;
+}
+
+// after the first potential evaluation at x0 and k_kinetic(p0)
+__global__ void k_hmc_begin(EvalStatus* st, int use_h, int use_b) {
+  st->lp0 = (use_h ? st->ell : 0.0) + (use_b ? st->bmds : 0.0);
+  st->kin0 = st->kinetic;
+  st->undef0 = use_h ? st->undefined : 0;
+}
+
+// after the trajectory and k_kinetic(p1): Metropolis accept iff log u < H0 - H1.  A
+// trajectory that left the support (ell = -inf) or diverged (|x| > 1e100, flagged by
+// k_drift / k_pack_x in bit 0 of *bad) has H1 = +inf and is rejected; its flag is cleared.
+__global__ void k_hmc_decide(EvalStatus* st, int* bad, int use_h, int use_b, uint2 key,
+                             unsigned long long it) {
+  const double lp1 = (use_h ? st->ell : 0.0) + (use_b ? st->bmds : 0.0);
+  const bool diverged = (use_h && st->undefined) || (*bad & 1) || !(lp1 > -INFINITY) ||
+                        !(st->kinetic < INFINITY);
+  const double la = diverged ? -INFINITY : (lp1 - st->kinetic) - (st->lp0 - st->kin0);
+  const uint4 w = philox10(make_uint4((unsigned)it, (unsigned)(it >> 32), 0xffffffffu, 1u), key);
+  const double u = u53(w.x, w.y);
+  st->log_alpha = la;
+  st->accepted = (!st->undef0 && log(u) < la) ? 1 : 0;
+  if (*bad & 1) atomicAnd(bad, ~1);
+  if (use_h) st->undefined = 0;
+}
+
+// the chain's new state: x' when accepted, else x0 (xstage holds x0 throughout)
+__global__ void k_hmc_select(double* __restrict__ xstage, const double* __restrict__ x1, long long n,
+                             const EvalStatus* st) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && st->accepted) xstage[i] = x1[i];
 }
 
 // diagnostics: the fast exp on an array (tests pin its accuracy)

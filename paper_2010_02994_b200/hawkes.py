@@ -152,6 +152,33 @@ class HawkesContext:
                                         ctypes.byref(ll), ctypes.byref(kin)), self._h)
         return x, p, ll.value, kin.value
 
+    def hmc_step(self, seed: int, iteration: int, step: float, n_steps: int, inv_mass=None,
+                 box_lo=None, box_hi=None, x_out=None):
+        """hawkes_hmc_step: one HMC transition from the context's locations with on-device
+        Philox momenta and Metropolis decision.  inv_mass / box / x_out share one memory kind
+        (host numpy or CUDA tensors).  Returns (accepted: bool, log_alpha: float); the new
+        state is written into x_out when given."""
+        arrs = [inv_mass, box_lo, box_hi, x_out]
+        ptrs, mems, keep = [], set(), []
+        for a in arrs:
+            if a is None:
+                ptrs.append(None)
+                continue
+            pa, ma, ka = _ptr_mem(a)
+            ptrs.append(pa)
+            mems.add(ma)
+            keep.append(ka)
+        if len(mems) > 1:
+            raise ValueError("inv_mass, box and x_out must live in the same memory")
+        if x_out is not None and keep[-1] is not x_out:
+            raise ValueError("x_out must be a contiguous float64 array/tensor")
+        mem = mems.pop() if mems else HAWKES_MEM_DEVICE
+        acc, la = ctypes.c_int32(), ctypes.c_double()
+        check(self._lib.hawkes_hmc_step(self._h, int(seed), int(iteration), float(step),
+                                        int(n_steps), ptrs[0], ptrs[1], ptrs[2], mem, ptrs[3],
+                                        ctypes.byref(acc), ctypes.byref(la)), self._h)
+        return bool(acc.value), la.value
+
     # -- Bayesian MDS (P:L158-184) and the HMC potential
     def set_bmds(self, Y, sigma: float):
         """hawkes_set_bmds: N x N dissimilarities (lower triangle read) and sigma."""
@@ -209,6 +236,13 @@ def diag_exp(a: torch.Tensor) -> torch.Tensor:
     a = a.contiguous()
     out = torch.empty_like(a)
     check(_lib.load().hawkes_diag_exp(a.data_ptr(), out.data_ptr(), a.numel()))
+    return out
+
+
+def diag_normals(seed: int, iteration: int, n: int, device: int = 0) -> torch.Tensor:
+    """The standard normals hawkes_hmc_step draws for (seed, iteration) (RNG parity tests)."""
+    out = torch.empty(n, dtype=torch.float64, device=f"cuda:{device}")
+    check(_lib.load().hawkes_diag_normals(int(seed), int(iteration), out.data_ptr(), int(n)))
     return out
 
 

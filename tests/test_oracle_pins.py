@@ -329,3 +329,67 @@ def test_bmds_gradient_invariances_and_differences():
         xm[n, d] -= h
         fd = (oracle.bmds(xp, Y, s, with_grad=False)[0] - oracle.bmds(xm, Y, s, with_grad=False)[0]) / (2 * h)
         assert abs(fd - g[n, d]) <= 1e-6 * max(abs(g[n, d]), S[n, d])
+
+
+# ---- HMC transition (Neal 2011) and its counter-based random numbers
+
+def test_philox_known_answers(golden_dir):
+    """Philox-4x32-10 against the published Random123 known-answer vectors."""
+    with open(os.path.join(golden_dir, "philox4x32_10_kat.json")) as f:
+        kat = json.load(f)
+    for v in kat["vectors"]:
+        ctr = [int(w, 16) for w in v["ctr"]]
+        key = [int(w, 16) for w in v["key"]]
+        assert oracle.philox4x32_10(ctr, key) == [int(w, 16) for w in v["out"]]
+
+
+def test_hmc_normals_are_standard_normal():
+    """Box-Muller of the Philox uniforms: Kolmogorov-Smirnov against N(0,1), moments, and
+    no correlation between the two normals of a block or between iterations/seeds."""
+    from scipy import stats
+    n = 200_001
+    z = oracle.hmc_normals(5, 3, n)
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+    assert abs(z.mean()) < 5 / math.sqrt(n)
+    assert abs(z.var() - 1) < 5 * math.sqrt(2 / n)
+    assert abs(np.mean(z ** 4) - 3) < 0.1          # kurtosis of the normal
+    m = (n - 1) // 2
+    assert abs(np.corrcoef(z[0:2 * m:2], z[1:2 * m:2])[0, 1]) < 5 / math.sqrt(m)
+    z2 = oracle.hmc_normals(5, 4, n)
+    z3 = oracle.hmc_normals(6, 3, n)
+    assert abs(np.corrcoef(z, z2)[0, 1]) < 5 / math.sqrt(n)
+    assert abs(np.corrcoef(z, z3)[0, 1]) < 5 / math.sqrt(n)
+    # prefix property: element e's draw does not depend on the length requested
+    assert np.array_equal(oracle.hmc_normals(5, 3, 101), z[:101])
+    # the uniform is (0,1) and varies with the iteration
+    u = np.array([oracle.hmc_uniform(5, it) for it in range(2000)])
+    assert u.min() > 0 and u.max() < 1 and stats.kstest(u, "uniform").pvalue > 1e-3
+
+
+def test_hmc_step_energy_error_is_second_order():
+    """log alpha = H0 - H1 of the leapfrog is O(step^2) (Neal 2011 sec. 5.2): halving the
+    step divides it by ~4.  A sign error in H (U - K instead of U + K) or a potential of the
+    wrong sign leaves an O(1) term and fails this."""
+    c = synth.config("C1", 200)
+    las = []
+    for step in (2e-4, 1e-4, 5e-5):
+        _, _, la = oracle.hmc_step(c.x, c.t, c.theta, 3, 0, step, int(round(4e-4 / step)))
+        las.append(abs(la))
+    assert 3.0 < las[0] / las[1] < 5.0 and 3.0 < las[1] / las[2] < 5.0
+
+
+def test_hmc_step_zero_steps_accepts_and_keeps_x():
+    """No trajectory: H1 = H0, log alpha = 0 and log u < 0 always accepts."""
+    c = synth.config("C1", 100)
+    x1, acc, la = oracle.hmc_step(c.x, c.t, c.theta, 9, 1, 1e-3, 0)
+    assert acc and la == 0.0 and np.array_equal(x1, c.x)
+
+
+def test_hmc_step_reversible():
+    """The transition's proposal is an involution: from (x1, -p1) the same leapfrog returns
+    to (x0, -p0), so a Metropolis step with H alone is valid (Neal 2011 sec. 3.2)."""
+    c = synth.config("C1", 150)
+    z = oracle.hmc_normals(4, 2, c.x.size).reshape(c.x.shape)
+    x1, p1, _, _ = oracle.leapfrog(c.x, z, c.t, c.theta, 2e-3, 6)
+    x2, p2, _, _ = oracle.leapfrog(x1, -p1, c.t, c.theta, 2e-3, 6)
+    assert np.allclose(x2, c.x, atol=1e-10) and np.allclose(-p2, z, atol=1e-8)
