@@ -297,3 +297,113 @@ def hmc_step(x, t, theta, seed: int, it: int, step: float, n_steps: int, inv_mas
     log_alpha = H0 - H1 if (np.isfinite(H1) and np.all(np.abs(x1) <= 1e100)) else -math.inf
     acc = math.log(hmc_uniform(seed, it)) < log_alpha
     return (x1 if acc else x.copy()), acc, log_alpha
+
+
+# ---- block Metropolis-Hastings over coarsened locations --------------------
+# Random numbers: the Philox-4x32-10 block with counter (it_lo, it_hi, b, tag) and key
+# (seed_lo, seed_hi); b = block index within the sweep.  Proposal draws for slot q use
+# tag = 0x80000000 | q << 12 | a (a = attempt / dimension pair), the accept uniform uses
+# tag = 0xC0000000.  Two 53-bit uniforms per block (words 0,1 and 2,3).
+_MH_TAG, _MH_ACCEPT = 0x80000000, 0xC0000000
+_M32 = 0xFFFFFFFF
+
+
+def _u53(a: int, b: int) -> float:
+    return ((a >> 5) * 67108864.0 + (b >> 6) + 0.5) / 9007199254740992.0
+
+
+def mh_uniforms(seed: int, it: int, b: int, tag: int):
+    w = philox4x32_10([it & _M32, (it >> 32) & _M32, b & _M32, tag & _M32],
+                      [seed & _M32, (seed >> 32) & _M32])
+    return _u53(w[0], w[1]), _u53(w[2], w[3])
+
+
+def _Phi(z: float) -> float:
+    return 0.5 * math.erfc(-z / math.sqrt(2.0))
+
+
+def _trunc_mass(x: float, lo: float, hi: float, s: float) -> float:
+    """Z(x) = Phi((hi - x)/s) - Phi((lo - x)/s): the N(x, s^2) mass of (lo, hi)."""
+    return 1.0 - 0.5 * math.erfc((hi - x) / s / math.sqrt(2.0)) - _Phi((lo - x) / s)
+
+
+def lens_area(R: float, rho: float, d: float) -> float:
+    """Area of the intersection of a disc of radius R and one of radius rho whose centres are
+    d apart (the 'asymmetric lens' of P:L248), by the textbook circle-circle formula."""
+    if d >= R + rho:
+        return 0.0
+    if d + rho <= R:
+        return math.pi * rho * rho
+    if d + R <= rho:
+        return math.pi * R * R
+    a1 = rho * rho * math.acos((d * d + rho * rho - R * R) / (2.0 * d * rho))
+    a2 = R * R * math.acos((d * d + R * R - rho * rho) / (2.0 * d * R))
+    k = 0.5 * math.sqrt((-d + rho + R) * (d + rho - R) * (d - rho + R) * (d + rho + R))
+    return a1 + a2 - k
+
+
+MH_MAX_ATTEMPTS = 4096
+
+
+def mh_propose(kind: str, x_n, centre_n, size_n: float, scale: float, seed: int, it: int,
+               b: int, q: int):
+    """Proposal for one event and its log Hastings term log q(x|x*) - log q(x*|x).
+    square (Eq. locsPrior1): per dimension a N(x_d, (scale*size)^2) draw truncated to
+      (c_d - size, c_d + size) by inverting the CDF: z = Phi^-1(Phi(alpha) + u Z), x* = x + s z;
+      Hastings prod_d Z_d(x) / Z_d(x*) (the truncation normalisers).
+    disc (Eq. circleKernel / locsPrior2): uniform on {|y - c| < r} cap {|y - x| < r eps},
+      eps = scale, by rejection from the disc of radius r eps around x; Hastings A(x)/A(x*)
+      with A the lens area.  After MH_MAX_ATTEMPTS failed attempts the proposal is x itself."""
+    from scipy.special import ndtri   # Phi^-1 (library primitive)
+    x_n = np.asarray(x_n, dtype=np.float64)
+    D = x_n.size
+    if kind == "square":
+        s = scale * size_n
+        xs = np.empty(D)
+        logh = 0.0
+        for d in range(D):
+            u = mh_uniforms(seed, it, b, _MH_TAG | (q << 12) | (d // 2))[d % 2]
+            lo, hi = centre_n[d] - size_n, centre_n[d] + size_n
+            alpha = (lo - x_n[d]) / s
+            Z0 = _trunc_mass(x_n[d], lo, hi, s)
+            z = float(ndtri(_Phi(alpha) + u * Z0))
+            xs[d] = min(max(x_n[d] + s * z, lo), hi)
+            logh += math.log(Z0) - math.log(_trunc_mass(xs[d], lo, hi, s))
+        return xs, logh
+    if kind == "disc":
+        r, rho = size_n, scale * size_n
+        for a in range(MH_MAX_ATTEMPTS):
+            u1, u2 = mh_uniforms(seed, it, b, _MH_TAG | (q << 12) | a)
+            rad, ang = rho * math.sqrt(u1), 2.0 * math.pi * u2
+            y = np.array([x_n[0] + rad * math.cos(ang), x_n[1] + rad * math.sin(ang)])
+            if (y[0] - centre_n[0]) ** 2 + (y[1] - centre_n[1]) ** 2 < r * r:
+                A0 = lens_area(r, rho, math.hypot(x_n[0] - centre_n[0], x_n[1] - centre_n[1]))
+                A1 = lens_area(r, rho, math.hypot(y[0] - centre_n[0], y[1] - centre_n[1]))
+                return y, math.log(A0) - math.log(A1)
+        return x_n.copy(), 0.0
+    raise ValueError(kind)
+
+
+def mh_sweep(x, t, theta, kind: str, centre, size, blocks, scale: float, seed: int, it: int):
+    """Sequential block MH updates: for block b (an array of k distinct events),
+    propose all k jointly, log alpha = [ell(X') - ell(X)] + sum log Hastings (uniform priors
+    cancel inside the regions), accept iff log u < log alpha.  Returns
+    (x_final, accepted list, log_alpha list).  ell by full evaluations (Eq. 1)."""
+    x = np.array(x, dtype=np.float64)
+    ell = loglik(x, t, theta)[0]
+    accs, las = [], []
+    for b, blk in enumerate(blocks):
+        xp = x.copy()
+        logh = 0.0
+        for q, n in enumerate(blk):
+            xp[n], h = mh_propose(kind, x[n], centre[n], float(size[n]), scale, seed, it, b, q)
+            logh += h
+        ell1 = loglik(xp, t, theta)[0]
+        la = (ell1 - ell) + logh if ell1 > -math.inf else -math.inf
+        u = mh_uniforms(seed, it, b, _MH_ACCEPT)[0]
+        acc = math.log(u) < la
+        if acc:
+            x, ell = xp, ell1
+        accs.append(acc)
+        las.append(la)
+    return x, accs, las

@@ -39,6 +39,10 @@ class Catalog:
     theta: Tuple[float, ...]
     name: str
     seed: int
+    # coarsening regions the locations were drawn in (C2: squares, C3: discs), else None
+    region: Optional[str] = None        # "square" | "disc"
+    centre: Optional[np.ndarray] = None  # N x D observed locations (box / disc centres)
+    size: Optional[np.ndarray] = None    # N: square half-width or disc radius
 
     @property
     def N(self) -> int:
@@ -106,7 +110,8 @@ def dc_shaped(N: int = 5000, replicate: int = 0) -> Catalog:
     x, t = _cluster(rng, N, n_bg, bx, bt, theta[4], theta[5], 8760.0)
     box = 100.0 * np.round(x / 100.0)
     x = box + rng.uniform(-50.0, 50.0, size=x.shape)
-    return Catalog(np.ascontiguousarray(x), t, theta, f"dc_shaped_N{N}", seed)
+    return Catalog(np.ascontiguousarray(x), t, theta, f"dc_shaped_N{N}", seed, "square",
+                   np.ascontiguousarray(box), np.full(N, 50.0))
 
 
 def alaska_shaped(N: int = 20000, replicate: int = 0) -> Catalog:
@@ -129,8 +134,10 @@ def alaska_shaped(N: int = 20000, replicate: int = 0) -> Catalog:
                  np.minimum(0.01 * (1.0 - rng.uniform(size=N)) ** (-1.0 / 1.06), 4.42))
     ang = rng.uniform(0.0, 2 * np.pi, size=N)
     rad = r * np.sqrt(rng.uniform(size=N))
+    centre = x
     x = x + np.column_stack([rad * np.cos(ang), rad * np.sin(ang)])
-    return Catalog(np.ascontiguousarray(x), t, theta, f"alaska_shaped_N{N}", seed)
+    return Catalog(np.ascontiguousarray(x), t, theta, f"alaska_shaped_N{N}", seed, "disc",
+                   np.ascontiguousarray(centre), np.ascontiguousarray(r))
 
 
 def with_ties(N: int, ndistinct: int, replicate: int = 0, D: int = 2) -> Catalog:

@@ -393,3 +393,96 @@ def test_hmc_step_reversible():
     x1, p1, _, _ = oracle.leapfrog(c.x, z, c.t, c.theta, 2e-3, 6)
     x2, p2, _, _ = oracle.leapfrog(x1, -p1, c.t, c.theta, 2e-3, 6)
     assert np.allclose(x2, c.x, atol=1e-10) and np.allclose(-p2, z, atol=1e-8)
+
+
+# ---- block MH over coarsened locations (Eq. circleKernel)
+
+def test_lens_area_closed_forms_and_monte_carlo():
+    """Two unit circles one radius apart: 2 pi/3 - sqrt(3)/2 (textbook); containment and
+    disjoint limits; continuity at the branch points; 2e6-point Monte Carlo elsewhere."""
+    la = oracle.lens_area
+    assert la(1.0, 1.0, 1.0) == pytest.approx(2 * math.pi / 3 - math.sqrt(3) / 2, rel=1e-14)
+    assert la(2.0, 0.5, 1.0) == pytest.approx(math.pi * 0.25, rel=1e-15)
+    assert la(0.5, 2.0, 1.0) == pytest.approx(math.pi * 0.25, rel=1e-15)
+    assert la(1.0, 1.0, 2.0) == 0.0
+    for R, rho in ((1.0, 0.3), (1.0, 1.7)):
+        dc = abs(R - rho)
+        assert la(R, rho, dc * (1 + 1e-9)) == pytest.approx(math.pi * min(R, rho) ** 2, rel=1e-4)
+        assert la(R, rho, (R + rho) * (1 - 1e-12)) < 1e-10
+    rng = np.random.default_rng(0)
+    for R, rho, d in ((1.0, 0.6, 0.8), (1.0, 1.0, 0.4), (2.0, 1.1, 1.9), (1.0, 1.5, 0.9)):
+        n = 2_000_000
+        p = rng.uniform(-rho, rho, size=(n, 2))
+        inside_small = np.sum(p * p, axis=1) < rho * rho
+        inside_big = (p[:, 0] + d) ** 2 + p[:, 1] ** 2 < R * R     # big disc centred at (-d, 0)
+        frac = np.mean(inside_small & inside_big)
+        se = math.sqrt(frac * (1 - frac) / n)
+        assert abs(la(R, rho, d) - 4 * rho * rho * frac) < 5 * 4 * rho * rho * se
+
+
+def test_truncated_normal_proposal_distribution():
+    """Square proposals (Eq. locsPrior1 region) follow N(x, s^2) truncated to the box:
+    Kolmogorov-Smirnov against scipy.stats.truncnorm, per dimension."""
+    from scipy import stats
+    x, c, h, scale = np.array([30.0, -45.0]), np.array([0.0, 0.0]), 50.0, 0.8
+    s = scale * h
+    draws = np.array([oracle.mh_propose("square", x, c, h, scale, 5, 1, b, 3)[0] for b in range(6000)])
+    for d in range(2):
+        a, b = (c[d] - h - x[d]) / s, (c[d] + h - x[d]) / s
+        assert stats.kstest(draws[:, d], stats.truncnorm(a, b, loc=x[d], scale=s).cdf).pvalue > 1e-3
+    assert np.all(np.abs(draws - c) <= h)
+
+
+def test_disc_proposal_is_uniform_on_the_lens():
+    """Disc proposals (Eq. circleKernel) are uniform on disc(c, r) cap disc(x, r eps):
+    two-sample KS per coordinate against an independent numpy rejection sampler."""
+    from scipy import stats
+    c, r, eps = np.array([0.0, 0.0]), 1.0, 0.9
+    x = np.array([0.7, 0.2])
+    draws = np.array([oracle.mh_propose("disc", x, c, r, eps, 9, 2, b, 0)[0] for b in range(6000)])
+    assert np.all(np.sum((draws - c) ** 2, axis=1) < r * r)
+    assert np.all(np.sum((draws - x) ** 2, axis=1) < (r * eps) ** 2)
+    rng = np.random.default_rng(1)
+    p = x + rng.uniform(-r * eps, r * eps, size=(60000, 2))
+    keep = (np.sum((p - x) ** 2, axis=1) < (r * eps) ** 2) & (np.sum((p - c) ** 2, axis=1) < r * r)
+    ref = p[keep]
+    for d in range(2):
+        assert stats.ks_2samp(draws[:, d], ref[:, d]).pvalue > 1e-3
+
+
+def _mh_chain_r2(kind, size, scale, T):
+    """One event of a 3-event catalog moved by the block MH kernel T times; returns the chain's
+    E|x - c|^2 with its batch-means standard error and the exact value by grid quadrature."""
+    t = np.array([0.0, 0.5, 0.7])
+    theta = (0.5, 0.6, 1.0, 0.5, 2.0, 0.4)
+    x0 = np.array([[0.8, 0.3], [0.0, 0.0], [-0.5, 0.9]])
+    centre, sz = np.zeros((3, 2)), np.full(3, size)
+    r2 = np.empty(T)
+    x = x0.copy()
+    for it in range(T):
+        x, _, _ = oracle.mh_sweep(x, t, theta, kind, centre, sz, [[1]], scale, 17, it)
+        r2[it] = x[1, 0] ** 2 + x[1, 1] ** 2
+    bm = r2.reshape(40, -1).mean(axis=1)
+    se = bm.std(ddof=1) / math.sqrt(len(bm))
+    G = 160
+    g = (np.arange(G) + 0.5) / G * 2 * size - size
+    w = np.zeros((G, G))
+    for i in range(G):
+        for j in range(G):
+            if kind == "disc" and g[i] ** 2 + g[j] ** 2 >= size ** 2:
+                continue
+            xp = x0.copy()
+            xp[1] = (g[i], g[j])
+            w[i, j] = math.exp(oracle.loglik(xp, t, theta)[0])
+    G2 = g[:, None] ** 2 + g[None, :] ** 2
+    return r2.mean(), se, float(np.sum(w * G2) / np.sum(w))
+
+
+@pytest.mark.parametrize("kind,scale", [("square", 1.0), ("disc", 1.0)])
+def test_block_mh_targets_the_posterior(kind, scale):
+    """Stationarity: the chain's E|x_n - c|^2 matches the exact posterior of one event
+    (likelihood x uniform region prior, grid quadrature).  The proposals here are strongly
+    asymmetric near the region edge, so dropping or inverting the Hastings term shifts this
+    moment by 9-15 standard errors (0.044 for the square, 0.055 for the disc at eps = 1)."""
+    m, se, exact = _mh_chain_r2(kind, 1.0, scale, 16000)
+    assert abs(m - exact) < max(4 * se, 0.004), (m, se, exact)
