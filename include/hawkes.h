@@ -179,6 +179,11 @@ int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double s
                     const double* box_hi, int32_t mem, double* x_out, int32_t* out_accepted,
                     double* out_log_alpha);
 
+/* The context's current locations (N*D row-major, host or device per mem): those of the
+ * last set_locations, leapfrog, accepted move / HMC transition / MH sweep.
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_STATE (no locations). */
+int hawkes_get_locations(hawkes_ctx* ctx, double* out_x, int32_t mem);
+
 /* Per-event quantities of the last evaluation (computing it if needed): lambda_n,
  * mu_n = sum_n' mu_nn', xi_n = sum_n' xi_nn' and Lambda_n; each pointer nullable, length N,
  * host or device per mem.  Full length on every rank. */
@@ -221,6 +226,40 @@ int hawkes_set_potential(hawkes_ctx* ctx, int32_t flags);
 int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const double* new_x,
                         int32_t mem, double* out_delta);
 int hawkes_accept_move(hawkes_ctx* ctx);
+
+/* Coarsening regions: the uniform location priors of the DC and Alaska models, which the
+ * block MH sweep samples under.  kind HAWKES_REGION_SQUARE: |x_nd - centre_nd| < size_n for
+ * every d (Eq. locsPrior1, size = the 50 m half-width); HAWKES_REGION_DISC:
+ * |x_n - centre_n|_2 < size_n (Eq. locsPrior2, size = r_n; D = 2 only, else
+ * HAWKES_ERR_DIM).  centre (N*D row-major) and size (N) are copied (host or device per
+ * mem).  The context's locations should lie inside their regions (prior support).
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_DIM, HAWKES_ERR_NONFINITE (size <= 0 or non-finite). */
+typedef enum { HAWKES_REGION_SQUARE = 1, HAWKES_REGION_DISC = 2 } hawkes_region;
+int hawkes_set_regions(hawkes_ctx* ctx, int32_t kind, const double* centre, const double* size,
+                       int32_t mem);
+
+/* On-device block Metropolis-Hastings sweep over locations: n_blocks
+ * sequential updates; block b moves the k distinct events blocks[b*k .. b*k+k) (host
+ * int32, 1 <= k <= 256) jointly:
+ *   square regions: x*_nd = x_nd + s z, z ~ N(0,1) truncated to the region by inverting its
+ *     CDF, s = scale * size_n; log Hastings sum_d log Z_d(x) - log Z_d(x*), Z_d = the
+ *     N(x_nd, s^2) mass of the region's interval ("truncated normal proposals");
+ *   disc regions: x* uniform on disc(centre_n, r_n) cap disc(x_n, scale r_n) (Eq.
+ *     circleKernel, eps = scale) by rejection (at most 4096 attempts, else x* = x); log
+ *     Hastings log A(x) - log A(x*), A the closed-form lens area;
+ *   log alpha = [ell(X') - ell(X)] + sum of the block's log Hastings terms (the uniform priors
+ *     cancel), ell(X') - ell(X) by the O(kN) update of hawkes_propose_move;
+ *   accept iff log u < log alpha; an accepted block updates the locations and cached rates.
+ * Random numbers: Philox-4x32-10 (as hawkes_hmc_step) with counter (it_lo, it_hi, b, tag),
+ * key (seed_lo, seed_hi): slot q's draws use tag 0x80000000 | q << 12 | a (a = dimension pair
+ * for squares, attempt for discs), the accept uniform tag 0xC0000000; each block gives two
+ * 53-bit uniforms (words 0,1 and 2,3).  The whole sweep runs on the device with one host
+ * synchronisation at the end.  out_accepted (n_blocks int32), out_log_alpha (n_blocks
+ * double), out_n_accepted: host, nullable.
+ * Errors: HAWKES_ERR_ARG, HAWKES_ERR_STATE (no regions / set_* missing). */
+int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t* blocks,
+                    double scale, uint64_t seed, uint64_t iteration, int32_t* out_accepted,
+                    double* out_log_alpha, int32_t* out_n_accepted);
 
 /* Kernel timing (CUDA events on the context stream around each launch of the two O(N^2)
  * pass kernels).  enable != 0 starts accumulating from zero.  hawkes_get_kernel_times

@@ -21,12 +21,14 @@ HAWKES_FP64, HAWKES_FP32 = 0, 1
 HAWKES_MEM_HOST, HAWKES_MEM_DEVICE = 0, 1
 ALGORITHMS = {"auto": 0, "rows": 1, "pairs": 2}
 POTENTIAL_HAWKES, POTENTIAL_BMDS = 1, 2
+REGIONS = {"square": 1, "disc": 2}
 
 # every symbol include/hawkes.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
     "hawkes_leapfrog", "hawkes_hmc_step", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move",
+    "hawkes_set_regions", "hawkes_mh_sweep", "hawkes_get_locations",
     "hawkes_set_bmds", "hawkes_bmds_logdensity", "hawkes_set_potential", "hawkes_enable_timing", "hawkes_get_kernel_times",
     "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_normals", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version",
@@ -77,6 +79,10 @@ def load() -> ctypes.CDLL:
     u64 = ctypes.c_uint64
     lib.hawkes_hmc_step.argtypes = [vp, u64, u64, ctypes.c_double, i32, dp, dp, dp, i32, dp,
                                     P(i32), P(ctypes.c_double)]
+    lib.hawkes_get_locations.argtypes = [vp, dp, i32]
+    lib.hawkes_set_regions.argtypes = [vp, i32, dp, dp, i32]
+    lib.hawkes_mh_sweep.argtypes = [vp, i32, i32, P(i32), ctypes.c_double, u64, u64, P(i32),
+                                    P(ctypes.c_double), P(i32)]
     lib.hawkes_diag_normals.argtypes = [u64, u64, dp, i64]
     lib.hawkes_get_rates.argtypes = [vp, dp, dp, dp, dp, i32]
     lib.hawkes_propose_move.argtypes = [vp, i32, P(i32), dp, i32, P(ctypes.c_double)]

@@ -34,6 +34,7 @@
 #include "hawkes_moves.cuh"
 #include "hawkes_bmds.cuh"
 #include "hawkes_ops.cuh"
+#include "hawkes_mh.cuh"
 #include "hawkes_plan.h"
 
 using namespace hk;
@@ -172,6 +173,14 @@ struct hawkes_ctx {
   double* d_move_part = nullptr;   // ceil(N/256) block sums
   double* d_move_rows_part = nullptr;  // MOVE_MAX x ceil(N/MOVE_SPLIT) x 2
   bool lam_valid = false;      // rates[][] hold lambda of the current state (all rows)
+  // coarsening regions and the on-device block MH sweep (hawkes_set_regions / hawkes_mh_sweep)
+  int reg_kind = 0;
+  double* d_reg_c = nullptr;   // N x D region centres
+  double* d_reg_s = nullptr;   // N half-widths / radii
+  int* d_mh_blocks = nullptr;  // mh_cap event indices of the current sweep
+  int* d_mh_acc = nullptr;     // mh_bcap decisions
+  double* d_mh_la = nullptr;   // mh_bcap log alphas
+  size_t mh_cap = 0, mh_bcap = 0;
   // BMDS (hawkes_set_bmds / hawkes_bmds_logdensity / hawkes_set_potential)
   double* d_Y = nullptr;       // N x N, lower triangle mirrored into the upper
   double* d_bgrad = nullptr;   // N x D
@@ -604,12 +613,23 @@ struct MoveD {
 
 template <int D>
 struct CommitD {
-  static int run(hawkes_ctx* ctx) {
-    const int n = (int)std::max<int64_t>(ctx->N, ctx->move_k);
+  static int run(hawkes_ctx* ctx, int k, int gated) {
+    const int n = (int)std::max<int64_t>(ctx->N, k);
     k_move_commit<D><<<(n + 255) / 256, 256, 0, ctx->stream>>>(
         ctx->rates, ctx->d_move_delta, ctx->d_move_rows, ctx->d_slot_of, ctx->d_move_idx,
-        ctx->d_move_x, ctx->move_k, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2, ctx->rec, ctx->rec32,
-        ctx->xstage, ctx->st);
+        ctx->d_move_x, k, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2, ctx->rec, ctx->rec32,
+        ctx->xstage, ctx->st, gated);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
+template <int D>
+struct MhProposeD {
+  static int run(hawkes_ctx* ctx, int b, int k, double scale, uint2 key, unsigned long long it) {
+    k_mh_propose<D><<<1, 256, 0, ctx->stream>>>(ctx->d_mh_blocks, b, k, ctx->xstage, ctx->d_reg_c,
+                                               ctx->d_reg_s, ctx->reg_kind, scale, key, it,
+                                               ctx->d_move_idx, ctx->d_move_x, ctx->d_slot_of, ctx->st);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -1244,7 +1264,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
   }
-  void* bufs[] = {ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
+  void* bufs[] = {ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
@@ -1533,7 +1553,10 @@ int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double s
     TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
     ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
   }
-  if (x_out) TRY(copy_out(ctx, x_out, ctx->xstage, n, mem));
+  if (x_out) {
+    TRY(copy_out(ctx, x_out, ctx->xstage, n, mem));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
   if (out_accepted) *out_accepted = acc ? 1 : 0;
   if (out_log_alpha) *out_log_alpha = ctx->h_st->log_alpha;
   return HAWKES_OK;
@@ -1599,12 +1622,136 @@ int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const do
 int hawkes_accept_move(hawkes_ctx* ctx) {
   ENTER(ctx);
   if (ctx->move_k <= 0) return set_err(ctx, HAWKES_ERR_STATE, "no pending move");
-  TRY(dispatchD<CommitD>(ctx->D, ctx));
+  TRY(dispatchD<CommitD>(ctx->D, ctx, ctx->move_k, 0));
   TRY(clear_move(ctx));
   ctx->rates_valid = ctx->grad_valid = false;   // rho', G1 and ell_n of the old state
   ctx->rates_exchanged = true;                  // every rank updated every row
   ctx->lam_valid = true;
   CU(cudaStreamSynchronize(ctx->stream));
+  return HAWKES_OK;
+}
+
+int hawkes_get_locations(hawkes_ctx* ctx, double* out_x, int32_t mem) {
+  ENTER(ctx);
+  if (!out_x || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_get_locations");
+  if (!ctx->have_x) return set_err(ctx, HAWKES_ERR_STATE, "no locations");
+  TRY(copy_out(ctx, out_x, ctx->xstage, (size_t)ctx->N * ctx->D, mem));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return HAWKES_OK;
+}
+
+int hawkes_set_regions(hawkes_ctx* ctx, int32_t kind, const double* centre, const double* size,
+                       int32_t mem) {
+  ENTER(ctx);
+  if (!centre || !size || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE) ||
+      (kind != HAWKES_REGION_SQUARE && kind != HAWKES_REGION_DISC))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_set_regions");
+  if (kind == HAWKES_REGION_DISC && ctx->D != 2)
+    return set_err(ctx, HAWKES_ERR_DIM, "disc regions (Eq. locsPrior2) need D = 2");
+  const size_t N = (size_t)ctx->N, D = (size_t)ctx->D;
+  std::vector<double> hc(N * D), hs(N);
+  if (mem == HAWKES_MEM_DEVICE) {
+    CU(cudaMemcpyAsync(hc.data(), centre, hc.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hs.data(), size, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  } else {
+    memcpy(hc.data(), centre, hc.size() * sizeof(double));
+    memcpy(hs.data(), size, hs.size() * sizeof(double));
+  }
+  for (size_t i = 0; i < N; ++i)
+    if (!(hs[i] > 0.0) || !finite_bounded(hs[i]))
+      return set_err(ctx, HAWKES_ERR_NONFINITE, "region size %zu must be finite and > 0", i);
+  for (double v : hc)
+    if (!finite_bounded(v)) return set_err(ctx, HAWKES_ERR_NONFINITE, "region centre not finite");
+  if (!ctx->d_reg_c) {
+    TRY(dalloc(ctx, &ctx->d_reg_c, N * D));
+    TRY(dalloc(ctx, &ctx->d_reg_s, N));
+  }
+  CU(cudaMemcpyAsync(ctx->d_reg_c, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_reg_s, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->reg_kind = kind;
+  return HAWKES_OK;
+}
+
+int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t* blocks, double scale,
+                    uint64_t seed, uint64_t iteration, int32_t* out_accepted, double* out_log_alpha,
+                    int32_t* out_n_accepted) {
+  ENTER(ctx);
+  if (n_blocks < 0 || k < 1 || k > MOVE_MAX || (n_blocks > 0 && !blocks) || !(scale > 0.0) ||
+      !isfinite(scale))
+    return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_mh_sweep (1 <= k <= %d, scale > 0)",
+                   MOVE_MAX);
+  TRY(check_ready(ctx));
+  if (!ctx->reg_kind) return set_err(ctx, HAWKES_ERR_STATE, "hawkes_set_regions is required");
+  {
+    std::vector<int> sorted(k);
+    for (int32_t b = 0; b < n_blocks; ++b) {
+      std::copy(blocks + (size_t)b * k, blocks + (size_t)(b + 1) * k, sorted.begin());
+      std::sort(sorted.begin(), sorted.end());
+      for (int q = 0; q < k; ++q)
+        if (sorted[q] < 0 || sorted[q] >= ctx->N || (q && sorted[q] == sorted[q - 1]))
+          return set_err(ctx, HAWKES_ERR_ARG, "block %d: indices must be distinct and in [0, N)", b);
+    }
+  }
+  if (out_n_accepted) *out_n_accepted = 0;
+  if (n_blocks == 0) return HAWKES_OK;
+  TRY(fetch_status(ctx));   // surface a pending device-side validation failure first
+  TRY(clear_move(ctx));
+  const size_t total = (size_t)n_blocks * k;
+  if (total > ctx->mh_cap) {
+    if (ctx->d_mh_blocks) cudaFree(ctx->d_mh_blocks);
+    ctx->d_mh_blocks = nullptr;
+    TRY(dalloc(ctx, &ctx->d_mh_blocks, total));
+    ctx->mh_cap = total;
+  }
+  if ((size_t)n_blocks > ctx->mh_bcap) {
+    if (ctx->d_mh_acc) cudaFree(ctx->d_mh_acc);
+    if (ctx->d_mh_la) cudaFree(ctx->d_mh_la);
+    ctx->d_mh_acc = nullptr;
+    ctx->d_mh_la = nullptr;
+    TRY(dalloc(ctx, &ctx->d_mh_acc, (size_t)n_blocks));
+    TRY(dalloc(ctx, &ctx->d_mh_la, (size_t)n_blocks));
+    ctx->mh_bcap = n_blocks;
+  }
+  CU(cudaMemcpyAsync(ctx->d_mh_blocks, blocks, total * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->lam_valid) {
+    ctx->rates_valid = false;
+    TRY(run_rates(ctx));
+    if (!ctx->pairs && !ctx->rates_exchanged) {
+      TRY(exchange_rows(ctx, ctx->rates, 4));
+      ctx->rates_exchanged = true;
+    }
+  }
+  const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
+  for (int32_t b = 0; b < n_blocks; ++b) {
+    TRY(dispatchD<MhProposeD>(ctx->D, ctx, (int)b, (int)k, scale, key, (unsigned long long)iteration));
+    TRY(dispatchD<MoveD>(ctx->D, ctx, (int)k));
+    k_mh_decide<<<1, 1, 0, ctx->stream>>>(ctx->st, (int)b, key, (unsigned long long)iteration,
+                                          ctx->d_mh_acc, ctx->d_mh_la);
+    CHECK_LAUNCH();
+    TRY(dispatchD<CommitD>(ctx->D, ctx, (int)k, 1));
+    k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 0);
+    CHECK_LAUNCH();
+  }
+  std::vector<int> acc(n_blocks);
+  CU(cudaMemcpyAsync(acc.data(), ctx->d_mh_acc, n_blocks * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (out_log_alpha)
+    CU(cudaMemcpyAsync(out_log_alpha, ctx->d_mh_la, n_blocks * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  int n_acc = 0;
+  for (int32_t b = 0; b < n_blocks; ++b) {
+    n_acc += acc[b];
+    if (out_accepted) out_accepted[b] = acc[b];
+  }
+  if (out_n_accepted) *out_n_accepted = n_acc;
+  if (n_acc > 0) {
+    ctx->rates_valid = ctx->grad_valid = false;   // rho', G1 and ell_n of the old state
+    ctx->rates_exchanged = true;                  // every rank updated every row
+  }
+  ctx->lam_valid = true;
   return HAWKES_OK;
 }
 

@@ -1,0 +1,132 @@
+// hawkes_mh.cuh -- on-device block Metropolis-Hastings over coarsened locations.
+//
+// The DC and Alaska samplers update the latent locations with "a Metropolis-Hastings
+// kernel with block-wise updates over sets of individual location variables":
+//   * square regions (Eq. locsPrior1, |x_nd - c_nd| < s_n): per dimension a normal
+//     proposal N(x_nd, (scale s_n)^2) truncated to the region ("truncated normal
+//     proposals"), drawn by inverting the CDF; Hastings ratio prod_d Z_d(x) / Z_d(x*) with
+//     Z_d the truncation mass;
+//   * disc regions (Eq. locsPrior2, |x_n - c_n| < r_n, D = 2): x* uniform on the
+//     intersection of disc(c_n, r_n) and disc(x_n, eps r_n), eps = scale (Eq. circleKernel),
+//     by rejection; Hastings ratio A(x)/A(x*) with A the closed-form lens area.
+// Per block: k_mh_propose (one CTA: proposals, proposal-slot map, Hastings sum in a fixed
+// order), the O(kN) Delta ell kernels of hawkes_moves.cuh, k_mh_decide (Metropolis test
+// with a counter-based uniform), a gated commit.  No host round trip between blocks.
+//
+// Random numbers: Philox-4x32-10 (hawkes_ops.cuh) with counter (it_lo, it_hi, b, tag), key
+// (seed_lo, seed_hi), b the block index within the sweep; proposal draws of slot q use
+// tag = 0x80000000 | q << 12 | a, the accept uniform tag = 0xC0000000.
+#pragma once
+#include "hawkes_moves.cuh"
+#include "hawkes_ops.cuh"
+
+namespace hk {
+
+constexpr unsigned MH_TAG = 0x80000000u, MH_ACCEPT_TAG = 0xC0000000u;
+constexpr int MH_MAX_ATTEMPTS = 4096;
+enum { REGION_SQUARE = 1, REGION_DISC = 2 };
+
+__device__ __forceinline__ double2 mh_uniforms(uint2 key, unsigned long long it, unsigned b, unsigned tag) {
+  const uint4 w = philox10(make_uint4((unsigned)it, (unsigned)(it >> 32), b, tag), key);
+  return make_double2(u53(w.x, w.y), u53(w.z, w.w));
+}
+
+// N(x, s^2) mass of (lo, hi): 1 - Q((hi - x)/s) - Phi((lo - x)/s), Q = upper tail
+__device__ __forceinline__ double trunc_mass(double x, double lo, double hi, double s) {
+  const double r2 = 0.70710678118654752440;
+  return 1.0 - 0.5 * erfc((hi - x) / s * r2) - 0.5 * erfc(-(lo - x) / s * r2);
+}
+
+// area of disc(0, R) cap disc(d e_1, rho)
+__device__ __forceinline__ double lens(double R, double rho, double d) {
+  const double pi = 3.14159265358979323846;
+  if (d >= R + rho) return 0.0;
+  if (d + rho <= R) return pi * rho * rho;
+  if (d + R <= rho) return pi * R * R;
+  const double t1 = rho * rho * acos((d * d + rho * rho - R * R) / (2.0 * d * rho));
+  const double t2 = R * R * acos((d * d + R * R - rho * rho) / (2.0 * d * R));
+  const double k = 0.5 * sqrt((-d + rho + R) * (d + rho - R) * (d - rho + R) * (d + rho + R));
+  return t1 + t2 - k;
+}
+
+// one CTA of 256 threads; slot q < k proposes for event n = blocks[b*k + q]
+template <int D>
+__global__ void __launch_bounds__(256) k_mh_propose(const int* __restrict__ blocks, int b, int k,
+                                                    const double* __restrict__ xcur,
+                                                    const double* __restrict__ centre,
+                                                    const double* __restrict__ size, int kind,
+                                                    double scale, uint2 key, unsigned long long it,
+                                                    int* __restrict__ move_idx,
+                                                    double* __restrict__ move_x,
+                                                    int* __restrict__ slot_of, EvalStatus* st) {
+  __shared__ double sh[256];
+  const int q = threadIdx.x;
+  double logh = 0.0;
+  if (q < k) {
+    const int n = blocks[(long long)b * k + q];
+    move_idx[q] = n;
+    slot_of[n] = q;
+    double x[D], c[D], y[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      x[d] = xcur[(long long)n * D + d];
+      c[d] = centre[(long long)n * D + d];
+    }
+    const double sz = size[n];
+    if (kind == REGION_SQUARE) {
+      const double s = scale * sz;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double2 uu = mh_uniforms(key, it, (unsigned)b, MH_TAG | ((unsigned)q << 12) | (unsigned)(d / 2));
+        const double u = (d & 1) ? uu.y : uu.x;
+        const double lo = c[d] - sz, hi = c[d] + sz;
+        const double Z0 = trunc_mass(x[d], lo, hi, s);
+        const double p = 0.5 * erfc(-(lo - x[d]) / s * 0.70710678118654752440) + u * Z0;
+        const double z = normcdfinv(p);
+        y[d] = fmin(fmax(fma(s, z, x[d]), lo), hi);
+        logh += log(Z0) - log(trunc_mass(y[d], lo, hi, s));
+      }
+    } else if constexpr (D >= 2) {   // REGION_DISC (the API admits it for D == 2 only)
+      const double r = sz, rho = scale * sz;
+#pragma unroll
+      for (int d = 0; d < D; ++d) y[d] = x[d];
+      for (int a = 0; a < MH_MAX_ATTEMPTS; ++a) {
+        const double2 uu = mh_uniforms(key, it, (unsigned)b, MH_TAG | ((unsigned)q << 12) | (unsigned)a);
+        const double rad = rho * sqrt(uu.x);
+        double sn, cs;
+        sincospi(2.0 * uu.y, &sn, &cs);
+        const double y0 = x[0] + rad * cs, y1 = x[1] + rad * sn;
+        const double e0 = y0 - c[0], e1 = y1 - c[1];
+        if (e0 * e0 + e1 * e1 < r * r) {
+          y[0] = y0;
+          y[1] = y1;
+          logh = log(lens(r, rho, hypot(x[0] - c[0], x[1] - c[1]))) - log(lens(r, rho, hypot(e0, e1)));
+          break;
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) move_x[q * D + d] = y[d];
+  }
+  sh[q] = logh;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (q < w) sh[q] += sh[q + w];
+    __syncthreads();
+  }
+  if (q == 0) st->mh_hastings = sh[0];
+}
+
+// log alpha = Delta ell + sum log Hastings; accept iff log u < log alpha
+__global__ void k_mh_decide(EvalStatus* st, int b, uint2 key, unsigned long long it,
+                            int* __restrict__ acc_out, double* __restrict__ la_out) {
+  const double dl = st->dell;
+  const double la = (dl > -INFINITY) ? dl + st->mh_hastings : -INFINITY;   // NaN -> -inf too
+  const double u = mh_uniforms(key, it, (unsigned)b, MH_ACCEPT_TAG).x;
+  const int acc = log(u) < la ? 1 : 0;
+  st->accepted = acc;
+  acc_out[b] = acc;
+  la_out[b] = la;
+}
+
+}  // namespace hk

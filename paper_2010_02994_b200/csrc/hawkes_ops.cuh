@@ -188,6 +188,7 @@ struct EvalStatus {
   double log_alpha;
   int accepted;
   int undef0;      // ell(x0) = -inf: the chain's state has zero density
+  double mh_hastings;   // block MH: sum of the proposal's log Hastings terms
 };
 
 // Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
@@ -239,7 +240,9 @@ __global__ void k_move_commit(double* __restrict__ rates, const double* __restri
                               const double* __restrict__ rows, const int* __restrict__ slot_of,
                               const int* __restrict__ idx, const double* __restrict__ new_x, int k,
                               int N, double tx2, double h2, double* __restrict__ rec,
-                              float* __restrict__ rec32, double* __restrict__ xcur, EvalStatus* st) {
+                              float* __restrict__ rec32, double* __restrict__ xcur, EvalStatus* st,
+                              int gated) {
+  if (gated && !st->accepted) return;   // block MH: the decision is on the device
   const double S1 = 1.0 / 18446744073709551616.0;   // 2^-64
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n == 0) st->ell += st->dell;

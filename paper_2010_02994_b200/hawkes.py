@@ -179,6 +179,41 @@ class HawkesContext:
                                         ctypes.byref(acc), ctypes.byref(la)), self._h)
         return bool(acc.value), la.value
 
+    # -- block Metropolis-Hastings over coarsened locations
+    def set_regions(self, kind: str, centre, size):
+        """hawkes_set_regions: "square" (Eq. locsPrior1, size = half-width) or "disc"
+        (Eq. locsPrior2, size = radius) uniform location priors, N x D centres, N sizes."""
+        pc, mc, kc = _ptr_mem(centre)
+        ps, ms, ks = _ptr_mem(size)
+        if mc != ms:
+            raise ValueError("centre and size must live in the same memory")
+        check(self._lib.hawkes_set_regions(self._h, _lib.REGIONS[kind], pc, ps, mc), self._h)
+
+    def mh_sweep(self, blocks, scale: float, seed: int, iteration: int):
+        """hawkes_mh_sweep: sequential block MH updates, blocks = (n_blocks, k) int array of
+        distinct event indices per row.  Returns (accepted bool array, log_alpha array)."""
+        blk = np.ascontiguousarray(np.asarray(blocks, dtype=np.int32))
+        if blk.ndim != 2:
+            raise ValueError("blocks must be (n_blocks, k)")
+        nb, k = blk.shape
+        acc = np.zeros(nb, dtype=np.int32)
+        la = np.zeros(nb, dtype=np.float64)
+        nacc = ctypes.c_int32()
+        check(self._lib.hawkes_mh_sweep(self._h, nb, k, blk.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                        float(scale), int(seed), int(iteration),
+                                        acc.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                        la.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        ctypes.byref(nacc)), self._h)
+        return acc.astype(bool), la
+
+    def get_locations(self, out=None):
+        """The context's current locations (N x D float64 CUDA tensor), e.g. after MH sweeps."""
+        if out is None:
+            out = torch.empty((self.N, self.D), dtype=torch.float64, device=f"cuda:{self.device}")
+        p, mem, keep = _ptr_mem(out)
+        check(self._lib.hawkes_get_locations(self._h, p, mem), self._h)
+        return out
+
     # -- Bayesian MDS (P:L158-184) and the HMC potential
     def set_bmds(self, Y, sigma: float):
         """hawkes_set_bmds: N x N dissimilarities (lower triangle read) and sigma."""

@@ -1,0 +1,111 @@
+"""GPU parity of the on-device block Metropolis-Hastings sweep (hawkes_mh_sweep):
+proposals (truncated normals in the DC squares, lens-uniform in the Alaska discs), Hastings
+terms, Delta ell, the Metropolis decisions and the final state against oracle.mh_sweep, which
+draws the same Philox numbers with its own generator and takes Delta ell from two full
+evaluations of Eq. 1."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(c, **kw):
+    from paper_2010_02994_b200 import HawkesContext
+    ctx = HawkesContext(c.N, c.D, **kw)
+    ctx.set_times(c.t)
+    ctx.set_locations(c.x)
+    ctx.set_params(c.theta)
+    ctx.set_regions(c.region, c.centre, c.size)
+    return ctx
+
+
+def _blocks(N, n_blocks, k, seed):
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.choice(N, size=k, replace=False) for _ in range(n_blocks)]).astype(np.int32)
+
+
+@pytest.mark.parametrize("name,scale,k", [("C2", 0.5, 8), ("C2", 1.5, 1), ("C3", 0.7, 8),
+                                          ("C3", 1.0, 32)])
+def test_mh_sweep_matches_oracle(name, scale, k):
+    c = synth.config(name, 400)
+    blocks = _blocks(c.N, 12, k, 5)
+    x_ref, acc_ref, la_ref = oracle.mh_sweep(c.x, c.t, c.theta, c.region, c.centre, c.size,
+                                             blocks, scale, 77, 3)
+    with _ctx(c) as ctx:
+        acc, la = ctx.mh_sweep(blocks, scale, 77, 3)
+        x = ctx.get_locations().cpu().numpy()
+        ell = ctx.loglik()
+    for b in range(len(blocks)):
+        assert la[b] == pytest.approx(la_ref[b], rel=1e-7, abs=1e-7), f"block {b}"
+        if abs(la_ref[b] - np.log(oracle.mh_uniforms(77, 3, b, 0xC0000000)[0])) > 1e-6:
+            assert acc[b] == acc_ref[b], f"block {b}"
+    assert list(acc) == list(acc_ref)
+    scale_x = np.abs(c.x).max()
+    assert np.max(np.abs(x - x_ref)) <= 1e-12 * scale_x
+    assert ell == pytest.approx(oracle.loglik(x_ref, c.t, c.theta)[0], rel=1e-9)
+    # every location stays in its region
+    if c.region == "square":
+        assert np.all(np.abs(x - c.centre) <= c.size[:, None])
+    else:
+        assert np.all(np.hypot(*(x - c.centre).T) < c.size)
+
+
+def test_mh_sweeps_chain_and_mix_with_other_calls():
+    """Consecutive sweeps (new iteration numbers) continue from the committed state, and a
+    gradient afterwards is that of the chain's state."""
+    c = synth.config("C2", 300, replicate=1)
+    x_ref = c.x.copy()
+    with _ctx(c) as ctx:
+        for it in range(3):
+            blocks = _blocks(c.N, 6, 4, it)
+            x_ref, acc_ref, _ = oracle.mh_sweep(x_ref, c.t, c.theta, "square", c.centre, c.size,
+                                                blocks, 0.6, 1, it)
+            acc, _ = ctx.mh_sweep(blocks, 0.6, 1, it)
+            assert list(acc) == list(acc_ref)
+        g, ell = ctx.grad_locations()
+        g_ref, _ = oracle.grad(x_ref, c.t, c.theta)
+        assert np.max(np.abs(g.cpu().numpy() - g_ref)) <= 1e-9 * np.abs(g_ref).max()
+
+
+def test_mh_sweep_rows_world_emulation_identical():
+    """The sweep's decisions do not depend on the decomposition or the emulated world."""
+    c = synth.config("C3", 500)
+    blocks = _blocks(c.N, 8, 8, 2)
+    res = []
+    for kw in ({}, {"algorithm": "rows", "emulate_world": 3}, {"algorithm": "pairs", "emulate_world": 2}):
+        with _ctx(c, **kw) as ctx:
+            acc, la = ctx.mh_sweep(blocks, 0.8, 4, 0)
+            res.append((acc, la, ctx.get_locations().cpu().numpy()))
+    for acc, la, x in res[1:]:
+        assert np.array_equal(acc, res[0][0])
+        assert np.allclose(la, res[0][1], rtol=1e-9, atol=1e-9)
+        assert np.allclose(x, res[0][2], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+def test_mh_errors():
+    from paper_2010_02994_b200 import HawkesContext, HawkesError
+    c = synth.config("C2", 100)
+    with HawkesContext(c.N, c.D) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_locations(c.x)
+        ctx.set_params(c.theta)
+        with pytest.raises(HawkesError, match="STATE"):
+            ctx.mh_sweep([[0, 1]], 0.5, 1, 0)
+        ctx.set_regions("square", c.centre, c.size)
+        with pytest.raises(HawkesError, match="ARG"):
+            ctx.mh_sweep([[0, 0]], 0.5, 1, 0)      # repeated index
+        with pytest.raises(HawkesError, match="ARG"):
+            ctx.mh_sweep([[0, 100]], 0.5, 1, 0)    # out of range
+        with pytest.raises(HawkesError, match="ARG"):
+            ctx.mh_sweep([[0, 1]], 0.0, 1, 0)
+        with pytest.raises(HawkesError, match="NONFINITE"):
+            ctx.set_regions("square", c.centre, np.zeros(c.N))
+    c1 = synth.config("C1", 50, )
+    with HawkesContext(c1.N, 3) as ctx:
+        with pytest.raises(HawkesError, match="DIM"):
+            ctx.set_regions("disc", np.zeros((c1.N, 3)), np.ones(c1.N))
