@@ -286,24 +286,29 @@ size_t pass_smem() {
          EXP_TABLE * sizeof(int2);
 }
 
-template <int D, int PASS, int R>
+template <int D, int PASS, int R, int V>
 size_t sym_smem() {
   const int KR = PASS == 1 ? 1 + D : D;
+  const int copies = (V & 2) ? TAB_COPIES : 1;
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
-         EXP_TABLE * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double);
+         (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
+         ((V & 4) ? (size_t)4 * 32 * Layout<D>::REC * sizeof(double) : 0);
 }
 
-// sym_kernel variants: R rows per lane, V = exp polynomial scheme (0 Horner, 1 Estrin)
-template <int D, int R, int V>
+// sym_kernel variants: R rows per lane; V1 / V2 = the pass-1 / pass-2 variant bits
+// (hawkes_kernels_sym.cuh).  Measured on B200 (profiles/r01_sym_variants.txt): the
+// interleaved exp table pays in pass 1 (-3.4 %) but not in pass 2, where it costs more
+// integer instructions than the bank conflicts it removes; the SoA columns pay in both.
+template <int D, int R, int V1, int V2>
 struct SymOps {
   static int setup(hawkes_ctx* ctx) {
-    auto s1 = sym_kernel<D, 1, R, V>;
-    auto s2 = sym_kernel<D, 2, R, V>;
-    CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 1, R>()));
-    CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 2, R>()));
+    auto s1 = sym_kernel<D, 1, R, V1>;
+    auto s2 = sym_kernel<D, 2, R, V2>;
+    CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 1, R, V1>()));
+    CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 2, R, V2>()));
     int b1 = 0, b2 = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym_smem<D, 1, R>()));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym_smem<D, 2, R>()));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym_smem<D, 1, R, V1>()));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym_smem<D, 2, R, V2>()));
     ctx->grid_s1 = std::max(1, b1) * ctx->sms;
     ctx->grid_s2 = std::max(1, b2) * ctx->sms;
     return HAWKES_OK;
@@ -311,17 +316,40 @@ struct SymOps {
   static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
     const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
     if (pass == 1)
-      sym_kernel<D, 1, R, V><<<grid, THREADS, sym_smem<D, 1, R>(), ctx->stream>>>(b);
+      sym_kernel<D, 1, R, V1><<<grid, THREADS, sym_smem<D, 1, R, V1>(), ctx->stream>>>(b);
     else
-      sym_kernel<D, 2, R, V><<<grid, THREADS, sym_smem<D, 2, R>(), ctx->stream>>>(b);
+      sym_kernel<D, 2, R, V2><<<grid, THREADS, sym_smem<D, 2, R, V2>(), ctx->stream>>>(b);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
 };
 
+// default: pass 1 V = 6 (interleaved table + SoA columns), pass 2 V = 4 (SoA columns);
+// HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant for both passes (diagnostics, A/B on one
+// box; 2 and 6-for-pass-2 exist for D = 2 only)
+static int sym_variant() {
+  static int v = [] {
+    const char* e = getenv("HAWKES_SYM_V");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+template <int D, int V1, int V2>
+int sym_call_v(hawkes_ctx* ctx, int pass, const SymArgs* b) {
+  return pass ? SymOps<D, 4, V1, V2>::launch(ctx, pass, *b) : SymOps<D, 4, V1, V2>::setup(ctx);
+}
+
 template <int D>
 int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
-  return pass ? SymOps<D, 4, 0>::launch(ctx, pass, *b) : SymOps<D, 4, 0>::setup(ctx);
+  const int v = sym_variant();
+  if (v == 0) return sym_call_v<D, 0, 0>(ctx, pass, b);
+  if constexpr (D == 2) {
+    if (v == 2) return sym_call_v<D, 2, 2>(ctx, pass, b);
+    if (v == 4) return sym_call_v<D, 4, 4>(ctx, pass, b);
+    if (v == 6) return sym_call_v<D, 6, 6>(ctx, pass, b);
+  }
+  return sym_call_v<D, 6, 4>(ctx, pass, b);
 }
 
 constexpr int SYM32_R = 4;
@@ -329,7 +357,43 @@ template <int D, int PASS>
 size_t sym32_smem() {
   const int KR = PASS == 1 ? 1 + D : D;
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t) +
-         (size_t)4 * 32 * SYM32_R * KR * sizeof(double);
+         (size_t)4 * 32 * SYM32_R * KR * sizeof(double) +
+         (size_t)4 * 32 * Layout32<D>::REC * sizeof(float);   // per-warp SoA column buffers
+}
+
+// fp32 sym kernels read columns from per-warp SoA buffers (SOA = true, the default);
+// HAWKES_SYM32_SOA=0 selects the AoS reads (diagnostics, D = 2 only)
+static bool sym32_soa() {
+  static bool v = [] {
+    const char* e = getenv("HAWKES_SYM32_SOA");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+template <int D, bool SOA>
+int sym32_setup(hawkes_ctx* ctx) {
+  auto s1 = sym_kernel_f32<D, 1, SYM32_R, SOA>;
+  auto s2 = sym_kernel_f32<D, 2, SYM32_R, SOA>;
+  CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1>()));
+  CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2>()));
+  int b1 = 0, b2 = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1>()));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2>()));
+  ctx->grid_s1 = std::max(1, b1) * ctx->sms;
+  ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+  return HAWKES_OK;
+}
+
+template <int D, bool SOA>
+int sym32_launch(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
+  const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+  if (pass == 1)
+    sym_kernel_f32<D, 1, SYM32_R, SOA><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
+  else
+    sym_kernel_f32<D, 2, SYM32_R, SOA><<<grid, THREADS, sym32_smem<D, 2>(), ctx->stream>>>(b);
+  CHECK_LAUNCH();
+  return HAWKES_OK;
 }
 
 template <int D>
@@ -352,14 +416,9 @@ struct SetupD {
       ctx->grid1 = std::max(1, b1) * ctx->sms;
       ctx->grid2 = std::max(1, b2) * ctx->sms;
       if constexpr (D <= SYM_MAX_D) if (ctx->pairs) {
-        auto s1 = sym_kernel_f32<D, 1, SYM32_R>;
-        auto s2 = sym_kernel_f32<D, 2, SYM32_R>;
-        CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1>()));
-        CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2>()));
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1>()));
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2>()));
-        ctx->grid_s1 = std::max(1, b1) * ctx->sms;
-        ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+        if constexpr (D == 2)
+          if (!sym32_soa()) return sym32_setup<D, false>(ctx);
+        return sym32_setup<D, true>(ctx);
       }
       return HAWKES_OK;
     }
@@ -491,12 +550,14 @@ struct PassD {
       b.chunk = ctx->chunk;
       b.nchunks = ctx->nchunks;
       b.c = ctx->pc32;
-      const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
-      if (pass == 1)
-        sym_kernel_f32<D, 1, SYM32_R><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
-      else
-        sym_kernel_f32<D, 2, SYM32_R><<<grid, THREADS, sym32_smem<D, 2>(), ctx->stream>>>(b);
-      CHECK_LAUNCH();
+      bool soa = true;
+      if constexpr (D == 2) soa = sym32_soa();
+      int rc = HAWKES_OK;
+      if (soa)
+        rc = sym32_launch<D, true>(ctx, pass, b);
+      else if constexpr (D == 2)
+        rc = sym32_launch<D, false>(ctx, pass, b);
+      if (rc != HAWKES_OK) return rc;
     }
     record_stop(ctx, pass == 1);
     return HAWKES_OK;

@@ -80,14 +80,26 @@ constexpr double EXP_C3 = 0.1666666688540192;
 constexpr int EXP_TABLE = 256;
 constexpr int EXP_BIAS_SHIFT = 12;                          // 20 - log2(EXP_TABLE)
 
-__device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab) {
+// STRIDE > 1: the table is stored interleaved in STRIDE copies (entry j of copy c at
+// j*STRIDE + c) and tab points at this thread's copy (see sym_kernel)
+template <int STRIDE = 1>
+__device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, int lane_off = 0) {
+  static_assert(STRIDE == 1 || STRIDE == 16, "interleaved tables have 16 copies");
   const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
   const double ac = __hiloint2double((int)ahi, __double2loint(a));
   const double y = fma(ac, EXP_K, EXP_SHIFT);
   const double kf = y - EXP_SHIFT;
   const double r = fma(kf, -EXP_C, ac);
   const int k = __double2loint(y);
-  const int2 T = tab[k & (EXP_TABLE - 1)];
+  int2 T;
+  if constexpr (STRIDE == 1) {
+    T = tab[k & (EXP_TABLE - 1)];
+  } else {
+    // interleaved copies: byte offset ((k mod 256) * STRIDE + copy) * 8, the copy's part
+    // (lane_off, 0..STRIDE-1 times 8) or-ed in: one shift + one LOP3, uniform table base
+    T = *reinterpret_cast<const int2*>(reinterpret_cast<const char*>(tab) +
+                                       (((k << 7) & ((EXP_TABLE - 1) << 7)) | lane_off));
+  }
   const double q = fma(fma(EXP_C3, r, EXP_C2), r, 1.0);
   const double p = q * r;                                      // e^r - 1
   const double Tm = __hiloint2double(T.y + k * (1 << EXP_BIAS_SHIFT), T.x);   // 2^(j/256) 2^m

@@ -387,7 +387,7 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR, bool SELF = true>
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA>
 __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag,
@@ -399,7 +399,24 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
 #pragma unroll 2
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
-    const float* rc = grp + src * REC;
+    // AoS record in the stage, or (SOA) the warp's transposed copy: float4 unit u of column
+    // e at [u][e], read without bank conflicts
+    float rbuf[REC];
+    const float* rc;
+    if (SOA) {
+      const float4* g4 = reinterpret_cast<const float4*>(grp);
+#pragma unroll
+      for (int u = 0; u < REC / 4; ++u) {
+        const float4 w = g4[u * 32 + src];
+        rbuf[4 * u] = w.x;
+        rbuf[4 * u + 1] = w.y;
+        rbuf[4 * u + 2] = w.z;
+        rbuf[4 * u + 3] = w.w;
+      }
+      rc = rbuf;
+    } else {
+      rc = grp + src * REC;
+    }
     float cxh[D], cxl[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -456,7 +473,7 @@ struct SymArgs32 {
   PassConst32 c;
 };
 
-template <int D, int PASS, int SR>
+template <int D, int PASS, int SR, bool SOA>
 __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArgs32 a) {
   static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
@@ -469,9 +486,11 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArg
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
   double* red = reinterpret_cast<double*>(bars + STAGES);   // [4 warps][SRT][KR]
+  float* soa = reinterpret_cast<float*>(red + 4 * SRT * KR);  // [4 warps][REC/4][32] float4
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* mysoa = soa + warp * 32 * REC;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -569,15 +588,24 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArg
         const float dtmin = fmaxf((st[L::TH] - th_rlast) + (st[L::TL] - tl_rlast), 0.f);
         const bool self_live = c.cs - c.omega * dtmin > -127.f;
         const bool bg_live = fmaf(c.kt * dtmin, dtmin, c.cb) > -127.f;
+        const float* grp = st + warp * 32 * REC;
+        if (SOA) {   // this lane's column record -> the warp's [unit][32] float4 buffer
+          const float4* rc4 = reinterpret_cast<const float4*>(grp + lane * REC);
+          float4* g4 = reinterpret_cast<float4*>(mysoa);
+#pragma unroll
+          for (int u = 0; u < REC / 4; ++u) g4[u * 32 + lane] = rc4[u];
+          __syncwarp();
+          grp = mysoa;
+        }
         if (!strict)
-          sym32_group<D, PASS, true, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                         jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, true, SR, true, SOA>(rp, grp, cg, cvalid, row0 + lane,
+                                                    jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
         else if (self_live)
-          sym32_group<D, PASS, false, SR>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                          jt + warp * 32, false, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, true, SOA>(rp, grp, cg, cvalid, row0 + lane,
+                                                     jt + warp * 32, false, rM32, rG32, cacc, c);
         else if (bg_live)
-          sym32_group<D, PASS, false, SR, false>(rp, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                                 jt + warp * 32, false, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, false, SOA>(rp, grp, cg, cvalid, row0 + lane,
+                                                      jt + warp * 32, false, rM32, rG32, cacc, c);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;

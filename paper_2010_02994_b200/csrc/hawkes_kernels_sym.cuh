@@ -32,6 +32,11 @@ constexpr int SYM_RMAX = 4;               // largest rows-per-lane variant
 // a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
 // treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
 constexpr double CULL_EXPONENT = -708.0;
+// V bits (DESIGN.md §4 "shared-memory banks"): 2 = the exp table in TAB_COPIES interleaved
+// copies, lane l reading copy l & 15, so a half-warp's 16 lookups hit 16 distinct bank pairs;
+// 4 = each warp transposes its 32-column group once per tile into a private structure-of-
+// arrays buffer of double2 pairs, so the 32 steps read columns without bank conflicts
+constexpr int TAB_COPIES = 16;
 
 struct SymArgs {
   const double* rec;
@@ -57,7 +62,7 @@ struct SymRow {
 };
 
 // one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
-template <int D, bool MASK, bool SELF>
+template <int D, bool MASK, bool SELF, int TS>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           bool dead, double& rM, double (&rG)[D], double& cM,
                                           double& cX, double (&cG)[D], const PassConst& c,
@@ -69,8 +74,9 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;   // >= 0: the column is the later event
-  double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
-  double es = SELF ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
+  const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
+  double eb = fexp<TS>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+  double es = SELF ? fexp<TS>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
@@ -86,7 +92,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   }
 }
 
-template <int D, bool MASK, bool SELF>
+template <int D, bool MASK, bool SELF, int TS>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           double crho, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
@@ -98,8 +104,9 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;
-  double eb = fexp(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab);
-  double es = SELF ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
+  const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
+  double eb = fexp<TS>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+  double es = SELF ? fexp<TS>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
@@ -116,7 +123,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R, bool SELF = true>
+template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp, int cg0, bool cvalid0,
                                           int ridx0, int cidx0, bool diag,
@@ -128,14 +135,30 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
 #pragma unroll 1
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
-    // column (l + s) mod 32 of this warp's group, straight from the staged tile
-    const double* rc = grp + src * REC;
+    // column (l + s) mod 32 of this warp's group: from the staged tile (AoS records), or
+    // from the warp's transposed copy (SOA: component pair p of column e at [p][e])
     double cx[D];
+    double ct, crho = 0.0;
+    if (SOA) {
+      const double2* g2 = reinterpret_cast<const double2*>(grp);
+      double v[REC];
 #pragma unroll
-    for (int d = 0; d < D; ++d) cx[d] = rc[d];
-    const double ct = rc[D];
-    double crho = 0.0;
-    if (PASS == 2) crho = rc[D + 1];
+      for (int p = 0; p < (PASS == 2 ? (D + 2 + 1) / 2 : (D + 1 + 1) / 2); ++p) {
+        const double2 w = g2[p * 32 + src];
+        v[2 * p] = w.x;
+        v[2 * p + 1] = w.y;
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) cx[d] = v[d];
+      ct = v[D];
+      if (PASS == 2) crho = v[D + 1];
+    } else {
+      const double* rc = grp + src * REC;
+#pragma unroll
+      for (int d = 0; d < D; ++d) cx[d] = rc[d];
+      ct = rc[D];
+      if (PASS == 2) crho = rc[D + 1];
+    }
     int cg = 0;
     bool cv = true;
     if (MASK) {
@@ -152,9 +175,9 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
                                  (diag && cidx0 + src <= ridx0 + 32 * r));
       if (PASS == 1)
-        sym_pair1<D, MASK, SELF>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
+        sym_pair1<D, MASK, SELF, TS>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
       else
-        sym_pair2<D, MASK, SELF>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
+        sym_pair2<D, MASK, SELF, TS>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -189,15 +212,20 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? L::K1 : L::K2;
   constexpr int KR = PASS == 1 ? 1 + D : D;   // row sums reduced over warps: (M, G) or G
+  constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
+  constexpr int TS = REPL ? TAB_COPIES : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(double));
   int2* tab = reinterpret_cast<int2*>(bars + STAGES);
-  double* red = reinterpret_cast<double*>(tab + EXP_TABLE);   // [4 warps][SYM_RT][KR]
+  double* red = reinterpret_cast<double*>(tab + EXP_TABLE * TS);   // [4 warps][SYM_RT][KR]
+  double* soa = red + 4 * SYM_RT * KR;                            // [4 warps][REC][32] if SOA
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int q = tid; q < EXP_TABLE; q += THREADS) tab[q] = a.tab[q];
+  for (int q = tid; q < EXP_TABLE * TS; q += THREADS) tab[q] = a.tab[q / TS];
+  const int2* mytab = tab;   // REPL: fexp or-s the lane's copy into the index
+  double* mysoa = soa + warp * 32 * REC;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -292,15 +320,24 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
         const double dtmin = fmax(st[D] - t_rlast, 0.0);
         const bool self_live = c.lnc_s - c.omega * dtmin > CULL_EXPONENT;
         const bool bg_live = fma(c.kt * dtmin, dtmin, c.lnc_b) > CULL_EXPONENT;
+        const double* grp = st + warp * 32 * REC;
+        if (SOA) {   // this lane's column record -> the warp's [pair][32] double2 buffer
+          const double* rc = grp + lane * REC;
+          double2* g2 = reinterpret_cast<double2*>(mysoa);
+#pragma unroll
+          for (int p = 0; p < REC / 2; ++p) g2[p * 32 + lane] = make_double2(rc[2 * p], rc[2 * p + 1]);
+          __syncwarp();
+          grp = mysoa;
+        }
         if (!strict)
-          sym_group<D, PASS, true, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                          jt + warp * 32, diag_tile, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, true, SYM_R, true, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+                                                         jt + warp * 32, diag_tile, rM, rG, cacc, c, mytab);
         else if (self_live)
-          sym_group<D, PASS, false, SYM_R>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                           jt + warp * 32, false, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, false, SYM_R, true, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+                                                          jt + warp * 32, false, rM, rG, cacc, c, mytab);
         else if (bg_live)
-          sym_group<D, PASS, false, SYM_R, false>(row, st + warp * 32 * REC, cg, cvalid, row0 + lane,
-                                                  jt + warp * 32, false, rM, rG, cacc, c, tab);
+          sym_group<D, PASS, false, SYM_R, false, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+                                                           jt + warp * 32, false, rM, rG, cacc, c, mytab);
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {

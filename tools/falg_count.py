@@ -1,0 +1,47 @@
+"""Algorithmic FP64 work per pair, counted the way SURVEY.md 8(d) froze F_alg: compile naive
+per-pair bodies (libdevice exp) for sm_100a and count the FP64-pipe instructions (DFMA,
+DADD, DMUL, DSETP) in each kernel's hot loop (the instructions between a backward branch's
+target and the branch).  tools/falg/naive_pairs.cu holds ordered-pair (SURVEY's accounting)
+and unordered-pair ("report against an unordered-pair F_alg") bodies.
+
+    python tools/falg_count.py            # prints one line per kernel; no GPU needed
+"""
+import os
+import re
+import subprocess
+import sys
+import tempfile
+from collections import Counter
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FP64 = ("DFMA", "DADD", "DMUL", "DSETP", "DMNMX")
+
+
+def main():
+    src = os.path.join(HERE, "falg", "naive_pairs.cu")
+    with tempfile.TemporaryDirectory() as d:
+        cubin = os.path.join(d, "n.cubin")
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-cubin",
+                               "-o", cubin, src])
+        sass = subprocess.check_output(["cuobjdump", "-sass", cubin], text=True)
+    for f in re.split(r"\n\s+Function : ", sass)[1:]:
+        name = f.split("\n")[0].strip()
+        ins = [(int(a, 16), b) for a, b in
+               re.findall(r"/\*([0-9a-f]{4})\*/\s+((?:@!?U?P\w+\s+)?[A-Z0-9_.]+[^;]*);", f)]
+        for addr, s in ins:
+            if "BRA" not in s:
+                continue
+            m = re.search(r"0x([0-9a-f]+)", s)
+            if not m or int(m.group(1), 16) >= addr:
+                continue
+            tgt = int(m.group(1), 16)
+            body = [re.sub(r"^@!?U?P\w+\s+", "", t).split()[0].split(".")[0]
+                    for a, t in ins if tgt <= a <= addr]
+            c = Counter(o for o in body if o in FP64)
+            per = "unordered" if name.startswith("uno") else "ordered"
+            print(f"{name}: hot loop {len(body)} instructions, FP64 pipe {sum(c.values())} per {per} pair "
+                  f"{dict(c)}")
+
+
+if __name__ == "__main__":
+    sys.exit(main())
