@@ -27,9 +27,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-8 B200"
-# Algorithmic FP64-pipe work per ordered pair:
-F_RATE, F_GRAD = 34.5, 49.0
+# FP64-pipe work per ordered pair (DESIGN.md §4 "Roofline"; tools/falg_count.py):
+#   F_IMPL  the unordered-pair algorithm as implemented: FP64 instructions of the shipped
+#           sym_kernel's unmasked hot loop / 8 (one step = 4 unordered pairs) -- the
+#           algorithmic work of this design, excluding masked / padding pairs (headline)
+#   F_UNO   SURVEY's method (naive per-pair bodies with libdevice exp) for unordered pairs
+#   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg
+F_IMPL = (16.0, 15.5)
+F_UNO = (26.0, 28.5)
+F_SURVEY = (34.5, 49.0)
 FP64_LANES_PER_SM = 64
+
+
+def _ncu_traffic(kernel):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed
+    ncu --set full capture (profiles/r01_ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[kernel]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def _env_int(k, d):
@@ -308,20 +326,19 @@ def run_ours(args):
     pairs_alg = pairs / world                   # each rank's launches cover 1/W of the pairs
     unordered = ctx.algorithm in ("auto", "pairs") and args.precision == "fp64"
     if unordered:
-        names = ("rate pass: sym_kernel<2,1,4,0>", "gradient pass: sym_kernel<2,2,4,0>")
-        executed = (17.0, 17.0)                 # FP64 instructions per ordered pair (SASS)
+        names = ("rate pass: sym_kernel<2,1,4,6>", "gradient pass: sym_kernel<2,2,4,4>")
+        F_impl = F_IMPL
     else:
         names = ("rate pass: pass_kernel<2,1>", "gradient pass: pass_kernel<2,2>")
-        executed = (26.5, 26.0)
-    if grad_avg >= rate_avg:
-        dom, avg_ms, F, Fx = names[1], grad_avg, F_GRAD, executed[1]
-    else:
-        dom, avg_ms, F, Fx = names[0], rate_avg, F_RATE, executed[0]
+        F_impl = (26.5, 26.0)                  # ROWS: ordered pairs, FP64 instructions (SASS)
+    pi = 1 if grad_avg >= rate_avg else 0
+    dom, avg_ms = names[pi], (grad_avg if pi else rate_avg)
     props = torch.cuda.get_device_properties(dev)
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     peak = props.multi_processor_count * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12   # T ops/s
-    achieved = F * pairs_alg / (avg_ms * 1e-3) / 1e12
-    achieved_exec = Fx * pairs_alg / (avg_ms * 1e-3) / 1e12
+    rate_units = pairs_alg / (avg_ms * 1e-3) / 1e12      # T ordered pairs/s x ops
+    achieved = F_impl[pi] * rate_units
+    traffic = _ncu_traffic(dom.split(": ")[1]) if unordered else None
     try:
         dfma_peak = diag_fp64_peak() / 1e12
     except Exception:
@@ -343,15 +360,17 @@ def run_ours(args):
         "kernel_ms": {"rate_pass_avg": rate_avg, "grad_pass_avg": grad_avg,
                       "rate_launches": kt["rate_launches"], "grad_launches": kt["grad_launches"]},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "T FP64-pipe ops/s (DFMA = 1 op)", "frac": achieved / peak,
-                     "traffic": None,
+                     "unit": "T FP64-pipe instructions/s (one per lane; DFMA = 1)", "frac": achieved / peak,
+                     "traffic": traffic,
                      "peak_basis": f"{props.multi_processor_count} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
-                     "algorithmic_ops_per_pair": F,
-                     "note": "achieved uses SURVEY.md 8(d)'s algorithmic FP64 work per ordered pair "
-                             "(naive per-pair bodies with libdevice exp), so a cheaper implementation "
-                             "reads above 1; executed_* is the FP64 pipe's actual utilisation",
-                     "executed_ops_per_pair": Fx, "executed_achieved": achieved_exec,
-                     "executed_frac": achieved_exec / peak, "measured_dfma_peak": dfma_peak},
+                     "ops_per_pair": F_impl[pi],
+                     "ops_per_pair_basis": "FP64 instructions per ordered pair of the shipped kernel's "
+                                           "unmasked hot loop (tools/falg_count.py --shipped)",
+                     "unordered_falg": {"ops_per_pair": F_UNO[pi], "frac": F_UNO[pi] * rate_units / peak,
+                                        "basis": "SURVEY's method (naive libdevice-exp bodies) for unordered pairs"},
+                     "survey_falg": {"ops_per_pair": F_SURVEY[pi], "frac": F_SURVEY[pi] * rate_units / peak,
+                                     "basis": "SURVEY.md 8(d) ordered-pair F_alg (frozen)"},
+                     "measured_dfma_peak": dfma_peak},
         "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": N * D * 8,
                 "d2h_bytes_per_step": N * D * 8 + 8},
         "hmc": hmc,

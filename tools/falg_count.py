@@ -5,6 +5,10 @@ target and the branch).  tools/falg/naive_pairs.cu holds ordered-pair (SURVEY's 
 and unordered-pair ("report against an unordered-pair F_alg") bodies.
 
     python tools/falg_count.py            # prints one line per kernel; no GPU needed
+
+It also counts the shipped sym_kernel<2, PASS, 4, V> hot loops (the unmasked 32-step loop:
+one step = 4 unordered pairs) in the built library, i.e. the FP64-pipe instructions this
+implementation needs per pair.
 """
 import os
 import re
@@ -43,5 +47,37 @@ def main():
                   f"{dict(c)}")
 
 
+def shipped():
+    lib = os.path.join(os.path.dirname(HERE), "paper_2010_02994_b200", "libhawkes_b200.so")
+    sass = subprocess.check_output(["cuobjdump", "-sass", lib], text=True, stderr=subprocess.DEVNULL)
+    for f in re.split(r"\n\s+Function : ", sass)[1:]:
+        name = f.split("\n")[0].strip()
+        m = re.match(r"_ZN2hk10sym_kernelILi2ELi([12])ELi4ELi(\d)EEEvNS_7SymArgsE", name)
+        if not m:
+            continue
+        ins = [(int(a, 16), b) for a, b in
+               re.findall(r"/\*([0-9a-f]{4,5})\*/\s+((?:@!?U?P\w+\s+)?[A-Z0-9_.]+[^;]*);", f)]
+        loops = []
+        for addr, s in ins:
+            if "BRA" not in s:
+                continue
+            mm = re.search(r"0x([0-9a-f]+)", s)
+            if not mm or int(mm.group(1), 16) >= addr:
+                continue
+            tgt = int(mm.group(1), 16)
+            body = [re.sub(r"^@!?U?P\w+\s+", "", t).split()[0].split(".")[0]
+                    for a, t in ins if tgt <= a <= addr]
+            if sum(1 for o in body if o == "LDS") >= 8:
+                loops.append(body)
+        body = min(loops, key=len)            # the unmasked, self-exciting 4-pair step
+        c = Counter(o for o in body if o in FP64)
+        n64 = sum(c.values())
+        print(f"sym_kernel<2,{m.group(1)},4,{m.group(2)}>: step {len(body)} instructions, FP64 pipe {n64} "
+              f"per 4 unordered pairs = {n64 / 8:.2f} per ordered pair, other {len(body) - n64}; "
+              f"dispatch-model FP64 utilisation {2 * n64 / (2 * n64 + len(body) - n64):.3f}")
+
+
 if __name__ == "__main__":
+    if "--shipped" in sys.argv:
+        sys.exit(shipped())
     sys.exit(main())
