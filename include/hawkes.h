@@ -87,7 +87,11 @@ typedef struct {
   int32_t precision;         /* hawkes_precision                                              */
   int32_t rank, world;       /* row sharding: this process's rank and the number of ranks     */
   const void* nccl_unique_id;/* world > 1: pointer to a 128-byte ncclUniqueId that every rank
-                                received from rank 0; the library builds its own communicator */
+                                received from rank 0; the library builds its own communicator.
+                                With world == 1 a non-NULL id builds a one-rank communicator
+                                and runs the sharded path with its real NCCL collectives on
+                                this GPU (single-GPU test of the multi-GPU plumbing; no
+                                CUDA graphs); cannot be combined with emulate_world > 1     */
   int32_t emulate_world;     /* world == 1 only: > 1 runs that many logical row shards one
                                 after another on this GPU, exchanging through device memory
                                 (exercises the sharded path without more GPUs); 0/1 = off      */

@@ -110,6 +110,8 @@ struct hawkes_ctx {
   std::vector<int> n_sym;
   int* d_own = nullptr;                     // [nchunks][nchunks] owner rank of pair (a <= b)
   int* d_every_tile = nullptr;              // all row tiles 0..ntiles-1
+  bool multi = false;                       // W > 1 (real or emulated) or an NCCL communicator:
+                                            // the sharded code path with its exchanges
   double* sums1 = nullptr;                  // W > 1: [W or 1][npad][K1] per-event sums
   double* sums2 = nullptr;                  // W > 1: [W or 1][npad][K2]
 
@@ -572,8 +574,8 @@ struct Fin1D {
     const bool all = ctx->pairs;
     const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
-    const bool sums = all && ctx->W > 1;
-    const bool final_here = all || ctx->W == 1;   // else rho' is exchanged first
+    const bool sums = all && ctx->multi;
+    const bool final_here = all || !ctx->multi;   // else rho' is exchanged first
     k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
         sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1, ctx->rl,
@@ -591,7 +593,7 @@ struct Fin2D {
     const bool all = ctx->pairs;
     const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
-    const bool sums = all && ctx->W > 1;
+    const bool sums = all && ctx->multi;
     k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
         sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->G1, ctx->rl, ctx->grad);
@@ -722,7 +724,7 @@ struct DriftD {
 
 // Exchange K values per row: own rows of every logical rank -> all rows everywhere.
 int exchange_rows(hawkes_ctx* ctx, double* rows, int K) {
-  if (ctx->W == 1) return HAWKES_OK;
+  if (!ctx->multi) return HAWKES_OK;
   const long long per_rank = (long long)ctx->max_tiles * RT * K;
   for (int r : ctx->my_ranks) {
     const int nt = (int)ctx->tiles_of[r].size();
@@ -855,7 +857,7 @@ int run_rates(hawkes_ctx* ctx) {
   CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
-    if (ctx->W > 1) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1_of(ctx->D)));
+    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1_of(ctx->D)));
     TRY(dispatchD<Fin1D>(ctx->D, ctx, 0));
   } else {
     for (int r : ctx->my_ranks) {
@@ -863,7 +865,7 @@ int run_rates(hawkes_ctx* ctx) {
       TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
     }
     TRY(exchange_rows(ctx, ctx->rl, 2));
-    if (ctx->W > 1) TRY(dispatchD<RhoD>(ctx->D, ctx));
+    if (ctx->multi) TRY(dispatchD<RhoD>(ctx->D, ctx));
   }
   k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
   CHECK_LAUNCH();
@@ -887,7 +889,7 @@ int run_grad(hawkes_ctx* ctx) {
   TRY(run_rates(ctx));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
-    if (ctx->W > 1) TRY(reduce_pair_partials(ctx, ctx->part2, ctx->sums2, K2_of(ctx->D)));
+    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part2, ctx->sums2, K2_of(ctx->D)));
     TRY(dispatchD<Fin2D>(ctx->D, ctx, 0));
   } else {
     for (int r : ctx->my_ranks) {
@@ -1133,8 +1135,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     return set_err(nullptr, HAWKES_ERR_ARG, "bad precision");
   if (o.world > 1 && !o.nccl_unique_id)
     return set_err(nullptr, HAWKES_ERR_ARG, "world > 1 needs nccl_unique_id");
-  if (o.world > 1 && o.emulate_world > 1)
-    return set_err(nullptr, HAWKES_ERR_ARG, "emulate_world needs world == 1");
+  if ((o.world > 1 || o.nccl_unique_id) && o.emulate_world > 1)
+    return set_err(nullptr, HAWKES_ERR_ARG, "emulate_world needs world == 1 and no NCCL id");
 
   ctx = new hawkes_ctx();
   ctx->N = N;
@@ -1180,6 +1182,9 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);
   ctx->nslots = ctx->nchunks + (ctx->pairs ? 1 : 0);   // PAIRS: + diagonal column slot
   ctx->W = o.world > 1 ? o.world : std::max(1, o.emulate_world);
+  // an NCCL id with world == 1 builds a one-rank communicator and runs the sharded path
+  // (exchanges included) on one GPU: the NCCL plumbing's single-GPU test
+  ctx->multi = ctx->W > 1 || o.nccl_unique_id != nullptr;
   if (o.world > 1)
     ctx->my_ranks = {o.rank};
   else
@@ -1215,7 +1220,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     return fail(rc);
   if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
-  if (o.world == 1 && ctx->W == 1 && !getenv("HAWKES_NO_GRAPHS")) {
+  if (!ctx->multi && !getenv("HAWKES_NO_GRAPHS")) {
     if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess)
@@ -1245,13 +1250,13 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
           cudaMemcpy(ctx->d_sym[r], sym[r].data(), sym[r].size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair items failed"));
     }
-    if (ctx->W > 1) {
-      const size_t copies = o.world > 1 ? 1 : (size_t)ctx->W + 1;
+    if (ctx->multi) {
+      const size_t copies = o.nccl_unique_id ? 1 : (size_t)ctx->W + 1;
       if ((rc = dalloc(ctx, &ctx->sums1, copies * ctx->npad * K1_of(D))) ||
           (rc = dalloc(ctx, &ctx->sums2, copies * ctx->npad * K2_of(D))))
         return fail(rc);
     }
-  } else if (ctx->W > 1) {
+  } else if (ctx->multi) {
     const size_t per_rank = (size_t)ctx->max_tiles * RT * std::max(4, D);
     if ((rc = dalloc(ctx, &ctx->sendbuf, per_rank)) ||
         (rc = dalloc(ctx, &ctx->recvbuf, per_rank * ctx->W)))
@@ -1297,7 +1302,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       cudaMemset(ctx->rec, 0, (size_t)ctx->npad * REC * sizeof(double)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   if ((rc = dispatchD<SetupD>(D, ctx))) return fail(rc);
-  if (o.world > 1) {
+  if (o.nccl_unique_id) {
     std::string e;
     if (!g_nccl.load(e)) return fail(set_err(ctx, HAWKES_ERR_NCCL, "%s", e.c_str()));
     ncclUniqueId id;

@@ -431,6 +431,14 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
       cg = __shfl_sync(0xffffffffu, cg0, src);
       cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
     }
+    // a padding column of a ragged tile holds stale shared memory (NaN patterns included):
+    // zero its values so the masked terms are exactly 0 (0 * NaN would not be)
+    const float crho_v = (MASK && !cv) ? 0.f : crho;
+    if (MASK && !cv) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) cxh[d] = cxl[d] = 0.f;
+    }
+    const float cth_v = (MASK && !cv) ? 0.f : cth, ctl_v = (MASK && !cv) ? 0.f : ctl;
     float2 cM = make_float2(cacc[0], 0.f), cX = make_float2(cacc[1], 0.f), cG[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) cG[d] = make_float2(cacc[2 + d], 0.f);
@@ -442,8 +450,8 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
         da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
         db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
       }
-      sym32_pair2<D, PASS, MASK, SELF>(rp[h], cxh, cxl, cth, ctl, crho, da, db, rM[h], rG[h], cM, cX,
-                                       cG, c);
+      sym32_pair2<D, PASS, MASK, SELF>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h], rG[h], cM,
+                                       cX, cG, c);
     }
     cacc[0] = cM.x + cM.y;
     cacc[1] = cX.x + cX.y;

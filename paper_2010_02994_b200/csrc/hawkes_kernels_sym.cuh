@@ -164,6 +164,15 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
     if (MASK) {
       cg = __shfl_sync(0xffffffffu, cg0, src);
       cv = __shfl_sync(0xffffffffu, (int)cvalid0, src) != 0;
+      // a padding column of a ragged tile holds stale shared memory (any bit pattern, NaN
+      // included): select its values to 0 so the masked terms below are exactly 0 (0 * NaN
+      // would not be)
+      if (!cv) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) cx[d] = 0.0;
+        ct = 0.0;
+        crho = 0.0;
+      }
     }
     double cG[D];
 #pragma unroll
