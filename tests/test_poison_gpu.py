@@ -41,3 +41,40 @@ def test_poisoned_memory_does_not_leak(N, D, precision, algorithm):
     assert np.isfinite(ell) and np.isfinite(g).all() and np.isfinite(lam).all()
     ell_r, _, _, g_r, S = oracle_eval(c.x, c.t, c.theta)
     assert_parity(ell, g, ell_r, g_r, S, precision=precision, what=f"poisoned {precision} {algorithm}")
+
+
+def test_poisoned_memory_moves_hmc_sweep_bmds():
+    """The other entry points on poisoned memory: block moves, the HMC transition, the MH
+    sweep and the BMDS density, against the oracle."""
+    import oracle
+    from paper_2010_02994_b200 import HawkesContext
+    c = synth.config("C2", 700)
+    _poison()
+    with HawkesContext(c.N, c.D) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_locations(c.x)
+        ctx.set_params(c.theta)
+        idx = np.array([5, 300, 699], dtype=np.int32)
+        new = c.x[idx] + 20.0
+        d = ctx.propose_move(idx, new)
+        x2 = c.x.copy()
+        x2[idx] = new
+        ell0 = oracle.loglik(c.x, c.t, c.theta)[0]
+        assert d == pytest.approx(oracle.loglik(x2, c.t, c.theta)[0] - ell0, rel=1e-7, abs=1e-7)
+        ctx.set_regions("square", c.centre, c.size)
+        blocks = np.arange(40, dtype=np.int32).reshape(10, 4)
+        x_ref, acc_ref, _ = oracle.mh_sweep(c.x, c.t, c.theta, "square", c.centre, c.size, blocks, 0.5, 2, 0)
+        acc, _ = ctx.mh_sweep(blocks, 0.5, 2, 0)
+        assert list(acc) == list(acc_ref)
+        x_ref, acc_ref, la_ref = oracle.hmc_step(x_ref, c.t, c.theta, 4, 0, 5.0, 3)
+        acc, la = ctx.hmc_step(4, 0, 5.0, 3)
+        assert acc == acc_ref and la == pytest.approx(la_ref, rel=1e-7, abs=1e-8)
+    cf, Y, s = synth.flu_shaped(300, 3)
+    _poison()
+    with HawkesContext(cf.N, cf.D) as ctx:
+        ctx.set_locations(cf.x)
+        ctx.set_bmds(Y, s)
+        lp, g = ctx.bmds_logdensity()
+        lp_r, g_r = oracle.bmds(cf.x, Y, s)
+        assert lp == pytest.approx(lp_r, rel=1e-10)
+        assert np.max(np.abs(g.cpu().numpy() - g_r)) <= 1e-9 * np.abs(g_r).max()
