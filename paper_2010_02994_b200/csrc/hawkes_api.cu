@@ -24,6 +24,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <string>
 #include <vector>
 
@@ -183,6 +184,11 @@ struct hawkes_ctx {
   int* d_mh_acc = nullptr;     // mh_bcap decisions
   double* d_mh_la = nullptr;   // mh_bcap log alphas
   size_t mh_cap = 0, mh_bcap = 0;
+  cudaGraphExec_t mh_gexec = nullptr;  // captured block step (k = mh_gk)
+  int mh_gk = 0;
+  int64_t mh_graph_launches = 0;       // kernel launches per replay
+  cudaStream_t mh_stream = nullptr;
+  cudaEvent_t mh_ev0 = nullptr, mh_ev1 = nullptr;
   // BMDS (hawkes_set_bmds / hawkes_bmds_logdensity / hawkes_set_potential)
   double* d_Y = nullptr;       // N x N, lower triangle mirrored into the upper
   double* d_bgrad = nullptr;   // N x D
@@ -644,7 +650,7 @@ struct PackTD {
 
 template <int D>
 struct MoveD {
-  static int run(hawkes_ctx* ctx, int k) {
+  static int run(hawkes_ctx* ctx, int k, int decide) {
     MoveArgs<D> a;
     a.rec = ctx->rec;
     a.gid = ctx->gid;
@@ -655,20 +661,18 @@ struct MoveD {
     a.N = (int)ctx->N;
     a.c = ctx->pc;
     a.tab = ctx->tab;
-    k_move_delta<D><<<(unsigned)((ctx->N + 255) / 256), 256, 0, ctx->stream>>>(a, ctx->tab, ctx->d_move_delta);
-    CHECK_LAUNCH();
-    const int nsplit = (int)((ctx->N + MOVE_SPLIT - 1) / MOVE_SPLIT);
-    k_move_rows<D><<<dim3(k, nsplit), 256, 0, ctx->stream>>>(a, ctx->tab, ctx->d_move_rows_part);
-    CHECK_LAUNCH();
-    k_move_rows_combine<<<(k + 127) / 128, 128, 0, ctx->stream>>>(ctx->d_move_rows_part, k, nsplit,
-                                                                  ctx->d_move_rows);
-    CHECK_LAUNCH();
+    // one launch for the rows outside S and the moved rows, one for the terms and their
+    // fixed-order sum (decide: the MH sweep's Metropolis decision in the same kernel)
     const int nb = (int)((ctx->N + 255) / 256);
-    k_move_terms<<<nb, 256, 0, ctx->stream>>>(ctx->rates, ctx->d_move_delta, ctx->d_move_rows,
-                                              ctx->d_slot_of, (int)ctx->N, ctx->fc.tx2, ctx->fc.h2,
-                                              ctx->fc.zero_floor, ctx->d_move_part);
+    const int nsplit = (int)((ctx->N + MOVE_SPLIT - 1) / MOVE_SPLIT);
+    k_move_delta_rows<D><<<(unsigned)(nb + k * nsplit), 256, 0, ctx->stream>>>(
+        a, ctx->tab, ctx->d_move_delta, ctx->d_move_rows_part, nb, nsplit);
     CHECK_LAUNCH();
-    k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_move_part, nb, &ctx->st->dell);
+    k_move_terms_final<<<nb, 256, 0, ctx->stream>>>(ctx->rates, ctx->d_move_delta, ctx->d_move_rows_part,
+                                                    nsplit, ctx->d_slot_of, (int)ctx->N, ctx->fc.tx2,
+                                                    ctx->fc.h2, ctx->fc.zero_floor, ctx->d_move_part,
+                                                    ctx->d_move_rows, ctx->st, decide, ctx->d_mh_acc,
+                                                    ctx->d_mh_la);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -689,10 +693,10 @@ struct CommitD {
 
 template <int D>
 struct MhProposeD {
-  static int run(hawkes_ctx* ctx, int b, int k, double scale, uint2 key, unsigned long long it) {
-    k_mh_propose<D><<<1, 256, 0, ctx->stream>>>(ctx->d_mh_blocks, b, k, ctx->xstage, ctx->d_reg_c,
-                                               ctx->d_reg_s, ctx->reg_kind, scale, key, it,
-                                               ctx->d_move_idx, ctx->d_move_x, ctx->d_slot_of, ctx->st);
+  static int run(hawkes_ctx* ctx, int k) {
+    k_mh_propose<D><<<1, 256, 0, ctx->stream>>>(ctx->d_mh_blocks, k, ctx->xstage, ctx->d_reg_c,
+                                               ctx->d_reg_s, ctx->reg_kind, ctx->d_move_idx,
+                                               ctx->d_move_x, ctx->d_slot_of, ctx->st);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -786,6 +790,12 @@ bool use_graph(const hawkes_ctx* ctx) {
   return ctx->graphs && !ctx->timing && !ctx->capturing && ctx->evals_same_consts >= 2;
 }
 
+void drop_mh_graph(hawkes_ctx* ctx) {
+  if (ctx->mh_gexec) cudaGraphExecDestroy(ctx->mh_gexec);
+  ctx->mh_gexec = nullptr;
+  ctx->mh_gk = 0;
+}
+
 void drop_graphs(hawkes_ctx* ctx) {
   for (auto& ge : ctx->gexec)
     if (ge) {
@@ -793,6 +803,7 @@ void drop_graphs(hawkes_ctx* ctx) {
       ge = nullptr;
     }
   ctx->evals_same_consts = 0;
+  drop_mh_graph(ctx);   // its launches carry the folded constants by value
 }
 
 // Capture one evaluation sequence (0: rate pass; 1: rate + gradient pass; 2: gradient pass
@@ -1324,6 +1335,13 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   if (ctx->comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->comm);
   for (auto& ge : ctx->gexec)
     if (ge) cudaGraphExecDestroy(ge);
+  if (ctx->mh_gexec) cudaGraphExecDestroy(ctx->mh_gexec);
+  if (ctx->mh_ev0) cudaEventDestroy(ctx->mh_ev0);
+  if (ctx->mh_ev1) cudaEventDestroy(ctx->mh_ev1);
+  if (ctx->mh_stream) {
+    cudaStreamSynchronize(ctx->mh_stream);
+    cudaStreamDestroy(ctx->mh_stream);
+  }
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   if (ctx->gstream) {
@@ -1679,7 +1697,7 @@ int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const do
   k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 1);
   CHECK_LAUNCH();
   ctx->move_k = k;
-  TRY(dispatchD<MoveD>(D, ctx, k));
+  TRY(dispatchD<MoveD>(D, ctx, k, 0));
   TRY(fetch_status(ctx));
   *out_delta = ctx->h_st->dell;
   return HAWKES_OK;
@@ -1738,6 +1756,7 @@ int hawkes_set_regions(hawkes_ctx* ctx, int32_t kind, const double* centre, cons
   CU(cudaMemcpyAsync(ctx->d_reg_s, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->reg_kind = kind;
+  drop_mh_graph(ctx);
   return HAWKES_OK;
 }
 
@@ -1769,6 +1788,7 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   if (total > ctx->mh_cap) {
     if (ctx->d_mh_blocks) cudaFree(ctx->d_mh_blocks);
     ctx->d_mh_blocks = nullptr;
+    drop_mh_graph(ctx);
     TRY(dalloc(ctx, &ctx->d_mh_blocks, total));
     ctx->mh_cap = total;
   }
@@ -1777,6 +1797,7 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
     if (ctx->d_mh_la) cudaFree(ctx->d_mh_la);
     ctx->d_mh_acc = nullptr;
     ctx->d_mh_la = nullptr;
+    drop_mh_graph(ctx);
     TRY(dalloc(ctx, &ctx->d_mh_acc, (size_t)n_blocks));
     TRY(dalloc(ctx, &ctx->d_mh_la, (size_t)n_blocks));
     ctx->mh_bcap = n_blocks;
@@ -1790,17 +1811,74 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
       ctx->rates_exchanged = true;
     }
   }
-  const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
-  for (int32_t b = 0; b < n_blocks; ++b) {
-    TRY(dispatchD<MhProposeD>(ctx->D, ctx, (int)b, (int)k, scale, key, (unsigned long long)iteration));
-    TRY(dispatchD<MoveD>(ctx->D, ctx, (int)k));
-    k_mh_decide<<<1, 1, 0, ctx->stream>>>(ctx->st, (int)b, key, (unsigned long long)iteration,
-                                          ctx->d_mh_acc, ctx->d_mh_la);
-    CHECK_LAUNCH();
+  // the sweep's parameters live on the device (EvalStatus mh_*), staged through the pinned
+  // status block: one block step (propose, Delta ell, terms + decision, gated commit) then
+  // serves every block, as plain launches or as one captured graph replayed per block
+  CU(cudaStreamSynchronize(ctx->stream));   // h_st is free to stage
+  ctx->h_st->mh_it = iteration;
+  ctx->h_st->mh_scale = scale;
+  ctx->h_st->mh_key_lo = (unsigned)seed;
+  ctx->h_st->mh_key_hi = (unsigned)(seed >> 32);
+  ctx->h_st->mh_block = 0;
+  ctx->h_st->mh_cur = 0;
+  ctx->h_st->mh_prevk = 0;
+  const size_t off = offsetof(EvalStatus, mh_it), len = offsetof(EvalStatus, mh_ticket) - off;
+  CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + off, reinterpret_cast<char*>(ctx->h_st) + off, len,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  auto block_step = [&]() -> int {
+    TRY(dispatchD<MhProposeD>(ctx->D, ctx, (int)k));
+    TRY(dispatchD<MoveD>(ctx->D, ctx, (int)k, 1));
     TRY(dispatchD<CommitD>(ctx->D, ctx, (int)k, 1));
-    k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 0);
-    CHECK_LAUNCH();
+    return HAWKES_OK;
+  };
+  const bool graph = n_blocks >= 8 && !getenv("HAWKES_NO_GRAPHS");
+  if (graph) {
+    if (!ctx->mh_stream) {
+      CU(cudaStreamCreateWithFlags(&ctx->mh_stream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&ctx->mh_ev0, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->mh_ev1, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(ctx->mh_ev0, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->mh_stream, ctx->mh_ev0, 0));
+    if (!ctx->mh_gexec || ctx->mh_gk != k) {
+      drop_mh_graph(ctx);
+      cudaStream_t user = ctx->stream;
+      const int64_t l0 = ctx->launches;
+      ctx->stream = ctx->mh_stream;
+      int rc = HAWKES_OK;
+      cudaError_t e = cudaStreamBeginCapture(ctx->mh_stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) rc = block_step();
+      cudaGraph_t g = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(ctx->mh_stream, &g);
+      ctx->stream = user;
+      ctx->mh_graph_launches = ctx->launches - l0;
+      ctx->launches = l0;
+      if (rc != HAWKES_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e != cudaSuccess || e2 != cudaSuccess)
+        return set_err(ctx, HAWKES_ERR_CUDA, "MH graph capture failed: %s",
+                       cudaGetErrorString(e != cudaSuccess ? e : e2));
+      cudaError_t e3 = cudaGraphInstantiate(&ctx->mh_gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (e3 != cudaSuccess) {
+        ctx->mh_gexec = nullptr;
+        return set_err(ctx, HAWKES_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e3));
+      }
+      ctx->mh_gk = k;
+    }
+    for (int32_t b = 0; b < n_blocks; ++b) CU(cudaGraphLaunch(ctx->mh_gexec, ctx->mh_stream));
+    ctx->launches += n_blocks * ctx->mh_graph_launches;
+    CU(cudaEventRecord(ctx->mh_ev1, ctx->mh_stream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->mh_ev1, 0));
+  } else {
+    for (int32_t b = 0; b < n_blocks; ++b) TRY(block_step());
   }
+  // clear the last block's proposal slots
+  k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 0);
+  CHECK_LAUNCH();
+  CU(cudaMemsetAsync(&ctx->st->mh_prevk, 0, sizeof(int), ctx->stream));
   std::vector<int> acc(n_blocks);
   CU(cudaMemcpyAsync(acc.data(), ctx->d_mh_acc, n_blocks * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   if (out_log_alpha)

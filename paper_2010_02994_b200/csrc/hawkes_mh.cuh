@@ -9,9 +9,11 @@
 //   * disc regions (Eq. locsPrior2, |x_n - c_n| < r_n, D = 2): x* uniform on the
 //     intersection of disc(c_n, r_n) and disc(x_n, eps r_n), eps = scale (Eq. circleKernel),
 //     by rejection; Hastings ratio A(x)/A(x*) with A the closed-form lens area.
-// Per block: k_mh_propose (one CTA: proposals, proposal-slot map, Hastings sum in a fixed
-// order), the O(kN) Delta ell kernels of hawkes_moves.cuh, k_mh_decide (Metropolis test
-// with a counter-based uniform), a gated commit.  No host round trip between blocks.
+// Per block, four launches (captured once as a CUDA graph and replayed per block):
+// k_mh_propose (one CTA: proposals, proposal-slot map, Hastings sum in a fixed order),
+// k_move_delta_rows (the O(kN) Delta ell work of hawkes_moves.cuh), k_move_terms_final
+// (the per-event terms; its last CTA sums them and takes the Metropolis decision with a
+// counter-based uniform), and k_move_commit gated on that decision.  No host round trip.
 //
 // Random numbers: Philox-4x32-10 (hawkes_ops.cuh) with counter (it_lo, it_hi, b, tag), key
 // (seed_lo, seed_hi), b the block index within the sweep; proposal draws of slot q use
@@ -50,17 +52,26 @@ __device__ __forceinline__ double lens(double R, double rho, double d) {
 }
 
 // one CTA of 256 threads; slot q < k proposes for event n = blocks[b*k + q]
+// The block index, key, iteration and scale come from st (device-resident), so the same
+// launch -- and a CUDA graph of the whole block step -- serves every block of a sweep.  The
+// previous block's proposal slots are cleared first (its commit has run).
 template <int D>
-__global__ void __launch_bounds__(256) k_mh_propose(const int* __restrict__ blocks, int b, int k,
+__global__ void __launch_bounds__(256) k_mh_propose(const int* __restrict__ blocks, int k,
                                                     const double* __restrict__ xcur,
                                                     const double* __restrict__ centre,
                                                     const double* __restrict__ size, int kind,
-                                                    double scale, uint2 key, unsigned long long it,
                                                     int* __restrict__ move_idx,
                                                     double* __restrict__ move_x,
                                                     int* __restrict__ slot_of, EvalStatus* st) {
   __shared__ double sh[256];
   const int q = threadIdx.x;
+  const int b = st->mh_block;
+  const int prevk = st->mh_prevk;
+  const uint2 key = make_uint2(st->mh_key_lo, st->mh_key_hi);
+  const unsigned long long it = st->mh_it;
+  const double scale = st->mh_scale;
+  if (q < prevk) slot_of[move_idx[q]] = -1;
+  __syncthreads();
   double logh = 0.0;
   if (q < k) {
     const int n = blocks[(long long)b * k + q];
@@ -114,19 +125,11 @@ __global__ void __launch_bounds__(256) k_mh_propose(const int* __restrict__ bloc
     if (q < w) sh[q] += sh[q + w];
     __syncthreads();
   }
-  if (q == 0) st->mh_hastings = sh[0];
-}
-
-// log alpha = Delta ell + sum log Hastings; accept iff log u < log alpha
-__global__ void k_mh_decide(EvalStatus* st, int b, uint2 key, unsigned long long it,
-                            int* __restrict__ acc_out, double* __restrict__ la_out) {
-  const double dl = st->dell;
-  const double la = (dl > -INFINITY) ? dl + st->mh_hastings : -INFINITY;   // NaN -> -inf too
-  const double u = mh_uniforms(key, it, (unsigned)b, MH_ACCEPT_TAG).x;
-  const int acc = log(u) < la ? 1 : 0;
-  st->accepted = acc;
-  acc_out[b] = acc;
-  la_out[b] = la;
+  if (q == 0) {
+    st->mh_hastings = sh[0];
+    st->mh_cur = b;
+    st->mh_prevk = k;
+  }
 }
 
 }  // namespace hk

@@ -44,9 +44,10 @@ __device__ __forceinline__ void move_pair(const double* xn, double tn, int gn, c
   es = gm < gn ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
 }
 
-// rows not in S: (delta M', delta X') from the k moved events
+// rows not in S: (delta M', delta X') from the k moved events (CTA blk of the delta role)
 template <int D>
-__global__ void k_move_delta(MoveArgs<D> a, const int2* __restrict__ gtab, double* __restrict__ dout) {
+__device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2* __restrict__ gtab,
+                                                double* __restrict__ dout, int blk) {
   using L = Layout<D>;
   __shared__ int2 tab[EXP_TABLE];
   __shared__ double sx_old[MOVE_MAX * D], sx_new[MOVE_MAX * D], st[MOVE_MAX];
@@ -64,7 +65,7 @@ __global__ void k_move_delta(MoveArgs<D> a, const int2* __restrict__ gtab, doubl
     sg[q] = a.gid[m];
   }
   __syncthreads();
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blk * blockDim.x + threadIdx.x;
   if (n >= a.N) return;
   double dM = 0.0, dX = 0.0;
   if (a.slot_of[n] < 0) {
@@ -92,20 +93,21 @@ __global__ void k_move_delta(MoveArgs<D> a, const int2* __restrict__ gtab, doubl
 constexpr int MOVE_SPLIT = 4096;
 
 template <int D>
-__global__ void k_move_rows(MoveArgs<D> a, const int2* __restrict__ gtab, double* __restrict__ rows_part) {
+__device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2* __restrict__ gtab,
+                                               double* __restrict__ rows_part, int q, int split,
+                                               int nsplit) {
   using L = Layout<D>;
   __shared__ int2 tab[EXP_TABLE];
   __shared__ double shM[256], shX[256];
-  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  for (int t = threadIdx.x; t < EXP_TABLE; t += blockDim.x) tab[t] = gtab[t];
   __syncthreads();
-  const int q = blockIdx.x;
   const int n = a.idx[q];
   double xn[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) xn[d] = a.new_x[q * D + d];
   const double tn = a.rec[(long long)n * L::REC + D];
   const int gn = a.gid[n];
-  const int j0 = blockIdx.y * MOVE_SPLIT, j1 = min(a.N, j0 + MOVE_SPLIT);
+  const int j0 = split * MOVE_SPLIT, j1 = min(a.N, j0 + MOVE_SPLIT);
   double M = 0.0, X = 0.0;
   for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     const double* rj = a.rec + (long long)j * L::REC;
@@ -127,23 +129,26 @@ __global__ void k_move_rows(MoveArgs<D> a, const int2* __restrict__ gtab, double
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const long long o = 2 * ((long long)q * gridDim.y + blockIdx.y);
+    const long long o = 2 * ((long long)q * nsplit + split);
     rows_part[o] = shM[0];
     rows_part[o + 1] = shX[0];
   }
 }
 
-__global__ void k_move_rows_combine(const double* __restrict__ rows_part, int k, int nsplit,
-                                    double* __restrict__ rows) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= k) return;
-  double M = 0.0, X = 0.0;
-  for (int s = 0; s < nsplit; ++s) {
-    M += rows_part[2 * ((long long)q * nsplit + s)];
-    X += rows_part[2 * ((long long)q * nsplit + s) + 1];
+// One launch, two CTA roles: CTAs [0, nb_delta) update the rows outside S
+// (move_delta_body), the k * nsplit others sum the moved events' full rows at X' over
+// MOVE_SPLIT-event j ranges (move_rows_body).
+template <int D>
+__global__ void __launch_bounds__(256) k_move_delta_rows(MoveArgs<D> a, const int2* __restrict__ gtab,
+                                                         double* __restrict__ dout,
+                                                         double* __restrict__ rows_part, int nb_delta,
+                                                         int nsplit) {
+  if ((int)blockIdx.x < nb_delta) {
+    move_delta_body<D>(a, gtab, dout, blockIdx.x);
+  } else {
+    const int u = blockIdx.x - nb_delta;
+    move_rows_body<D>(a, gtab, rows_part, u / nsplit, u % nsplit, nsplit);
   }
-  rows[2 * q] = M;
-  rows[2 * q + 1] = X;
 }
 
 }  // namespace hk

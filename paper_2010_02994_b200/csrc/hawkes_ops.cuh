@@ -174,6 +174,27 @@ __global__ void k_rho_to_rec(double* __restrict__ rec, float* __restrict__ rec32
     rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
 }
 
+// ---- HMC transition (P:L267; Neal 2011): counter-based random numbers on the device.
+// Philox-4x32-10 (Salmon et al. 2011): 10 rounds of the two 32x32->64 multiplies with the
+// Weyl key schedule; the counter is (iteration lo, hi, block, lane) and the key the seed, so
+// every rank (and every world size) draws the same numbers without any state.
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// 53-bit uniform in (0, 1) from two words (high 27 bits of a, high 26 of b)
+__device__ __forceinline__ double u53(unsigned a, unsigned b) {
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) * (1.0 / 9007199254740992.0);
+}
+
 // sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W
 struct EvalStatus {
   double ell;
@@ -189,15 +210,38 @@ struct EvalStatus {
   int accepted;
   int undef0;      // ell(x0) = -inf: the chain's state has zero density
   double mh_hastings;   // block MH: sum of the proposal's log Hastings terms
+  // block MH sweep parameters, device-resident so one captured block step serves every block
+  unsigned long long mh_it;
+  double mh_scale;
+  unsigned mh_key_lo, mh_key_hi;
+  int mh_block;         // next block of the sweep
+  int mh_cur;           // block being processed
+  int mh_prevk;         // proposal slots of the previous block still set (cleared by propose)
+  unsigned mh_ticket;   // last-CTA-done counter of k_move_terms_final
 };
 
-// Delta ell of a block move: per event log(lambda'/lambda); block b of k_move_terms sums
-// events [256 b, 256 b + 256) in a fixed tree, k_sum_partials adds the block sums in order.
-// rates[n] = (lambda, mu, xi, Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.
-__global__ void k_move_terms(const double* __restrict__ rates, const double* __restrict__ delta,
-                             const double* __restrict__ rows, const int* __restrict__ slot_of,
-                             int N, double tx2, double h2, double floor_, double* __restrict__ part) {
+// Delta ell of a block move: per event log(lambda'/lambda); CTA b sums events
+// [256 b, 256 b + 256) in a fixed tree into part[b], and the last CTA to finish (ticket)
+// adds the part[] in index order into st->dell.  Events in S combine their row partials
+// (split order) and store the combined (M', X') row for the commit.  rates[n] = (lambda,
+// mu, xi, Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.  With decide != 0
+// (MH sweep) the last CTA also takes the Metropolis decision of block st->mh_cur:
+// log alpha = dell + st->mh_hastings, accept iff log u < log alpha (u: Philox block
+// (it, b, MH_ACCEPT_TAG), the same stream as hawkes_mh.cuh).
+__device__ __forceinline__ double mh_accept_uniform(unsigned klo, unsigned khi, unsigned long long it,
+                                                    unsigned b) {
+  const uint4 w = philox10(make_uint4((unsigned)it, (unsigned)(it >> 32), b, 0xC0000000u),
+                           make_uint2(klo, khi));
+  return u53(w.x, w.y);
+}
+
+__global__ void __launch_bounds__(256) k_move_terms_final(
+    const double* __restrict__ rates, const double* __restrict__ delta,
+    const double* __restrict__ rows_part, int nsplit, const int* __restrict__ slot_of, int N,
+    double tx2, double h2, double floor_, double* __restrict__ part, double* __restrict__ rows_out,
+    EvalStatus* st, int decide, int* __restrict__ acc_out, double* __restrict__ la_out) {
   __shared__ double sh[256];
+  __shared__ bool last;
   const double S = 18446744073709551616.0;   // 2^64
   const int n = blockIdx.x * 256 + threadIdx.x;
   double term = 0.0;
@@ -208,7 +252,14 @@ __global__ void k_move_terms(const double* __restrict__ rates, const double* __r
       const double d = fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2);
       term = (d == 0.0) ? 0.0 : ((L0 + d > floor_) ? log1p(d / L0) : -INFINITY);
     } else {
-      const double L1 = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2);
+      double M = 0.0, X = 0.0;
+      for (int s = 0; s < nsplit; ++s) {
+        M += rows_part[2 * ((long long)q * nsplit + s)];
+        X += rows_part[2 * ((long long)q * nsplit + s) + 1];
+      }
+      rows_out[2 * q] = M;
+      rows_out[2 * q + 1] = X;
+      const double L1 = fma(M, tx2, X * h2);
       term = ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
     }
   }
@@ -218,7 +269,37 @@ __global__ void k_move_terms(const double* __restrict__ rates, const double* __r
     if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = sh[0];
+    __threadfence();
+    last = atomicAdd(&st->mh_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) v += __ldcg(part + i);
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double dl = sh[0];
+    st->dell = dl;
+    st->mh_ticket = 0;
+    if (decide) {
+      const int b = st->mh_cur;
+      const double la = (dl > -INFINITY) ? dl + st->mh_hastings : -INFINITY;   // NaN -> -inf
+      const double u = mh_accept_uniform(st->mh_key_lo, st->mh_key_hi, st->mh_it, (unsigned)b);
+      const int acc = log(u) < la ? 1 : 0;
+      st->accepted = acc;
+      acc_out[b] = acc;
+      la_out[b] = la;
+      st->mh_block = b + 1;
+    }
+  }
 }
 
 __global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
@@ -397,27 +478,6 @@ __global__ void k_kinetic(const double* __restrict__ p, const double* __restrict
     __syncthreads();
   }
   if (threadIdx.x == 0) st->kinetic = 0.5 * sh[0];
-}
-
-// ---- HMC transition (P:L267; Neal 2011): counter-based random numbers on the device.
-// Philox-4x32-10 (Salmon et al. 2011): 10 rounds of the two 32x32->64 multiplies with the
-// Weyl key schedule; the counter is (iteration lo, hi, block, lane) and the key the seed, so
-// every rank (and every world size) draws the same numbers without any state.
-__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
-}
-
-// 53-bit uniform in (0, 1) from two words (high 27 bits of a, high 26 of b)
-__device__ __forceinline__ double u53(unsigned a, unsigned b) {
-  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) * (1.0 / 9007199254740992.0);
 }
 
 // standard normals z[2q], z[2q+1] from block (it, q): Box-Muller of (u1, u2)

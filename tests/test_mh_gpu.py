@@ -109,3 +109,44 @@ def test_mh_errors():
     with HawkesContext(c1.N, 3) as ctx:
         with pytest.raises(HawkesError, match="DIM"):
             ctx.set_regions("disc", np.zeros((c1.N, 3)), np.ones(c1.N))
+
+
+def test_mh_sweep_graph_replay_matches_plain_launches(monkeypatch):
+    """A sweep of >= 8 blocks replays one captured block step; with HAWKES_NO_GRAPHS it runs
+    plain launches.  Same kernels, same order: bitwise identical decisions and states."""
+    c = synth.config("C3", 600)
+    blocks = _blocks(c.N, 24, 4, 9)
+    res = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("HAWKES_NO_GRAPHS", "1")
+        with _ctx(c) as ctx:
+            acc, la = ctx.mh_sweep(blocks, 0.8, 6, 2)
+            res.append((acc, la, ctx.get_locations().cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
+
+
+def test_mh_sweep_recaptures_on_k_and_params_change():
+    """The captured step bakes in k and the folded constants: a sweep with another k, and one
+    after set_params, must match the oracle with the new values."""
+    c = synth.config("C2", 400, replicate=2)
+    theta2 = tuple(v * f for v, f in zip(c.theta, (1.1, 0.9, 1.2, 0.8, 1.0, 1.05)))
+    x_ref = c.x.copy()
+    with _ctx(c) as ctx:
+        b1 = _blocks(c.N, 10, 2, 1)
+        x_ref, a_ref, _ = oracle.mh_sweep(x_ref, c.t, c.theta, "square", c.centre, c.size, b1, 0.5, 3, 0)
+        acc, _ = ctx.mh_sweep(b1, 0.5, 3, 0)
+        assert list(acc) == list(a_ref)
+        b2 = _blocks(c.N, 10, 5, 2)
+        x_ref, a_ref, _ = oracle.mh_sweep(x_ref, c.t, c.theta, "square", c.centre, c.size, b2, 0.5, 3, 1)
+        acc, _ = ctx.mh_sweep(b2, 0.5, 3, 1)
+        assert list(acc) == list(a_ref)
+        ctx.set_params(theta2)
+        b3 = _blocks(c.N, 10, 5, 3)
+        x_ref, a_ref, la_ref = oracle.mh_sweep(x_ref, c.t, theta2, "square", c.centre, c.size, b3, 0.5, 3, 2)
+        acc, la = ctx.mh_sweep(b3, 0.5, 3, 2)
+        assert list(acc) == list(a_ref)
+        assert np.allclose(la, la_ref, rtol=1e-7, atol=1e-7)
+        assert np.max(np.abs(ctx.get_locations().cpu().numpy() - x_ref)) <= 1e-12 * np.abs(x_ref).max()
