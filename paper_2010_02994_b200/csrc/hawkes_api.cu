@@ -174,7 +174,7 @@ struct hawkes_ctx {
   double* d_move_delta = nullptr;  // Npad x 2
   double* d_move_rows = nullptr;   // MOVE_MAX x 2
   double* d_move_part = nullptr;   // ceil(N/256) block sums
-  double* d_move_rows_part = nullptr;  // MOVE_MAX x ceil(N/MOVE_SPLIT) x 2
+  double* d_move_rows_part = nullptr;  // MOVE_MAX x nsplit (<= MOVE_NSPLIT) x 2
   bool lam_valid = false;      // rates[][] hold lambda of the current state (all rows)
   // coarsening regions and the on-device block MH sweep (hawkes_set_regions / hawkes_mh_sweep)
   int reg_kind = 0;
@@ -664,7 +664,8 @@ struct MoveD {
     // one launch for the rows outside S and the moved rows, one for the terms and their
     // fixed-order sum (decide: the MH sweep's Metropolis decision in the same kernel)
     const int nb = (int)((ctx->N + 255) / 256);
-    const int nsplit = (int)((ctx->N + MOVE_SPLIT - 1) / MOVE_SPLIT);
+    const int len = move_split_len((int)ctx->N);
+    const int nsplit = (int)((ctx->N + len - 1) / len);
     k_move_delta_rows<D><<<(unsigned)(nb + k * nsplit), 256, 0, ctx->stream>>>(
         a, ctx->tab, ctx->d_move_delta, ctx->d_move_rows_part, nb, nsplit);
     CHECK_LAUNCH();
@@ -1227,7 +1228,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->d_move_delta, (size_t)ctx->npad * 2)) ||
       (rc = dalloc(ctx, &ctx->d_move_rows, (size_t)MOVE_MAX * 2)) ||
       (rc = dalloc(ctx, &ctx->d_move_part, (size_t)(N + 255) / 256)) ||
-      (rc = dalloc(ctx, &ctx->d_move_rows_part, (size_t)MOVE_MAX * 2 * ((N + MOVE_SPLIT - 1) / MOVE_SPLIT))))
+      (rc = dalloc(ctx, &ctx->d_move_rows_part, (size_t)MOVE_MAX * 2 * MOVE_NSPLIT)))
     return fail(rc);
   if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));

@@ -88,9 +88,15 @@ __device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2
 }
 
 // rows in S: full (M', X') at the proposed configuration.  Block (q, s) sums the j range
-// [s*MOVE_SPLIT, (s+1)*MOVE_SPLIT) for moved event q (strided per thread, fixed tree);
+// [s*len, (s+1)*len), len = move_split_len(N), for moved event q (strided per thread, fixed tree);
 // k_move_rows_combine adds the split partials in order.
-constexpr int MOVE_SPLIT = 4096;
+// j-range length: 256 events per CTA for small N (latency), at most MOVE_NSPLIT ranges for
+// large N (the in-order combine of k_move_terms_final stays short)
+constexpr int MOVE_NSPLIT = 64;
+__host__ __device__ inline int move_split_len(int N) {
+  const int per = (N + MOVE_NSPLIT - 1) / MOVE_NSPLIT;
+  return per <= 256 ? 256 : ((per + 255) / 256) * 256;
+}
 
 template <int D>
 __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2* __restrict__ gtab,
@@ -107,7 +113,8 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
   for (int d = 0; d < D; ++d) xn[d] = a.new_x[q * D + d];
   const double tn = a.rec[(long long)n * L::REC + D];
   const int gn = a.gid[n];
-  const int j0 = split * MOVE_SPLIT, j1 = min(a.N, j0 + MOVE_SPLIT);
+  const int len = move_split_len(a.N);
+  const int j0 = split * len, j1 = min(a.N, j0 + len);
   double M = 0.0, X = 0.0;
   for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     const double* rj = a.rec + (long long)j * L::REC;
@@ -137,7 +144,7 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
 
 // One launch, two CTA roles: CTAs [0, nb_delta) update the rows outside S
 // (move_delta_body), the k * nsplit others sum the moved events' full rows at X' over
-// MOVE_SPLIT-event j ranges (move_rows_body).
+// move_split_len(N)-event j ranges (move_rows_body).
 template <int D>
 __global__ void __launch_bounds__(256) k_move_delta_rows(MoveArgs<D> a, const int2* __restrict__ gtab,
                                                          double* __restrict__ dout,
