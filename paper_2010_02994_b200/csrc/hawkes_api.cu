@@ -297,7 +297,7 @@ size_t pass_smem() {
 template <int D, int PASS, int R, int V>
 size_t sym_smem() {
   const int KR = PASS == 1 ? 1 + D : D;
-  const int copies = (V & 2) ? TAB_COPIES : 1;
+  const int copies = ((V & 2) && EXP_TABLE == 256) ? TAB_COPIES : 1;
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
          (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
          ((V & 4) ? (size_t)4 * 32 * Layout<D>::REC * sizeof(double) : 0);
@@ -332,9 +332,10 @@ struct SymOps {
   }
 };
 
-// default: pass 1 V = 6 (interleaved table + SoA columns), pass 2 V = 4 (SoA columns);
-// HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant for both passes (diagnostics, A/B on one
-// box; 2 and 6-for-pass-2 exist for D = 2 only)
+// default: V = 4 (SoA columns) in both passes -- the interleaved exp table (V bit 2) needs
+// the 256-entry exp (-DHK_EXP256: pass 1 V = 6 measured 3.4 % faster there); with the
+// default 2048-entry table it is inactive.  HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant
+// for both passes (diagnostics, A/B on one box; 2 and 6 exist for D = 2 only)
 static int sym_variant() {
   static int v = [] {
     const char* e = getenv("HAWKES_SYM_V");
@@ -357,7 +358,8 @@ int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
     if (v == 4) return sym_call_v<D, 4, 4>(ctx, pass, b);
     if (v == 6) return sym_call_v<D, 6, 6>(ctx, pass, b);
   }
-  return sym_call_v<D, 6, 4>(ctx, pass, b);
+  if constexpr (EXP_TABLE == 256) return sym_call_v<D, 6, 4>(ctx, pass, b);
+  return sym_call_v<D, 4, 4>(ctx, pass, b);
 }
 
 constexpr int SYM32_R = 4;
@@ -412,6 +414,8 @@ size_t pass_smem32() {
 template <int D>
 struct SetupD {
   static int run(hawkes_ctx* ctx) {
+    CU(cudaFuncSetAttribute(k_move_delta_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)move_smem_bytes<D>(MOVE_MAX)));
     if (ctx->rec32) {
       auto k1 = pass_kernel_f32<D, 1, R_ROWS>;
       auto k2 = pass_kernel_f32<D, 2, R_ROWS>;
@@ -666,7 +670,7 @@ struct MoveD {
     const int nb = (int)((ctx->N + 255) / 256);
     const int len = move_split_len((int)ctx->N);
     const int nsplit = (int)((ctx->N + len - 1) / len);
-    k_move_delta_rows<D><<<(unsigned)(nb + k * nsplit), 256, 0, ctx->stream>>>(
+    k_move_delta_rows<D><<<(unsigned)(nb + k * nsplit), 256, move_smem_bytes<D>(k), ctx->stream>>>(
         a, ctx->tab, ctx->d_move_delta, ctx->d_move_rows_part, nb, nsplit);
     CHECK_LAUNCH();
     k_move_terms_final<<<nb, 256, 0, ctx->stream>>>(ctx->rates, ctx->d_move_delta, ctx->d_move_rows_part,

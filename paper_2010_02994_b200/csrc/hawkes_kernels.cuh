@@ -56,35 +56,50 @@ struct PassConst {
 // e^a for the pair kernels.  On sm_100 an FP64 instruction holds its SM sub-partition's
 // dispatch for two cycles and every other instruction for one (measured: the FP64 pipe
 // utilisation of a kernel tracks 2*n_fp64 / (2*n_fp64 + n_other)), so this exp is
-// built to minimise both: 7 FP64 instructions and 5 integer/shared-memory ones.
+// built to minimise both: 6 FP64 instructions and 5 integer/shared-memory ones.
 //   a' = max(a, AMIN)            one unsigned min on the high word (AMIN = -707: for
 //                                negative doubles a larger high word means a larger |a|;
 //                                positive a, high bit clear, pass through)
-//   y  = a' * 256/ln2 + 1.5*2^52 rounds to an integer: y's low word is
-//                                k = rint(a' * 256/ln2) = 256m + j
-//   r  = a' - k ln2/256          |r| <= ln2/512
-//   T  = 2^(j/256) from a 256-entry (2 KB) shared table whose high words are pre-biased
-//        by -(j << 12), so that one integer multiply-add, hi + (k << 12), also adds m to
-//        the exponent field
-//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r + c3 r^2)  (minimax, tools/
-//        fit_exp_poly.py 256 3: |rel. err.| <= 2.4e-14 on |r| <= ln2/512)
+//   y  = a' * 2048/ln2 + 1.5*2^52 rounds to an integer: y's low word is
+//                                k = rint(a' * 2048/ln2) = 2048m + j
+//   r  = a' - k ln2/2048         |r| <= ln2/4096
+//   T  = 2^(j/2048) from a 2048-entry (16 KB) shared table whose high words are
+//        pre-biased by -(j << 9), so that one integer multiply-add, hi + (k << 9), also
+//        adds m to the exponent field
+//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r)  (minimax, tools/fit_exp_poly.py 2048 2:
+//        |rel. err.| <= 8.1e-13 on |r| <= ln2/4096)
+// The 2048-entry table and degree 2 save one FP64 instruction per exp against a 256-entry
+// table with degree 3 (-DHK_EXP256, 2.4e-14): 4.7 % per evaluation at N = 100k
+// (profiles/r01_sym_variants.txt), and 8e-13 stays three orders of magnitude inside the
+// 1e-9 parity tolerance (reading R23).
 // Arguments below AMIN return e^(a') ~ e^-707 instead of a smaller number (callers treat
 // sums below N e^-700 as zero; reading R23).  Arguments must be < ~700
 // (guaranteed by the validated kernel constants).
+#ifndef HK_EXP256
+constexpr double EXP_K = 2954.639443740597;                 // 2048/ln2
+constexpr double EXP_C = 3.3845077175778579e-04;            // ln2/2048
+constexpr double EXP_C2 = 0.499999996420339;
+constexpr double EXP_C3 = 0.0;                              // unused
+constexpr int EXP_TABLE = 2048;
+constexpr int EXP_BIAS_SHIFT = 9;                           // 20 - log2(EXP_TABLE)
+constexpr int EXP_DEGREE = 2;
+#else   // the 256-entry, degree-3 exp (tools/fit_exp_poly.py 256 3: 2.4e-14)
 constexpr double EXP_K = 369.3299304675746;                // 256/ln2
-constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
 constexpr double EXP_C = 0.0027076061740622863;            // ln2/256
-constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
 constexpr double EXP_C2 = 0.5000000632802307;
 constexpr double EXP_C3 = 0.1666666688540192;
 constexpr int EXP_TABLE = 256;
 constexpr int EXP_BIAS_SHIFT = 12;                          // 20 - log2(EXP_TABLE)
+constexpr int EXP_DEGREE = 3;
+#endif
+constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
+constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
 
 // STRIDE > 1: the table is stored interleaved in STRIDE copies (entry j of copy c at
 // j*STRIDE + c) and tab points at this thread's copy (see sym_kernel)
 template <int STRIDE = 1>
 __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, int lane_off = 0) {
-  static_assert(STRIDE == 1 || STRIDE == 16, "interleaved tables have 16 copies");
+  static_assert(STRIDE == 1 || (STRIDE == 16 && EXP_TABLE == 256), "interleaved tables: 16 x 256");
   const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
   const double ac = __hiloint2double((int)ahi, __double2loint(a));
   const double y = fma(ac, EXP_K, EXP_SHIFT);
@@ -100,7 +115,7 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, i
     T = *reinterpret_cast<const int2*>(reinterpret_cast<const char*>(tab) +
                                        (((k << 7) & ((EXP_TABLE - 1) << 7)) | lane_off));
   }
-  const double q = fma(fma(EXP_C3, r, EXP_C2), r, 1.0);
+  const double q = EXP_DEGREE == 2 ? fma(EXP_C2, r, 1.0) : fma(fma(EXP_C3, r, EXP_C2), r, 1.0);
   const double p = q * r;                                      // e^r - 1
   const double Tm = __hiloint2double(T.y + k * (1 << EXP_BIAS_SHIFT), T.x);   // 2^(j/256) 2^m
   return fma(Tm, p, Tm);

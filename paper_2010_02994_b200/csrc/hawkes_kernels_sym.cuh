@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArg
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? L::K1 : L::K2;
   constexpr int KR = PASS == 1 ? 1 + D : D;   // row sums reduced over warps: (M, G) or G
-  constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
+  constexpr bool REPL = (V & 2) != 0 && EXP_TABLE == 256, SOA = (V & 4) != 0;
   constexpr int TS = REPL ? TAB_COPIES : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage = reinterpret_cast<double*>(smem_raw);

@@ -46,13 +46,13 @@ __device__ __forceinline__ void move_pair(const double* xn, double tn, int gn, c
 
 // rows not in S: (delta M', delta X') from the k moved events (CTA blk of the delta role)
 template <int D>
-__device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2* __restrict__ gtab,
-                                                double* __restrict__ dout, int blk) {
+__device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2* __restrict__ tab,
+                                                double* __restrict__ dout, int blk, double* dyn) {
   using L = Layout<D>;
-  __shared__ int2 tab[EXP_TABLE];
-  __shared__ double sx_old[MOVE_MAX * D], sx_new[MOVE_MAX * D], st[MOVE_MAX];
-  __shared__ int sg[MOVE_MAX];
-  for (int q = threadIdx.x; q < EXP_TABLE; q += blockDim.x) tab[q] = gtab[q];
+  double* sx_old = dyn;                       // [k][D]
+  double* sx_new = sx_old + a.k * D;          // [k][D]
+  double* st = sx_new + a.k * D;              // [k]
+  int* sg = reinterpret_cast<int*>(st + a.k); // [k]
   for (int q = threadIdx.x; q < a.k; q += blockDim.x) {
     const int m = a.idx[q];
     const double* rm = a.rec + (long long)m * L::REC;
@@ -99,14 +99,12 @@ __host__ __device__ inline int move_split_len(int N) {
 }
 
 template <int D>
-__device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2* __restrict__ gtab,
+__device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2* __restrict__ tab,
                                                double* __restrict__ rows_part, int q, int split,
-                                               int nsplit) {
+                                               int nsplit, double* dyn) {
   using L = Layout<D>;
-  __shared__ int2 tab[EXP_TABLE];
-  __shared__ double shM[256], shX[256];
-  for (int t = threadIdx.x; t < EXP_TABLE; t += blockDim.x) tab[t] = gtab[t];
-  __syncthreads();
+  double* shM = dyn;
+  double* shX = dyn + 256;
   const int n = a.idx[q];
   double xn[D];
 #pragma unroll
@@ -144,17 +142,31 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
 
 // One launch, two CTA roles: CTAs [0, nb_delta) update the rows outside S
 // (move_delta_body), the k * nsplit others sum the moved events' full rows at X' over
-// move_split_len(N)-event j ranges (move_rows_body).
+// move_split_len(N)-event j ranges (move_rows_body).  Dynamic shared memory: the exp table,
+// then the k moved events (delta role) or the reduction buffers (rows role).
+template <int D>
+__host__ __device__ constexpr size_t move_smem_bytes(int k) {
+  return (size_t)EXP_TABLE * sizeof(int2) +
+         ((size_t)k * (2 * D + 1) * sizeof(double) + (size_t)k * sizeof(int) > 512 * sizeof(double)
+              ? (size_t)k * (2 * D + 1) * sizeof(double) + (size_t)k * sizeof(int)
+              : 512 * sizeof(double));
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_move_delta_rows(MoveArgs<D> a, const int2* __restrict__ gtab,
                                                          double* __restrict__ dout,
                                                          double* __restrict__ rows_part, int nb_delta,
                                                          int nsplit) {
+  extern __shared__ __align__(16) unsigned char mv_smem[];
+  int2* tab = reinterpret_cast<int2*>(mv_smem);
+  double* dyn = reinterpret_cast<double*>(tab + EXP_TABLE);
+  for (int t = threadIdx.x; t < EXP_TABLE; t += blockDim.x) tab[t] = gtab[t];
+  __syncthreads();
   if ((int)blockIdx.x < nb_delta) {
-    move_delta_body<D>(a, gtab, dout, blockIdx.x);
+    move_delta_body<D>(a, tab, dout, blockIdx.x, dyn);
   } else {
     const int u = blockIdx.x - nb_delta;
-    move_rows_body<D>(a, gtab, rows_part, u / nsplit, u % nsplit, nsplit);
+    move_rows_body<D>(a, tab, rows_part, u / nsplit, u % nsplit, nsplit, dyn);
   }
 }
 

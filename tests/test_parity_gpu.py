@@ -217,7 +217,8 @@ def test_full_size_c4_sampled_rows_and_properties():
 
 def test_fast_exp_accuracy():
     """The kernels' exp (256-entry table + degree-3 minimax polynomial) against glibc exp:
-    relative error <= 3e-14 + 1.2e-16 |a| on [-707, 700]; below -707 the argument is
+    relative error <= 8.5e-13 + 1.2e-16 |a| on [-707, 700] (the degree-2 minimax bound
+    8.1e-13 of tools/fit_exp_poly.py 2048 2, plus rounding); below -707 the argument is
     clamped, so the result is e^(-707 +- 1e-3), never above e^-706 (R23)."""
     from paper_2010_02994_b200 import diag_exp
     a = np.concatenate([np.linspace(-800.0, 700.0, 600001), np.linspace(-1.0, 1.0, 100001),
@@ -227,7 +228,7 @@ def test_fast_exp_accuracy():
         ref = np.exp(a)
     live = a >= -707.0
     rel = np.abs(out[live] - ref[live]) / ref[live]
-    assert np.all(rel <= 3e-14 + 1.2e-16 * np.abs(a[live])), float(rel.max())
+    assert np.all(rel <= 8.5e-13 + 1.2e-16 * np.abs(a[live])), float(rel.max())
     dead = ~live
     assert np.all(out[dead] > 0) and np.all(out[dead] <= math.exp(-706.0))
 
