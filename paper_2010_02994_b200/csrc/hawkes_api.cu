@@ -36,6 +36,7 @@
 #include "hawkes_bmds.cuh"
 #include "hawkes_ops.cuh"
 #include "hawkes_mh.cuh"
+#include "hawkes_mh_coop.cuh"
 #include "hawkes_plan.h"
 
 using namespace hk;
@@ -181,11 +182,13 @@ struct hawkes_ctx {
   double* d_reg_c = nullptr;   // N x D region centres
   double* d_reg_s = nullptr;   // N half-widths / radii
   int* d_mh_blocks = nullptr;  // mh_cap event indices of the current sweep
+  int* d_mh_stamp = nullptr;   // N: cooperative sweep's (block << 8) | slot stamps
   int* d_mh_acc = nullptr;     // mh_bcap decisions
   double* d_mh_la = nullptr;   // mh_bcap log alphas
   size_t mh_cap = 0, mh_bcap = 0;
   cudaGraphExec_t mh_gexec = nullptr;  // captured block step (k = mh_gk)
   int mh_gk = 0;
+  bool coop_ok = false;                // device supports cooperative launches
   int64_t mh_graph_launches = 0;       // kernel launches per replay
   cudaStream_t mh_stream = nullptr;
   cudaEvent_t mh_ev0 = nullptr, mh_ev1 = nullptr;
@@ -707,6 +710,56 @@ struct MhProposeD {
   }
 };
 
+// the whole sweep as one cooperative launch (hawkes_mh_coop.cuh)
+template <int D>
+struct MhCoopD {
+  static int run(hawkes_ctx* ctx, int n_blocks, int k) {
+    const int N = (int)ctx->N;
+    const int len = move_split_len(N);
+    MhCoopArgs<D> a;
+    a.rec = ctx->rec;
+    a.rec32 = ctx->rec32;
+    a.gid = ctx->gid;
+    a.blocks = ctx->d_mh_blocks;
+    a.n_blocks = n_blocks;
+    a.k = k;
+    a.N = N;
+    a.nsplit = (N + len - 1) / len;
+    a.centre = ctx->d_reg_c;
+    a.size = ctx->d_reg_s;
+    a.kind = ctx->reg_kind;
+    a.xcur = ctx->xstage;
+    a.rates = ctx->rates;
+    a.delta = ctx->d_move_delta;
+    a.rows_part = ctx->d_move_rows_part;
+    a.part = ctx->d_move_part;
+    a.rows = ctx->d_move_rows;
+    a.stamp = ctx->d_mh_stamp;
+    a.gtab = ctx->tab;
+    a.c = ctx->pc;
+    a.tx2 = ctx->fc.tx2;
+    a.h2 = ctx->fc.h2;
+    a.floor_ = ctx->fc.zero_floor;
+    a.st = ctx->st;
+    a.acc_out = ctx->d_mh_acc;
+    a.la_out = ctx->d_mh_la;
+    const size_t smem = mh_coop_smem<D>(k);
+    auto kern = k_mh_sweep_coop<D>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mh_coop_smem<D>(MOVE_MAX)));
+    int per_sm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) return set_err(ctx, HAWKES_ERR_CUDA, "cooperative MH sweep does not fit on an SM");
+    const int nb = (N + 255) / 256;
+    const char* e = getenv("HAWKES_MH_COOP_CTAS");   // diagnostics: CTAs per SM
+    const int want = e ? std::max(1, atoi(e)) : per_sm;
+    const int grid = std::max(1, std::min(std::min(want, per_sm) * ctx->sms, nb + k * a.nsplit));
+    void* args[] = {&a};
+    CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, ctx->stream));
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
 template <int D>
 struct BmdsD {
   static int run(hawkes_ctx* ctx, const double* x) {
@@ -1175,6 +1228,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       return HAWKES_ERR_CUDA;
     }
     ctx->sms = prop.multiProcessorCount;
+    ctx->coop_ok = prop.cooperativeLaunch != 0;
   }
   auto fail = [&](int rc) {
     if (!ctx->err.empty()) g_create_error = ctx->err;
@@ -1353,7 +1407,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
   }
-  void* bufs[] = {ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
+  void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
@@ -1769,8 +1823,8 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
                     uint64_t seed, uint64_t iteration, int32_t* out_accepted, double* out_log_alpha,
                     int32_t* out_n_accepted) {
   ENTER(ctx);
-  if (n_blocks < 0 || k < 1 || k > MOVE_MAX || (n_blocks > 0 && !blocks) || !(scale > 0.0) ||
-      !isfinite(scale))
+  if (n_blocks < 0 || n_blocks >= (1 << 23) || k < 1 || k > MOVE_MAX || (n_blocks > 0 && !blocks) ||
+      !(scale > 0.0) || !isfinite(scale))
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_mh_sweep (1 <= k <= %d, scale > 0)",
                    MOVE_MAX);
   TRY(check_ready(ctx));
@@ -1836,8 +1890,18 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
     TRY(dispatchD<CommitD>(ctx->D, ctx, (int)k, 1));
     return HAWKES_OK;
   };
-  const bool graph = n_blocks >= 8 && !getenv("HAWKES_NO_GRAPHS");
-  if (graph) {
+  // the cooperative persistent kernel for small blocks (k <= 8: launch latency dominates;
+  // profiles/r01_mh_sweep.jsonl), the launch-based block step for larger ones (its kernels
+  // run at higher occupancy: 37 vs 72 registers), replayed as a CUDA graph for >= 8 blocks
+  // unless HAWKES_NO_GRAPHS.  HAWKES_MH_COOP=0 / 1 forces either (diagnostics, tests).
+  const char* coop_env = getenv("HAWKES_MH_COOP");
+  const bool coop = ctx->coop_ok && (coop_env ? atoi(coop_env) != 0 : k <= 8);
+  const bool graph = !coop && n_blocks >= 8 && !getenv("HAWKES_NO_GRAPHS");
+  if (coop) {
+    if (!ctx->d_mh_stamp) TRY(dalloc(ctx, &ctx->d_mh_stamp, (size_t)ctx->N));
+    CU(cudaMemsetAsync(ctx->d_mh_stamp, 0xff, (size_t)ctx->N * sizeof(int), ctx->stream));
+    TRY(dispatchD<MhCoopD>(ctx->D, ctx, (int)n_blocks, (int)k));
+  } else if (graph) {
     if (!ctx->mh_stream) {
       CU(cudaStreamCreateWithFlags(&ctx->mh_stream, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&ctx->mh_ev0, cudaEventDisableTiming));
@@ -1880,10 +1944,11 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   } else {
     for (int32_t b = 0; b < n_blocks; ++b) TRY(block_step());
   }
-  // clear the last block's proposal slots
-  k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 0);
-  CHECK_LAUNCH();
-  CU(cudaMemsetAsync(&ctx->st->mh_prevk, 0, sizeof(int), ctx->stream));
+  if (!coop) {   // clear the last block's proposal slots
+    k_scatter_slots<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx, k, 0);
+    CHECK_LAUNCH();
+    CU(cudaMemsetAsync(&ctx->st->mh_prevk, 0, sizeof(int), ctx->stream));
+  }
   std::vector<int> acc(n_blocks);
   CU(cudaMemcpyAsync(acc.data(), ctx->d_mh_acc, n_blocks * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   if (out_log_alpha)

@@ -331,13 +331,14 @@ __global__ void k_move_commit(double* __restrict__ rates, const double* __restri
     const int q = slot_of[n];
     double mu, xi;
     if (q < 0) {
-      mu = rates[4 * (long long)n + 1] + delta[2 * (long long)n] * tx2 * S1;
-      xi = rates[4 * (long long)n + 2] + delta[2 * (long long)n + 1] * h2 * S1;
-      rates[4 * (long long)n] += fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2) * S1;
+      mu = __dadd_rn(rates[4 * (long long)n + 1], __dmul_rn(__dmul_rn(delta[2 * (long long)n], tx2), S1));
+      xi = __dadd_rn(rates[4 * (long long)n + 2], __dmul_rn(__dmul_rn(delta[2 * (long long)n + 1], h2), S1));
+      rates[4 * (long long)n] = __dadd_rn(rates[4 * (long long)n],
+          __dmul_rn(fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2), S1));
     } else {
-      mu = rows[2 * q] * tx2 * S1;
-      xi = rows[2 * q + 1] * h2 * S1;
-      rates[4 * (long long)n] = fma(rows[2 * q], tx2, rows[2 * q + 1] * h2) * S1;
+      mu = __dmul_rn(__dmul_rn(rows[2 * q], tx2), S1);
+      xi = __dmul_rn(__dmul_rn(rows[2 * q + 1], h2), S1);
+      rates[4 * (long long)n] = __dmul_rn(fma(rows[2 * q], tx2, rows[2 * q + 1] * h2), S1);
     }
     rates[4 * (long long)n + 1] = mu;
     rates[4 * (long long)n + 2] = xi;

@@ -150,3 +150,23 @@ def test_mh_sweep_recaptures_on_k_and_params_change():
         assert list(acc) == list(a_ref)
         assert np.allclose(la, la_ref, rtol=1e-7, atol=1e-7)
         assert np.max(np.abs(ctx.get_locations().cpu().numpy() - x_ref)) <= 1e-12 * np.abs(x_ref).max()
+
+
+@pytest.mark.parametrize("name,k,nb", [("C2", 1, 30), ("C3", 8, 20), ("C2", 32, 6)])
+def test_mh_sweep_cooperative_kernel_matches_launch_path(monkeypatch, name, k, nb):
+    """The persistent cooperative sweep (HAWKES_MH_COOP=1; default for k <= 8) and the
+    launch-based block step (HAWKES_MH_COOP=0) use the same arithmetic and reduction orders:
+    bitwise identical decisions, log alphas, locations and rates."""
+    c = synth.config(name, 900)
+    blocks = _blocks(c.N, nb, k, 4)
+    res = []
+    for coop in (True, False):
+        monkeypatch.setenv("HAWKES_MH_COOP", "1" if coop else "0")
+        with _ctx(c) as ctx:
+            acc, la = ctx.mh_sweep(blocks, 0.7, 12, 5)
+            lam = ctx.get_rates()["lambda"]
+            res.append((acc, la, ctx.get_locations().cpu().numpy(), lam))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
+    assert np.array_equal(res[0][3], res[1][3])
