@@ -320,6 +320,38 @@ def run_ours(args):
                "acceptance": sum(accs) / hK, "log_alpha": las}
         hctx.close()
 
+    # ---- the paper's location sampler for the coarsened DC / Alaska catalogs:
+    # on-device block-MH sweeps (k = 1 event per block) at the catalogs' sizes
+    mh = None
+    if not args.no_hmc:
+        mh = {}
+        for name, nev, rkind in (("C2", 3982, "square"), ("C3", 2925, "disc")):
+            cm = synth.config(name, nev)
+            if world > 1:
+                mctx = init_distributed_context(cm.N, D, precision=args.precision, algorithm=args.algorithm)
+            else:
+                mctx = HawkesContext(cm.N, D, device=local, precision=args.precision, algorithm=args.algorithm)
+            mctx.set_times(torch.from_numpy(cm.t).to(dev))
+            mctx.set_params(cm.theta)
+            mctx.set_locations(torch.from_numpy(cm.x).to(dev))
+            mctx.set_regions(rkind, cm.centre, cm.size)
+            nblk = 4000
+            blk = np.random.default_rng(11).integers(0, cm.N, size=(nblk, 1)).astype(np.int32)
+            mctx.mh_sweep(blk[:50], 0.5, 2010, 0)        # warm-up (rates computed once)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record(mctx.stream)
+            acc, _ = mctx.mh_sweep(blk, 0.5, 2010, 1)
+            m1.record(mctx.stream)
+            torch.cuda.synchronize()
+            us = m0.elapsed_time(m1) * 1e3 / nblk
+            mh[name] = {"config": f"{name}-shaped N={cm.N}, {rkind} regions, {nblk} blocks of k=1, "
+                                  "scale 0.5", "us_per_block": us, "blocks_per_s": 1e6 / us,
+                        "acceptance": float(acc.mean())}
+            mctx.close()
+
     # ---- roofline of the dominant pass (FP64 pipe), from the library's own CUDA events
     rate_avg = kt["rate_ms"] / max(1, kt["rate_launches"])
     grad_avg = kt["grad_ms"] / max(1, kt["grad_launches"])
@@ -374,6 +406,7 @@ def run_ours(args):
         "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": N * D * 8,
                 "d2h_bytes_per_step": N * D * 8 + 8},
         "hmc": hmc,
+        "mh_sweep": mh,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline()
