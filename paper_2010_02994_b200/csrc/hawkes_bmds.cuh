@@ -55,10 +55,17 @@ __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict_
     const double y = yrow[m];
     const double delta = sqrt(r2);
     const double z = delta * c.inv_s;
-    const double q = 0.5 * erfc(z * 0.70710678118654752440);   // 1 - Phi(z), z >= 0
+    // 1 - Phi(z), z >= 0.  Beyond z = 9 it is below 1.2e-19: 1/(1 - q) is 1 in double and
+    // log1p(-q) adds less than 1.2e-19 per pair, so the erfc / log1p are skipped there
+    // (most pairs of a spread-out configuration; whole warps skip the branch)
+    double q = 0.0, lphi = 0.0;
+    if (z < 9.0) {
+      q = 0.5 * erfc(z * 0.70710678118654752440);
+      lphi = log1p(-q);
+    }
     if (m < n) {
       const double e = y - delta;
-      v -= c.half_log + 0.5 * e * e * c.inv_s2 + log1p(-q);
+      v -= c.half_log + 0.5 * e * e * c.inv_s2 + lphi;
     }
     if (delta > 0.0) {
       const double phi = exp(-0.5 * z * z) * 0.39894228040143267794;
