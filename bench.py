@@ -283,6 +283,32 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_val = e2e_steps / (float(e2e_ms.item()) * 1e-3)
 
+    # ---- loglik-only evaluations (S0-S4: rate pass, finalize, exchange),
+    # same staging and L2 flush as the timed step
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            ctx.set_locations(x_dev)
+            ctx.loglik()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.fill_(k)
+            lev[k][0].record(stream)
+            ctx.set_locations(x_dev)
+            ctx.loglik()
+            lev[k][1].record(stream)
+    torch.cuda.synchronize()
+    lms = torch.tensor([sum(a.elapsed_time(b) for a, b in lev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(lms, op=dist.ReduceOp.MAX)
+    loglik_only = {"evals_per_s": args.steps / (float(lms.item()) * 1e-3),
+                   "ms_per_eval": float(lms.item()) / args.steps,
+                   "note": "ell alone (rate pass + finalize), same staging and L2 flush"}
+
     # ---- C5 (BASELINE configs[4]): full HMC transitions over X at N = 50k through
     # hawkes_hmc_step -- on-device Philox momenta, a 20-step leapfrog, the Metropolis decision;
     # an accepted transition leaves the end-point gradient cached for the next one
@@ -317,6 +343,8 @@ def run_ours(args):
         hmc = {"config": f"C5 N=50000 D=2, {hK} HMC transitions of {hL} leapfrog steps, step {hstep}, "
                          "identity mass, Philox momenta + Metropolis on the device",
                "ms_per_transition": float(hms.item()), "transitions_per_s": 1e3 / float(hms.item()),
+               "grad_evals_per_transition": hL,   # (hL + 1 after a rejected transition)
+               "grad_evals_per_s": hL * 1e3 / float(hms.item()),
                "acceptance": sum(accs) / hK, "log_alpha": las}
         hctx.close()
 
@@ -405,6 +433,7 @@ def run_ours(args):
                      "measured_dfma_peak": dfma_peak},
         "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": N * D * 8,
                 "d2h_bytes_per_step": N * D * 8 + 8},
+        "loglik_only": loglik_only,
         "hmc": hmc,
         "mh_sweep": mh,
     }
