@@ -1246,7 +1246,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     delete ctx;
     return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_ALGO_PAIRS supports D <= %d", SYM_MAX_D);
   }
-  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || (o.algorithm == HAWKES_ALGO_AUTO && D <= SYM_MAX_D);
+  ctx->pairs = o.algorithm == HAWKES_ALGO_PAIRS || (o.algorithm == HAWKES_ALGO_AUTO && D <= SYM_AUTO_MAX_D);
   ctx->chunk = ctx->pairs ? chunk_pairs_of(N, o.world > 1 ? o.world : std::max(1, o.emulate_world))
                            : chunk_of(N);
   ctx->nchunks = (int)((N + ctx->chunk - 1) / ctx->chunk);

@@ -482,7 +482,7 @@ struct SymArgs32 {
 };
 
 template <int D, int PASS, int SR, bool SOA>
-__global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : 3) sym_kernel_f32(SymArgs32 a) {
+__global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_kernel_f32(SymArgs32 a) {
   static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
   using L = Layout32<D>;

@@ -214,7 +214,7 @@ struct TileWalk {
 };
 
 template <int D, int PASS, int SYM_R, int V>
-__global__ void __launch_bounds__(THREADS, SYM_R >= 4 ? 3 : 4) sym_kernel(SymArgs a) {
+__global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a) {
   static_assert(32 * SYM_R == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SYM_RT = 32 * SYM_R;
   using L = Layout<D>;

@@ -13,7 +13,10 @@
 namespace hk {
 
 constexpr int R_ROWS = 2;                    // rows per thread
-constexpr int SYM_MAX_D = 4;                 // unordered-pair kernels: register tile of 4 rows
+constexpr int SYM_MAX_D = 8;                 // unordered-pair kernels are built for every D
+constexpr int SYM_AUTO_MAX_D = 8;            // ... and chosen by HAWKES_ALGO_AUTO up to this D
+                                             // (2x ROWS at N = 4733, >= ROWS at 20k for D <= 7;
+                                             // profiles/r01_ab_algo.jsonl)
 constexpr int RT = THREADS * R_ROWS;         // rows per row tile
 constexpr int FIN_THREADS = RT;              // finalize: one thread per row of a tile
 constexpr double LN2 = 0.693147180559945309417232121458;

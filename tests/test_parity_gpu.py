@@ -18,8 +18,9 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
 
-def _check(c, what, precision="fp64", emulate_world=0):
-    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision=precision, emulate_world=emulate_world)
+def _check(c, what, precision="fp64", emulate_world=0, algorithm="auto"):
+    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision=precision, emulate_world=emulate_world,
+                             algorithm=algorithm)
     ell_ref, lam_ref, Lam_ref, g_ref, S = oracle_eval(c.x, c.t, c.theta)
     if ell_ref == -math.inf:
         assert ell == -math.inf, what
@@ -63,10 +64,12 @@ def test_ties(N, k):
     _check(synth.with_ties(N, k), f"ties N={N} k={k}")
 
 
-@pytest.mark.parametrize("D", [1, 3, 4, 5, 6, 8])
-def test_other_dimensions(D):
-    """D = 1..8 (the flu model's latent space uses D up to 8); D > 4 runs ROWS."""
-    _check(synth.unit_square(900, config=22, D=D), f"D={D}")
+@pytest.mark.parametrize("algorithm", ["pairs", "rows"])
+@pytest.mark.parametrize("D", [1, 3, 4, 5, 6, 7, 8])
+def test_other_dimensions(D, algorithm):
+    """D = 1..8 (the flu model's latent space uses D up to 8), both decompositions
+    (AUTO runs PAIRS for every D)."""
+    _check(synth.unit_square(900, config=22, D=D), f"D={D} {algorithm}", algorithm=algorithm)
 
 
 def test_special_parameters():
@@ -291,9 +294,10 @@ def test_fp32_ragged_and_ties(N):
     _check_fp32(synth.with_ties(N, max(2, N // 10)), f"fp32 ties N={N}")
 
 
-@pytest.mark.parametrize("D", [1, 3, 4, 6, 8])
-def test_fp32_other_dimensions(D):
-    _check_fp32(synth.unit_square(700, config=26, D=D), f"fp32 D={D}")
+@pytest.mark.parametrize("algorithm", ["pairs", "rows"])
+@pytest.mark.parametrize("D", [1, 3, 4, 5, 6, 7, 8])
+def test_fp32_other_dimensions(D, algorithm):
+    _check_fp32(synth.unit_square(700, config=26, D=D), f"fp32 D={D} {algorithm}", algorithm=algorithm)
 
 
 def test_fp32_emulated_world():
@@ -317,8 +321,8 @@ def test_fp32_rows_algorithm(name):
     assert_parity(ell, g, ell_ref, g_ref, S, precision="fp32", what=f"fp32 ROWS {name}")
 
 
-def _check_fp32(c, what):
-    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision="fp32")
+def _check_fp32(c, what, algorithm="auto"):
+    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision="fp32", algorithm=algorithm)
     ell_ref, lam_ref, Lam_ref, g_ref, S = oracle_eval(c.x, c.t, c.theta)
     np.testing.assert_allclose(rates["lambda"], lam_ref, rtol=1e-4, err_msg=what)
     return assert_parity(ell, g, ell_ref, g_ref, S, precision="fp32", what=what)
