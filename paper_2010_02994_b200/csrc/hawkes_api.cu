@@ -764,7 +764,7 @@ template <int D>
 struct BmdsD {
   static int run(hawkes_ctx* ctx, const double* x) {
     k_bmds<D><<<(unsigned)ctx->N, BMDS_THREADS, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N, ctx->bc,
-                                                                   ctx->d_bgrad, ctx->d_brow);
+                                                                   ctx->tab, ctx->d_bgrad, ctx->d_brow);
     CHECK_LAUNCH();
     k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_brow, (int)ctx->N, &ctx->st->bmds);
     CHECK_LAUNCH();
@@ -1994,6 +1994,8 @@ int hawkes_set_bmds(hawkes_ctx* ctx, const double* Y, int32_t mem, double sigma)
   ctx->bc.inv_s = 1.0 / sigma;
   ctx->bc.inv_s2 = 1.0 / (sigma * sigma);
   ctx->bc.half_log = 0.5 * log(2.0 * 3.14159265358979323846 * sigma * sigma);
+  ctx->bc.mhalf_inv_s2 = -0.5 / (sigma * sigma);
+  ctx->bc.lphi_c = -log(sigma) - 0.5 * log(2.0 * 3.14159265358979323846);
   ctx->have_bmds = true;
   return HAWKES_OK;
 }

@@ -10,11 +10,14 @@
 // HMC over X needs this gradient next to the Hawkes one.  One 128-thread CTA per
 // event n: threads stride over n' (row n of Y is contiguous, so the loads coalesce), the D
 // gradient components and the value (pairs n' < n only, so each pair counts once) are
-// reduced over the CTA in a fixed tree.  Per pair: one sqrt, one erfc, one exp, one log1p
-// (libdevice); the per-pair chain is long and dependent, so the kernel needs many warps.
+// reduced over the CTA in a fixed tree.  Per pair: one rsqrt and one table exp (plus an erfc
+// and a log1p for the few pairs with delta < 9 sigma); the per-pair chain is long and
+// dependent, so the kernel needs many warps.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "hawkes_kernels.cuh"
 
 namespace hk {
 
@@ -22,18 +25,31 @@ struct BmdsConst {
   double inv_s;        // 1/sigma
   double inv_s2;       // 1/sigma^2
   double half_log;     // 1/2 log(2 pi sigma^2)
+  double mhalf_inv_s2; // -1/(2 sigma^2)
+  double lphi_c;       // log(1/(sigma sqrt(2 pi))): phi(z)/sigma = e^(r2 mhalf_inv_s2 + lphi_c)
 };
 
 constexpr int BMDS_THREADS = 128;
 
+// Per ordered pair: 1/delta = rsqrt(r2) gives delta = r2/delta and replaces the division in
+// the gradient weight; phi(z)/sigma = e^(-r2/(2 sigma^2)) / (sigma sqrt(2 pi)) comes straight
+// from r2 through the kernels' table exp (constant folded into the exponent); beyond
+// z = 9 the tail 1 - Phi(z) is below 1.2e-19, so 1/Phi(z) is 1 in double and log Phi(z)
+// adds under 1.2e-19 per pair -- the erfc, log1p and the division by Phi are skipped
+// there (most pairs of a spread-out configuration; whole warps skip the branch).
+// (A 4-rows-per-CTA variant that loads each x_n' once for 4 events was 1.7x slower: the
+// per-pair chain is latency-bound and the larger register tile cut the warps in flight.)
 template <int D>
 __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict__ x,
                                                        const double* __restrict__ Y, int N,
-                                                       BmdsConst c, double* __restrict__ grad,
+                                                       BmdsConst c, const int2* __restrict__ gtab,
+                                                       double* __restrict__ grad,
                                                        double* __restrict__ row_value) {
+  __shared__ int2 tab[EXP_TABLE];
   __shared__ double red[BMDS_THREADS][D + 1];
   const int n = blockIdx.x;
   const int tid = threadIdx.x;
+  for (int t = tid; t < EXP_TABLE; t += BMDS_THREADS) tab[t] = gtab[t];
   double xn[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) xn[d] = x[(long long)n * D + d];
@@ -41,6 +57,7 @@ __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict_
   double g[D], v = 0.0;
 #pragma unroll
   for (int d = 0; d < D; ++d) g[d] = 0.0;
+  __syncthreads();
 #pragma unroll 2
   for (int m = tid; m < N; m += BMDS_THREADS) {
     if (m == n) continue;
@@ -53,24 +70,21 @@ __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict_
     // hawkes_set_bmds mirrored the lower triangle (Eq. bmdsLikelihood's n > n') into the
     // upper one, so row n holds y_{nn'} for every n' and the loads coalesce
     const double y = yrow[m];
-    const double delta = sqrt(r2);
+    const bool apart = r2 > 0.0;
+    const double inv_d = apart ? rsqrt(r2) : 0.0;
+    const double delta = r2 * inv_d;
     const double z = delta * c.inv_s;
-    // 1 - Phi(z), z >= 0.  Beyond z = 9 it is below 1.2e-19: 1/(1 - q) is 1 in double and
-    // log1p(-q) adds less than 1.2e-19 per pair, so the erfc / log1p are skipped there
-    // (most pairs of a spread-out configuration; whole warps skip the branch)
     double q = 0.0, lphi = 0.0;
     if (z < 9.0) {
-      q = 0.5 * erfc(z * 0.70710678118654752440);
+      q = 0.5 * erfc(z * 0.70710678118654752440);   // 1 - Phi(z), z >= 0
       lphi = log1p(-q);
     }
-    if (m < n) {
-      const double e = y - delta;
-      v -= c.half_log + 0.5 * e * e * c.inv_s2 + lphi;
-    }
-    if (delta > 0.0) {
-      const double phi = exp(-0.5 * z * z) * 0.39894228040143267794;
-      const double drdd = -(y - delta) * c.inv_s2 + phi * c.inv_s / (1.0 - q);
-      const double s = -drdd / delta;
+    const double e = y - delta;
+    if (m < n) v -= c.half_log + 0.5 * e * e * c.inv_s2 + lphi;
+    if (apart) {
+      double phis = fexp(fma(r2, c.mhalf_inv_s2, c.lphi_c), tab);   // phi(z) / sigma
+      if (z < 9.0) phis = phis / (1.0 - q);
+      const double s = (e * c.inv_s2 - phis) * inv_d;                // -r'(delta) / delta
 #pragma unroll
       for (int d = 0; d < D; ++d) g[d] = fma(s, u[d], g[d]);
     }
