@@ -386,7 +386,7 @@ def run_ours(args):
     pairs_alg = pairs / world                   # each rank's launches cover 1/W of the pairs
     unordered = ctx.algorithm in ("auto", "pairs") and args.precision == "fp64"
     if unordered:
-        names = ("rate pass: sym_kernel<2,1,4,4>", "gradient pass: sym_kernel<2,2,4,4>")
+        names = ("rate pass: sym_kernel<2,1,4,6>", "gradient pass: sym_kernel<2,2,4,4>")
         F_impl = F_IMPL
     else:
         names = ("rate pass: pass_kernel<2,1>", "gradient pass: pass_kernel<2,2>")

@@ -300,7 +300,7 @@ size_t pass_smem() {
 template <int D, int PASS, int R, int V>
 size_t sym_smem() {
   const int KR = PASS == 1 ? 1 + D : D;
-  const int copies = ((V & 2) && EXP_TABLE == 256) ? TAB_COPIES : 1;
+  const int copies = (V & 2) ? TAB_COPIES : 1;
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
          (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
          ((V & 4) ? (size_t)4 * 32 * Layout<D>::REC * sizeof(double) : 0);
@@ -335,10 +335,11 @@ struct SymOps {
   }
 };
 
-// default: V = 4 (SoA columns) in both passes -- the interleaved exp table (V bit 2) needs
-// the 256-entry exp (-DHK_EXP256: pass 1 V = 6 measured 3.4 % faster there); with the
-// default 2048-entry table it is inactive.  HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant
-// for both passes (diagnostics, A/B on one box; 2 and 6 exist for D = 2 only)
+// default: pass 1 V = 6 (interleaved exp table copies + SoA columns), pass 2 V = 4 (SoA
+// columns): the copies cut pass 1's bank conflicts (2 copies of the 2048-entry table:
+// -1.6 %; 16 copies of the -DHK_EXP256 table: -3.4 %) but cost pass 2 an extra LOP3 per exp
+// (+2.3 %).  HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant for both passes (diagnostics,
+// A/B on one box; 2 and 6-for-pass-2 exist for D = 2 only)
 static int sym_variant() {
   static int v = [] {
     const char* e = getenv("HAWKES_SYM_V");
@@ -361,8 +362,7 @@ int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
     if (v == 4) return sym_call_v<D, 4, 4>(ctx, pass, b);
     if (v == 6) return sym_call_v<D, 6, 6>(ctx, pass, b);
   }
-  if constexpr (EXP_TABLE == 256) return sym_call_v<D, 6, 4>(ctx, pass, b);
-  return sym_call_v<D, 4, 4>(ctx, pass, b);
+  return sym_call_v<D, 6, 4>(ctx, pass, b);
 }
 
 constexpr int SYM32_R = 4;

@@ -99,7 +99,7 @@ constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707
 // j*STRIDE + c) and tab points at this thread's copy (see sym_kernel)
 template <int STRIDE = 1>
 __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, int lane_off = 0) {
-  static_assert(STRIDE == 1 || (STRIDE == 16 && EXP_TABLE == 256), "interleaved tables: 16 x 256");
+  static_assert(STRIDE == 1 || STRIDE == 2 || STRIDE == 4 || STRIDE == 16, "interleaved copies");
   const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
   const double ac = __hiloint2double((int)ahi, __double2loint(a));
   const double y = fma(ac, EXP_K, EXP_SHIFT);
@@ -112,8 +112,9 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, i
   } else {
     // interleaved copies: byte offset ((k mod 256) * STRIDE + copy) * 8, the copy's part
     // (lane_off, 0..STRIDE-1 times 8) or-ed in: one shift + one LOP3, uniform table base
+    constexpr int SH = 3 + (STRIDE == 2 ? 1 : STRIDE == 4 ? 2 : 4);   // log2(8 * STRIDE)
     T = *reinterpret_cast<const int2*>(reinterpret_cast<const char*>(tab) +
-                                       (((k << 7) & ((EXP_TABLE - 1) << 7)) | lane_off));
+                                       (((k << SH) & ((EXP_TABLE - 1) << SH)) | lane_off));
   }
   const double q = EXP_DEGREE == 2 ? fma(EXP_C2, r, 1.0) : fma(fma(EXP_C3, r, EXP_C2), r, 1.0);
   const double p = q * r;                                      // e^r - 1

@@ -36,7 +36,8 @@ constexpr double CULL_EXPONENT = -708.0;
 // copies, lane l reading copy l & 15, so a half-warp's 16 lookups hit 16 distinct bank pairs;
 // 4 = each warp transposes its 32-column group once per tile into a private structure-of-
 // arrays buffer of double2 pairs, so the 32 steps read columns without bank conflicts
-constexpr int TAB_COPIES = 16;
+// 16 copies of the 256-entry table (32 KB); the 2048-entry table (16 KB) fits 2 copies
+constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : 2;
 
 struct SymArgs {
   const double* rec;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? L::K1 : L::K2;
   constexpr int KR = PASS == 1 ? 1 + D : D;   // row sums reduced over warps: (M, G) or G
-  constexpr bool REPL = (V & 2) != 0 && EXP_TABLE == 256, SOA = (V & 4) != 0;
+  constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
   constexpr int TS = REPL ? TAB_COPIES : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage = reinterpret_cast<double*>(smem_raw);
