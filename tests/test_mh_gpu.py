@@ -170,3 +170,31 @@ def test_mh_sweep_cooperative_kernel_matches_launch_path(monkeypatch, name, k, n
     assert np.array_equal(res[0][1], res[1][1])
     assert np.array_equal(res[0][2], res[1][2])
     assert np.array_equal(res[0][3], res[1][3])
+
+
+def test_samplers_in_fp32_contexts():
+    """fp32 contexts: the sweep's Delta ell comes from fp32-accurate cached rates and the
+    commits update the fp32 records too; decisions agree with the oracle wherever log u is not
+    within the fp32 error of log alpha, and a later fp32 evaluation sees the chain's state.
+    (A dense catalog: in sparse ones an isolated event's rate underflows fp32's range,
+    reading R23, and ell is -inf there.)"""
+    c0 = synth.config("C1", 500)
+    centre = 0.01 * np.round(c0.x / 0.01)                 # 0.01-boxes (Eq. locsPrior1 style)
+    c = synth.Catalog(c0.x, c0.t, c0.theta, "C1-boxed", c0.seed, "square", centre,
+                      np.full(c0.N, 0.005))
+    blocks = _blocks(c.N, 16, 2, 8)
+    x_ref, acc_ref, la_ref = oracle.mh_sweep(c.x, c.t, c.theta, "square", c.centre, c.size, blocks,
+                                             0.6, 5, 1)
+    with _ctx(c, precision="fp32") as ctx:
+        acc, la = ctx.mh_sweep(blocks, 0.6, 5, 1)
+        for b in range(len(blocks)):
+            lu = np.log(oracle.mh_uniforms(5, 1, b, 0xC0000000)[0])
+            if abs(la_ref[b] - lu) > 1e-3:
+                assert acc[b] == acc_ref[b], b
+            assert la[b] == pytest.approx(la_ref[b], abs=1e-3)
+        x = ctx.get_locations().cpu().numpy()
+        if list(acc) == list(acc_ref):
+            assert np.max(np.abs(x - x_ref)) <= 1e-12
+            assert ctx.loglik() == pytest.approx(oracle.loglik(x_ref, c.t, c.theta)[0], rel=1e-5)
+        acc_h, la_h = ctx.hmc_step(3, 0, 1e-3, 3)
+        assert np.isfinite(la_h)
