@@ -413,7 +413,10 @@ def run_ours(args):
         "config": {"workload": f"C4 unit-square Hawkes catalog N={N} D=2 (BASELINE configs[3])",
                    "N": N, "D": 2, "precision": args.precision, "algorithm": ctx.algorithm,
                    "l2": "flushed before every timed step (256 MiB device write, outside the step events)",
-                   "parallelism": f"row-sharded x{world} (zig-zag tiles, NCCL allgather of 1/lambda)"
+                   "parallelism": (f"chunk-pair sharded x{world} (LPT-dealt unordered chunk pairs, NCCL "
+                                   "allreduce of per-event partial sums per pass)"
+                                   if ctx.algorithm in ("auto", "pairs") else
+                                   f"row-sharded x{world} (zig-zag tiles, NCCL allgather of 1/lambda)")
                    if world > 1 else "1 GPU"},
         "clocks": clocks,
         "gpu_launches": kt["total_launches"],
