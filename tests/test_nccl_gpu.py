@@ -71,3 +71,29 @@ def test_nccl_id_with_emulation_rejected():
     from paper_2010_02994_b200 import HawkesContext, HawkesError, nccl_unique_id
     with pytest.raises(HawkesError, match="ARG"):
         HawkesContext(100, 2, nccl_id=nccl_unique_id(), emulate_world=2)
+
+
+@pytest.mark.parametrize("algorithm", ["pairs", "rows"])
+def test_one_rank_nccl_hmc_and_mh_sweep(algorithm):
+    """The HMC transition (gradient exchanges every leapfrog step) and the MH sweep (exchanged
+    rates for ROWS) on the sharded path with a real one-rank communicator: the same decisions
+    as a plain context."""
+    from paper_2010_02994_b200 import HawkesContext, nccl_unique_id
+    c = synth.config("C2", 700)
+    rng = np.random.default_rng(1)
+    blocks = np.stack([rng.choice(c.N, size=3, replace=False) for _ in range(12)]).astype(np.int32)
+    res = []
+    for nccl in (True, False):
+        kw = {"nccl_id": nccl_unique_id()} if nccl else {}
+        with HawkesContext(c.N, c.D, algorithm=algorithm, **kw) as ctx:
+            ctx.set_times(c.t)
+            ctx.set_locations(c.x)
+            ctx.set_params(c.theta)
+            ctx.set_regions(c.region, c.centre, c.size)
+            acc, la = ctx.mh_sweep(blocks, 0.5, 9, 0)
+            h = [ctx.hmc_step(9, it, 20.0, 4) for it in range(3)]
+            res.append((acc, la, h, ctx.get_locations().cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.allclose(res[0][1], res[1][1], rtol=1e-12, atol=1e-12)
+    assert [a for a, _ in res[0][2]] == [a for a, _ in res[1][2]]
+    assert np.allclose(res[0][3], res[1][3], rtol=0, atol=1e-9)
