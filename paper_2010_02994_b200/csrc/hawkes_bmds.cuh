@@ -37,8 +37,11 @@ constexpr int BMDS_THREADS = 128;
 // z = 9 the tail 1 - Phi(z) is below 1.2e-19, so 1/Phi(z) is 1 in double and log Phi(z)
 // adds under 1.2e-19 per pair -- the erfc, log1p and the division by Phi are skipped
 // there (most pairs of a spread-out configuration; whole warps skip the branch).
-// (A 4-rows-per-CTA variant that loads each x_n' once for 4 events was 1.7x slower: the
-// per-pair chain is latency-bound and the larger register tile cut the warps in flight.)
+// The kernel is latency-bound (ncu at the flu shape: FP64 pipe 42 %, 28 warps/SM, DRAM only
+// Y once).  Tried and slower: 4 events per CTA sharing each x_n' load (1.7x: the larger
+// register tile cut the warps in flight); unroll 1 or 4 instead of 2 (+14 %); forcing 10-12
+// CTAs/SM with launch bounds (spills, +8-53 %) -- shared memory (exp table 16 KB + the
+// reduction) allows 9 CTAs anyway.
 template <int D>
 __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict__ x,
                                                        const double* __restrict__ Y, int N,
