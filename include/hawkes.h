@@ -199,7 +199,8 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
  * mem; only the lower triangle y[n*N + n'], n > n', is read, as in Eq. bmdsLikelihood) and
  * sigma > 0 (the paper's mdsSD).  Every y_{nn'} (n > n') must be finite and > 0 (the
  * truncated-normal support), else HAWKES_ERR_NONFINITE (host input: now; device input: at
- * the next evaluation).  The context then holds 8 N^2 bytes of device memory.
+ * the next evaluation).  The context then holds 8 N^2 bytes of device memory for Y plus
+ * 8 (ceil(N/32) + 1) N (D + 1) bytes of per-block partial sums (the unordered-pair kernel).
  * hawkes_bmds_logdensity writes
  *   log p(Y | X) = sum_{n > n'} [-1/2 log(2 pi sigma^2) - (y - delta)^2/(2 sigma^2)
  *                                - log Phi(delta/sigma)],   delta = |x_n - x_n'|

@@ -196,6 +196,7 @@ struct hawkes_ctx {
   double* d_Y = nullptr;       // N x N, lower triangle mirrored into the upper
   double* d_bgrad = nullptr;   // N x D
   double* d_brow = nullptr;    // N per-row values
+  double* d_bpart = nullptr;   // (NB + 1) x N x (D + 1) unordered-pair BMDS slots, NB = ceil(N/32)
   BmdsConst bc{};
   bool have_bmds = false;
   int potential = HAWKES_POTENTIAL_HAWKES;
@@ -762,10 +763,30 @@ struct MhCoopD {
 
 template <int D>
 struct BmdsD {
+  // default: the unordered-pair kernel (each pair once); HAWKES_BMDS_SYM=0 selects the
+  // per-row kernel (each ordered pair; diagnostics, A/B)
   static int run(hawkes_ctx* ctx, const double* x) {
-    k_bmds<D><<<(unsigned)ctx->N, BMDS_THREADS, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N, ctx->bc,
-                                                                   ctx->tab, ctx->d_bgrad, ctx->d_brow);
-    CHECK_LAUNCH();
+    const char* e = getenv("HAWKES_BMDS_SYM");
+    if (ctx->d_bpart && !(e && atoi(e) == 0)) {
+      const int N = (int)ctx->N;
+      const long long NB = (N + 31) / 32;
+      const size_t smem = bmds_sym_smem<D>();
+      auto kern = k_bmds_sym<D>;
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * BSYM_WARPS, smem));
+      const long long ntasks = NB * (NB + 1) / 2;
+      const long long want = (ntasks + BSYM_WARPS - 1) / BSYM_WARPS;
+      const int grid = (int)std::max(1LL, std::min<long long>((long long)std::max(1, per_sm) * ctx->sms, want));
+      kern<<<grid, 32 * BSYM_WARPS, smem, ctx->stream>>>(x, ctx->d_Y, N, ctx->bc, ctx->tab, ctx->d_bpart, ntasks);
+      CHECK_LAUNCH();
+      k_bmds_sym_fin<D><<<(N + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_bpart, N, ctx->d_bgrad, ctx->d_brow);
+      CHECK_LAUNCH();
+    } else {
+      k_bmds<D><<<(unsigned)ctx->N, BMDS_THREADS, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N, ctx->bc,
+                                                                     ctx->tab, ctx->d_bgrad, ctx->d_brow);
+      CHECK_LAUNCH();
+    }
     k_sum_partials<<<1, 1024, 0, ctx->stream>>>(ctx->d_brow, (int)ctx->N, &ctx->st->bmds);
     CHECK_LAUNCH();
     return HAWKES_OK;
@@ -1407,7 +1428,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
   }
-  void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
+  void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
                   ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
@@ -1987,6 +2008,7 @@ int hawkes_set_bmds(hawkes_ctx* ctx, const double* Y, int32_t mem, double sigma)
     TRY(dalloc(ctx, &ctx->d_Y, (size_t)(N * N)));
     TRY(dalloc(ctx, &ctx->d_bgrad, (size_t)N * ctx->D));
     TRY(dalloc(ctx, &ctx->d_brow, (size_t)N));
+    TRY(dalloc(ctx, &ctx->d_bpart, (size_t)((N + 31) / 32 + 1) * N * (ctx->D + 1)));
   }
   TRY(copy_in(ctx, ctx->d_Y, Y, (size_t)(N * N), mem));
   k_bmds_mirror<<<(unsigned)((N * N + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_Y, (int)N, ctx->bad);
