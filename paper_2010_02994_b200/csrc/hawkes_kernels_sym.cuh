@@ -133,7 +133,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const int2* __restrict__ tab) {
   constexpr int REC = Layout<D>::REC;
   const int lane = threadIdx.x & 31;
-#pragma unroll 1
+#pragma unroll 1   // unrolling by 2 halves the loop overhead but measured 1 % slower
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
     // column (l + s) mod 32 of this warp's group: from the staged tile (AoS records), or
