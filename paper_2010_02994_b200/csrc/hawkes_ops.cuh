@@ -509,7 +509,9 @@ __global__ void k_hmc_momenta(double* __restrict__ p, const double* __restrict__
 __global__ void k_hmc_begin(EvalStatus* st, int use_h, int use_b) {
   st->lp0 = (use_h ? st->ell : 0.0) + (use_b ? st->bmds : 0.0);
   st->kin0 = st->kinetic;
-  st->undef0 = use_h ? st->undefined : 0;
+  // ell(x0) itself, not the undefined flag: a cached evaluation of x0 (rates reused from an
+  // earlier call) does not run k_ell_reduce again, so the flag would stay clear
+  st->undef0 = (use_h && !(st->ell > -INFINITY)) ? 1 : 0;
 }
 
 // after the trajectory and k_kinetic(p1): Metropolis accept iff log u < H0 - H1.  A

@@ -198,3 +198,54 @@ def test_samplers_in_fp32_contexts():
             assert ctx.loglik() == pytest.approx(oracle.loglik(x_ref, c.t, c.theta)[0], rel=1e-5)
         acc_h, la_h = ctx.hmc_step(3, 0, 1e-3, 3)
         assert np.isfinite(la_h)
+
+
+@pytest.mark.parametrize("D", [1, 3])
+def test_mh_sweep_square_regions_other_dimensions(D):
+    """Square regions (Eq. locsPrior1) in D = 1 and 3: truncated normals per dimension."""
+    c0 = synth.unit_square(400, config=31, D=D)
+    centre = 0.02 * np.round(c0.x / 0.02)
+    c = synth.Catalog(c0.x, c0.t, c0.theta, f"boxed D={D}", c0.seed, "square", centre, np.full(c0.N, 0.01))
+    blocks = _blocks(c.N, 10, 3, 2)
+    x_ref, acc_ref, la_ref = oracle.mh_sweep(c.x, c.t, c.theta, "square", c.centre, c.size, blocks, 0.7, 4, 0)
+    with _ctx(c) as ctx:
+        acc, la = ctx.mh_sweep(blocks, 0.7, 4, 0)
+        x = ctx.get_locations().cpu().numpy()
+    assert list(acc) == list(acc_ref)
+    assert np.allclose(la, la_ref, rtol=1e-7, atol=1e-7)
+    assert np.max(np.abs(x - x_ref)) <= 1e-12
+
+
+def test_samplers_tiny_and_degenerate_catalogs():
+    """N = 2: both samplers against the oracle.  N = 1: ell = -inf (reading R11); the HMC
+    transition reports GRAD_UNDEFINED, the MH sweep rejects (-inf - -inf is not a gain)."""
+    from paper_2010_02994_b200 import HawkesContext, HawkesError
+    x2 = np.array([[0.40, 0.50], [0.43, 0.52]])
+    t2 = np.array([0.1, 0.3])
+    th = (0.6, 0.1, 0.1, 0.4, 20.0, 0.03)
+    xr, acc_r, la_r = oracle.hmc_step(x2, t2, th, 6, 0, 1e-3, 5)
+    with HawkesContext(2, 2) as ctx:
+        ctx.set_times(t2)
+        ctx.set_locations(x2)
+        ctx.set_params(th)
+        out = np.empty_like(x2)
+        acc, la = ctx.hmc_step(6, 0, 1e-3, 5, x_out=out)
+        assert acc == acc_r and la == pytest.approx(la_r, rel=1e-8, abs=1e-10)
+        assert np.max(np.abs(out - xr)) <= 1e-12
+        ctx.set_locations(x2)
+        centre = np.round(x2, 1)
+        ctx.set_regions("square", centre, np.full(2, 0.05))
+        x_ref, a_ref, l_ref = oracle.mh_sweep(x2, t2, th, "square", centre, np.full(2, 0.05),
+                                              [[0], [1], [0, 1]][:2], 0.5, 1, 0)
+        acc2, la2 = ctx.mh_sweep(np.array([[0], [1]], dtype=np.int32), 0.5, 1, 0)
+        assert list(acc2) == list(a_ref) and np.allclose(la2, l_ref, rtol=1e-8, atol=1e-10)
+    with HawkesContext(1, 2) as ctx:
+        ctx.set_times(np.array([0.5]))
+        ctx.set_locations(np.array([[0.2, 0.2]]))
+        ctx.set_params(th)
+        assert ctx.loglik() == -np.inf
+        with pytest.raises(HawkesError, match="GRAD_UNDEFINED"):
+            ctx.hmc_step(1, 0, 1e-3, 2)
+        ctx.set_regions("square", np.array([[0.2, 0.2]]), np.array([0.05]))
+        acc, la = ctx.mh_sweep(np.array([[0]], dtype=np.int32), 0.5, 1, 0)
+        assert not acc[0] and la[0] == -np.inf
