@@ -18,6 +18,7 @@ WANT = [
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_xu.sum",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
