@@ -167,6 +167,22 @@ def test_bitwise_determinism_and_emulated_world():
         assert_parity(ew, gw, ell_ref, g_ref, S, what=f"PAIRS W={W}")
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("D", [3, 6])
+def test_emulated_world_other_dimensions(D, precision):
+    """The sharded PAIRS path (per-rank slot sums, rank-ordered exchange) at D = 3 and 6 (the
+    D >= 5 kernels run at 2 CTAs/SM), both precisions: W = 3 agrees with W = 1 to rounding
+    and with the oracle under the tolerance rule."""
+    c = synth.unit_square(1800, config=32, D=D)
+    ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
+    e1, g1, r1 = gpu_eval(c.x, c.t, c.theta, precision=precision, algorithm="pairs")
+    e3, g3, r3 = gpu_eval(c.x, c.t, c.theta, precision=precision, emulate_world=3, algorithm="pairs")
+    tol = 1e-13 if precision == "fp64" else 1e-9
+    assert abs(e3 - e1) <= tol * abs(e1)
+    assert np.all(np.abs(g3 - g1) <= tol * (np.abs(g1) + S))
+    assert_parity(e3, g3, ell_ref, g_ref, S, precision=precision, what=f"PAIRS W=3 D={D} {precision}")
+
+
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_rows_algorithm_configs(name):
     """The ordered-pair (ROWS) decomposition on the small configs."""
