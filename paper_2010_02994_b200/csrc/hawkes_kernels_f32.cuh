@@ -282,52 +282,6 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 4 : 3) pass_kernel_f32(PassA
 
 namespace hk {
 
-template <int D>
-struct SymRow32 {
-  float xh[D], xl[D];
-  float th, tl, rho;
-  int g;
-};
-
-template <int D, int PASS, bool MASK>
-__device__ __forceinline__ void sym32_pair(const SymRow32<D>& row, const float* __restrict__ rc,
-                                           bool dead, float& rM, float (&rG)[D], float& cM,
-                                           float& cX, float (&cG)[D], const PassConst32& c) {
-  using L = Layout32<D>;
-  float dx[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) dx[d] = (rc[L::XH + d] - row.xh[d]) + (rc[L::XL + d] - row.xl[d]);
-  float r2 = dx[0] * dx[0];
-#pragma unroll
-  for (int d = 1; d < D; ++d) r2 = fmaf(dx[d], dx[d], r2);
-  const float dt = (rc[L::TH] - row.th) + (rc[L::TL] - row.tl);   // >= 0
-  float eb = ex2f(fmaf(c.kx, r2, fmaf(c.kt * dt, dt, c.cb)));
-  float es = ex2f(fmaf(c.ks, r2, fmaf(-c.omega, dt, c.cs)));
-  if (MASK) {
-    eb = dead ? 0.f : eb;
-    es = dead ? 0.f : es;
-  }
-  if (PASS == 1) {
-    rM += eb;
-    cM += eb;
-    cX += es;
-    const float cc = eb + es;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      rG[d] = fmaf(eb, dx[d], rG[d]);
-      cG[d] = fmaf(-cc, dx[d], cG[d]);
-    }
-  } else {
-    const float cr = rc[L::RHO] * (eb + es);
-    const float cc = row.rho * eb;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      rG[d] = fmaf(cr, dx[d], rG[d]);
-      cG[d] = fmaf(-cc, dx[d], cG[d]);
-    }
-  }
-}
-
 // Two rows of one lane against one column, packed into f32x2 instructions (sm_100
 // FADD2/FMUL2/FFMA2): every FP32 instruction serves two pairs; the two exps stay on MUFU.
 // Row data are stored negated (nxh = -x_hi, ...) so differences are packed adds.
