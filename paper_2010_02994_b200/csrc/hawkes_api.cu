@@ -1,18 +1,19 @@
-// hawkes_api.cu -- context, C ABI (include/hawkes.h), O(N) kernels and row sharding.
+// hawkes_api.cu -- context, C ABI (include/hawkes.h), kernel launch plumbing, exchanges.
 //
-// One evaluation (ell and d ell/dx) on rank r of W:
-//   pass 1   pass_kernel<PASS=1> over this rank's row tiles x all j chunks
-//            -> per-chunk partials (M', X', G1')                       [rate pass, Alg. 2 step 1]
-//   fin1     fixed-order chunk sum; lambda, rho' = 1/Lambda', Lambda_n (erfc, expm1),
+// One evaluation (ell and d ell/dx) on rank r of W, PAIRS (default):
+//   pass 1   sym_kernel<PASS=1> over this rank's chunk pairs (a <= b), each unordered pair
+//            once -> per-(slot, event) partials (M', X', G1')     [rate pass, Alg. 2 step 1]
+//   exchange W > 1: per-event slot sums, ncclAllReduce                       [S4]
+//   fin1     fixed-order slot sum; lambda, rho' = 2^-64 / lambda, Lambda_n (erfc, expm1),
 //            ell_n = log lambda_n - Lambda_n                            [Eq. 1, P:L92-101]
-//   exchange allgather of (rho', ell_n) over NCCL (W > 1)              [S4]
-//   ell      fixed-order reduction of ell_n over all N rows (same on every rank)
-//   pass 2   pass_kernel<PASS=2> -> per-chunk partials G2'             [gradient pass, step 2]
-//   fin2     g_i = rho'_i G1'_i + sum_chunks G2'_i                      [App. A, P:L385]
-//   exchange allgather of gradient rows (W > 1)                        [S6]
-// Row tiles are dealt to ranks zig-zag (tile k of each group of 2W goes to rank k or
-// 2W-1-k) to balance the causal self-excitation work.  Chunk boundaries and per-row
-// summation order do not depend on W, so every output is bitwise identical for any W.
+//   ell      fixed-order reduction of ell_n over all N events (same on every rank)
+//   pass 2   sym_kernel<PASS=2> -> partials G2'                        [gradient pass, step 2]
+//   exchange W > 1: per-event slot sums, ncclAllReduce                       [S6]
+//   fin2     g_i = rho'_i G1'_i + G2'_i                                 [App. A, P:L385]
+// ROWS (ordered pairs, pass_kernel): row tiles dealt to ranks zig-zag, allgather of (rho',
+// ell_n) rows between the passes and of gradient rows at the end; bitwise identical for any
+// W.  Around the evaluation: the HMC leapfrog / transition, block-MH moves and the on-device
+// MH sweep, the BMDS density, CUDA-graph capture and replay, kernel timing and diagnostics.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -201,7 +202,6 @@ struct hawkes_ctx {
   bool have_bmds = false;
   int potential = HAWKES_POTENTIAL_HAWKES;
   int move_k = 0;              // pending proposal size (0: none)
-  int sym_variant = 40;     // 10 * rows-per-lane + exp scheme (tuning knob HAWKES_SYM_VARIANT)
 };
 
 namespace {
