@@ -1262,7 +1262,6 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     delete ctx;
     return set_err(nullptr, HAWKES_ERR_ARG, "bad algorithm");
   }
-  if (const char* v = getenv("HAWKES_SYM_VARIANT")) ctx->sym_variant = atoi(v);
   if (o.algorithm == HAWKES_ALGO_PAIRS && D > SYM_MAX_D) {
     delete ctx;
     return set_err(nullptr, HAWKES_ERR_ARG, "HAWKES_ALGO_PAIRS supports D <= %d", SYM_MAX_D);
