@@ -1,0 +1,283 @@
+// hawkes_context.cuh -- part of hawkes_api.cu (one translation unit; included once, in
+// order): includes, NCCL via dlopen, the context struct, error and allocation helpers,
+// dispatch on D.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/hawkes.h"
+#include "hawkes_kernels.cuh"
+#include "hawkes_kernels_f32.cuh"
+#include "hawkes_kernels_sym.cuh"
+#include "hawkes_moves.cuh"
+#include "hawkes_bmds.cuh"
+#include "hawkes_ops.cuh"
+#include "hawkes_mh.cuh"
+#include "hawkes_mh_coop.cuh"
+#include "hawkes_plan.h"
+
+using namespace hk;
+
+namespace {
+
+
+thread_local std::string g_create_error;
+
+// ------------------------------------------------------------------ NCCL via dlopen
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    if (!commInitRank || !allGather || !allReduce || !commDestroy || !errStr) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+}  // namespace
+
+// ======================================================================= context
+struct hawkes_ctx {
+  int64_t N = 0;
+  int D = 0;
+  int npad = 0;
+  int ntiles = 0;          // row tiles of RT rows
+  int chunk = 0, nchunks = 0, nslots = 0;
+  hawkes_opts opts{};
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+  std::string err;
+  int sticky = HAWKES_OK;
+
+  // sharding: logical ranks this process runs (1, or emulate_world), their tile lists
+  int W = 1;               // world size of the row sharding (real or emulated)
+  std::vector<int> my_ranks;
+  std::vector<std::vector<int>> tiles_of;   // per rank
+  int max_tiles = 0;
+  int* d_all_tiles = nullptr;               // [W][max_tiles], -1 padded
+  std::vector<int*> d_tiles;                // per rank (points into d_all_tiles)
+  std::vector<int2*> d_items1, d_items2;    // per rank
+  std::vector<int> n_items;                 // per rank
+  ncclComm_t comm = nullptr;
+  // HAWKES_ALGO_PAIRS
+  bool pairs = false;
+  std::vector<int2*> d_sym;                 // per rank: off-diagonal chunk pairs
+  std::vector<int> n_sym;
+  int* d_own = nullptr;                     // [nchunks][nchunks] owner rank of pair (a <= b)
+  int* d_every_tile = nullptr;              // all row tiles 0..ntiles-1
+  bool multi = false;                       // W > 1 (real or emulated) or an NCCL communicator:
+                                            // the sharded code path with its exchanges
+  double* sums1 = nullptr;                  // W > 1: [W or 1][npad][K1] per-event sums
+  double* sums2 = nullptr;                  // W > 1: [W or 1][npad][K2]
+
+  // device buffers
+  double* rec = nullptr;   // npad x REC
+  float* rec32 = nullptr;  // npad x REC32 (fp32 path only)
+  int* gid = nullptr;      // npad
+  double* part1 = nullptr; // nchunks x npad x K1
+  double* part2 = nullptr; // nchunks x npad x K2
+  double* G1 = nullptr;    // npad x D
+  double* rl = nullptr;    // npad x 2 (rho', ell_n)
+  double* rates = nullptr; // npad x 4 (lambda, mu, xi, Lambda)
+  double* grad = nullptr;  // npad x D
+  double* xstage = nullptr;// N x D staging
+  double* sendbuf = nullptr;
+  double* recvbuf = nullptr;
+  int* counters = nullptr; // 4 per logical rank
+  int2* tab = nullptr;     // exp table
+  int* bad = nullptr;      // device-side input validation flag
+  EvalStatus* st = nullptr;
+  EvalStatus* h_st = nullptr;  // pinned
+  // leapfrog state
+  double *lf_x = nullptr, *lf_p = nullptr, *lf_minv = nullptr, *lf_lo = nullptr, *lf_hi = nullptr;
+
+  // state
+  bool have_t = false, have_x = false, have_p = false;
+  bool rates_valid = false;   // pass 1 + exchange done for current (x, t, Theta)
+  bool grad_valid = false;
+  bool rates_exchanged = false;
+  double tN = 0.0;
+  hawkes_params params{};
+  PassConst pc{};
+  PassConst32 pc32{};
+  FinConst fc{};
+
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_rate, ev_grad;
+  std::vector<cudaEvent_t> ev_pool;
+  double acc_rate_ms = 0, acc_grad_ms = 0;
+  int64_t n_rate = 0, n_grad = 0;
+  int64_t launches = 0;
+
+  int grid1 = 0, grid2 = 0;
+  int grid_s1 = 0, grid_s2 = 0;
+  DevConsts* d_consts = nullptr;
+  // CUDA graphs of one evaluation (single process, W = 1, timing off)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};   // rates, rates+grad, grad only
+  bool graphs = false;
+  bool capturing = false;
+  int64_t graph_launches[3] = {0, 0, 0};
+  int evals_same_consts = 0;   // evaluations since the last constants change
+  // block moves (hawkes_propose_move / hawkes_accept_move)
+  int* d_slot_of = nullptr;    // N, -1 or the event's index in the pending proposal
+  int* d_move_idx = nullptr;   // MOVE_MAX
+  double* d_move_x = nullptr;  // MOVE_MAX x D
+  double* d_move_delta = nullptr;  // Npad x 2
+  double* d_move_rows = nullptr;   // MOVE_MAX x 2
+  double* d_move_part = nullptr;   // ceil(N/256) block sums
+  double* d_move_rows_part = nullptr;  // MOVE_MAX x nsplit (<= MOVE_NSPLIT) x 2
+  bool lam_valid = false;      // rates[][] hold lambda of the current state (all rows)
+  // coarsening regions and the on-device block MH sweep (hawkes_set_regions / hawkes_mh_sweep)
+  int reg_kind = 0;
+  double* d_reg_c = nullptr;   // N x D region centres
+  double* d_reg_s = nullptr;   // N half-widths / radii
+  int* d_mh_blocks = nullptr;  // mh_cap event indices of the current sweep
+  int* d_mh_stamp = nullptr;   // N: cooperative sweep's (block << 8) | slot stamps
+  int* d_mh_acc = nullptr;     // mh_bcap decisions
+  double* d_mh_la = nullptr;   // mh_bcap log alphas
+  size_t mh_cap = 0, mh_bcap = 0;
+  cudaGraphExec_t mh_gexec = nullptr;  // captured block step (k = mh_gk)
+  int mh_gk = 0;
+  bool coop_ok = false;                // device supports cooperative launches
+  int64_t mh_graph_launches = 0;       // kernel launches per replay
+  cudaStream_t mh_stream = nullptr;
+  cudaEvent_t mh_ev0 = nullptr, mh_ev1 = nullptr;
+  // BMDS (hawkes_set_bmds / hawkes_bmds_logdensity / hawkes_set_potential)
+  double* d_Y = nullptr;       // N x N, lower triangle mirrored into the upper
+  double* d_bgrad = nullptr;   // N x D
+  double* d_brow = nullptr;    // N per-row values
+  double* d_bpart = nullptr;   // (NB + 1) x N x (D + 1) unordered-pair BMDS slots, NB = ceil(N/32)
+  BmdsConst bc{};
+  bool have_bmds = false;
+  int potential = HAWKES_POTENTIAL_HAWKES;
+  int move_k = 0;              // pending proposal size (0: none)
+};
+
+namespace {
+
+int set_err(hawkes_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code == HAWKES_ERR_CUDA || code == HAWKES_ERR_NCCL) c->sticky = code;
+  } else {
+    g_create_error = buf;
+  }
+  return code;
+}
+
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_CUDA, "%s failed: %s (%s:%d)", #call,              \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define CHECK_LAUNCH()                                                                  \
+  do {                                                                                  \
+    ++ctx->launches;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_CUDA, "kernel launch failed: %s (%s:%d)",          \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return set_err(ctx, HAWKES_ERR_NCCL, "%s failed: %s", #call, g_nccl.errStr(r_));  \
+  } while (0)
+
+#define ENTER(ctx)                                                                      \
+  do {                                                                                  \
+    if (!(ctx)) return HAWKES_ERR_ARG;                                                  \
+    if ((ctx)->sticky != HAWKES_OK) return (ctx)->sticky;                               \
+    cudaError_t e_ = cudaSetDevice((ctx)->opts.device);                                 \
+    if (e_ != cudaSuccess) return set_err(ctx, HAWKES_ERR_CUDA, "cudaSetDevice: %s",    \
+                                          cudaGetErrorString(e_));                      \
+  } while (0)
+
+template <typename T>
+int dalloc(hawkes_ctx* ctx, T** p, size_t count) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, HAWKES_ERR_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                   cudaGetErrorString(e));
+  }
+  return HAWKES_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    int rc_ = (x);                  \
+    if (rc_ != HAWKES_OK) return rc_; \
+  } while (0)
+
+int K1_of(int D) { return ((D + 3) / 2) * 2; }
+int K2_of(int D) { return ((D + 1) / 2) * 2; }
+int REC_of(int D) { return ((D + 3) / 2) * 2; }
+int Layout32Rec(int D) { return ((2 * D + 3 + 3) / 4) * 4; }
+
+// ---------------------------------------------------------------- dispatch on D
+template <template <int> class F, typename... A>
+int dispatchD(int D, A&&... a) {
+  switch (D) {
+    case 1: return F<1>::run(a...);
+    case 2: return F<2>::run(a...);
+    case 3: return F<3>::run(a...);
+    case 4: return F<4>::run(a...);
+    case 5: return F<5>::run(a...);
+    case 6: return F<6>::run(a...);
+    case 7: return F<7>::run(a...);
+    case 8: return F<8>::run(a...);
+  }
+  return HAWKES_ERR_DIM;
+}
+
+}  // namespace

@@ -1,0 +1,394 @@
+// hawkes_engine.cuh -- part of hawkes_api.cu (one translation unit): the exchanges
+// (NCCL or emulated ranks), CUDA-graph capture and replay, the rate and gradient
+// evaluations, status handling, the work plans, the folded constants and the exp table.
+#pragma once
+namespace {
+
+// Exchange K values per row: own rows of every logical rank -> all rows everywhere.
+int exchange_rows(hawkes_ctx* ctx, double* rows, int K) {
+  if (!ctx->multi) return HAWKES_OK;
+  const long long per_rank = (long long)ctx->max_tiles * RT * K;
+  for (int r : ctx->my_ranks) {
+    const int nt = (int)ctx->tiles_of[r].size();
+    const long long tot = (long long)nt * RT * K;
+    if (tot == 0) continue;
+    // with a real communicator the rank packs into its send buffer; emulated ranks pack
+    // directly into their slot of the gather buffer (the loop-back "allgather")
+    double* dst = ctx->comm ? ctx->sendbuf : ctx->recvbuf + r * per_rank;
+    k_pack_rows<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(rows, K, ctx->d_tiles[r], nt,
+                                                                       (int)ctx->N, dst);
+    CHECK_LAUNCH();
+  }
+  if (ctx->comm) {
+    // zero the tail of the send buffer beyond this rank's rows (fixed message size)
+    const int r = ctx->my_ranks[0];
+    const long long tot = (long long)ctx->tiles_of[r].size() * RT * K;
+    if (tot < per_rank)
+      CU(cudaMemsetAsync(ctx->sendbuf + tot, 0, (per_rank - tot) * sizeof(double), ctx->stream));
+    NC(g_nccl.allGather(ctx->sendbuf, ctx->recvbuf, (size_t)per_rank, ncclDouble, ctx->comm,
+                        ctx->stream));
+  }
+  const long long all = per_rank * ctx->W;
+  k_unpack_rows<<<(unsigned)((all + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->recvbuf, K, ctx->d_all_tiles, ctx->max_tiles, ctx->W, (int)ctx->N, rows);
+  CHECK_LAUNCH();
+  return HAWKES_OK;
+}
+
+// rate pass + finalize + exchange + ell reduction (device-side; no host sync)
+// PAIRS, W > 1: per-event sums over this process's chunk pairs, then the exchange
+// (NCCL allreduce, or the rank-ordered sum of the emulated ranks' buffers)
+int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int K) {
+  const long long n = (long long)ctx->N * K;
+  const long long stride = (long long)ctx->npad * K;
+  for (int r : ctx->my_ranks) {
+    double* out = ctx->comm ? sums : sums + (1 + r) * stride;
+    k_slot_sum<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        part, ctx->npad, ctx->nchunks, ctx->chunk, K, ctx->d_own, r, (int)ctx->N, out);
+    CHECK_LAUNCH();
+  }
+  if (ctx->comm) {
+    NC(g_nccl.allReduce(sums, sums, (size_t)n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  } else {
+    k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(sums + stride, stride, ctx->W,
+                                                                     n, sums);
+    CHECK_LAUNCH();
+  }
+  return HAWKES_OK;
+}
+
+int run_rates(hawkes_ctx* ctx);
+int run_grad(hawkes_ctx* ctx);
+
+// Graphs bake the kernel constants in (they are kernel parameters, so the FP64 instructions
+// read them from the constant bank); set_params / set_times drop the graphs, and a graph is
+// captured only at the second evaluation with unchanged constants, so MCMC moves that
+// change Theta every step never pay for a capture.
+bool use_graph(const hawkes_ctx* ctx) {
+  return ctx->graphs && !ctx->timing && !ctx->capturing && ctx->evals_same_consts >= 2;
+}
+
+void drop_mh_graph(hawkes_ctx* ctx) {
+  if (ctx->mh_gexec) cudaGraphExecDestroy(ctx->mh_gexec);
+  ctx->mh_gexec = nullptr;
+  ctx->mh_gk = 0;
+}
+
+void drop_graphs(hawkes_ctx* ctx) {
+  for (auto& ge : ctx->gexec)
+    if (ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
+  ctx->evals_same_consts = 0;
+  drop_mh_graph(ctx);   // its launches carry the folded constants by value
+}
+
+// Capture one evaluation sequence (0: rate pass; 1: rate + gradient pass; 2: gradient pass
+// with cached rates) on the context's own stream and instantiate it.
+int capture(hawkes_ctx* ctx, int which) {
+  cudaStream_t user = ctx->stream;
+  const bool rv = ctx->rates_valid, gv = ctx->grad_valid;
+  const int64_t l0 = ctx->launches;
+  ctx->stream = ctx->gstream;
+  ctx->capturing = true;
+  int rc = HAWKES_OK;
+  cudaError_t e = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    ctx->rates_valid = which == 2;
+    ctx->grad_valid = false;
+    rc = which == 0 ? run_rates(ctx) : run_grad(ctx);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->gstream, &g);
+  ctx->stream = user;
+  ctx->capturing = false;
+  ctx->rates_valid = rv;
+  ctx->grad_valid = gv;
+  if (rc != HAWKES_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return set_err(ctx, HAWKES_ERR_CUDA, "graph capture failed: %s",
+                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+  cudaError_t e3 = cudaGraphInstantiate(&ctx->gexec[which], g, 0);
+  cudaGraphDestroy(g);
+  if (e3 != cudaSuccess)
+    return set_err(ctx, HAWKES_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e3));
+  ctx->graph_launches[which] = ctx->launches - l0;
+  ctx->launches = l0;
+  return HAWKES_OK;
+}
+
+int replay(hawkes_ctx* ctx, int which) {
+  if (!ctx->gexec[which]) TRY(capture(ctx, which));
+  CU(cudaEventRecord(ctx->ev_in, ctx->stream));
+  CU(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
+  CU(cudaGraphLaunch(ctx->gexec[which], ctx->gstream));
+  CU(cudaEventRecord(ctx->ev_out, ctx->gstream));
+  CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
+  ctx->launches += ctx->graph_launches[which];
+  return HAWKES_OK;
+}
+
+int run_rates(hawkes_ctx* ctx) {
+  if (ctx->rates_valid) return HAWKES_OK;
+  if (!ctx->capturing) ++ctx->evals_same_consts;
+  if (use_graph(ctx)) {
+    TRY(replay(ctx, 0));
+    ctx->rates_valid = true;
+    ctx->rates_exchanged = false;
+    ctx->grad_valid = false;
+    ctx->lam_valid = true;
+    return HAWKES_OK;
+  }
+  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
+  if (ctx->pairs) {
+    for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
+    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1_of(ctx->D)));
+    TRY(dispatchD<Fin1D>(ctx->D, ctx, 0));
+  } else {
+    for (int r : ctx->my_ranks) {
+      TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
+      TRY(dispatchD<Fin1D>(ctx->D, ctx, r));
+    }
+    TRY(exchange_rows(ctx, ctx->rl, 2));
+    if (ctx->multi) TRY(dispatchD<RhoD>(ctx->D, ctx));
+  }
+  k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
+  CHECK_LAUNCH();
+  ctx->rates_valid = true;
+  ctx->rates_exchanged = false;
+  ctx->grad_valid = false;
+  ctx->lam_valid = true;
+  return HAWKES_OK;
+}
+
+int run_grad(hawkes_ctx* ctx) {
+  if (ctx->grad_valid) return HAWKES_OK;
+  if (!ctx->capturing && !ctx->rates_valid) ++ctx->evals_same_consts;
+  if (use_graph(ctx)) {
+    TRY(replay(ctx, ctx->rates_valid ? 2 : 1));
+    if (!ctx->rates_valid) ctx->rates_exchanged = false;
+    ctx->rates_valid = ctx->grad_valid = true;
+    ctx->lam_valid = true;
+    return HAWKES_OK;
+  }
+  TRY(run_rates(ctx));
+  if (ctx->pairs) {
+    for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
+    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part2, ctx->sums2, K2_of(ctx->D)));
+    TRY(dispatchD<Fin2D>(ctx->D, ctx, 0));
+  } else {
+    for (int r : ctx->my_ranks) {
+      TRY(dispatchD<PassD>(ctx->D, ctx, 2, r));
+      TRY(dispatchD<Fin2D>(ctx->D, ctx, r));
+    }
+    TRY(exchange_rows(ctx, ctx->grad, ctx->D));
+  }
+  ctx->grad_valid = true;
+  return HAWKES_OK;
+}
+
+int fetch_status(hawkes_ctx* ctx) {
+  CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  int bad = 0;
+  CU(cudaMemcpyAsync(&ctx->h_st->nonfinite, ctx->bad, sizeof(int), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  bad = ctx->h_st->nonfinite;
+  if (bad) {
+    CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
+    if (bad & 2) {
+      ctx->have_bmds = false;
+      return set_err(ctx, HAWKES_ERR_NONFINITE,
+                     "BMDS dissimilarities must be finite and > 0 below the diagonal");
+    }
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+    ctx->have_x = false;
+    return set_err(ctx, HAWKES_ERR_NONFINITE,
+                   "locations contain NaN/Inf or |x| > 1e100 (device-side validation)");
+  }
+  return HAWKES_OK;
+}
+
+// drop a pending block move (restores the event -> proposal-slot map)
+int clear_move(hawkes_ctx* ctx) {
+  if (ctx->move_k > 0) {
+    k_scatter_slots<<<(ctx->move_k + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_slot_of, ctx->d_move_idx,
+                                                                        ctx->move_k, 0);
+    CHECK_LAUNCH();
+    ctx->move_k = 0;
+  }
+  return HAWKES_OK;
+}
+
+int check_ready(hawkes_ctx* ctx) {
+  if (!ctx->have_t || !ctx->have_x || !ctx->have_p)
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times, set_locations and set_params are all required");
+  return HAWKES_OK;
+}
+
+void build_plan_pairs(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
+                      std::vector<std::vector<int2>>& it2, std::vector<std::vector<int2>>& sym,
+                      std::vector<int>& own) {
+  const int W = ctx->W, C = ctx->nchunks, N = (int)ctx->N;
+  own = pair_owners(N, ctx->chunk, W);
+  ctx->tiles_of.assign(W, {});
+  ctx->max_tiles = 0;
+  it1.assign(W, {});
+  it2.assign(W, {});
+  sym.assign(W, {});
+  for (int r = 0; r < W; ++r) {
+    std::vector<std::pair<double, int2>> items;   // (pair count, (a, b)); heaviest first
+    for (int a = 0; a < C; ++a)
+      for (int b = a; b < C; ++b) {
+        if (own[(size_t)a * C + b] != r) continue;
+        const double na = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)a * ctx->chunk);
+        const double nb = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)b * ctx->chunk);
+        items.push_back({a == b ? 0.5 * na * na : na * nb, make_int2(a, b)});
+      }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<double, int2>& x, const std::pair<double, int2>& y) {
+                       return x.first > y.first;
+                     });
+    for (auto& e : items) sym[r].push_back(e.second);
+  }
+}
+
+void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
+                std::vector<std::vector<int2>>& it2) {
+  const int W = ctx->W;
+  ctx->tiles_of.assign(W, {});
+  for (int k = 0; k < ctx->ntiles; ++k) ctx->tiles_of[owner_of_tile(k, W)].push_back(k);
+  ctx->max_tiles = 0;
+  for (auto& v : ctx->tiles_of) ctx->max_tiles = std::max<int>(ctx->max_tiles, (int)v.size());
+  it1.assign(W, {});
+  it2.assign(W, {});
+  const int N = (int)ctx->N;
+  for (int r = 0; r < W; ++r) {
+    std::vector<std::pair<long long, int2>> c1, c2;
+    for (int tile : ctx->tiles_of[r]) {
+      const int row0 = tile * RT, row1 = std::min(N, row0 + RT);
+      for (int ck = 0; ck < ctx->nchunks; ++ck) {
+        long long w1 = 0, w2 = 0;
+        const int j0 = ck * ctx->chunk, j1 = std::min(N, j0 + ctx->chunk);
+        for (int jt = j0; jt < j1; jt += TILE_J) {
+          const int je = std::min(j1, jt + TILE_J) - 1;
+          const long long n = (long long)(je - jt + 1);
+          if (je < row0) { w1 += 33 * n; w2 += 20 * n; }        // earlier: pass1 both exps
+          else if (jt > row1 - 1) { w1 += 20 * n; w2 += 32 * n; } // later: pass2 both exps
+          else { w1 += 40 * n; w2 += 40 * n; }
+        }
+        c1.push_back({w1, make_int2(tile, ck)});
+        c2.push_back({w2, make_int2(tile, ck)});
+      }
+    }
+    auto cmp = [](const std::pair<long long, int2>& a, const std::pair<long long, int2>& b) {
+      return a.first > b.first;
+    };
+    std::stable_sort(c1.begin(), c1.end(), cmp);
+    std::stable_sort(c2.begin(), c2.end(), cmp);
+    for (auto& e : c1) it1[r].push_back(e.second);
+    for (auto& e : c2) it2[r].push_back(e.second);
+  }
+}
+
+void drop_graphs(hawkes_ctx* ctx);
+
+int upload_consts(hawkes_ctx* ctx) {
+  drop_graphs(ctx);
+  DevConsts h;
+  h.pc = ctx->pc;
+  h.pc32 = ctx->pc32;
+  h.fc = ctx->fc;
+  CU(cudaMemcpyAsync(ctx->d_consts, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  return HAWKES_OK;
+}
+
+// Kernel constants for Theta; written to ctx only when every check passes.
+int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
+  const int D = ctx->D;
+  const double two_pi = 6.283185307179586476925286766559;
+  // background weight mu0/((2pi)^{D/2} tau_x^D * sqrt(2pi) tau_t), times alpha = 1/tau_x^2
+  const double lnw_b = log(p.mu0) - 0.5 * (D + 1) * log(two_pi) - D * log(p.tau_x) - log(p.tau_t) -
+                       2.0 * log(p.tau_x);
+  // self-excitation weight theta omega/((2pi)^{D/2} h^D), times beta = 1/h^2
+  const double lnw_s = log(p.theta) + log(p.omega) - 0.5 * D * log(two_pi) - D * log(p.sigma_x) -
+                       2.0 * log(p.sigma_x);
+  if ((p.mu0 > 0 && !(fabs(lnw_b) < 600.0)) || (p.theta > 0 && !(fabs(lnw_s) < 600.0)))
+    return set_err(ctx, HAWKES_ERR_PARAM,
+                   "Theta puts the kernel constants outside the fp64 exp range (|log w| >= 600)");
+  PassConst pc;
+  pc.kx = -0.5 / (p.tau_x * p.tau_x);
+  pc.kt = -0.5 / (p.tau_t * p.tau_t);
+  pc.ks = -0.5 / (p.sigma_x * p.sigma_x);
+  pc.omega = p.omega;
+  pc.lnc_b = p.mu0 > 0 ? lnw_b + 64.0 * LN2 : -INFINITY;
+  pc.lnc_s = p.theta > 0 ? lnw_s + 64.0 * LN2 : -INFINITY;
+  if (!isfinite(pc.kx) || !isfinite(pc.kt) || !isfinite(pc.ks))
+    return set_err(ctx, HAWKES_ERR_PARAM, "bandwidths too small for fp64");
+  FinConst fc;
+  fc.tx2 = p.tau_x * p.tau_x;
+  fc.h2 = p.sigma_x * p.sigma_x;
+  fc.mu0 = p.mu0;
+  fc.tau_t = p.tau_t;
+  fc.theta = p.theta;
+  fc.omega = p.omega;
+  fc.tN = tN;
+  fc.scale_log2 = -64.0;
+  // every clamped pair term is <= e^-706.9 in the kernels' scaled units
+  fc.zero_floor = (double)ctx->N * exp(-700.0) * std::max(fc.tx2, fc.h2);
+  if (ctx->opts.precision == HAWKES_FP32) {
+    // log2 domain; one power-of-two scale 2^-E puts the largest possible term near 2^20
+    const double L2E = 1.4426950408889634074;
+    const double l2b = p.mu0 > 0 ? lnw_b * L2E : -INFINITY;
+    const double l2s = p.theta > 0 ? lnw_s * L2E : -INFINITY;
+    const double E = floor(std::max(l2b, l2s)) - 20.0;
+    PassConst32 c32;
+    c32.kx = (float)(pc.kx * L2E);
+    c32.kt = (float)(pc.kt * L2E);
+    c32.ks = (float)(pc.ks * L2E);
+    c32.omega = (float)(p.omega * L2E);
+    c32.cb = (float)(l2b - E);
+    c32.cs = (float)(l2s - E);
+    if (!isfinite(c32.kx) || !isfinite(c32.kt) || !isfinite(c32.ks) || !isfinite(c32.omega) ||
+        c32.kx == 0.f || c32.kt == 0.f || c32.ks == 0.f)
+      return set_err(ctx, HAWKES_ERR_PARAM, "Theta outside the fp32 path's range");
+    fc.scale_log2 = E;
+    fc.zero_floor = 0.0;   // ex2.approx.ftz flushes to exact zeros
+    ctx->pc32 = c32;
+  }
+  ctx->pc = pc;
+  ctx->fc = fc;
+  return upload_consts(ctx);
+}
+
+int copy_in(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     mem == HAWKES_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return HAWKES_OK;
+}
+int copy_out(hawkes_ctx* ctx, double* dst, const double* src, size_t n, int mem) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                     mem == HAWKES_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  return HAWKES_OK;
+}
+
+bool finite_bounded(double v) { return fabs(v) <= 1e100; }
+
+// fexp's table: T[j] = 2^(j/EXP_TABLE) as (low word, high word - (j << EXP_BIAS_SHIFT))
+// (the bias lets one integer multiply-add insert the binary exponent; hawkes_kernels.cuh)
+void make_exp_table(int2* h) {
+  for (int j = 0; j < EXP_TABLE; ++j) {
+    const double v = (double)exp2l((long double)j / (long double)EXP_TABLE);
+    long long b;
+    memcpy(&b, &v, 8);
+    h[j] = make_int2((int)(b & 0xffffffffLL), (int)(b >> 32) - (j << EXP_BIAS_SHIFT));
+  }
+}
+
+}  // namespace
