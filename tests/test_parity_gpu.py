@@ -443,3 +443,37 @@ def test_leapfrog_energy_error_is_second_order():
             errs.append(abs(-ell + kin - H0))
     r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
     assert 3.0 < r1 < 5.5 and 3.0 < r2 < 5.5, errs
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_largest_size_1m_sampled_rows_and_properties(precision):
+    """The scaling sweep's largest size (BASELINE configs[3], N = 1M): lambda on sampled rows
+    against the oracle computed row by row (O(N) each), sum_n g_n = 0, and the directional
+    derivative of the GPU's own ell against <g, V> -- the properties that hold at any size
+    (the oracle's full gradient would need every rate, O(N^2) = 1e12 pair terms)."""
+    from paper_2010_02994_b200 import HawkesContext
+    c = synth.config("C4", 1_000_000)
+    N = c.N
+    rows = np.unique(np.concatenate([np.arange(0, N, N // 12), [N - 1, 767, 768]]))
+    tol = 1e-11 if precision == "fp64" else 1e-4
+    with HawkesContext(N, 2, precision=precision) as ctx:
+        ctx.set_times(torch.from_numpy(c.t).cuda())
+        ctx.set_params(c.theta)
+        x = torch.from_numpy(c.x).cuda()
+        ctx.set_locations(x)
+        g, ell = ctx.grad_locations()
+        g = g.cpu().numpy()
+        lam = ctx.get_rates()["lambda"]
+        for r in rows:
+            ref = oracle.rates(c.x, c.t, c.theta, rows=slice(int(r), int(r) + 1))[0][r]
+            assert abs(lam[r] - ref) <= tol * ref, (r, lam[r], ref)
+        gs = np.abs(g).sum(axis=0)
+        assert np.all(np.abs(g.sum(axis=0)) <= (1e-11 if precision == "fp64" else 1e-5) * gs)
+        if precision == "fp64":
+            V = np.random.default_rng(5).normal(size=c.x.shape)
+            eps = 1e-6
+            ctx.set_locations(x + eps * torch.from_numpy(V).cuda())
+            lp = ctx.loglik()
+            ctx.set_locations(x - eps * torch.from_numpy(V).cuda())
+            lm = ctx.loglik()
+            assert abs((lp - lm) / (2 * eps) - float(np.sum(g * V))) <= 1e-6 * np.sum(np.abs(g * V))
