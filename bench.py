@@ -33,7 +33,7 @@ METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-
 #           algorithmic work of this design, excluding masked / padding pairs (headline)
 #   F_UNO   SURVEY's method (naive per-pair bodies with libdevice exp) for unordered pairs
 #   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg
-F_IMPL = (15.0, 14.5)
+F_IMPL = (12.5, 14.5)
 F_UNO = (26.0, 28.5)
 F_SURVEY = (34.5, 49.0)
 FP64_LANES_PER_SM = 64
@@ -386,7 +386,7 @@ def run_ours(args):
     pairs_alg = pairs / world                   # each rank's launches cover 1/W of the pairs
     unordered = ctx.algorithm in ("auto", "pairs") and args.precision == "fp64"
     if unordered:
-        names = ("rate pass: sym_kernel<2,1,4,6>", "gradient pass: sym_kernel<2,2,4,4>")
+        names = ("rate pass: sym_kernel<2,1,4,4>", "gradient pass: sym_kernel<2,2,4,4>")
         F_impl = F_IMPL
     else:
         names = ("rate pass: pass_kernel<2,1>", "gradient pass: pass_kernel<2,2>")

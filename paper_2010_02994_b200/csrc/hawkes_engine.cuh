@@ -146,7 +146,7 @@ int run_rates(hawkes_ctx* ctx) {
   CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
-    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1_of(ctx->D)));
+    if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1P));
     TRY(dispatchD<Fin1D>(ctx->D, ctx, 0));
   } else {
     for (int r : ctx->my_ranks) {

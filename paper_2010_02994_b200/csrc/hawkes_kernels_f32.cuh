@@ -319,23 +319,17 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
     eb.y = dead_b ? 0.f : eb.y;
     es.y = dead_b ? 0.f : es.y;
   }
-  if (PASS == 1) {
+  if (PASS == 1) {   // rates only (the gradient comes out of pass 2)
     rM = __fadd2_rn(rM, eb);
     cM = __fadd2_rn(cM, eb);
     if (SELF) cX = __fadd2_rn(cX, es);
-    const float2 ncc = SELF ? __fadd2_rn(make_float2(-eb.x, -eb.y), make_float2(-es.x, -es.y))
-                            : make_float2(-eb.x, -eb.y);
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      rG[d] = __ffma2_rn(eb, dx[d], rG[d]);
-      cG[d] = __ffma2_rn(ncc, dx[d], cG[d]);
-    }
   } else {
-    const float2 cr = __fmul2_rn(f2(crho), SELF ? __fadd2_rn(eb, es) : eb);
-    const float2 ncc = __fmul2_rn(make_float2(-rp.rho.x, -rp.rho.y), eb);
+    // the pair's App. A coefficient rho'_i mu' + rho'_j (mu' + xi'), the same for both events
+    const float2 cc = __ffma2_rn(rp.rho, eb, __fmul2_rn(f2(crho), SELF ? __fadd2_rn(eb, es) : eb));
+    const float2 ncc = make_float2(-cc.x, -cc.y);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      rG[d] = __ffma2_rn(cr, dx[d], rG[d]);
+      rG[d] = __ffma2_rn(cc, dx[d], rG[d]);
       cG[d] = __ffma2_rn(ncc, dx[d], cG[d]);
     }
   }
@@ -407,17 +401,21 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
       sym32_pair2<D, PASS, MASK, SELF>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h], rG[h], cM,
                                        cX, cG, c);
     }
-    cacc[0] = cM.x + cM.y;
-    cacc[1] = cX.x + cX.y;
+    if (PASS == 1) {
+      cacc[0] = cM.x + cM.y;
+      cacc[1] = cX.x + cX.y;
+    } else {
 #pragma unroll
-    for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d].x + cG[d].y;
+      for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d].x + cG[d].y;
+    }
     const int nxt = (lane + 1) & 31;
     if (PASS == 1) {
       cacc[0] = __shfl_sync(0xffffffffu, cacc[0], nxt);
       cacc[1] = __shfl_sync(0xffffffffu, cacc[1], nxt);
-    }
+    } else {
 #pragma unroll
-    for (int d = 0; d < D; ++d) cacc[2 + d] = __shfl_sync(0xffffffffu, cacc[2 + d], nxt);
+      for (int d = 0; d < D; ++d) cacc[2 + d] = __shfl_sync(0xffffffffu, cacc[2 + d], nxt);
+    }
   }
 }
 
@@ -442,8 +440,8 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
   using L = Layout32<D>;
   using L64 = Layout<D>;
   constexpr int REC = L::REC;
-  constexpr int K = PASS == 1 ? L64::K1 : L64::K2;
-  constexpr int KR = PASS == 1 ? 1 + D : D;
+  constexpr int K = PASS == 1 ? K1P : L64::K2;
+  constexpr int KR = PASS == 1 ? 1 : D;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
@@ -581,7 +579,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         if (cvalid) {
           if (PASS == 1) {
 #pragma unroll
-            for (int q = 0; q < 2 + D; ++q) cpart[q] = (rt ? cpart[q] : 0.0) + (double)cacc[q];
+            for (int q = 0; q < 2; ++q) cpart[q] = (rt ? cpart[q] : 0.0) + (double)cacc[q];
           } else {
 #pragma unroll
             for (int d = 0; d < D; ++d) cpart[d] = (rt ? cpart[d] : 0.0) + (double)cacc[2 + d];
@@ -601,8 +599,6 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         double* o = red + ((long long)warp * SRT + lane + 32 * r) * KR;
         if (PASS == 1) {
           o[0] = rM[r];
-#pragma unroll
-          for (int d = 0; d < D; ++d) o[1 + d] = rG[r][d];
         } else {
 #pragma unroll
           for (int d = 0; d < D; ++d) o[d] = rG[r][d];
@@ -618,12 +614,8 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         v += red[(3 * SRT + rr) * KR + kk];
         double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;
         if (PASS == 1) {
-          if (kk == 0) {
-            o[0] = v;
-            o[1] = 0.0;
-          } else {
-            o[1 + kk] = v;
-          }
+          o[0] = v;
+          o[1] = 0.0;
         } else {
           o[kk] = v;
         }

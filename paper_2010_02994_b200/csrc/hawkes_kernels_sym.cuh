@@ -3,12 +3,13 @@
 // SURVEY.md §8(f) NEXT-1.  mu_ij = mu_ji, and for t_i < t_j only xi_ji is non-zero
 // (P:L98-99), so one evaluation of the two exps of an unordered pair {i, j} (i earlier)
 // serves both events:
-//   pass 1  row i: M += mu'                 G1_i += mu' dx            (xi_ij = 0)
-//           col j: M += mu', X += xi'       G1_j -= (mu' + xi') dx
-//   pass 2  row i: G2_i += rho'_j (mu' + xi') dx
-//           col j: G2_j -= rho'_i mu' dx
+//   pass 1  row i: M += mu'                 col j: M += mu', X += xi'   (rates only)
+//   pass 2  c = rho'_i mu' + rho'_j (mu' + xi'):   g_i += c dx,   g_j -= c dx
 // with dx = x_j - x_i and the scaled-domain terms of hawkes_kernels.cuh (mu' = alpha mu 2^64,
-// xi' = beta xi_ji 2^64).  Work items are chunk pairs (a, b), a <= b.  For a < b every event
+// xi' = beta xi_ji 2^64).  App. A's coefficient of the pair is the same for both events
+// ((mu_ij/lambda_i + mu_ji/lambda_j)/tau_x^2 + (xi_ij/lambda_i + xi_ji/lambda_j)/h^2 with
+// xi_ij = 0), so the whole gradient comes out of pass 2 and pass 1 computes the rates alone
+// (K1P = 2 partials per event: M', X').  Work items are chunk pairs (a, b), a <= b.  For a < b every event
 // of chunk a precedes every event of chunk b in the time-sorted catalog; a diagonal item
 // (a, a) visits only the upper triangle of its tile pairs and masks j <= i (by index, which
 // is time order) on the diagonal tiles.  An item writes the row partial of chunk a's events
@@ -29,6 +30,7 @@
 namespace hk {
 
 constexpr int SYM_RMAX = 4;               // largest rows-per-lane variant
+constexpr int K1P = 2;                    // pass-1 partials of the unordered-pair kernels: M', X' 
 // a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
 // treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
 constexpr double CULL_EXPONENT = -708.0;
@@ -65,9 +67,8 @@ struct SymRow {
 // one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
 template <int D, bool MASK, bool SELF, int TS>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
-                                          bool dead, double& rM, double (&rG)[D], double& cM,
-                                          double& cX, double (&cG)[D], const PassConst& c,
-                                          const int2* __restrict__ tab) {
+                                          bool dead, double& rM, double& cM, double& cX,
+                                          const PassConst& c, const int2* __restrict__ tab) {
   double dx[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) dx[d] = cx[d] - row.x[d];
@@ -85,12 +86,6 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   rM += eb;
   cM += eb;
   if (SELF) cX += es;
-  const double cc = SELF ? eb + es : eb;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    rG[d] = fma(eb, dx[d], rG[d]);
-    cG[d] = fma(-cc, dx[d], cG[d]);
-  }
 }
 
 template <int D, bool MASK, bool SELF, int TS>
@@ -112,11 +107,11 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
   }
-  const double cr = crho * (SELF ? eb + es : eb);
-  const double cc = row.rho * eb;
+  // the pair's App. A coefficient, the same for both events
+  const double cc = fma(row.rho, eb, crho * (SELF ? eb + es : eb));
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    rG[d] = fma(cr, dx[d], rG[d]);
+    rG[d] = fma(cc, dx[d], rG[d]);
     cG[d] = fma(-cc, dx[d], cG[d]);
   }
 }
@@ -185,7 +180,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
                                  (diag && cidx0 + src <= ridx0 + 32 * r));
       if (PASS == 1)
-        sym_pair1<D, MASK, SELF, TS>(row[r], cx, ct, dead, rM[r], rG[r], cacc[0], cacc[1], cG, c, tab);
+        sym_pair1<D, MASK, SELF, TS>(row[r], cx, ct, dead, rM[r], cacc[0], cacc[1], c, tab);
       else
         sym_pair2<D, MASK, SELF, TS>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
     }
@@ -197,8 +192,10 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       cacc[0] = shfl(cacc[0], nxt);
       cacc[1] = shfl(cacc[1], nxt);
     }
+    if (PASS == 2) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) cacc[2 + d] = shfl(cacc[2 + d], nxt);
+      for (int d = 0; d < D; ++d) cacc[2 + d] = shfl(cacc[2 + d], nxt);
+    }
   }
 }
 
@@ -220,8 +217,8 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
   constexpr int SYM_RT = 32 * SYM_R;
   using L = Layout<D>;
   constexpr int REC = L::REC;
-  constexpr int K = PASS == 1 ? L::K1 : L::K2;
-  constexpr int KR = PASS == 1 ? 1 + D : D;   // row sums reduced over warps: (M, G) or G
+  constexpr int K = PASS == 1 ? K1P : L::K2;
+  constexpr int KR = PASS == 1 ? 1 : D;       // row sums reduced over warps: M or G
   constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
   constexpr int TS = REPL ? TAB_COPIES : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -315,8 +312,8 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
 #pragma unroll
           for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.0;
         } else if (PASS == 1) {
-#pragma unroll
-          for (int q = 0; q < 2 + D; ++q) cacc[q] = cpart[q];
+          cacc[0] = cpart[0];
+          cacc[1] = cpart[1];
         } else {
           cacc[0] = cacc[1] = 0.0;
 #pragma unroll
@@ -351,8 +348,8 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {
-#pragma unroll
-            for (int q = 0; q < 2 + D; ++q) cpart[q] = cacc[q];
+            cpart[0] = cacc[0];
+            cpart[1] = cacc[1];
           } else {
 #pragma unroll
             for (int d = 0; d < D; ++d) cpart[d] = cacc[2 + d];
@@ -373,8 +370,6 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         double* o = red + ((long long)warp * SYM_RT + lane + 32 * r) * KR;
         if (PASS == 1) {
           o[0] = rM[r];
-#pragma unroll
-          for (int d = 0; d < D; ++d) o[1 + d] = rG[r][d];
         } else {
 #pragma unroll
           for (int d = 0; d < D; ++d) o[d] = rG[r][d];
@@ -390,12 +385,8 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         v += red[(3 * SYM_RT + rr) * KR + kk];
         double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;   // slot b
         if (PASS == 1) {
-          if (kk == 0) {
-            o[0] = v;      // M
-            o[1] = 0.0;    // X: xi_ij = 0 for a later j
-          } else {
-            o[1 + kk] = v; // G
-          }
+          o[0] = v;      // M
+          o[1] = 0.0;    // X: xi_ij = 0 for a later j
         } else {
           o[kk] = v;
         }

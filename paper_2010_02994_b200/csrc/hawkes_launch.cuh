@@ -12,7 +12,7 @@ size_t pass_smem() {
 
 template <int D, int PASS, int R, int V>
 size_t sym_smem() {
-  const int KR = PASS == 1 ? 1 + D : D;
+  const int KR = PASS == 1 ? 1 : D;
   const int copies = (V & 2) ? TAB_COPIES : 1;
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
          (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
@@ -48,11 +48,13 @@ struct SymOps {
   }
 };
 
-// default: pass 1 V = 6 (interleaved exp table copies + SoA columns), pass 2 V = 4 (SoA
-// columns): the copies cut pass 1's bank conflicts (2 copies of the 2048-entry table:
-// -1.6 %; 16 copies of the -DHK_EXP256 table: -3.4 %) but cost pass 2 an extra LOP3 per exp
-// (+2.3 %).  HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant for both passes (diagnostics,
-// A/B on one box; 2 and 6-for-pass-2 exist for D = 2 only)
+// default: V = 4 (SoA columns) in both passes.  The interleaved exp-table copies (V bit 2)
+// cut pass 1's bank conflicts while pass 1 also accumulated the row-local gradient (-1.6 %
+// with 2 copies of the 2048-entry table, -3.4 % with 16 copies of the -DHK_EXP256 table);
+// since pass 1 computes the rates alone (142 registers), the copies' index arithmetic costs
+// more than the conflicts (+3.3 %), as it always did in pass 2 (profiles/r01_sym_variants.txt).
+// HAWKES_SYM_V = 0 / 2 / 4 / 6 forces one variant for both passes (diagnostics, A/B on one
+// box; 2 and 6 exist for D = 2 only)
 static int sym_variant() {
   static int v = [] {
     const char* e = getenv("HAWKES_SYM_V");
@@ -75,13 +77,13 @@ int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
     if (v == 4) return sym_call_v<D, 4, 4>(ctx, pass, b);
     if (v == 6) return sym_call_v<D, 6, 6>(ctx, pass, b);
   }
-  return sym_call_v<D, 6, 4>(ctx, pass, b);
+  return sym_call_v<D, 4, 4>(ctx, pass, b);
 }
 
 constexpr int SYM32_R = 4;
 template <int D, int PASS>
 size_t sym32_smem() {
-  const int KR = PASS == 1 ? 1 + D : D;
+  const int KR = PASS == 1 ? 1 : D;
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t) +
          (size_t)4 * 32 * SYM32_R * KR * sizeof(double) +
          (size_t)4 * 32 * Layout32<D>::REC * sizeof(float);   // per-warp SoA column buffers
@@ -302,7 +304,9 @@ struct Fin1D {
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->multi;
     const bool final_here = all || !ctx->multi;   // else rho' is exchanged first
-    k_fin1<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
+    // PAIRS: (M', X') partials, gradient from pass 2 alone; ROWS: (M', X', G1') partials
+    auto fin = all ? k_fin1<D, K1P, false> : k_fin1<D, Layout<D>::K1, true>;
+    fin<<<nt, FIN_THREADS, 0, ctx->stream>>>(
         sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1, ctx->rl,
         ctx->rates, &ctx->d_consts->fc,
@@ -320,7 +324,8 @@ struct Fin2D {
     const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->multi;
-    k_fin2<D><<<nt, FIN_THREADS, 0, ctx->stream>>>(
+    auto fin = all ? k_fin2<D, false> : k_fin2<D, true>;
+    fin<<<nt, FIN_THREADS, 0, ctx->stream>>>(
         sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots,
         all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->G1, ctx->rl, ctx->grad);
     CHECK_LAUNCH();

@@ -120,7 +120,9 @@ struct DevConsts {
 
 // Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
 // lambda, rho' and ell_n.  rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda).
-template <int D>
+// K: partial stride (Layout<D>::K1 = (M', X', G1') for ROWS; 2 = (M', X') for PAIRS, whose
+// gradient comes out of pass 2 alone); HAS_G1: also sum and store the row-local G1'.
+template <int D, int K, bool HAS_G1>
 __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
                        const int* __restrict__ tiles, int N, const double* __restrict__ rec,
                        double* __restrict__ G1, double* __restrict__ rl,
@@ -134,11 +136,13 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
 #pragma unroll
   for (int d = 0; d < D; ++d) G[d] = 0.0;
   for (int c = 0; c < nchunks; ++c) {
-    const double* p = part + ((long long)c * npad + i) * L::K1;
+    const double* p = part + ((long long)c * npad + i) * K;
     M += p[0];
     X += p[1];
+    if (HAS_G1) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) G[d] += p[2 + d];
+      for (int d = 0; d < D; ++d) G[d] += p[2 + d];
+    }
   }
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
@@ -153,8 +157,10 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   const double qb = 0.5 * erfc(tn / f.tau_t * 0.70710678118654752440);
   const double Lam = f.mu0 * ((1.0 - qa) - qb) - f.theta * expm1(-f.omega * (f.tN - tn));
   const double ell = (Lp > 0.0) ? (log(Lp) + f.scale_log2 * LN2) - Lam : -INFINITY;
+  if (HAS_G1) {
 #pragma unroll
-  for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
+    for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
+  }
   rl[2 * (long long)i] = rho;
   rl[2 * (long long)i + 1] = ell;
   // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
@@ -383,7 +389,8 @@ __global__ void k_ell_reduce(const double* __restrict__ rl, int N, EvalStatus* s
   }
 }
 
-template <int D>
+// HAS_G1 (ROWS): g_i = rho'_i G1'_i + sum of the G2' partials; PAIRS: the partials alone
+template <int D, bool HAS_G1>
 __global__ void k_fin2(const double* __restrict__ part, long long npad, int nchunks,
                        const int* __restrict__ tiles, int N, const double* __restrict__ G1,
                        const double* __restrict__ rl, double* __restrict__ grad) {
@@ -398,9 +405,14 @@ __global__ void k_fin2(const double* __restrict__ part, long long npad, int nchu
 #pragma unroll
     for (int d = 0; d < D; ++d) G[d] += p[d];
   }
-  const double rho = rl[2 * (long long)i];
+  if (HAS_G1) {
+    const double rho = rl[2 * (long long)i];
 #pragma unroll
-  for (int d = 0; d < D; ++d) grad[(long long)i * D + d] = fma(rho, G1[(long long)i * D + d], G[d]);
+    for (int d = 0; d < D; ++d) grad[(long long)i * D + d] = fma(rho, G1[(long long)i * D + d], G[d]);
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) grad[(long long)i * D + d] = G[d];
+  }
 }
 
 // rows of this rank's tiles -> contiguous send buffer (tile-list order), K values per row
