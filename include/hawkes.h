@@ -18,7 +18,12 @@
  * (phi_D = D-variate standard normal density; the gradient's sigma_x is the paper's h;
  * see DESIGN.md "Readings").  One gradient evaluation is the two-pass computation of
  * Alg. 1/2: a rate pass producing lambda_n, then a gradient pass through
- * 1/lambda.  hawkes_leapfrog runs the HMC leapfrog integrator over X.
+ * 1/lambda.  Around it, the samplers that call it run on the device too: the HMC leapfrog
+ * (hawkes_leapfrog) and a whole HMC transition with Philox momenta and the Metropolis
+ * decision (hawkes_hmc_step) over X; block Metropolis-Hastings moves in O(kN)
+ * (hawkes_propose_move / hawkes_accept_move) and the paper's coarsened-location sampler as
+ * an on-device sweep (hawkes_set_regions / hawkes_mh_sweep); and the flu
+ * model's Bayesian MDS density (hawkes_set_bmds).
  *
  * Conventions (all functions):
  *  - Every function returns a hawkes_status; no C++ exception crosses this boundary.
@@ -43,7 +48,7 @@
 extern "C" {
 #endif
 
-#define HAWKES_ABI_VERSION 2
+#define HAWKES_ABI_VERSION 3   /* 3: HMC transition, coarsening regions + MH sweep, get_locations */
 
 typedef struct hawkes_ctx hawkes_ctx; /* opaque; owns all device memory */
 
