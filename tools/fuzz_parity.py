@@ -1,0 +1,77 @@
+"""Randomised parity fuzzing: random catalogs (N, D, parameters across their valid ranges,
+ties, clustered / spread locations, large coordinate offsets) and random decomposition,
+precision and emulated world, each against the oracle under the tolerance rule
+(tests/gpu_helpers.py).  Prints one JSON line per failure and a summary.
+
+    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--nmax 2500]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import traceback
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from tests.gpu_helpers import TOL, gpu_eval  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cases", type=int, default=200)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--nmax", type=int, default=2500)
+a = ap.parse_args()
+rng = np.random.default_rng(a.seed)
+fails = 0
+worst = {"fp64": 0.0, "fp32": 0.0}
+for case in range(a.cases):
+    N = int(rng.integers(2, a.nmax))
+    D = int(rng.integers(1, 9))
+    scale = float(10 ** rng.uniform(-2, 3))            # spatial units
+    tscale = float(10 ** rng.uniform(-1, 3))           # time units
+    if rng.uniform() < 0.5:                            # clustered
+        centres = rng.uniform(-scale, scale, size=(int(rng.integers(1, 20)), D))
+        x = centres[rng.integers(0, len(centres), N)] + rng.normal(0, 0.05 * scale, size=(N, D))
+    else:
+        x = rng.uniform(-scale, scale, size=(N, D))
+    x = x + float(10 ** rng.uniform(0, 4)) * (rng.uniform() < 0.3)   # offset (translation)
+    t = np.sort(rng.uniform(0, tscale, size=N))
+    if rng.uniform() < 0.3:                            # ties
+        t = np.floor(t / tscale * int(rng.integers(2, max(3, N // 3)))) * tscale / max(2, N // 3)
+        t = np.sort(t)
+    tau_x = float(scale * 10 ** rng.uniform(-1.5, 0))
+    h = float(tau_x * 10 ** rng.uniform(-1, 0))
+    tau_t = float(tscale * 10 ** rng.uniform(-2, 0))
+    omega = float(10 ** rng.uniform(-1, 1.5) / tau_t * 10)
+    th = (float(rng.uniform(0.05, 1.5)), tau_x, tau_t, float(rng.uniform(0.0, 1.5)), omega, h)
+    prec = "fp64" if rng.uniform() < 0.7 else "fp32"
+    alg = ["auto", "pairs", "rows"][int(rng.integers(0, 3))]
+    W = int(rng.choice([0, 0, 0, 2, 3]))
+    info = {"case": case, "N": N, "D": D, "prec": prec, "alg": alg, "W": W, "theta": th}
+    try:
+        ell_r, lam_r, _ = oracle.loglik(x, t, th)
+        if not np.isfinite(ell_r):
+            ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
+            if prec == "fp64" and np.isfinite(ell):
+                fails += 1
+                print(json.dumps({**info, "fail": "oracle -inf, gpu finite", "ell": ell}), flush=True)
+            continue
+        g_r, S = oracle.grad(x, t, th, lam=lam_r)
+        ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
+        if prec == "fp32" and not np.isfinite(ell):
+            continue                                   # fp32 range (reading R23)
+        tol, floor = TOL[prec]
+        e_ell = abs(ell - ell_r) / abs(ell_r)
+        bound = tol * np.maximum(np.abs(g_r), floor * S)
+        ratio = float(np.max(np.abs(g - g_r) / np.maximum(bound, 1e-300))) if g is not None else math.inf
+        worst[prec] = max(worst[prec], ratio)
+        if e_ell > tol or ratio > 1.0:
+            fails += 1
+            print(json.dumps({**info, "fail": "tolerance", "ell_rel": e_ell, "grad_ratio": ratio}), flush=True)
+    except Exception as e:  # noqa: BLE001
+        fails += 1
+        print(json.dumps({**info, "fail": "exception", "error": repr(e)[:300]}), flush=True)
+        traceback.print_exc()
+print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "worst_grad_ratio": worst}), flush=True)
