@@ -30,10 +30,11 @@ METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-
 # FP64-pipe work per ordered pair (DESIGN.md §4 "Roofline"; tools/falg_count.py):
 #   F_IMPL  the unordered-pair algorithm as implemented: FP64 instructions of the shipped
 #           sym_kernel's unmasked hot loop / 8 (one step = 4 unordered pairs) -- the
-#           algorithmic work of this design, excluding masked / padding pairs (headline)
+#           algorithmic work of this design, excluding masked / padding pairs (headline);
+#           the gradient pass's 8 I2F.F64 per step run on the conversion pipe, not counted
 #   F_UNO   SURVEY's method (naive per-pair bodies with libdevice exp) for unordered pairs
 #   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg
-F_IMPL = (12.5, 14.5)
+F_IMPL = (12.5, 13.5)
 F_UNO = (26.0, 28.5)
 F_SURVEY = (34.5, 49.0)
 FP64_LANES_PER_SM = 64

@@ -500,7 +500,7 @@ int hawkes_diag_fp64_mode(int32_t mode, int32_t warps_per_sm, double* iters_per_
   CU(cudaMalloc(&tab, sizeof h));
   CU(cudaMemcpy(tab, h, sizeof h, cudaMemcpyHostToDevice));
   const int threads = 128, blocks = sms * std::max(1, warps_per_sm / 4);
-  const int iters = mode == 4 ? 1 << 11 : 1 << 14;
+  const int iters = (mode == 4 || mode == 15) ? 1 << 11 : 1 << 14;
   k_diag_mode<<<blocks, threads>>>(out, 16, mode, tab);
   cudaEvent_t a, b;
   cudaEventCreate(&a);

@@ -97,15 +97,20 @@ constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707
 
 // STRIDE > 1: the table is stored interleaved in STRIDE copies (entry j of copy c at
 // j*STRIDE + c) and tab points at this thread's copy (see sym_kernel)
-template <int STRIDE = 1>
+template <int STRIDE = 1, bool KF_I2F = false>
 __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, int lane_off = 0) {
   static_assert(STRIDE == 1 || STRIDE == 2 || STRIDE == 4 || STRIDE == 16, "interleaved copies");
   const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
   const double ac = __hiloint2double((int)ahi, __double2loint(a));
   const double y = fma(ac, EXP_K, EXP_SHIFT);
-  const double kf = y - EXP_SHIFT;
-  const double r = fma(kf, -EXP_C, ac);
   const int k = __double2loint(y);
+  // k as a double: y - shift (FP64 pipe) or I2F.F64 (a quarter-rate conversion pipe beside
+  // it), both exact, so both forms give the same bits.  The conversion pays where the FP64
+  // pipe is the tighter limit: sym_kernel's gradient pass for D <= 5 (-1.4 % at D = 2,
+  // N = 100k; -0.5 to -2.8 % for D = 2..5), while pass 1 (+2.6 %) and the 255-register
+  // D >= 6 gradient passes (+0.4 to +2 %) lose more to its latency (profiles/r01_sym_variants.txt)
+  const double kf = KF_I2F ? __int2double_rn(k) : y - EXP_SHIFT;
+  const double r = fma(kf, -EXP_C, ac);
   int2 T;
   if constexpr (STRIDE == 1) {
     T = tab[k & (EXP_TABLE - 1)];

@@ -101,8 +101,8 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
-  double eb = fexp<TS>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
-  double es = SELF ? fexp<TS>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+  double eb = fexp<TS, (D <= 5)>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+  double es = SELF ? fexp<TS, (D <= 5)>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;

@@ -622,6 +622,36 @@ __global__ void k_diag_mode(double* out, int iters, int mode, const int2* __rest
     for (int k = 0; k < iters; ++k)
 #pragma unroll
       for (int q = 0; q < 8; ++q) a[q] = (q & 1) ? fma(a[q], one, b[q]) : fma(a[q], b[q], c);
+  } else if (mode == 13) {     // DFMA stream + an independent I2F.F64 per DFMA (pipe sharing)
+    int acc = threadIdx.x;
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        a[q] = fma(a[q], m, c);
+        acc ^= __double2loint(__int2double_rn(acc + q));
+      }
+    a[0] += acc;
+  } else if (mode == 14) {     // I2F.F64 stream alone
+    int acc = threadIdx.x;
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc ^= __double2loint(__int2double_rn(acc + q));
+    a[0] += acc;
+  } else if (mode == 15) {     // fast exp with kf = I2F(k) in place of y - shift
+    for (int k = 0; k < iters; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double x = -a[q] * 1e-3;
+        const unsigned ahi = min((unsigned)__double2hiint(x), EXP_AMIN_HI);
+        const double ac = __hiloint2double((int)ahi, __double2loint(x));
+        const double y = fma(ac, EXP_K, EXP_SHIFT);
+        const int kk = __double2loint(y);
+        const double r = fma(__int2double_rn(kk), -EXP_C, ac);
+        const int2 T = tab[kk & (EXP_TABLE - 1)];
+        const double p = fma(EXP_C2, r, 1.0) * r;
+        const double Tm = __hiloint2double(T.y + kk * (1 << EXP_BIAS_SHIFT), T.x);
+        a[q] = -fma(Tm, p, Tm);
+      }
   } else if (mode == 9) {      // one dependent DFMA chain per thread (latency probe)
     for (int k = 0; k < iters; ++k)
 #pragma unroll
