@@ -231,25 +231,28 @@ __global__ void __launch_bounds__(32 * BSYM_WARPS) k_bmds_sym(const double* __re
 }
 
 // every event's NB + 1 slots in index order (slots a < block(n) hold column roles, slots
-// b >= block(n) row roles, slot NB the diagonal task's column role)
+// b >= block(n) row roles, slot NB the diagonal task's column role).  One thread per
+// (event, component): consecutive threads read consecutive doubles of a slot (coalesced), and
+// each sum runs over the slots in the same order as one thread per event did (bitwise the
+// same result); at the flu size that is 33k independent sums instead of 4733 (ncu: the
+// per-event form took 88 us, long-scoreboard bound, next to the pair kernel's 154 us)
 template <int D>
 __global__ void k_bmds_sym_fin(const double* __restrict__ part, int N, double* __restrict__ grad,
                                double* __restrict__ row_value) {
   constexpr int K = D + 1;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)N * K) return;
+  const int n = (int)(q / K), k = (int)(q % K);
   const int NB = (N + 31) / 32;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  for (int sl = 0; sl <= NB; ++sl) {
-    const double* p = part + ((long long)sl * N + n) * K;
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] += p[k];
-  }
-#pragma unroll
-  for (int d = 0; d < D; ++d) grad[(long long)n * D + d] = acc[d];
-  row_value[n] = acc[D];
+  const long long stride = (long long)N * K;
+  const double* p = part + q;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int sl = 0; sl <= NB; ++sl) acc += __ldg(p + sl * stride);
+  if (k < D)
+    grad[(long long)n * D + k] = acc;
+  else
+    row_value[n] = acc;
 }
 
 // mirror the lower triangle into the upper one (device copy of Y), flag bad entries

@@ -304,14 +304,19 @@ struct Fin1D {
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->multi;
     const bool final_here = all || !ctx->multi;   // else rho' is exchanged first
-    // PAIRS: (M', X') partials, gradient from pass 2 alone; ROWS: (M', X', G1') partials
-    auto fin = all ? k_fin1<D, K1P, false> : k_fin1<D, Layout<D>::K1, true>;
-    fin<<<nt, FIN_THREADS, 0, ctx->stream>>>(
-        sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots,
-        all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1, ctx->rl,
-        ctx->rates, &ctx->d_consts->fc,
-        final_here && !ctx->rec32 ? ctx->rec + Layout<D>::RHO : nullptr,
-        final_here && ctx->rec32 ? ctx->rec32 + Layout32<D>::RHO : nullptr);
+    double* rr = final_here && !ctx->rec32 ? ctx->rec + Layout<D>::RHO : nullptr;
+    float* rr32 = final_here && ctx->rec32 ? ctx->rec32 + Layout32<D>::RHO : nullptr;
+    if (all) {   // PAIRS: (M', X') partials, gradient from pass 2 alone
+      static_assert(K1P == 2, "k_fin1p pairs (M', X') lanes");
+      const long long n = 2 * ctx->N;
+      k_fin1p<D><<<(unsigned)((n + FINP_THREADS - 1) / FINP_THREADS), FINP_THREADS, 0, ctx->stream>>>(
+          sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
+          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32);
+    } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
+      k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
+          ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,
+          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32);
+    }
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -324,10 +329,15 @@ struct Fin2D {
     const int nt = all ? ctx->ntiles : (int)ctx->tiles_of[rank].size();
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->multi;
-    auto fin = all ? k_fin2<D, false> : k_fin2<D, true>;
-    fin<<<nt, FIN_THREADS, 0, ctx->stream>>>(
-        sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots,
-        all ? ctx->d_every_tile : ctx->d_tiles[rank], (int)ctx->N, ctx->G1, ctx->rl, ctx->grad);
+    if (all) {
+      const long long n = ctx->N * D;
+      k_fin2p<D><<<(unsigned)((n + FINP_THREADS - 1) / FINP_THREADS), FINP_THREADS, 0, ctx->stream>>>(
+          sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->grad);
+    } else {
+      k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,
+                                                           ctx->d_tiles[rank], (int)ctx->N, ctx->G1,
+                                                           ctx->rl, ctx->grad);
+    }
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -497,7 +507,7 @@ struct BmdsD {
       const int grid = (int)std::max(1LL, std::min<long long>((long long)std::max(1, per_sm) * ctx->sms, want));
       kern<<<grid, 32 * BSYM_WARPS, smem, ctx->stream>>>(x, ctx->d_Y, N, ctx->bc, ctx->tab, ctx->d_bpart, ntasks);
       CHECK_LAUNCH();
-      k_bmds_sym_fin<D><<<(N + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_bpart, N, ctx->d_bgrad, ctx->d_brow);
+      k_bmds_sym_fin<D><<<(unsigned)(((long long)N * (D + 1) + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_bpart, N, ctx->d_bgrad, ctx->d_brow);
       CHECK_LAUNCH();
     } else {
       k_bmds<D><<<(unsigned)ctx->N, BMDS_THREADS, 0, ctx->stream>>>(x, ctx->d_Y, (int)ctx->N, ctx->bc,

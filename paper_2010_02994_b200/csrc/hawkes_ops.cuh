@@ -118,32 +118,14 @@ struct DevConsts {
   FinConst fc;
 };
 
-// Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
-// lambda, rho' and ell_n.  rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda).
-// K: partial stride (Layout<D>::K1 = (M', X', G1') for ROWS; 2 = (M', X') for PAIRS, whose
-// gradient comes out of pass 2 alone); HAS_G1: also sum and store the row-local G1'.
-template <int D, int K, bool HAS_G1>
-__global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
-                       const int* __restrict__ tiles, int N, const double* __restrict__ rec,
-                       double* __restrict__ G1, double* __restrict__ rl,
-                       double* __restrict__ rates, const FinConst* __restrict__ fcp,
-                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho) {
+// lambda, rho' and ell_n of event i from its summed pass-1 partials (M', X'), then the
+// stores: rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda); rho' into the records
+template <int D>
+__device__ __forceinline__ void fin1_event(int i, double M, double X, const double* __restrict__ rec,
+                                           double* __restrict__ rl, double* __restrict__ rates,
+                                           const FinConst& f, double* __restrict__ rec_rho,
+                                           float* __restrict__ rec32_rho) {
   using L = Layout<D>;
-  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
-  if (i >= N) return;
-  const FinConst f = *fcp;
-  double M = 0.0, X = 0.0, G[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) G[d] = 0.0;
-  for (int c = 0; c < nchunks; ++c) {
-    const double* p = part + ((long long)c * npad + i) * K;
-    M += p[0];
-    X += p[1];
-    if (HAS_G1) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) G[d] += p[2 + d];
-    }
-  }
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
   const double Lp = (mu_s + xi_s > f.zero_floor) ? mu_s + xi_s : 0.0;
@@ -157,10 +139,6 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   const double qb = 0.5 * erfc(tn / f.tau_t * 0.70710678118654752440);
   const double Lam = f.mu0 * ((1.0 - qa) - qb) - f.theta * expm1(-f.omega * (f.tN - tn));
   const double ell = (Lp > 0.0) ? (log(Lp) + f.scale_log2 * LN2) - Lam : -INFINITY;
-  if (HAS_G1) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
-  }
   rl[2 * (long long)i] = rho;
   rl[2 * (long long)i + 1] = ell;
   // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
@@ -170,6 +148,78 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   rates[4 * (long long)i + 1] = mu_s * sc;
   rates[4 * (long long)i + 2] = xi_s * sc;
   rates[4 * (long long)i + 3] = Lam;
+}
+
+// Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
+// fin1_event.  K: partial stride (Layout<D>::K1 = (M', X', G1') for ROWS; 2 = (M', X') for
+// PAIRS, whose gradient comes out of pass 2 alone); HAS_G1: also sum and store the row-local G1'.
+template <int D, int K, bool HAS_G1>
+__global__ void k_fin1(const double* __restrict__ part, long long npad, int nchunks,
+                       const int* __restrict__ tiles, int N, const double* __restrict__ rec,
+                       double* __restrict__ G1, double* __restrict__ rl,
+                       double* __restrict__ rates, const FinConst* __restrict__ fcp,
+                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho) {
+  const int i = tiles[blockIdx.x] * RT + threadIdx.x;
+  if (i >= N) return;
+  double M = 0.0, X = 0.0, G[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) G[d] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* p = part + ((long long)c * npad + i) * K;
+    M += p[0];
+    X += p[1];
+    if (HAS_G1) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) G[d] += p[2 + d];
+    }
+  }
+  if (HAS_G1) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
+  }
+  fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+}
+
+// PAIRS finalizes (every event final on this process): one thread per (event, component),
+// so a warp's loads of one slot are contiguous and 2 (pass 1) / D (pass 2) times as many
+// independent slot sums run as with one thread per event; each component is still summed
+// over the slots in index order (the same bits as k_fin1 / k_fin2).  At N = 5000 the
+// per-event forms took 15 / 12 us next to 37 / 43 us of pair kernels (latency-bound: one
+// warp per SM walking 41 slots).
+constexpr int FINP_THREADS = 128;
+template <int D>
+__global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
+                                                        int nslots, int N, const double* __restrict__ rec,
+                                                        double* __restrict__ rl, double* __restrict__ rates,
+                                                        const FinConst* __restrict__ fcp,
+                                                        double* __restrict__ rec_rho,
+                                                        float* __restrict__ rec32_rho) {
+  const long long q = (long long)blockIdx.x * FINP_THREADS + threadIdx.x;   // (event, M' or X')
+  const int i = (int)(q >> 1);
+  double acc = 0.0;
+  if (i < N) {
+    const double* p = part + q;   // part[(c npad + i) K1P + k], K1P = 2
+    const long long stride = npad * 2;
+#pragma unroll 8
+    for (int c = 0; c < nslots; ++c) acc += p[c * stride];
+  }
+  const double X = __shfl_down_sync(0xffffffffu, acc, 1);
+  if (i < N && (threadIdx.x & 1) == 0) fin1_event<D>(i, acc, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+}
+
+template <int D>
+__global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, long long npad,
+                                                        int nslots, int N, double* __restrict__ grad) {
+  constexpr int K = Layout<D>::K2;
+  const long long q = (long long)blockIdx.x * FINP_THREADS + threadIdx.x;   // (event, d)
+  if (q >= (long long)N * D) return;
+  const int i = (int)(q / D), d = (int)(q % D);
+  const double* p = part + (long long)i * K + d;
+  const long long stride = npad * K;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < nslots; ++c) acc += p[c * stride];
+  grad[q] = acc;
 }
 
 template <int D>
