@@ -124,7 +124,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->grad, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
       (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W)) ||
-      (rc = dalloc(ctx, &ctx->tab, EXP_TABLE)) || (rc = dalloc(ctx, &ctx->bad, 1)) ||
+      (rc = dalloc(ctx, &ctx->tab, EXP_TABLE)) ||
       (rc = dalloc(ctx, &ctx->st, 1)) || (rc = dalloc(ctx, &ctx->d_consts, 1)) ||
       (rc = dalloc(ctx, &ctx->d_slot_of, (size_t)N)) || (rc = dalloc(ctx, &ctx->d_move_idx, MOVE_MAX)) ||
       (rc = dalloc(ctx, &ctx->d_move_x, (size_t)MOVE_MAX * D)) ||
@@ -136,10 +136,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   if (!ctx->multi && !getenv("HAWKES_NO_GRAPHS")) {
-    if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess)
-      return fail(set_err(ctx, HAWKES_ERR_CUDA, "stream/event creation failed"));
+    if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "stream creation failed"));
     ctx->graphs = true;
   }
   if (o.precision == HAWKES_FP32) {
@@ -212,8 +210,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     if (cudaMemcpy(ctx->tab, h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of exp table failed"));
   }
-  if (cudaMemset(ctx->bad, 0, sizeof(int)) != cudaSuccess ||
-      cudaMemset(ctx->st, 0, sizeof(EvalStatus)) != cudaSuccess ||
+  ctx->bad = &ctx->st->nonfinite;
+  if (cudaMemset(ctx->st, 0, sizeof(EvalStatus)) != cudaSuccess ||
       cudaMemset(ctx->rec, 0, (size_t)ctx->npad * REC * sizeof(double)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   if ((rc = dispatchD<SetupD>(D, ctx))) return fail(rc);
@@ -246,8 +244,6 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamSynchronize(ctx->mh_stream);
     cudaStreamDestroy(ctx->mh_stream);
   }
-  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
-  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   if (ctx->gstream) {
     cudaStreamSynchronize(ctx->gstream);
     cudaStreamDestroy(ctx->gstream);
@@ -255,7 +251,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
-                  ctx->bad, ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
+                  ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -316,8 +312,12 @@ int hawkes_set_locations(hawkes_ctx* ctx, const double* x, int32_t mem) {
       if (!finite_bounded(x[k]))
         return set_err(ctx, HAWKES_ERR_NONFINITE, "x[%zu] = %g is not finite (or |x| > 1e100)", k, x[k]);
   }
-  TRY(copy_in(ctx, ctx->xstage, x, n, mem));
-  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
+  if (mem == HAWKES_MEM_DEVICE) {   // pack straight from the caller's array (stream-ordered)
+    TRY(dispatchD<PackXD>(ctx->D, ctx, x, ctx->xstage));
+  } else {
+    TRY(copy_in(ctx, ctx->xstage, x, n, mem));
+    TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
+  }
   ctx->have_x = true;
   ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
   TRY(clear_move(ctx));

@@ -121,7 +121,7 @@ struct hawkes_ctx {
   double* recvbuf = nullptr;
   int* counters = nullptr; // 4 per logical rank
   int2* tab = nullptr;     // exp table
-  int* bad = nullptr;      // device-side input validation flag
+  int* bad = nullptr;      // device-side input validation flag: &st->nonfinite
   EvalStatus* st = nullptr;
   EvalStatus* h_st = nullptr;  // pinned
   // leapfrog state
@@ -151,7 +151,6 @@ struct hawkes_ctx {
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};   // rates, rates+grad, grad only
   bool graphs = false;
   bool capturing = false;

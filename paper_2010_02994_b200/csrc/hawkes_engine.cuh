@@ -123,11 +123,9 @@ int capture(hawkes_ctx* ctx, int which) {
 
 int replay(hawkes_ctx* ctx, int which) {
   if (!ctx->gexec[which]) TRY(capture(ctx, which));
-  CU(cudaEventRecord(ctx->ev_in, ctx->stream));
-  CU(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
-  CU(cudaGraphLaunch(ctx->gexec[which], ctx->gstream));
-  CU(cudaEventRecord(ctx->ev_out, ctx->gstream));
-  CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_out, 0));
+  // captured on the private stream (capture cannot run on the legacy default stream), launched
+  // into the caller's stream: stream order alone sequences it
+  CU(cudaGraphLaunch(ctx->gexec[which], ctx->stream));
   ctx->launches += ctx->graph_launches[which];
   return HAWKES_OK;
 }
@@ -192,10 +190,9 @@ int run_grad(hawkes_ctx* ctx) {
 }
 
 int fetch_status(hawkes_ctx* ctx) {
+  // (ctx->bad is st->nonfinite: one copy brings the flags and the results)
   CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
   int bad = 0;
-  CU(cudaMemcpyAsync(&ctx->h_st->nonfinite, ctx->bad, sizeof(int), cudaMemcpyDeviceToHost,
-                     ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   bad = ctx->h_st->nonfinite;
   if (bad) {

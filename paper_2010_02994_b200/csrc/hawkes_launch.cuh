@@ -355,9 +355,9 @@ struct RhoD {
 
 template <int D>
 struct PackXD {
-  static int run(hawkes_ctx* ctx, const double* xdev) {
+  static int run(hawkes_ctx* ctx, const double* xdev, double* xcopy = nullptr) {
     k_pack_x<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec, xdev, (int)ctx->N,
-                                                                  ctx->npad, ctx->bad);
+                                                                  ctx->npad, ctx->bad, xcopy);
     CHECK_LAUNCH();
     if (ctx->rec32) {
       k_pack_x32<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec32, xdev,

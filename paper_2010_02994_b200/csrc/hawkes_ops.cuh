@@ -22,9 +22,11 @@ constexpr int FIN_THREADS = RT;              // finalize: one thread per row of 
 constexpr double LN2 = 0.693147180559945309417232121458;
 
 // --------------------------------------------------------------------- O(N) kernels
+// xcopy (optional): also keep the locations in the context's N x D copy (device input to
+// set_locations: one pass over the user's array instead of a copy and a pass)
 template <int D>
 __global__ void k_pack_x(double* __restrict__ rec, const double* __restrict__ x, int N, int npad,
-                         int* __restrict__ bad) {
+                         int* __restrict__ bad, double* __restrict__ xcopy) {
   using L = Layout<D>;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npad) return;
@@ -34,6 +36,7 @@ __global__ void k_pack_x(double* __restrict__ rec, const double* __restrict__ x,
     const double v = x[(long long)src * D + d];
     if (!(fabs(v) <= 1e100)) atomicOr(bad, 1);
     rec[(long long)i * L::REC + d] = v;
+    if (xcopy && i < N) xcopy[(long long)i * D + d] = v;
   }
 }
 
