@@ -396,19 +396,25 @@ struct MoveD {
     a.N = (int)ctx->N;
     a.c = ctx->pc;
     a.tab = ctx->tab;
-    // one launch for the rows outside S and the moved rows, one for the terms and their
-    // fixed-order sum (decide: the MH sweep's Metropolis decision in the same kernel)
+    a.rates = ctx->rates;
+    a.tx2 = ctx->fc.tx2;
+    a.h2 = ctx->fc.h2;
+    a.floor_ = ctx->fc.zero_floor;
+    a.part = ctx->d_move_part;
+    // one launch for the rows outside S (with their Delta-ell terms) and the moved rows, one
+    // CTA for the moved events' terms and the fixed-order sum (decide: the MH sweep's
+    // Metropolis decision in the same kernel)
     const int nb = (int)((ctx->N + 255) / 256);
     const int len = move_split_len((int)ctx->N);
     const int nsplit = (int)((ctx->N + len - 1) / len);
     k_move_delta_rows<D><<<(unsigned)(nb + k * nsplit), 256, move_smem_bytes<D>(k), ctx->stream>>>(
         a, ctx->tab, ctx->d_move_delta, ctx->d_move_rows_part, nb, nsplit);
     CHECK_LAUNCH();
-    k_move_terms_final<<<nb, 256, 0, ctx->stream>>>(ctx->rates, ctx->d_move_delta, ctx->d_move_rows_part,
-                                                    nsplit, ctx->d_slot_of, (int)ctx->N, ctx->fc.tx2,
-                                                    ctx->fc.h2, ctx->fc.zero_floor, ctx->d_move_part,
-                                                    ctx->d_move_rows, ctx->st, decide, ctx->d_mh_acc,
-                                                    ctx->d_mh_la);
+    k_move_terms_final<<<1, MOVE_FINAL_THREADS, 0, ctx->stream>>>(ctx->rates, ctx->d_move_rows_part, nsplit,
+                                                   ctx->d_move_idx, k, ctx->d_move_part, nb,
+                                                   ctx->fc.tx2, ctx->fc.h2, ctx->fc.zero_floor,
+                                                   ctx->d_move_rows, ctx->st, decide, ctx->d_mh_acc,
+                                                   ctx->d_mh_la);
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -461,7 +467,6 @@ struct MhCoopD {
     a.delta = ctx->d_move_delta;
     a.rows_part = ctx->d_move_rows_part;
     a.part = ctx->d_move_part;
-    a.rows = ctx->d_move_rows;
     a.stamp = ctx->d_mh_stamp;
     a.gtab = ctx->tab;
     a.c = ctx->pc;

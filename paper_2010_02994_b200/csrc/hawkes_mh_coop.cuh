@@ -4,19 +4,21 @@
 // The launch-based sweep (hawkes_mh.cuh + hawkes_moves.cuh, replayed as a CUDA graph) pays
 // four dependent kernel launches per block; at the paper's catalog sizes (N = 2925 / 3982)
 // the pair work of a block is ~1 us and the launches dominate.  Here one grid of
-// co-resident CTAs (cudaLaunchCooperativeKernel) walks all blocks with three grid-wide
+// co-resident CTAs (cudaLaunchCooperativeKernel) walks all blocks with two grid-wide
 // barriers per block:
 //   A  every CTA draws the block's k proposals itself (same Philox stream, same values),
 //      keeps them in shared memory and stamps the events' slots as (block << 8) | slot in a
 //      global map -- identical concurrent writes, and no clearing between blocks, so no
 //      barrier is needed before phase B
-//   B  rows outside S (the k moved events' pair changes) and the moved rows at X',
-//      grid-stride over the same work units as k_move_delta_rows          | grid.sync
-//   C  per-event terms log(lambda'/lambda) and their 256-event tree sums   | grid.sync
-//   D  every CTA sums the terms in the same fixed order, takes the Metropolis decision
-//      (identical everywhere), and commits its share of the rates / records | grid.sync
-// Arithmetic and reduction orders are those of the launch-based path (tests check the two
-// agree bitwise).
+//   B  rows outside S (the k moved events' pair changes, their Delta-ell terms and the
+//      terms' 256-event tree sums) and the moved rows at X', grid-stride over the same work
+//      units as k_move_delta_rows                                          | grid.sync
+//   D  every CTA forms the moved events' terms, sums everything in the same fixed order,
+//      takes the Metropolis decision (identical everywhere), and commits its share of the
+//      rates / records                                                     | grid.sync
+// (A third barrier, for the per-event terms as a phase of their own, cost 2.5-3 us per block.)
+// Arithmetic and reduction orders are those of the launch-based path (hawkes_moves.cuh;
+// tests check the two agree bitwise).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -39,7 +41,6 @@ struct MhCoopArgs {
   double* delta;           // Npad x 2
   double* rows_part;       // k x nsplit x 2
   double* part;            // ceil(N/256) term sums
-  double* rows;            // k x 2 combined moved rows
   int* stamp;              // N: (block << 8) | slot of the events moved so far, -1 initially
   const int2* gtab;
   PassConst c;
@@ -64,7 +65,7 @@ struct StampSlots {
 template <int D>
 __host__ __device__ constexpr size_t mh_coop_smem(int k) {
   return (size_t)EXP_TABLE * sizeof(int2) + (size_t)k * (2 * D + 1) * sizeof(double) +
-         512 * sizeof(double) + (size_t)2 * k * sizeof(int);
+         512 * sizeof(double) + (size_t)4 * k * sizeof(double) + (size_t)2 * k * sizeof(int);
 }
 
 template <int D>
@@ -79,7 +80,10 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
   double* sx_new = sx_old + k * D;                               // [k][D]
   double* stt = sx_new + k * D;                                  // [k] times
   double* red = stt + k;                                         // [512] reductions
-  int* sraw = reinterpret_cast<int*>(red + 512);                 // [k] event of slot q
+  double* srow = red + 512;                                      // [k][2] moved rows (M', X')
+  double* sterm = srow + 2 * k;                                  // [k] moved events' terms
+  double* sL0 = sterm + k;                                       // [k] their Lambda' before
+  int* sraw = reinterpret_cast<int*>(sL0 + k);                   // [k] event of slot q
   int* sg = sraw + k;                                            // [k] tie group of slot q
   __shared__ int s_acc;
   __shared__ double s_hast;
@@ -108,6 +112,9 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
       }
       stt[tid] = rn[D];
       sg[tid] = a.gid[n];
+      // read before any CTA's phase-D commit can rewrite it (written by another CTA's commit
+      // of an earlier block: bypass L1)
+      sL0[tid] = __ldcg(a.rates + 4 * (long long)n) * S;
     }
     red[tid] = logh;
     __syncthreads();
@@ -123,6 +130,7 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
     for (int u = blockIdx.x; u < nb + k * nsplit; u += gridDim.x) {
       if (u < nb) {
         const int n = u * 256 + tid;
+        double term = 0.0;
         if (n < N) {
           double dM = 0.0, dX = 0.0;
           if (slots(n) < 0) {
@@ -139,10 +147,14 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
               dM += eb1 - eb0;
               dX += es1 - es0;
             }
+            term = move_term_out(a.rates[4 * (long long)n] * S, dM, dX, a.tx2, a.h2, a.floor_);
           }
           a.delta[2 * (long long)n] = dM;
           a.delta[2 * (long long)n + 1] = dX;
         }
+        tree256(term, red);
+        if (tid == 0) a.part[u] = red[0];
+        __syncthreads();
       } else {
         const int q = (u - nb) / nsplit, split = (u - nb) % nsplit;
         double xn[D];
@@ -181,50 +193,22 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
     }
     grid.sync();
 
-    // ---- C: per-event terms log(lambda'/lambda), 256-event tree sums
-    for (int cb = blockIdx.x; cb < nb; cb += gridDim.x) {
-      const int n = cb * 256 + tid;
-      double term = 0.0;
-      if (n < N) {
-        const double L0 = a.rates[4 * (long long)n] * S;
-        const int q = slots(n);
-        if (q < 0) {
-          const double d = fma(a.delta[2 * (long long)n], a.tx2, a.delta[2 * (long long)n + 1] * a.h2);
-          term = (d == 0.0) ? 0.0 : ((L0 + d > a.floor_) ? log1p(d / L0) : -INFINITY);
-        } else {
-          double M = 0.0, X = 0.0;
-          for (int s = 0; s < nsplit; ++s) {
-            M += a.rows_part[2 * ((long long)q * nsplit + s)];
-            X += a.rows_part[2 * ((long long)q * nsplit + s) + 1];
-          }
-          a.rows[2 * q] = M;
-          a.rows[2 * q + 1] = X;
-          const double L1 = fma(M, a.tx2, X * a.h2);
-          term = ((L1 > a.floor_) ? log(L1) : -INFINITY) - log(L0);
-        }
+    // ---- D: the moved events' terms, the sum in the fixed order, the decision, the commit
+    for (int q = tid >> 5; q < k; q += 8) {   // one warp per moved event
+      double M, X;
+      const double t = move_term_in(sL0[q], a.rows_part, q, nsplit, a.tx2, a.h2, a.floor_, M, X);
+      if ((tid & 31) == 0) {
+        sterm[q] = t;
+        srow[2 * q] = M;
+        srow[2 * q + 1] = X;
       }
-      red[tid] = term;
-      __syncthreads();
-      for (int w = 128; w > 0; w >>= 1) {
-        if (tid < w) red[tid] += red[tid + w];
-        __syncthreads();
-      }
-      if (tid == 0) a.part[cb] = red[0];
-      __syncthreads();
     }
-    grid.sync();
-
-    // ---- D: the sum of the terms in a fixed order, the decision, the commit
     double v = 0.0;
     for (int i = tid; i < nb; i += 256) v += __ldcg(a.part + i);
-    red[tid] = v;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
-    }
+    tree256(v, red);
     if (tid == 0) {
-      const double dl = red[0];
+      double dl = red[0];
+      for (int q = 0; q < k; ++q) dl += sterm[q];
       const double la = (dl > -INFINITY) ? dl + s_hast : -INFINITY;   // NaN -> -inf
       const double u = mh_uniforms(key, it, (unsigned)b, MH_ACCEPT_TAG).x;
       const int acc = log(u) < la ? 1 : 0;
@@ -249,9 +233,9 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
           a.rates[4 * (long long)n] = __dadd_rn(a.rates[4 * (long long)n],
               __dmul_rn(fma(a.delta[2 * (long long)n], a.tx2, a.delta[2 * (long long)n + 1] * a.h2), S1));
         } else {
-          mu = __dmul_rn(__dmul_rn(a.rows[2 * q], a.tx2), S1);
-          xi = __dmul_rn(__dmul_rn(a.rows[2 * q + 1], a.h2), S1);
-          a.rates[4 * (long long)n] = __dmul_rn(fma(a.rows[2 * q], a.tx2, a.rows[2 * q + 1] * a.h2), S1);
+          mu = __dmul_rn(__dmul_rn(srow[2 * q], a.tx2), S1);
+          xi = __dmul_rn(__dmul_rn(srow[2 * q + 1], a.h2), S1);
+          a.rates[4 * (long long)n] = __dmul_rn(fma(srow[2 * q], a.tx2, srow[2 * q + 1] * a.h2), S1);
         }
         a.rates[4 * (long long)n + 1] = mu;
         a.rates[4 * (long long)n + 2] = xi;

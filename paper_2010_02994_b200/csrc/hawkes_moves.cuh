@@ -9,6 +9,11 @@
 //   Delta ell = sum_n log(lambda_n' / lambda_n)              (Eq. 1)
 // so a proposal costs O(k N) instead of the O(N^2) of a fresh evaluation.  Pair terms use
 // the same scaled-domain exps as the pass kernels (alpha mu 2^64, beta xi 2^64).
+// Summation order of Delta ell (shared by the launch path and the cooperative sweep, which
+// tests compare bitwise): the terms of the events outside S in fixed 256-event trees (the
+// moved events contribute 0 there), the tree sums over the 256-event blocks in a fixed
+// tree, then the k moved events' terms added one by one in slot order.  The events outside
+// S get their terms in the same pass that computes their rate changes.
 #pragma once
 #include "hawkes_kernels.cuh"
 
@@ -26,7 +31,50 @@ struct MoveArgs {
   int k, N;
   PassConst c;
   const int2* tab;
+  const double* rates;     // N x 4 (lambda, mu, xi, Lambda) at the current state
+  double tx2, h2, floor_;  // Lambda' = M' tau_x^2 + X' h^2; at or below floor_: lambda = 0
+  double* part;            // ceil(N/256): tree sums of the outside-S terms
 };
+
+// Delta-ell term of an event outside S from its rate changes (scaled units, L0 = Lambda')
+__device__ __forceinline__ double move_term_out(double L0, double dM, double dX, double tx2, double h2,
+                                                double floor_) {
+  const double d = fma(dM, tx2, dX * h2);
+  return (d == 0.0) ? 0.0 : ((L0 + d > floor_) ? log1p(d / L0) : -INFINITY);
+}
+
+// term of a moved event from its full row at X', by one warp: lane l sums the split ranges
+// l, l + 32, ... in order, a shuffle-down tree combines the lanes (a fixed order); M', X'
+// and the term are valid in lane 0.  (One thread walking the up to 64 ranges put a chain of
+// dependent L2 loads on the MH sweep's critical path.)
+__device__ __forceinline__ double move_term_in(double L0, const double* __restrict__ rows_part, int q,
+                                               int nsplit, double tx2, double h2, double floor_,
+                                               double& M, double& X) {
+  const int lane = threadIdx.x & 31;
+  M = 0.0;
+  X = 0.0;
+  for (int s = lane; s < nsplit; s += 32) {
+    M += __ldcg(rows_part + 2 * ((long long)q * nsplit + s));
+    X += __ldcg(rows_part + 2 * ((long long)q * nsplit + s) + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    M += __shfl_down_sync(0xffffffffu, M, o);
+    X += __shfl_down_sync(0xffffffffu, X, o);
+  }
+  const double L1 = fma(M, tx2, X * h2);
+  return ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
+}
+
+// fixed tree over a 256-thread CTA (red: 256 doubles of shared memory); result in red[0]
+__device__ __forceinline__ void tree256(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+}
 
 // pair term parts (scaled) for event n at xn against event m at xm, times/ties from records
 template <int D>
@@ -44,12 +92,14 @@ __device__ __forceinline__ void move_pair(const double* xn, double tn, int gn, c
   es = gm < gn ? fexp(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab) : 0.0;
 }
 
-// rows not in S: (delta M', delta X') from the k moved events (CTA blk of the delta role)
+// rows not in S: (delta M', delta X') from the k moved events and their Delta-ell terms,
+// tree-summed over the CTA's 256 events into part[blk] (CTA blk of the delta role)
 template <int D>
 __device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2* __restrict__ tab,
                                                 double* __restrict__ dout, int blk, double* dyn) {
   using L = Layout<D>;
-  double* sx_old = dyn;                       // [k][D]
+  double* red = dyn;                          // [256]
+  double* sx_old = dyn + 256;                 // [k][D]
   double* sx_new = sx_old + a.k * D;          // [k][D]
   double* st = sx_new + a.k * D;              // [k]
   int* sg = reinterpret_cast<int*>(st + a.k); // [k]
@@ -66,25 +116,31 @@ __device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2
   }
   __syncthreads();
   const int n = blk * blockDim.x + threadIdx.x;
-  if (n >= a.N) return;
-  double dM = 0.0, dX = 0.0;
-  if (a.slot_of[n] < 0) {
-    const double* rn = a.rec + (long long)n * L::REC;
-    double xn[D];
+  double term = 0.0;
+  if (n < a.N) {
+    double dM = 0.0, dX = 0.0;
+    if (a.slot_of[n] < 0) {
+      const double* rn = a.rec + (long long)n * L::REC;
+      double xn[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) xn[d] = rn[d];
-    const double tn = rn[D];
-    const int gn = a.gid[n];
-    for (int q = 0; q < a.k; ++q) {
-      double eb0, es0, eb1, es1;
-      move_pair<D>(xn, tn, gn, sx_old + q * D, st[q], sg[q], a.c, tab, eb0, es0);
-      move_pair<D>(xn, tn, gn, sx_new + q * D, st[q], sg[q], a.c, tab, eb1, es1);
-      dM += eb1 - eb0;
-      dX += es1 - es0;
+      for (int d = 0; d < D; ++d) xn[d] = rn[d];
+      const double tn = rn[D];
+      const int gn = a.gid[n];
+      for (int q = 0; q < a.k; ++q) {
+        double eb0, es0, eb1, es1;
+        move_pair<D>(xn, tn, gn, sx_old + q * D, st[q], sg[q], a.c, tab, eb0, es0);
+        move_pair<D>(xn, tn, gn, sx_new + q * D, st[q], sg[q], a.c, tab, eb1, es1);
+        dM += eb1 - eb0;
+        dX += es1 - es0;
+      }
+      term = move_term_out(a.rates[4 * (long long)n] * 18446744073709551616.0, dM, dX, a.tx2,
+                           a.h2, a.floor_);
     }
+    dout[2 * (long long)n] = dM;
+    dout[2 * (long long)n + 1] = dX;
   }
-  dout[2 * (long long)n] = dM;
-  dout[2 * (long long)n + 1] = dX;
+  tree256(term, red);
+  if (threadIdx.x == 0) a.part[blk] = red[0];
 }
 
 // rows in S: full (M', X') at the proposed configuration.  Block (q, s) sums the j range
@@ -147,8 +203,8 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
 template <int D>
 __host__ __device__ constexpr size_t move_smem_bytes(int k) {
   return (size_t)EXP_TABLE * sizeof(int2) +
-         ((size_t)k * (2 * D + 1) * sizeof(double) + (size_t)k * sizeof(int) > 512 * sizeof(double)
-              ? (size_t)k * (2 * D + 1) * sizeof(double) + (size_t)k * sizeof(int)
+         ((size_t)(256 + k * (2 * D + 1)) * sizeof(double) + (size_t)k * sizeof(int) > 512 * sizeof(double)
+              ? (size_t)(256 + k * (2 * D + 1)) * sizeof(double) + (size_t)k * sizeof(int)
               : 512 * sizeof(double));
 }
 

@@ -9,6 +9,7 @@
 
 #include "hawkes_kernels.cuh"
 #include "hawkes_kernels_f32.cuh"
+#include "hawkes_moves.cuh"
 
 namespace hk {
 
@@ -279,17 +280,16 @@ struct EvalStatus {
   int mh_block;         // next block of the sweep
   int mh_cur;           // block being processed
   int mh_prevk;         // proposal slots of the previous block still set (cleared by propose)
-  unsigned mh_ticket;   // last-CTA-done counter of k_move_terms_final
 };
 
-// Delta ell of a block move: per event log(lambda'/lambda); CTA b sums events
-// [256 b, 256 b + 256) in a fixed tree into part[b], and the last CTA to finish (ticket)
-// adds the part[] in index order into st->dell.  Events in S combine their row partials
-// (split order) and store the combined (M', X') row for the commit.  rates[n] = (lambda,
-// mu, xi, Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.  With decide != 0
-// (MH sweep) the last CTA also takes the Metropolis decision of block st->mh_cur:
-// log alpha = dell + st->mh_hastings, accept iff log u < log alpha (u: Philox block
-// (it, b, MH_ACCEPT_TAG), the same stream as hawkes_mh.cuh).
+// Delta ell of a block move (summation order: hawkes_moves.cuh), one CTA: the
+// tree sums part[] of the outside-S terms (written by k_move_delta_rows) in a fixed tree,
+// then the k moved events' terms log(lambda_n'/lambda_n) from their combined rows (stored
+// in rows_out for the commit) one by one in slot order.  rates[n] = (lambda, mu, xi,
+// Lambda); Lambda' = 2^64 lambda is the kernels' scaled unit.  With decide != 0 (MH sweep)
+// it also takes the Metropolis decision of block st->mh_cur: log alpha = dell +
+// st->mh_hastings, accept iff log u < log alpha (u: Philox block (it, b, MH_ACCEPT_TAG), the
+// same stream as hawkes_mh.cuh).
 __device__ __forceinline__ double mh_accept_uniform(unsigned klo, unsigned khi, unsigned long long it,
                                                     unsigned b) {
   const uint4 w = philox10(make_uint4((unsigned)it, (unsigned)(it >> 32), b, 0xC0000000u),
@@ -297,60 +297,40 @@ __device__ __forceinline__ double mh_accept_uniform(unsigned klo, unsigned khi, 
   return u53(w.x, w.y);
 }
 
-__global__ void __launch_bounds__(256) k_move_terms_final(
-    const double* __restrict__ rates, const double* __restrict__ delta,
-    const double* __restrict__ rows_part, int nsplit, const int* __restrict__ slot_of, int N,
-    double tx2, double h2, double floor_, double* __restrict__ part, double* __restrict__ rows_out,
-    EvalStatus* st, int decide, int* __restrict__ acc_out, double* __restrict__ la_out) {
+constexpr int MOVE_FINAL_THREADS = 1024;   // 32 warps: one per moved event for k <= 32
+__global__ void __launch_bounds__(MOVE_FINAL_THREADS) k_move_terms_final(
+    const double* __restrict__ rates, const double* __restrict__ rows_part, int nsplit,
+    const int* __restrict__ idx, int k, const double* __restrict__ part, int nb, double tx2,
+    double h2, double floor_, double* __restrict__ rows_out, EvalStatus* st, int decide,
+    int* __restrict__ acc_out, double* __restrict__ la_out) {
   __shared__ double sh[256];
-  __shared__ bool last;
+  __shared__ double sterm[MOVE_MAX];
   const double S = 18446744073709551616.0;   // 2^64
-  const int n = blockIdx.x * 256 + threadIdx.x;
-  double term = 0.0;
-  if (n < N) {
-    const double L0 = rates[4 * (long long)n] * S;
-    const int q = slot_of[n];
-    if (q < 0) {
-      const double d = fma(delta[2 * (long long)n], tx2, delta[2 * (long long)n + 1] * h2);
-      term = (d == 0.0) ? 0.0 : ((L0 + d > floor_) ? log1p(d / L0) : -INFINITY);
-    } else {
-      double M = 0.0, X = 0.0;
-      for (int s = 0; s < nsplit; ++s) {
-        M += rows_part[2 * ((long long)q * nsplit + s)];
-        X += rows_part[2 * ((long long)q * nsplit + s) + 1];
-      }
+  for (int q = threadIdx.x >> 5; q < k; q += MOVE_FINAL_THREADS / 32) {   // a warp per moved event
+    double M, X;
+    const double t = move_term_in(rates[4 * (long long)idx[q]] * S, rows_part, q, nsplit, tx2, h2,
+                                  floor_, M, X);
+    if ((threadIdx.x & 31) == 0) {
+      sterm[q] = t;
       rows_out[2 * q] = M;
       rows_out[2 * q + 1] = X;
-      const double L1 = fma(M, tx2, X * h2);
-      term = ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
     }
   }
-  sh[threadIdx.x] = term;
+  // the tree of the cooperative sweep's 256-thread CTAs (tree256), on threads 0-255
+  if (threadIdx.x < 256) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 256) v += part[i];
+    sh[threadIdx.x] = v;
+  }
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    part[blockIdx.x] = sh[0];
-    __threadfence();
-    last = atomicAdd(&st->mh_ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double v = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) v += __ldcg(part + i);
-  sh[threadIdx.x] = v;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double dl = sh[0];
+    double dl = sh[0];
+    for (int q = 0; q < k; ++q) dl += sterm[q];
     st->dell = dl;
-    st->mh_ticket = 0;
     if (decide) {
       const int b = st->mh_cur;
       const double la = (dl > -INFINITY) ? dl + st->mh_hastings : -INFINITY;   // NaN -> -inf

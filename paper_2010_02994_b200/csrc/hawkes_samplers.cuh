@@ -334,7 +334,7 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   ctx->h_st->mh_block = 0;
   ctx->h_st->mh_cur = 0;
   ctx->h_st->mh_prevk = 0;
-  const size_t off = offsetof(EvalStatus, mh_it), len = offsetof(EvalStatus, mh_ticket) - off;
+  const size_t off = offsetof(EvalStatus, mh_it), len = offsetof(EvalStatus, mh_prevk) + sizeof(int) - off;
   CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + off, reinterpret_cast<char*>(ctx->h_st) + off, len,
                      cudaMemcpyHostToDevice, ctx->stream));
   auto block_step = [&]() -> int {
