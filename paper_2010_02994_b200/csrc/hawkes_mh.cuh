@@ -142,14 +142,9 @@ __global__ void __launch_bounds__(256) k_mh_propose(const int* __restrict__ bloc
 #pragma unroll
     for (int d = 0; d < D; ++d) move_x[q * D + d] = y[d];
   }
-  sh[q] = logh;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (q < w) sh[q] += sh[q + w];
-    __syncthreads();
-  }
+  logh = cta_sum256(logh, sh);
   if (q == 0) {
-    st->mh_hastings = sh[0];
+    st->mh_hastings = logh;
     st->mh_cur = b;
     st->mh_prevk = k;
   }

@@ -116,13 +116,8 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
       // of an earlier block: bypass L1)
       sL0[tid] = __ldcg(a.rates + 4 * (long long)n) * S;
     }
-    red[tid] = logh;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
-    }
-    if (tid == 0) s_hast = red[0];
+    logh = cta_sum256(logh, red);
+    if (tid == 0) s_hast = logh;
     __syncthreads();
     const StampSlots slots{a.stamp, b};
 
@@ -152,8 +147,8 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
           a.delta[2 * (long long)n] = dM;
           a.delta[2 * (long long)n + 1] = dX;
         }
-        tree256(term, red);
-        if (tid == 0) a.part[u] = red[0];
+        const double tsum = cta_sum256(term, red);
+        if (tid == 0) a.part[u] = tsum;
         __syncthreads();
       } else {
         const int q = (u - nb) / nsplit, split = (u - nb) % nsplit;
@@ -173,20 +168,11 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
           M += eb;
           X += es;
         }
-        red[tid] = M;
-        red[256 + tid] = X;
-        __syncthreads();
-        for (int w = 128; w > 0; w >>= 1) {
-          if (tid < w) {
-            red[tid] += red[tid + w];
-            red[256 + tid] += red[256 + tid + w];
-          }
-          __syncthreads();
-        }
+        cta_sum256x2(M, X, red);
         if (tid == 0) {
           const long long o = 2 * ((long long)q * nsplit + split);
-          a.rows_part[o] = red[0];
-          a.rows_part[o + 1] = red[256];
+          a.rows_part[o] = M;
+          a.rows_part[o + 1] = X;
         }
         __syncthreads();
       }
@@ -205,9 +191,9 @@ __global__ void __launch_bounds__(256) k_mh_sweep_coop(MhCoopArgs<D> a) {
     }
     double v = 0.0;
     for (int i = tid; i < nb; i += 256) v += __ldcg(a.part + i);
-    tree256(v, red);
+    v = cta_sum256(v, red);
     if (tid == 0) {
-      double dl = red[0];
+      double dl = v;
       for (int q = 0; q < k; ++q) dl += sterm[q];
       const double la = (dl > -INFINITY) ? dl + s_hast : -INFINITY;   // NaN -> -inf
       const double u = mh_uniforms(key, it, (unsigned)b, MH_ACCEPT_TAG).x;

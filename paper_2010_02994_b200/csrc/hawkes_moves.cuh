@@ -66,14 +66,37 @@ __device__ __forceinline__ double move_term_in(double L0, const double* __restri
   return ((L1 > floor_) ? log(L1) : -INFINITY) - log(L0);
 }
 
-// fixed tree over a 256-thread CTA (red: 256 doubles of shared memory); result in red[0]
-__device__ __forceinline__ void tree256(double v, double* red) {
-  red[threadIdx.x] = v;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
+// fixed-order sum over the first 256 threads of a CTA (every thread calls it; red: 16
+// doubles of shared memory): a shuffle-down tree in each of warps 0-7, then warp 0 combines
+// the 8 warp sums the same way.  The result is valid in thread 0; one barrier instead of the
+// eight of a shared-memory tree (the MH sweep's block step is a chain of such sums).  The
+// two-value form sums (a, b) pairs in the same order.
+__device__ __forceinline__ void cta_sum256x2(double& a, double& b, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
   }
+  if (lane == 0 && warp < 8) {
+    red[warp] = a;
+    red[8 + warp] = b;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    a = lane < 8 ? red[lane] : 0.0;
+    b = lane < 8 ? red[8 + lane] : 0.0;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+  }
+}
+__device__ __forceinline__ double cta_sum256(double v, double* red) {
+  double z = 0.0;
+  cta_sum256x2(v, z, red);
+  return v;
 }
 
 // pair term parts (scaled) for event n at xn against event m at xm, times/ties from records
@@ -139,8 +162,8 @@ __device__ __forceinline__ void move_delta_body(const MoveArgs<D>& a, const int2
     dout[2 * (long long)n] = dM;
     dout[2 * (long long)n + 1] = dX;
   }
-  tree256(term, red);
-  if (threadIdx.x == 0) a.part[blk] = red[0];
+  const double tsum = cta_sum256(term, red);
+  if (threadIdx.x == 0) a.part[blk] = tsum;
 }
 
 // rows in S: full (M', X') at the proposed configuration.  Block (q, s) sums the j range
@@ -159,8 +182,7 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
                                                double* __restrict__ rows_part, int q, int split,
                                                int nsplit, double* dyn) {
   using L = Layout<D>;
-  double* shM = dyn;
-  double* shX = dyn + 256;
+  double* red = dyn;   // 16 doubles (cta_sum256x2)
   const int n = a.idx[q];
   double xn[D];
 #pragma unroll
@@ -179,20 +201,11 @@ __device__ __forceinline__ void move_rows_body(const MoveArgs<D>& a, const int2*
     M += eb;
     X += es;
   }
-  shM[threadIdx.x] = M;
-  shX[threadIdx.x] = X;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      shM[threadIdx.x] += shM[threadIdx.x + w];
-      shX[threadIdx.x] += shX[threadIdx.x + w];
-    }
-    __syncthreads();
-  }
+  cta_sum256x2(M, X, red);
   if (threadIdx.x == 0) {
     const long long o = 2 * ((long long)q * nsplit + split);
-    rows_part[o] = shM[0];
-    rows_part[o + 1] = shX[0];
+    rows_part[o] = M;
+    rows_part[o + 1] = X;
   }
 }
 

@@ -316,19 +316,13 @@ __global__ void __launch_bounds__(MOVE_FINAL_THREADS) k_move_terms_final(
       rows_out[2 * q + 1] = X;
     }
   }
-  // the tree of the cooperative sweep's 256-thread CTAs (tree256), on threads 0-255
-  if (threadIdx.x < 256) {
-    double v = 0.0;
+  // the cooperative sweep's sum (cta_sum256 over its 256-thread CTAs), on threads 0-255
+  double v = 0.0;
+  if (threadIdx.x < 256)
     for (int i = threadIdx.x; i < nb; i += 256) v += part[i];
-    sh[threadIdx.x] = v;
-  }
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
+  v = cta_sum256(v, sh);
   if (threadIdx.x == 0) {
-    double dl = sh[0];
+    double dl = v;
     for (int q = 0; q < k; ++q) dl += sterm[q];
     st->dell = dl;
     if (decide) {
