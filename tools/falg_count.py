@@ -67,7 +67,7 @@ def shipped():
             tgt = int(mm.group(1), 16)
             body = [re.sub(r"^@!?U?P\w+\s+", "", t).split()[0].split(".")[0]
                     for a, t in ins if tgt <= a <= addr]
-            if sum(1 for o in body if o == "LDS") >= 8:
+            if sum(1 for o in body if o == "LDS") >= 8 and "DFMA" in body:   # the pair loop
                 loops.append(body)
         body = min(loops, key=len)            # the unmasked, self-exciting 4-pair step
         c = Counter(o for o in body if o in FP64)
