@@ -120,10 +120,11 @@ __global__ void __launch_bounds__(BMDS_THREADS) k_bmds(const double* __restrict_
 // reads Y[l][(l + s) mod 32], two wavefronts (the ideal for 8-byte loads).  The pair's value
 // goes to the row, +s u to the row's gradient and -s u to the column's.  Row partials go to
 // slot b, column partials to slot a (slot NB for diagonal tasks), so every (slot, event) is
-// written exactly once and k_bmds_sym_fin sums the NB + 1 slots in order.  Half the pair
-// work of k_bmds: 2.63 vs 3.79 ms at N = 20k; at the flu size (N = 4733, ~5 tasks per warp,
-// 16 warps/SM for the staged Y blocks) the per-task latency chain limits it to 0.257 vs
-// 0.279 ms.
+// written exactly once and k_bmds_sym_fin sums the NB + 1 slots in order.  Each lane
+// takes two pairs per step (columns (l + s) and (l + s + 16) mod 32, 16 steps), their main
+// chains branch-free so they interleave (128 registers, 16 warps/SM): 5 % over one pair
+// per step.  Half the pair work of k_bmds: 2.3 vs 3.79 ms at N = 20k; 0.19 vs 0.28 ms at
+// the flu size (N = 4733), where ~5 tasks per warp and their staging latency limit it.
 constexpr int BSYM_WARPS = 4;
 
 template <int D>
@@ -169,51 +170,66 @@ __global__ void __launch_bounds__(32 * BSYM_WARPS) k_bmds_sym(const double* __re
       }
     }
     __syncwarp();
-    double gr[D], gc[D], v = 0.0;
+    // two pairs per lane and step (columns (l + s) and (l + s + 16) mod 32, s = 0..15): two
+    // independent dependency chains per lane, whose column sums rotate together
+    double gr[D], gc[2][D], v = 0.0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) gr[d] = gc[d] = 0.0;
-#pragma unroll 1   // (unrolling by 2 or 4 measured no faster)
-    for (int s = 0; s < 32; ++s) {
-      const int cidx = (lane + s) & 31;
-      const int j = j0 + cidx;
-      const bool live = irow && j < N && (!diag || j > i);
-      if (live) {
-        double u[D], r2 = 0.0;
+    for (int d = 0; d < D; ++d) gr[d] = gc[0][d] = gc[1][d] = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < 16; ++s) {
+      // both pairs' main chains branch-free (a dead pair -- padding, or j <= i on a diagonal
+      // task -- computes on a clamped column and is selected to 0), so the compiler can
+      // interleave them; the erfc / log1p tail (z < 9) stays a branch, rarely taken
+      double u[2][D], r2[2], inv_d[2], z[2], e[2], phis[2];
+      bool live[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cidx = (lane + s + 16 * h) & 31;
+        const int j = j0 + cidx;
+        live[h] = irow && j < N && (!diag || j > i);
+        r2[h] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          u[d] = xi[d] - xs[cidx * D + d];
-          r2 = fma(u[d], u[d], r2);
+          u[h][d] = xi[d] - xs[cidx * D + d];
+          r2[h] = fma(u[h][d], u[h][d], r2[h]);
         }
         const double y = Ys[lane * 32 + cidx];
-        const bool apart = r2 > 0.0;
-        const double inv_d = apart ? rsqrt(r2) : 0.0;
-        const double delta = r2 * inv_d;
-        const double z = delta * c.inv_s;
-        double q = 0.0, lphi = 0.0;
-        if (z < 9.0) {
-          q = 0.5 * erfc(z * 0.70710678118654752440);
-          lphi = log1p(-q);
-        }
-        const double e = y - delta;
-        v -= c.half_log + 0.5 * e * e * c.inv_s2 + lphi;
-        if (apart) {
-          double phis = fexp(fma(r2, c.mhalf_inv_s2, c.lphi_c), tab);
-          if (z < 9.0) phis = phis / (1.0 - q);
-          const double sw = (e * c.inv_s2 - phis) * inv_d;
+        const bool apart = r2[h] > 0.0;
+        inv_d[h] = apart ? rsqrt(r2[h]) : 0.0;
+        const double delta = r2[h] * inv_d[h];
+        z[h] = delta * c.inv_s;
+        e[h] = y - delta;
+        phis[h] = apart ? fexp(fma(r2[h], c.mhalf_inv_s2, c.lphi_c), tab) : 0.0;
+      }
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            gr[d] = fma(sw, u[d], gr[d]);
-            gc[d] = fma(-sw, u[d], gc[d]);
-          }
+      for (int h = 0; h < 2; ++h) {
+        double lphi = 0.0;
+        if (z[h] < 9.0) {
+          const double q = 0.5 * erfc(z[h] * 0.70710678118654752440);
+          lphi = log1p(-q);
+          phis[h] = phis[h] / (1.0 - q);
+        }
+        const double sw = live[h] ? (e[h] * c.inv_s2 - phis[h]) * inv_d[h] : 0.0;
+        if (live[h]) v -= c.half_log + 0.5 * e[h] * e[h] * c.inv_s2 + lphi;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          gr[d] = fma(sw, u[h][d], gr[d]);
+          gc[h][d] = fma(-sw, u[h][d], gc[h][d]);
         }
       }
-      // rotate the column sums one lane down: lane l then holds column (l + s + 1) mod 32
+      // rotate both column sums one lane down: lane l then holds columns (l + s + 1) and
+      // (l + s + 17) mod 32
       const int nxt = (lane + 1) & 31;
 #pragma unroll
-      for (int d = 0; d < D; ++d) gc[d] = __shfl_sync(0xffffffffu, gc[d], nxt);
+      for (int d = 0; d < D; ++d) {
+        gc[0][d] = __shfl_sync(0xffffffffu, gc[0][d], nxt);
+        gc[1][d] = __shfl_sync(0xffffffffu, gc[1][d], nxt);
+      }
     }
     __syncwarp();
-    // lane l now holds column l's sums again
+    // lane l now holds, for column (l + 16) mod 32, the sums over rows l' = l + 16 + t (mod 32,
+    // t < 16: its gc[0] half) and, for column l, those over rows l - 16 - t (gc[1]): the
+    // column's total is its gc[1] plus the gc[0] of lane (l + 16) mod 32
     if (irow) {
       double* o = part + ((long long)b * N + i) * K;
 #pragma unroll
@@ -221,10 +237,12 @@ __global__ void __launch_bounds__(32 * BSYM_WARPS) k_bmds_sym(const double* __re
       o[D] = v;
     }
     const int jl = j0 + lane;
+#pragma unroll
+    for (int d = 0; d < D; ++d) gc[1][d] += __shfl_sync(0xffffffffu, gc[0][d], (lane + 16) & 31);
     if (jl < N) {
       double* o = part + ((long long)(diag ? NB : a) * N + jl) * K;
 #pragma unroll
-      for (int d = 0; d < D; ++d) o[d] = gc[d];
+      for (int d = 0; d < D; ++d) o[d] = gc[1][d];
       o[D] = 0.0;
     }
   }
