@@ -35,6 +35,11 @@ METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-
 #   F_UNO   SURVEY's method (naive per-pair bodies with libdevice exp) for unordered pairs
 #   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg
 F_IMPL = (12.5, 13.5)
+# fp32 variant: FMA-pipe instructions per ordered pair of sym_kernel_f32's hot loop (packed
+# FFMA2 / FADD2 / FMUL2 = 1 per lane; tools/falg_count.py's method on its SASS); its peak is
+# one packed warp-instruction per 2 cycles per SMSP = 64 lanes/clk/SM, which reproduces ncu's
+# FMA-pipe utilisation of these kernels (profiles/r01_ncu_full_summary_fp32.txt: 76.7 / 74.2 %)
+F_IMPL32 = (5.0, 6.0)
 F_UNO = (26.0, 28.5)
 F_SURVEY = (34.5, 49.0)
 FP64_LANES_PER_SM = 64
@@ -386,9 +391,13 @@ def run_ours(args):
     grad_avg = kt["grad_ms"] / max(1, kt["grad_launches"])
     pairs_alg = pairs / world                   # each rank's launches cover 1/W of the pairs
     unordered = ctx.algorithm in ("auto", "pairs") and args.precision == "fp64"
+    fp32_pairs = ctx.algorithm in ("auto", "pairs") and args.precision == "fp32"
     if unordered:
         names = ("rate pass: sym_kernel<2,1,4,4>", "gradient pass: sym_kernel<2,2,4,4>")
         F_impl = F_IMPL
+    elif fp32_pairs:
+        names = ("rate pass: sym_kernel_f32<2,1,4,1>", "gradient pass: sym_kernel_f32<2,2,4,1>")
+        F_impl = F_IMPL32
     else:
         names = ("rate pass: pass_kernel<2,1>", "gradient pass: pass_kernel<2,2>")
         F_impl = (26.5, 26.0)                  # ROWS: ordered pairs, FP64 instructions (SASS)
@@ -405,10 +414,34 @@ def run_ours(args):
     except Exception:
         dfma_peak = None
 
+    if fp32_pairs:
+        roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "unit": "T FMA-pipe instructions/s (one per lane; packed FFMA2/FADD2/FMUL2 = 1)",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "peak_basis": f"{props.multi_processor_count} SMs x 64 lanes x {sm_max:.0f} MHz "
+                                  "(one packed FP32 warp-instruction per 2 cycles per SMSP)",
+                    "ops_per_pair": F_impl[pi],
+                    "ops_per_pair_basis": "FMA-pipe instructions per ordered pair of the shipped "
+                                          "sym_kernel_f32's hot loop (SASS)"}
+    else:
+        roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "unit": "T FP64-pipe instructions/s (one per lane; DFMA = 1)", "frac": achieved / peak,
+                    "traffic": traffic,
+                    "peak_basis": f"{props.multi_processor_count} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
+                    "ops_per_pair": F_impl[pi],
+                    "ops_per_pair_basis": "FP64 instructions per ordered pair of the shipped kernel's "
+                                          "unmasked hot loop (tools/falg_count.py --shipped)",
+                    "unordered_falg": {"ops_per_pair": F_UNO[pi], "frac": F_UNO[pi] * rate_units / peak,
+                                       "basis": "SURVEY's method (naive libdevice-exp bodies) for unordered pairs"},
+                    "survey_falg": {"ops_per_pair": F_SURVEY[pi], "frac": F_SURVEY[pi] * rate_units / peak,
+                                    "basis": "SURVEY.md 8(d) ordered-pair F_alg (frozen)"},
+                    "measured_dfma_peak": dfma_peak}
     out = {
         "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        # the pair arithmetic's type: fp64, or fp32 pair terms (per-tile sums promoted to fp64)
+        "dtype": "f64" if args.precision == "fp64" else "f32",
         "data": "synthetic (C4 generator: seeded Philox cluster process, SURVEY.md §8(d))",
         "pairs_per_s": evals_per_s * pairs, "loglik": ell,
         "config": {"workload": f"C4 unit-square Hawkes catalog N={N} D=2 (BASELINE configs[3])",
@@ -423,18 +456,7 @@ def run_ours(args):
         "gpu_launches": kt["total_launches"],
         "kernel_ms": {"rate_pass_avg": rate_avg, "grad_pass_avg": grad_avg,
                       "rate_launches": kt["rate_launches"], "grad_launches": kt["grad_launches"]},
-        "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "T FP64-pipe instructions/s (one per lane; DFMA = 1)", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "peak_basis": f"{props.multi_processor_count} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
-                     "ops_per_pair": F_impl[pi],
-                     "ops_per_pair_basis": "FP64 instructions per ordered pair of the shipped kernel's "
-                                           "unmasked hot loop (tools/falg_count.py --shipped)",
-                     "unordered_falg": {"ops_per_pair": F_UNO[pi], "frac": F_UNO[pi] * rate_units / peak,
-                                        "basis": "SURVEY's method (naive libdevice-exp bodies) for unordered pairs"},
-                     "survey_falg": {"ops_per_pair": F_SURVEY[pi], "frac": F_SURVEY[pi] * rate_units / peak,
-                                     "basis": "SURVEY.md 8(d) ordered-pair F_alg (frozen)"},
-                     "measured_dfma_peak": dfma_peak},
+        "roofline": roofline,
         "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": N * D * 8,
                 "d2h_bytes_per_step": N * D * 8 + 8},
         "loglik_only": loglik_only,
