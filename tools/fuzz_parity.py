@@ -3,7 +3,7 @@ ties, clustered / spread locations, large coordinate offsets) and random decompo
 precision and emulated world, each against the oracle under the tolerance rule
 (tests/gpu_helpers.py).  Prints one JSON line per failure and a summary.
 
-    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--nmax 2500]
+    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--nmax 2500] [--only CASE [--alg A]]
 """
 import argparse
 import json
@@ -22,6 +22,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=200)
 ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--nmax", type=int, default=2500)
+ap.add_argument("--only", type=int, default=-1, help="re-run one case (same random stream)")
+ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
 a = ap.parse_args()
 rng = np.random.default_rng(a.seed)
 fails = 0
@@ -49,6 +51,10 @@ for case in range(a.cases):
     prec = "fp64" if rng.uniform() < 0.7 else "fp32"
     alg = ["auto", "pairs", "rows"][int(rng.integers(0, 3))]
     W = int(rng.choice([0, 0, 0, 2, 3]))
+    if a.only >= 0:
+        if case != a.only:
+            continue
+        alg = a.alg or alg
     info = {"case": case, "N": N, "D": D, "prec": prec, "alg": alg, "W": W, "theta": th}
     try:
         ell_r, lam_r, _ = oracle.loglik(x, t, th)
