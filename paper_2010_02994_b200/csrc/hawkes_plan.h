@@ -3,6 +3,7 @@
 // greedy deal of PAIRS' chunk pairs.  Included by hawkes_api.cu only.
 #pragma once
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -25,6 +26,10 @@ int chunk_of(long long N) {
 // catalogs still fill the GPU).  PAIRS sums are not bitwise W-independent anyway (the
 // per-event partials meet in an allreduce), so the chunk may depend on W.
 int chunk_pairs_of(long long N, int W) {
+  if (const char* e = getenv("HAWKES_PAIRS_CHUNK")) {   // diagnostics: A/B of the chunk size
+    const long long c = atoll(e) / TILE_J * TILE_J;
+    if (c >= TILE_J) return (int)c;
+  }
   const double C = 138.0 * sqrt((double)std::max(1, W));
   long long c = (long long)llround((double)N / C / TILE_J) * TILE_J;   // nearest multiple
   return (int)std::max<long long>(TILE_J, c);
