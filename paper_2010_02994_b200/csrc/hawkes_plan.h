@@ -32,6 +32,11 @@ int chunk_pairs_of(long long N, int W) {
   }
   const double C = 138.0 * sqrt((double)std::max(1, W));
   long long c = (long long)llround((double)N / C / TILE_J) * TILE_J;   // nearest multiple
+  // one-tile chunks make every item a single 128 x 128 tile pair, whose fixed cost (row
+  // tile load, 4-warp row reduction, partial writes) shows: where 256-event chunks still
+  // leave >= 64 sqrt(W) chunks (>= ~4.7 items per CTA slot) take them (N = 20k: -2 %,
+  // profiles/r01_chunk_sweep.txt)
+  if (c <= TILE_J && (double)N / (2 * TILE_J) >= 64.0 * sqrt((double)std::max(1, W))) c = 2 * TILE_J;
   return (int)std::max<long long>(TILE_J, c);
 }
 
