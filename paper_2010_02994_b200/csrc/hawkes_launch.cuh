@@ -309,7 +309,7 @@ struct Fin1D {
     if (all) {   // PAIRS: (M', X') partials, gradient from pass 2 alone
       static_assert(K1P == 2, "k_fin1p pairs (M', X') lanes");
       const long long n = 2 * ctx->N;
-      k_fin1p<D><<<(unsigned)((n + FINP_THREADS - 1) / FINP_THREADS), FINP_THREADS, 0, ctx->stream>>>(
+      k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32);
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
@@ -331,7 +331,7 @@ struct Fin2D {
     const bool sums = all && ctx->multi;
     if (all) {
       const long long n = ctx->N * D;
-      k_fin2p<D><<<(unsigned)((n + FINP_THREADS - 1) / FINP_THREADS), FINP_THREADS, 0, ctx->stream>>>(
+      k_fin2p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->grad);
     } else {
       k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,

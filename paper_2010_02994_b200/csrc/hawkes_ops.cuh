@@ -184,13 +184,34 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
   fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
 }
 
-// PAIRS finalizes (every event final on this process): one thread per (event, component),
-// so a warp's loads of one slot are contiguous and 2 (pass 1) / D (pass 2) times as many
-// independent slot sums run as with one thread per event; each component is still summed
-// over the slots in index order (the same bits as k_fin1 / k_fin2).  At N = 5000 the
-// per-event forms took 15 / 12 us next to 37 / 43 us of pair kernels (latency-bound: one
-// warp per SM walking 41 slots).
-constexpr int FINP_THREADS = 128;
+// PAIRS finalizes (every event final on this process): one warp-lane per (event, component)
+// so a warp's loads of one slot are contiguous, and the slots split over the CTA's
+// FINP_SPLIT warps (warp w sums its contiguous slot range in index order; warp 0 adds the
+// FINP_SPLIT range sums in warp order): a fixed summation order, so results are bitwise
+// reproducible.  At N = 5000 (41 slots) one thread per (event, component) walking all slots
+// took 8.2 / 8.8 us on 78 / 79 CTAs (latency-bound); the split runs 4x the loads in flight.
+constexpr int FINP_SPLIT = 4;
+constexpr int FINP_THREADS = 32 * FINP_SPLIT;
+
+__device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, long long stride,
+                                                int nslots, bool live) {
+  const int per = (nslots + FINP_SPLIT - 1) / FINP_SPLIT;
+  const int w = threadIdx.x >> 5;
+  const int c0 = w * per, c1 = min(nslots, c0 + per);
+  double acc = 0.0;
+  if (live) {
+#pragma unroll 4
+    for (int c = c0; c < c1; ++c) acc += p[c * stride];
+  }
+  __shared__ double sh[FINP_SPLIT][32];
+  sh[w][threadIdx.x & 31] = acc;
+  __syncthreads();
+  double tot = sh[0][threadIdx.x & 31];
+#pragma unroll
+  for (int k = 1; k < FINP_SPLIT; ++k) tot += sh[k][threadIdx.x & 31];
+  return tot;   // meaningful in warp 0
+}
+
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
                                                         int nslots, int N, const double* __restrict__ rec,
@@ -198,32 +219,24 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
                                                         const FinConst* __restrict__ fcp,
                                                         double* __restrict__ rec_rho,
                                                         float* __restrict__ rec32_rho) {
-  const long long q = (long long)blockIdx.x * FINP_THREADS + threadIdx.x;   // (event, M' or X')
+  const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, M' or X')
   const int i = (int)(q >> 1);
-  double acc = 0.0;
-  if (i < N) {
-    const double* p = part + q;   // part[(c npad + i) K1P + k], K1P = 2
-    const long long stride = npad * 2;
-#pragma unroll 8
-    for (int c = 0; c < nslots; ++c) acc += p[c * stride];
-  }
-  const double X = __shfl_down_sync(0xffffffffu, acc, 1);
-  if (i < N && (threadIdx.x & 1) == 0) fin1_event<D>(i, acc, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+  // part[(c npad + i) K1P + k], K1P = 2
+  const double M = finp_slot_sum(part + q, npad * 2, nslots, i < N);
+  if (threadIdx.x >= 32) return;
+  const double X = __shfl_down_sync(0xffffffffu, M, 1);
+  if (i < N && (threadIdx.x & 1) == 0) fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
 }
 
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, long long npad,
                                                         int nslots, int N, double* __restrict__ grad) {
   constexpr int K = Layout<D>::K2;
-  const long long q = (long long)blockIdx.x * FINP_THREADS + threadIdx.x;   // (event, d)
-  if (q >= (long long)N * D) return;
+  const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, d)
+  const bool live = q < (long long)N * D;
   const int i = (int)(q / D), d = (int)(q % D);
-  const double* p = part + (long long)i * K + d;
-  const long long stride = npad * K;
-  double acc = 0.0;
-#pragma unroll 8
-  for (int c = 0; c < nslots; ++c) acc += p[c * stride];
-  grad[q] = acc;
+  const double g = finp_slot_sum(part + (long long)i * K + d, npad * K, nslots, live);
+  if (threadIdx.x < 32 && live) grad[q] = g;
 }
 
 template <int D>
