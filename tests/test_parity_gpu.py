@@ -42,9 +42,11 @@ def test_c1_unit_square_seeds(rep):
     _check(synth.config("C1", replicate=rep), f"C1 rep {rep}")
 
 
-@pytest.mark.parametrize("N", [2, 3, 127, 128, 255, 256, 257, 511, 513, 1003, 4097, 35_584, 35_841])
+@pytest.mark.parametrize("N", [2, 3, 127, 128, 255, 256, 257, 511, 513, 1003, 4097, 16_383, 16_384, 16_411,
+                               35_584, 35_841])
 def test_ragged_sizes(N):
-    """Tile edges: row tiles of 256, j tiles of 128, chunks >= 512."""
+    """Tile edges: row tiles of 256, j tiles of 128, chunks >= 512; N = 16383 / 16384 / 16411
+    straddle PAIRS' 256-event chunk floor (hawkes_plan.h chunk_pairs_of)."""
     _check(synth.unit_square(N, config=21, replicate=N), f"N={N}")
 
 
@@ -308,6 +310,12 @@ def test_fp32_configs(name):
 def test_fp32_ragged_and_ties(N):
     _check_fp32(synth.unit_square(N, config=25, replicate=N), f"fp32 N={N}")
     _check_fp32(synth.with_ties(N, max(2, N // 10)), f"fp32 ties N={N}")
+
+
+@pytest.mark.parametrize("N", [16_384, 16_411])
+def test_fp32_chunk_floor_sizes(N):
+    """fp32 PAIRS at sizes that take the 256-event chunk floor (hawkes_plan.h chunk_pairs_of)."""
+    _check_fp32(synth.unit_square(N, config=25, replicate=N), f"fp32 N={N}")
 
 
 @pytest.mark.parametrize("algorithm", ["pairs", "rows"])
