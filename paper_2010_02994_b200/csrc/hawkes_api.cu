@@ -123,7 +123,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->rates, (size_t)ctx->npad * 4)) ||
       (rc = dalloc(ctx, &ctx->grad, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
-      (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W)) ||
+      (rc = dalloc(ctx, &ctx->counters, (size_t)4 * ctx->W + 1)) ||
+      (rc = dalloc(ctx, &ctx->ell_part, (size_t)(N + 15) / 16)) ||
       (rc = dalloc(ctx, &ctx->tab, EXP_TABLE)) ||
       (rc = dalloc(ctx, &ctx->st, 1)) || (rc = dalloc(ctx, &ctx->d_consts, 1)) ||
       (rc = dalloc(ctx, &ctx->d_slot_of, (size_t)N)) || (rc = dalloc(ctx, &ctx->d_move_idx, MOVE_MAX)) ||
@@ -250,7 +251,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   }
   void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
-                  ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->tab,
+                  ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->ell_part, ctx->tab,
                   ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
   for (void* b : bufs)

@@ -119,7 +119,8 @@ struct hawkes_ctx {
   double* xstage = nullptr;// N x D staging
   double* sendbuf = nullptr;
   double* recvbuf = nullptr;
-  int* counters = nullptr; // 4 per logical rank
+  int* counters = nullptr; // 4 per logical rank, + 1: k_fin1p's block ticket (PAIRS ell)
+  double* ell_part = nullptr; // PAIRS: k_fin1p's per-CTA ell sums (ceil(N / 16))
   int2* tab = nullptr;     // exp table
   int* bad = nullptr;      // device-side input validation flag: &st->nonfinite
   EvalStatus* st = nullptr;

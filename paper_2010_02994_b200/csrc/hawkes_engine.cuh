@@ -141,7 +141,7 @@ int run_rates(hawkes_ctx* ctx) {
     ctx->lam_valid = true;
     return HAWKES_OK;
   }
-  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * 4 * ctx->W, ctx->stream));
+  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1), ctx->stream));
   if (ctx->pairs) {
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
     if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1P));
@@ -154,8 +154,10 @@ int run_rates(hawkes_ctx* ctx) {
     TRY(exchange_rows(ctx, ctx->rl, 2));
     if (ctx->multi) TRY(dispatchD<RhoD>(ctx->D, ctx));
   }
-  k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
-  CHECK_LAUNCH();
+  if (!ctx->pairs) {   // PAIRS: k_fin1p's last CTA reduces ell
+    k_ell_reduce<<<1, 1024, 0, ctx->stream>>>(ctx->rl, (int)ctx->N, ctx->st);
+    CHECK_LAUNCH();
+  }
   ctx->rates_valid = true;
   ctx->rates_exchanged = false;
   ctx->grad_valid = false;

@@ -311,7 +311,8 @@ struct Fin1D {
       const long long n = 2 * ctx->N;
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
-          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32);
+          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32, ctx->ell_part,
+          ctx->counters + 4 * ctx->W, ctx->st);
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,

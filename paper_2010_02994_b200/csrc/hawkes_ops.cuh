@@ -122,10 +122,35 @@ struct DevConsts {
   FinConst fc;
 };
 
+// device-side evaluation status (ell, flags, HMC / MH state), one per context
+struct EvalStatus {
+  double ell;
+  int nonfinite;   // device-side input validation failed
+  int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
+  double kinetic;
+  double dell;     // Delta ell of the pending block move
+  double bmds;     // BMDS log density of the last BMDS evaluation
+  // HMC transition (hawkes_hmc_step)
+  double lp0;      // log density at the chain's current state
+  double kin0;     // 1/2 sum Minv p0^2
+  double log_alpha;
+  int accepted;
+  int undef0;      // ell(x0) = -inf: the chain's state has zero density
+  double mh_hastings;   // block MH: sum of the proposal's log Hastings terms
+  // block MH sweep parameters, device-resident so one captured block step serves every block
+  unsigned long long mh_it;
+  double mh_scale;
+  unsigned mh_key_lo, mh_key_hi;
+  int mh_block;         // next block of the sweep
+  int mh_cur;           // block being processed
+  int mh_prevk;         // proposal slots of the previous block still set (cleared by propose)
+};
+
 // lambda, rho' and ell_n of event i from its summed pass-1 partials (M', X'), then the
-// stores: rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda); rho' into the records
+// stores: rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda); rho' into the records;
+// returns ell_i
 template <int D>
-__device__ __forceinline__ void fin1_event(int i, double M, double X, const double* __restrict__ rec,
+__device__ __forceinline__ double fin1_event(int i, double M, double X, const double* __restrict__ rec,
                                            double* __restrict__ rl, double* __restrict__ rates,
                                            const FinConst& f, double* __restrict__ rec_rho,
                                            float* __restrict__ rec32_rho) {
@@ -152,6 +177,7 @@ __device__ __forceinline__ void fin1_event(int i, double M, double X, const doub
   rates[4 * (long long)i + 1] = mu_s * sc;
   rates[4 * (long long)i + 2] = xi_s * sc;
   rates[4 * (long long)i + 3] = Lam;
+  return ell;
 }
 
 // Fixed-order chunk reduction of pass-1 partials for the rows of one row tile, then
@@ -212,20 +238,53 @@ __device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, lo
   return tot;   // meaningful in warp 0
 }
 
+// ... and the ell reduction (S3): each CTA sums its 16 events' ell_i in lane order into
+// ell_part[block]; the CTA that draws the last ticket sums ell_part in a fixed order (thread
+// k: blocks k, k + 128, ...; then a fixed shared-memory tree) into st->ell and re-arms the
+// ticket.  Replaces k_ell_reduce (one launch and a one-CTA pass over N) on the PAIRS path.
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
                                                         int nslots, int N, const double* __restrict__ rec,
                                                         double* __restrict__ rl, double* __restrict__ rates,
                                                         const FinConst* __restrict__ fcp,
                                                         double* __restrict__ rec_rho,
-                                                        float* __restrict__ rec32_rho) {
+                                                        float* __restrict__ rec32_rho,
+                                                        double* __restrict__ ell_part, int* ticket,
+                                                        EvalStatus* st) {
   const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, M' or X')
   const int i = (int)(q >> 1);
   // part[(c npad + i) K1P + k], K1P = 2
   const double M = finp_slot_sum(part + q, npad * 2, nslots, i < N);
-  if (threadIdx.x >= 32) return;
-  const double X = __shfl_down_sync(0xffffffffu, M, 1);
-  if (i < N && (threadIdx.x & 1) == 0) fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+  __shared__ int last;
+  __shared__ double red[FINP_THREADS];
+  if (threadIdx.x < 32) {
+    const double X = __shfl_down_sync(0xffffffffu, M, 1);
+    double e = 0.0;
+    if (i < N && (threadIdx.x & 1) == 0) e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
+    if (threadIdx.x == 0) {
+      ell_part[blockIdx.x] = e;
+      __threadfence();
+      last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += FINP_THREADS) s += __ldcg(ell_part + b);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = FINP_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->ell = red[0];
+    if (!(red[0] > -INFINITY)) st->undefined = 1;
+    *ticket = 0;
+  }
 }
 
 template <int D>
@@ -270,30 +329,6 @@ __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
 __device__ __forceinline__ double u53(unsigned a, unsigned b) {
   return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) * (1.0 / 9007199254740992.0);
 }
-
-// sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W
-struct EvalStatus {
-  double ell;
-  int nonfinite;   // device-side input validation failed
-  int undefined;   // some evaluation produced ell = -inf inside a leapfrog trajectory
-  double kinetic;
-  double dell;     // Delta ell of the pending block move
-  double bmds;     // BMDS log density of the last BMDS evaluation
-  // HMC transition (hawkes_hmc_step)
-  double lp0;      // log density at the chain's current state
-  double kin0;     // 1/2 sum Minv p0^2
-  double log_alpha;
-  int accepted;
-  int undef0;      // ell(x0) = -inf: the chain's state has zero density
-  double mh_hastings;   // block MH: sum of the proposal's log Hastings terms
-  // block MH sweep parameters, device-resident so one captured block step serves every block
-  unsigned long long mh_it;
-  double mh_scale;
-  unsigned mh_key_lo, mh_key_hi;
-  int mh_block;         // next block of the sweep
-  int mh_cur;           // block being processed
-  int mh_prevk;         // proposal slots of the previous block still set (cleared by propose)
-};
 
 // Delta ell of a block move (summation order: hawkes_moves.cuh), one CTA: the
 // tree sums part[] of the outside-S terms (written by k_move_delta_rows) in a fixed tree,
@@ -413,6 +448,8 @@ __global__ void k_scatter_slots(int* __restrict__ slot_of, const int* __restrict
   if (q < k) slot_of[idx[q]] = set ? q : -1;
 }
 
+// sum of ell_n over all rows in a fixed order (one CTA): deterministic for any W (ROWS;
+// PAIRS reduces ell in k_fin1p)
 __global__ void k_ell_reduce(const double* __restrict__ rl, int N, EvalStatus* st) {
   __shared__ double sh[1024];
   double s = 0.0;
