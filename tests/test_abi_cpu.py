@@ -85,7 +85,7 @@ def test_nccl_unique_id_is_fresh():
     assert len(a) == 128 and a != b
 
 
-@pytest.mark.parametrize("N", [1, 300, 5000, 100_000, 1_000_000])
+@pytest.mark.parametrize("N", [1, 300, 5000, 16_384, 20_000, 100_000, 1_000_000])
 @pytest.mark.parametrize("W", [1, 2, 3, 8])
 def test_pair_plan_covers_every_pair_once(N, W):
     """HAWKES_ALGO_PAIRS: the chunk pairs (a <= b) of all ranks cover each unordered chunk
@@ -112,3 +112,14 @@ def test_pair_plan_covers_every_pair_once(N, W):
     assert chunk % 128 == 0
     if N >= 100_000:
         assert max(loads) / (sum(loads) / W) < 1.03
+
+
+@pytest.mark.parametrize("N,W,chunk", [(5000, 1, 128), (16_383, 1, 128), (16_384, 1, 256),
+                                       (20_000, 1, 256), (20_000, 2, 128), (23_168, 2, 128), (23_200, 2, 256),
+                                       (50_000, 1, 384), (100_000, 1, 768), (100_000, 8, 256)])
+def test_pair_chunk_heuristic(N, W, chunk):
+    """chunk_pairs_of (hawkes_plan.h): ~N / (138 sqrt(W)) rounded to 128-event tiles, floored
+    at 256 events where that leaves >= 64 sqrt(W) chunks (profiles/r01_chunk_sweep.txt,
+    r01_chunk256.txt)."""
+    from paper_2010_02994_b200 import sharding
+    assert sharding.plan_pairs(N, W, 0)[1] == chunk
