@@ -395,6 +395,110 @@ def test_hmc_step_reversible():
     assert np.allclose(x2, c.x, atol=1e-10) and np.allclose(-p2, z, atol=1e-8)
 
 
+# ---- leapfrog / HMC branches with a diagonal mass and a reflecting box (reading R15:
+# diagonal M, optional reflecting box).  These pin the oracle's mass and box arithmetic against
+# properties they must have, not against a retyped formula: a reflection that is not an
+# involution breaks reversibility; M instead of M^-1 in the drift breaks the scaling
+# equivalence; p0 = z sqrt(Minv) instead of z / sqrt(Minv) breaks the momentum covariance.
+
+def _mass_box_case(N=120, seed=7):
+    c = synth.config("C1", N)
+    rng = np.random.default_rng(seed)
+    minv = rng.uniform(0.25, 4.0, size=c.x.shape)          # non-identity diagonal M^-1
+    half = 0.004                                            # box of +-half around x0
+    return c, minv, c.x - half, c.x + half
+
+
+def _reflections(x0, p0, c, minv, lo, hi, step, L):
+    """Count the components whose momentum sign flips in the trajectory (proof the box was hit)."""
+    x, p = x0.copy(), p0.copy()
+    flips = 0
+    for _ in range(L):
+        x1, p1, _, _ = oracle.leapfrog(x, p, c.t, c.theta, step, 1, inv_mass=minv, box_lo=lo, box_hi=hi)
+        flips += int(np.sum(np.sign(p1) != np.sign(p + 0.5 * step * oracle.grad(x, c.t, c.theta)[0])))
+        x, p = x1, p1
+    return flips
+
+
+def test_leapfrog_box_and_mass_reversible():
+    """Leapfrog with a reflecting box and a diagonal mass is an involution up to the momentum
+    sign: (x1, -p1) integrates back to (x0, -p0).  The box is hit (momenta flip) on the way,
+    and every state stays inside it."""
+    c, minv, lo, hi = _mass_box_case()
+    z = oracle.hmc_normals(11, 0, c.x.size).reshape(c.x.shape)
+    p0 = z / np.sqrt(minv)
+    step, L = 2e-3, 8
+    assert _reflections(c.x, p0, c, minv, lo, hi, step, L) > 20
+    x1, p1, _, _ = oracle.leapfrog(c.x, p0, c.t, c.theta, step, L, inv_mass=minv, box_lo=lo, box_hi=hi)
+    assert np.all(x1 >= lo) and np.all(x1 <= hi)
+    assert not np.allclose(x1, c.x, atol=1e-6)
+    x2, p2, _, _ = oracle.leapfrog(x1, -p1, c.t, c.theta, step, L, inv_mass=minv, box_lo=lo, box_hi=hi)
+    assert np.allclose(x2, c.x, rtol=0, atol=1e-11)
+    assert np.allclose(-p2, p0, rtol=1e-9, atol=1e-9 * np.abs(p0).max())
+
+
+def test_leapfrog_mass_energy_error_is_second_order():
+    """With a non-identity diagonal mass, H = -ell + 1/2 sum Minv p^2 is conserved to O(step^2):
+    halving the step divides the energy error by ~4 (a kinetic energy of the wrong form,
+    e.g. 1/2 sum p^2 / Minv, leaves an O(step) or O(1) error)."""
+    c, minv, _, _ = _mass_box_case(N=150, seed=3)
+    z = oracle.hmc_normals(2, 5, c.x.size).reshape(c.x.shape)
+    p0 = z / np.sqrt(minv)
+    H0 = -oracle.loglik(c.x, c.t, c.theta)[0] + 0.5 * float(np.sum(minv * p0 * p0))
+    errs = []
+    for step in (1e-4, 5e-5, 2.5e-5):
+        _, _, ell, kin = oracle.leapfrog(c.x, p0, c.t, c.theta, step, int(round(4e-4 / step)),
+                                         inv_mass=minv)
+        errs.append(abs(-ell + kin - H0))
+    assert 3.0 < errs[0] / errs[1] < 5.0 and 3.0 < errs[1] / errs[2] < 5.0
+
+
+def test_leapfrog_scaling_equivalence_with_mass_and_box():
+    """Coordinates scaled by a (x -> a x, tau_x -> a tau_x, h -> a h, box -> a box,
+    M^-1 -> a^2 M^-1, p -> p / a): ell changes by -N D ln a (pin P7(iv)), the gradient by 1/a,
+    so the leapfrog must give exactly a times the trajectory and 1/a times the momenta, with
+    the same kinetic energy.  Pins that the drift multiplies by M^-1 (not M) and that the
+    reflection is applied to the scaled box."""
+    c, minv, lo, hi = _mass_box_case(N=100, seed=5)
+    z = oracle.hmc_normals(8, 1, c.x.size).reshape(c.x.shape)
+    p0 = z / np.sqrt(minv)
+    step, L, a = 2e-3, 6, 8.0          # power of two: the scaling is exact in fp64
+    mu0, tx, tt, th, om, h = c.theta
+    theta_a = (mu0, a * tx, tt, th, om, a * h)
+    x1, p1, ell1, k1 = oracle.leapfrog(c.x, p0, c.t, c.theta, step, L, inv_mass=minv, box_lo=lo, box_hi=hi)
+    xa, pa, ella, ka = oracle.leapfrog(a * c.x, p0 / a, c.t, theta_a, step, L, inv_mass=a * a * minv,
+                                       box_lo=a * lo, box_hi=a * hi)
+    assert np.allclose(xa, a * x1, rtol=0, atol=1e-12 * a)
+    assert np.allclose(pa, p1 / a, rtol=1e-10, atol=1e-10 * np.abs(p1).max() / a)
+    assert ka == pytest.approx(k1, rel=1e-10)
+    assert ella == pytest.approx(ell1 - c.N * c.D * math.log(a), rel=1e-12)
+
+
+def test_hmc_step_momenta_have_covariance_M():
+    """hmc_step draws p0 ~ N(0, M) (p0 = z / sqrt(Minv)).  With a zero potential (hawkes=False,
+    no BMDS) one leapfrog step is x1 = x0 + step Minv p0 exactly and H is conserved (always
+    accepted), so (x1 - x0) / (step sqrt(Minv)) must be standard normal per component: KS and
+    variance against N(0, 1) with Minv spanning 1/16..16 (p0 = z sqrt(Minv) would give
+    variances Minv^2 and fail)."""
+    from scipy import stats
+    N, D = 4000, 3
+    rng = np.random.default_rng(1)
+    x0 = rng.uniform(0, 1, size=(N, D))
+    minv = np.exp(rng.uniform(np.log(1 / 16), np.log(16), size=(N, D)))
+    t = np.sort(rng.uniform(0, 1, N))
+    step = 1e-3
+    x1, acc, la = oracle.hmc_step(x0, t, (0.6, 0.1, 0.1, 0.4, 20.0, 0.03), 21, 4, step, 1,
+                                  inv_mass=minv, hawkes=False)
+    assert acc and abs(la) < 1e-9
+    w = ((x1 - x0) / (step * np.sqrt(minv))).ravel()
+    assert stats.kstest(w, "norm").pvalue > 1e-3
+    assert abs(w.var() - 1.0) < 5 * math.sqrt(2.0 / w.size)
+    # and the scale really depends on Minv: the raw displacements' variance tracks Minv
+    hi, lo = minv.ravel() > 4, minv.ravel() < 0.25
+    dx = ((x1 - x0) / step).ravel()
+    assert dx[hi].var() / dx[lo].var() > 16
+
+
 # ---- block MH over coarsened locations (P:L245-248, Eq. circleKernel)
 
 def test_lens_area_closed_forms_and_monte_carlo():
