@@ -386,6 +386,16 @@ def run_ours(args):
                         "acceptance": float(acc.mean())}
             mctx.close()
 
+    # ---- per-rank pass-kernel time (library CUDA events): the load balance of the plan
+    pass_ms = [float(kt["rate_ms"] + kt["grad_ms"]) / max(1, kt["rate_launches"])]
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, pass_ms[0])
+        pass_ms = [float(v) for v in allr]
+    ranks = {"world": world, "pass_kernel_ms_per_rank": pass_ms,
+             "balance": (sum(pass_ms) / len(pass_ms)) / max(pass_ms) if max(pass_ms) > 0 else None,
+             "note": "mean / max over ranks of the per-evaluation pass-kernel time (1 = perfect deal)"}
+
     # ---- roofline of the dominant pass (FP64 pipe), from the library's own CUDA events
     rate_avg = kt["rate_ms"] / max(1, kt["rate_launches"])
     grad_avg = kt["grad_ms"] / max(1, kt["grad_launches"])
@@ -448,11 +458,12 @@ def run_ours(args):
                    "N": N, "D": 2, "precision": args.precision, "algorithm": ctx.algorithm,
                    "l2": "flushed before every timed step (256 MiB device write, outside the step events)",
                    "parallelism": (f"chunk-pair sharded x{world} (LPT-dealt unordered chunk pairs, NCCL "
-                                   "allreduce of per-event partial sums per pass)"
+                                   "allgather of per-event partial sums per pass, added in rank order)"
                                    if ctx.algorithm in ("auto", "pairs") else
                                    f"row-sharded x{world} (zig-zag tiles, NCCL allgather of 1/lambda)")
                    if world > 1 else "1 GPU"},
         "clocks": clocks,
+        "ranks": ranks,
         "gpu_launches": kt["total_launches"],
         "kernel_ms": {"rate_pass_avg": rate_avg, "grad_pass_avg": grad_avg,
                       "rate_launches": kt["rate_launches"], "grad_launches": kt["grad_launches"]},
@@ -490,9 +501,32 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hmc", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def relaunch(args):
+    """`--gpus N > 1` without a torchrun environment: re-launch this command as N ranks
+    (one process per GPU, rendezvous on 127.0.0.1), as the driver would."""
+    if args.impl == "ours":
+        import torch
+        n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if n < args.gpus:
+            print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "value": None,
+                              "error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}"}),
+                  flush=True)
+            return 1
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -2,14 +2,15 @@
 //
 // One evaluation (ell and d ell/dx) on rank r of W, PAIRS (default):
 //   pass 1   sym_kernel<PASS=1> over this rank's chunk pairs (a <= b), each unordered pair
-//            once -> per-(slot, event) partials (M', X', G1')     [rate pass, Alg. 2 step 1]
-//   exchange W > 1: per-event slot sums, ncclAllReduce                       [S4]
+//            once -> per-(slot, event) rate partials (M', X')  [rate pass, Alg. 2 step 1]
+//   exchange W > 1: per-event slot sums, ncclAllGather, rank-ordered sum     [S4]
 //   fin1     fixed-order slot sum; lambda, rho' = 2^-64 / lambda, Lambda_n (erfc, expm1),
-//            ell_n = log lambda_n - Lambda_n                            [Eq. 1, P:L92-101]
-//   ell      fixed-order reduction of ell_n over all N events (same on every rank)
-//   pass 2   sym_kernel<PASS=2> -> partials G2'                        [gradient pass, step 2]
-//   exchange W > 1: per-event slot sums, ncclAllReduce                       [S6]
-//   fin2     g_i = rho'_i G1'_i + G2'_i                                 [App. A, P:L385]
+//            ell_n = log lambda_n - Lambda_n; fixed-order ell reduction over all N events
+//            (k_fin1p's last CTA)                                       [Eq. 1, P:L92-101]
+//   pass 2   sym_kernel<PASS=2>: the pair coefficient c = rho'_i mu' + rho'_j (mu' + xi')
+//            and both events' gradient partials c dx, -c dx            [gradient pass, step 2]
+//   exchange W > 1: per-event slot sums, ncclAllGather, rank-ordered sum     [S6]
+//   fin2     g_i = fixed-order sum of the slots                         [App. A, P:L385]
 // ROWS (ordered pairs, pass_kernel): row tiles dealt to ranks zig-zag, allgather of (rho',
 // ell_n) rows between the passes and of gradient rows at the end; bitwise identical for any
 // W.  Around the evaluation: the HMC leapfrog / transition, block-MH moves and the on-device
@@ -165,7 +166,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
         return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair items failed"));
     }
     if (ctx->multi) {
-      const size_t copies = o.nccl_unique_id ? 1 : (size_t)ctx->W + 1;
+      const size_t copies = (size_t)ctx->W + 1;   // row 0: the sum; rows 1..W: per-rank sums
       if ((rc = dalloc(ctx, &ctx->sums1, copies * ctx->npad * K1_of(D))) ||
           (rc = dalloc(ctx, &ctx->sums2, copies * ctx->npad * K2_of(D))))
         return fail(rc);
@@ -275,7 +276,7 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   std::vector<double> h(N);
   if (mem == HAWKES_MEM_DEVICE) {
     CU(cudaMemcpyAsync(h.data(), t, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_stream(ctx));
   } else {
     memcpy(h.data(), t, N * sizeof(double));
   }
@@ -293,7 +294,7 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   CU(cudaMemcpyAsync(ctx->rl, h.data(), N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyAsync(ctx->gid, g.data(), ctx->npad * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   TRY(dispatchD<PackTD>(ctx->D, ctx, (const double*)ctx->rl));
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   ctx->tN = h[N - 1];
   ctx->fc.tN = ctx->tN;
   TRY(upload_consts(ctx));

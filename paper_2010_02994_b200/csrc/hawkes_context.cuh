@@ -11,6 +11,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <algorithm>
 #include <cstddef>
@@ -45,6 +46,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.4): polled while a host thread waits on a stream with collectives,
+  // so a failed peer returns HAWKES_ERR_NCCL instead of hanging every rank
+  ncclResult_t (*asyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -61,6 +66,8 @@ struct NcclApi {
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    asyncError = (decltype(asyncError))dlsym(h, "ncclCommGetAsyncError");
+    commAbort = (decltype(commAbort))dlsym(h, "ncclCommAbort");
     if (!commInitRank || !allGather || !allReduce || !commDestroy || !errStr) {
       err = "libnccl.so.2 lacks required symbols";
       return false;
@@ -258,6 +265,47 @@ int dalloc(hawkes_ctx* ctx, T** p, size_t count) {
     int rc_ = (x);                  \
     if (rc_ != HAWKES_OK) return rc_; \
   } while (0)
+
+// Host wait on the context stream.  With an NCCL communicator the wait polls
+// ncclCommGetAsyncError (and an optional HAWKES_NCCL_TIMEOUT_S deadline, default 900 s): a
+// peer that failed aborts the communicator and returns HAWKES_ERR_NCCL (sticky) instead of
+// leaving every rank blocked in cudaStreamSynchronize.
+int wait_stream(hawkes_ctx* ctx) {
+  if (!ctx->comm) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    return HAWKES_OK;
+  }
+  static const double limit_s = [] {
+    const char* e = getenv("HAWKES_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 900.0;
+  }();
+  timespec t0;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(ctx->stream);
+    if (q == cudaSuccess) return HAWKES_OK;
+    if (q != cudaErrorNotReady)
+      return set_err(ctx, HAWKES_ERR_CUDA, "stream wait failed: %s", cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    bool failed = false;
+    if (g_nccl.asyncError && g_nccl.asyncError(ctx->comm, &ar) == ncclSuccess && ar != ncclSuccess &&
+        ar != ncclInProgress)
+      failed = true;
+    timespec t1;
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    const double el = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+    if (failed || (limit_s > 0 && el > limit_s)) {
+      if (g_nccl.commAbort) g_nccl.commAbort(ctx->comm);
+      ctx->comm = nullptr;
+      if (failed) return set_err(ctx, HAWKES_ERR_NCCL, "NCCL asynchronous error: %s", g_nccl.errStr(ar));
+      return set_err(ctx, HAWKES_ERR_NCCL, "NCCL collective did not complete in %.0f s", limit_s);
+    }
+    if (spin > 64) {   // short waits spin; long ones (a whole evaluation) sleep 20 us per poll
+      timespec d{0, 20000};
+      nanosleep(&d, nullptr);
+    }
+  }
+}
 
 int K1_of(int D) { return ((D + 3) / 2) * 2; }
 int K2_of(int D) { return ((D + 1) / 2) * 2; }

@@ -35,25 +35,30 @@ int exchange_rows(hawkes_ctx* ctx, double* rows, int K) {
   return HAWKES_OK;
 }
 
-// rate pass + finalize + exchange + ell reduction (device-side; no host sync)
-// PAIRS, W > 1: per-event sums over this process's chunk pairs, then the exchange
-// (NCCL allreduce, or the rank-ordered sum of the emulated ranks' buffers)
+// PAIRS, W > 1 (S4 / S6): each logical rank sums its own chunk pairs' slots per event in a
+// fixed order (k_slot_sum) into row 1 + r of sums[W + 1][npad][K]; the W rows are then
+// gathered (ncclAllGather in place, or already in place for emulated ranks) and added in
+// rank order into row 0 (k_sum_ranks).  The result is bitwise reproducible run to run at a
+// fixed W on every rank: unlike an ncclAllReduce, it does not depend on NCCL's algorithm
+// or protocol choice (ring / tree / NVLS), and every rank adds the same W values in the
+// same order.
 int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int K) {
   const long long n = (long long)ctx->N * K;
   const long long stride = (long long)ctx->npad * K;
   for (int r : ctx->my_ranks) {
-    double* out = ctx->comm ? sums : sums + (1 + r) * stride;
     k_slot_sum<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
-        part, ctx->npad, ctx->nchunks, ctx->chunk, K, ctx->d_own, r, (int)ctx->N, out);
+        part, ctx->npad, ctx->nchunks, ctx->chunk, K, ctx->d_own, r, (int)ctx->N,
+        sums + (1 + r) * stride);
     CHECK_LAUNCH();
   }
   if (ctx->comm) {
-    NC(g_nccl.allReduce(sums, sums, (size_t)n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-  } else {
-    k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(sums + stride, stride, ctx->W,
-                                                                     n, sums);
-    CHECK_LAUNCH();
+    const int r = ctx->my_ranks[0];
+    NC(g_nccl.allGather(sums + (1 + r) * stride, sums + stride, (size_t)stride, ncclDouble, ctx->comm,
+                        ctx->stream));
   }
+  k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(sums + stride, stride, ctx->W, n,
+                                                                   sums);
+  CHECK_LAUNCH();
   return HAWKES_OK;
 }
 
@@ -195,7 +200,7 @@ int fetch_status(hawkes_ctx* ctx) {
   // (ctx->bad is st->nonfinite: one copy brings the flags and the results)
   CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
   int bad = 0;
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   bad = ctx->h_st->nonfinite;
   if (bad) {
     CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));

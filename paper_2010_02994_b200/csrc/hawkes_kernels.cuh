@@ -245,7 +245,7 @@ struct PassArgs {
   const int2* items;     // (row tile, chunk)
   int* counter;          // work counter, zeroed before launch
   double* part;          // [chunks][Npad][K]
-  const int2* tab;       // 32-entry exp table in global memory
+  const int2* tab;       // EXP_TABLE-entry exp table in global memory
   long long npad;
   int N;
   int n_items;

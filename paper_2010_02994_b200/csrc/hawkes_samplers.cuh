@@ -151,7 +151,7 @@ int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double s
   }
   if (x_out) {
     TRY(copy_out(ctx, x_out, ctx->xstage, n, mem));
-    CU(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_stream(ctx));
   }
   if (out_accepted) *out_accepted = acc ? 1 : 0;
   if (out_log_alpha) *out_log_alpha = ctx->h_st->log_alpha;
@@ -188,7 +188,7 @@ int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const do
   std::vector<double> hx((size_t)k * D);
   if (mem == HAWKES_MEM_DEVICE) {
     CU(cudaMemcpyAsync(hx.data(), new_x, hx.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_stream(ctx));
   } else {
     memcpy(hx.data(), new_x, hx.size() * sizeof(double));
   }
@@ -223,7 +223,7 @@ int hawkes_accept_move(hawkes_ctx* ctx) {
   ctx->rates_valid = ctx->grad_valid = false;   // rho', G1 and ell_n of the old state
   ctx->rates_exchanged = true;                  // every rank updated every row
   ctx->lam_valid = true;
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   return HAWKES_OK;
 }
 
@@ -233,7 +233,7 @@ int hawkes_get_locations(hawkes_ctx* ctx, double* out_x, int32_t mem) {
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_get_locations");
   if (!ctx->have_x) return set_err(ctx, HAWKES_ERR_STATE, "no locations");
   TRY(copy_out(ctx, out_x, ctx->xstage, (size_t)ctx->N * ctx->D, mem));
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   return HAWKES_OK;
 }
 
@@ -250,7 +250,7 @@ int hawkes_set_regions(hawkes_ctx* ctx, int32_t kind, const double* centre, cons
   if (mem == HAWKES_MEM_DEVICE) {
     CU(cudaMemcpyAsync(hc.data(), centre, hc.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hs.data(), size, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_stream(ctx));
   } else {
     memcpy(hc.data(), centre, hc.size() * sizeof(double));
     memcpy(hs.data(), size, hs.size() * sizeof(double));
@@ -266,7 +266,7 @@ int hawkes_set_regions(hawkes_ctx* ctx, int32_t kind, const double* centre, cons
   }
   CU(cudaMemcpyAsync(ctx->d_reg_c, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyAsync(ctx->d_reg_s, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   ctx->reg_kind = kind;
   drop_mh_graph(ctx);
   return HAWKES_OK;
@@ -326,7 +326,7 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   // the sweep's parameters live on the device (EvalStatus mh_*), staged through the pinned
   // status block: one block step (propose, Delta ell, terms + decision, gated commit) then
   // serves every block, as plain launches or as one captured graph replayed per block
-  CU(cudaStreamSynchronize(ctx->stream));   // h_st is free to stage
+  TRY(wait_stream(ctx));   // h_st is free to stage
   ctx->h_st->mh_it = iteration;
   ctx->h_st->mh_scale = scale;
   ctx->h_st->mh_key_lo = (unsigned)seed;
@@ -407,7 +407,7 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   if (out_log_alpha)
     CU(cudaMemcpyAsync(out_log_alpha, ctx->d_mh_la, n_blocks * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(wait_stream(ctx));
   int n_acc = 0;
   for (int32_t b = 0; b < n_blocks; ++b) {
     n_acc += acc[b];
