@@ -199,6 +199,17 @@ int hawkes_get_locations(hawkes_ctx* ctx, double* out_x, int32_t mem);
 int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, double* Lambda,
                      int32_t mem);
 
+/* The pair-kernel precision this context evaluates with now (*out: hawkes_precision).
+ * An HAWKES_FP32 context reports HAWKES_FP64 after its range guard tripped (DESIGN.md
+ * reading R23): when some event's rate Lambda' falls within 2^24 N flush quanta of the fp32
+ * flush threshold (terms ex2.approx.ftz sets to 0 could then carry more than 2^-24 of it),
+ * the call that saw it is redone by the fp64 kernels -- hawkes_loglik,
+ * hawkes_grad_locations, hawkes_get_rates, hawkes_leapfrog and hawkes_hmc_step return the
+ * fp64 result; block moves and MH sweeps check the guard before using fresh rates -- and
+ * the context stays on fp64 until the next hawkes_set_times / hawkes_set_params.
+ * Errors: HAWKES_ERR_ARG. */
+int hawkes_precision_in_use(const hawkes_ctx* ctx, int32_t* out);
+
 /* Bayesian MDS: the flu application's second O(N^2)
  * term.  hawkes_set_bmds copies the N*N row-major dissimilarity matrix Y (host or device per
  * mem; only the lower triangle y[n*N + n'], n > n', is read, as in Eq. bmdsLikelihood) and

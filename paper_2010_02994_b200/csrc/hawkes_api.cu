@@ -254,7 +254,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
                   ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->ell_part, ctx->tab,
                   ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
-                  ctx->lf_lo, ctx->lf_hi, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
+                  ctx->lf_lo, ctx->lf_hi, ctx->lf_x0, ctx->lf_p0, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto* p : ctx->d_items1) if (p) cudaFree(p);
@@ -299,6 +299,7 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   ctx->fc.tN = ctx->tN;
   TRY(upload_consts(ctx));
   ctx->have_t = true;
+  ctx->fb64 = false;   // a new catalog: the fp32 range guard decides again
   ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
   TRY(clear_move(ctx));
   return HAWKES_OK;
@@ -338,6 +339,8 @@ int hawkes_set_params(hawkes_ctx* ctx, const hawkes_params* p) {
   TRY(compute_constants(ctx, *p, ctx->tN));
   ctx->params = *p;
   ctx->have_p = true;
+  if (ctx->fb64) drop_graphs(ctx);
+  ctx->fb64 = false;   // new constants: the fp32 range guard decides again
   ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
   TRY(clear_move(ctx));
   return HAWKES_OK;
@@ -347,8 +350,7 @@ int hawkes_loglik(hawkes_ctx* ctx, double* out) {
   ENTER(ctx);
   if (!out) return set_err(ctx, HAWKES_ERR_ARG, "out_loglik is NULL");
   TRY(check_ready(ctx));
-  TRY(run_rates(ctx));
-  TRY(fetch_status(ctx));
+  TRY(checked_rates(ctx));
   *out = ctx->h_st->ell;
   return HAWKES_OK;
 }
@@ -358,10 +360,12 @@ int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double
   if (!out_grad || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_grad_locations");
   TRY(check_ready(ctx));
-  TRY(run_rates(ctx));
-  TRY(run_grad(ctx));
-  TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
-  TRY(fetch_status(ctx));
+  do {   // twice only if the fp32 range guard sent the context to fp64
+    TRY(run_rates(ctx));
+    TRY(run_grad(ctx));
+    TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
+    TRY(fetch_status(ctx));
+  } while (take_retry(ctx));
   if (out_ll) *out_ll = ctx->h_st->ell;
   if (!(ctx->h_st->ell > -INFINITY))
     return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "some lambda_n = 0: ell = -inf, gradient undefined");
@@ -374,7 +378,7 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
   if (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE)
     return set_err(ctx, HAWKES_ERR_ARG, "bad mem");
   TRY(check_ready(ctx));
-  TRY(run_rates(ctx));
+  TRY(checked_rates(ctx));
   if (!ctx->rates_exchanged && !ctx->pairs) {
     TRY(exchange_rows(ctx, ctx->rates, 4));
     ctx->rates_exchanged = true;
@@ -393,6 +397,12 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
     else
       CU(cudaMemcpy(outs[k], col.data(), N * sizeof(double), cudaMemcpyHostToDevice));
   }
+  return HAWKES_OK;
+}
+
+int hawkes_precision_in_use(const hawkes_ctx* ctx, int32_t* out) {
+  if (!ctx || !out) return HAWKES_ERR_ARG;
+  *out = use32(ctx) ? HAWKES_FP32 : HAWKES_FP64;
   return HAWKES_OK;
 }
 

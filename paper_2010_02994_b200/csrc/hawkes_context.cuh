@@ -134,6 +134,7 @@ struct hawkes_ctx {
   EvalStatus* h_st = nullptr;  // pinned
   // leapfrog state
   double *lf_x = nullptr, *lf_p = nullptr, *lf_minv = nullptr, *lf_lo = nullptr, *lf_hi = nullptr;
+  double *lf_x0 = nullptr, *lf_p0 = nullptr;   // start of the trajectory (fp64 re-run)
 
   // state
   bool have_t = false, have_x = false, have_p = false;
@@ -145,6 +146,12 @@ struct hawkes_ctx {
   PassConst pc{};
   PassConst32 pc32{};
   FinConst fc{};
+  FinConst fc64{};            // fc of the fp64 kernels (== fc on an fp64 context)
+  // fp32 range guard (R23): an fp32 context whose evaluation tripped the guard
+  // evaluates with the fp64 kernels (records and constants of both precisions are kept)
+  // until set_times / set_params; retry = the current call must be redone in fp64
+  bool fb64 = false;
+  bool retry = false;
 
   // timing
   bool timing = false;
@@ -156,6 +163,7 @@ struct hawkes_ctx {
 
   int grid1 = 0, grid2 = 0;
   int grid_s1 = 0, grid_s2 = 0;
+  int grid32_1 = 0, grid32_2 = 0, grid32_s1 = 0, grid32_s2 = 0;   // fp32 kernels
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;
@@ -306,6 +314,10 @@ int wait_stream(hawkes_ctx* ctx) {
     }
   }
 }
+
+// the fp32 pass kernels run unless the range guard sent this context to fp64
+inline bool use32(const hawkes_ctx* ctx) { return ctx->rec32 != nullptr && !ctx->fb64; }
+inline const FinConst& fcur(const hawkes_ctx* ctx) { return use32(ctx) ? ctx->fc : ctx->fc64; }
 
 int K1_of(int D) { return ((D + 3) / 2) * 2; }
 int K2_of(int D) { return ((D + 1) / 2) * 2; }

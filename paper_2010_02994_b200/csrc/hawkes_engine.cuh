@@ -202,6 +202,16 @@ int fetch_status(hawkes_ctx* ctx) {
   int bad = 0;
   TRY(wait_stream(ctx));
   bad = ctx->h_st->nonfinite;
+  if (ctx->h_st->range32) {
+    CU(cudaMemsetAsync(&ctx->st->range32, 0, sizeof(int), ctx->stream));
+    ctx->h_st->range32 = 0;
+    if (use32(ctx)) {   // the fp32 result is not trusted: this call is redone in fp64
+      ctx->fb64 = true;
+      ctx->retry = true;
+      drop_graphs(ctx);
+      ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+    }
+  }
   if (bad) {
     CU(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
     if (bad & 2) {
@@ -215,6 +225,22 @@ int fetch_status(hawkes_ctx* ctx) {
                    "locations contain NaN/Inf or |x| > 1e100 (device-side validation)");
   }
   return HAWKES_OK;
+}
+
+// true once if the last fetch_status asked for the call to be redone (fp32 range guard)
+bool take_retry(hawkes_ctx* ctx) {
+  const bool r = ctx->retry;
+  ctx->retry = false;
+  return r;
+}
+
+// rates for the current state, checked against the fp32 range guard (one host sync)
+int checked_rates(hawkes_ctx* ctx) {
+  for (;;) {
+    TRY(run_rates(ctx));
+    TRY(fetch_status(ctx));
+    if (!take_retry(ctx)) return HAWKES_OK;
+  }
 }
 
 // drop a pending block move (restores the event -> proposal-slot map)
@@ -307,6 +333,7 @@ int upload_consts(hawkes_ctx* ctx) {
   h.pc = ctx->pc;
   h.pc32 = ctx->pc32;
   h.fc = ctx->fc;
+  h.fc64 = ctx->fc64;
   CU(cudaMemcpyAsync(ctx->d_consts, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
   return HAWKES_OK;
 }
@@ -344,6 +371,8 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   fc.scale_log2 = -64.0;
   // every clamped pair term is <= e^-706.9 in the kernels' scaled units
   fc.zero_floor = (double)ctx->N * exp(-700.0) * std::max(fc.tx2, fc.h2);
+  fc.range_floor = 0.0;
+  ctx->fc64 = fc;
   if (ctx->opts.precision == HAWKES_FP32) {
     // log2 domain; one power-of-two scale 2^-E puts the largest possible term near 2^20
     const double L2E = 1.4426950408889634074;
@@ -362,6 +391,10 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
       return set_err(ctx, HAWKES_ERR_PARAM, "Theta outside the fp32 path's range");
     fc.scale_log2 = E;
     fc.zero_floor = 0.0;   // ex2.approx.ftz flushes to exact zeros
+    // every flushed term is < 2^-126 in these scaled units and an event has at most N - 1
+    // of them: below 2^24 N 2^-126 max(tau_x^2, h^2) the flushed mass could exceed 2^-24
+    // of Lambda' (R23), and the evaluation is redone in fp64
+    fc.range_floor = (double)ctx->N * ldexp(1.0, -102) * std::max(fc.tx2, fc.h2);
     ctx->pc32 = c32;
   }
   ctx->pc = pc;

@@ -108,14 +108,14 @@ int sym32_setup(hawkes_ctx* ctx) {
   int b1 = 0, b2 = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1>()));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2>()));
-  ctx->grid_s1 = std::max(1, b1) * ctx->sms;
-  ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+  ctx->grid32_s1 = std::max(1, b1) * ctx->sms;
+  ctx->grid32_s2 = std::max(1, b2) * ctx->sms;
   return HAWKES_OK;
 }
 
 template <int D, bool SOA>
 int sym32_launch(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
-  const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+  const int grid = std::min(pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2, b.n_items);
   if (pass == 1)
     sym_kernel_f32<D, 1, SYM32_R, SOA><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
   else
@@ -143,14 +143,17 @@ struct SetupD {
       int b1 = 0, b2 = 0;
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, THREADS, sm));
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, THREADS, sm));
-      ctx->grid1 = std::max(1, b1) * ctx->sms;
-      ctx->grid2 = std::max(1, b2) * ctx->sms;
+      ctx->grid32_1 = std::max(1, b1) * ctx->sms;
+      ctx->grid32_2 = std::max(1, b2) * ctx->sms;
       if constexpr (D <= SYM_MAX_D) if (ctx->pairs) {
-        if constexpr (D == 2)
-          if (!sym32_soa()) return sym32_setup<D, false>(ctx);
-        return sym32_setup<D, true>(ctx);
+        bool soa = true;
+        if constexpr (D == 2) soa = sym32_soa();
+        int rc = HAWKES_OK;
+        if (soa) rc = sym32_setup<D, true>(ctx);
+        else if constexpr (D == 2) rc = sym32_setup<D, false>(ctx);
+        if (rc != HAWKES_OK) return rc;
       }
-      return HAWKES_OK;
+      // and the fp64 kernels below: the fp32 range guard can send this context to them
     }
     auto k1 = pass_kernel<D, 1, R_ROWS>;
     auto k2 = pass_kernel<D, 2, R_ROWS>;
@@ -203,7 +206,7 @@ void harvest_events(hawkes_ctx* ctx) {
 template <int D>
 struct PassD {
   static int run(hawkes_ctx* ctx, int pass, int rank) {
-    if (ctx->rec32) return run32(ctx, pass, rank);
+    if (use32(ctx)) return run32(ctx, pass, rank);
     PassArgs a;
     a.rec = ctx->rec;
     a.gid = ctx->gid;
@@ -260,7 +263,7 @@ struct PassD {
     record_start(ctx, pass == 1);
     if (a.n_items > 0) {
       const size_t sm = pass_smem32<D>();
-      const int grid = std::min(pass == 1 ? ctx->grid1 : ctx->grid2, a.n_items);
+      const int grid = std::min(pass == 1 ? ctx->grid32_1 : ctx->grid32_2, a.n_items);
       if (pass == 1)
         pass_kernel_f32<D, 1, R_ROWS><<<grid, THREADS, sm, ctx->stream>>>(a);
       else
@@ -304,19 +307,21 @@ struct Fin1D {
     if (!nt) return HAWKES_OK;
     const bool sums = all && ctx->multi;
     const bool final_here = all || !ctx->multi;   // else rho' is exchanged first
-    double* rr = final_here && !ctx->rec32 ? ctx->rec + Layout<D>::RHO : nullptr;
+    // rho' into both records (an fp32 context can switch to the fp64 kernels)
+    double* rr = final_here ? ctx->rec + Layout<D>::RHO : nullptr;
     float* rr32 = final_here && ctx->rec32 ? ctx->rec32 + Layout32<D>::RHO : nullptr;
+    const FinConst* fcp = use32(ctx) ? &ctx->d_consts->fc : &ctx->d_consts->fc64;
     if (all) {   // PAIRS: (M', X') partials, gradient from pass 2 alone
       static_assert(K1P == 2, "k_fin1p pairs (M', X') lanes");
       const long long n = 2 * ctx->N;
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
-          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32, ctx->ell_part,
+          ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
           ctx->counters + 4 * ctx->W, ctx->st);
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,
-          ctx->rl, ctx->rates, &ctx->d_consts->fc, rr, rr32);
+          ctx->rl, ctx->rates, fcp, rr, rr32, &ctx->st->range32);
     }
     CHECK_LAUNCH();
     return HAWKES_OK;
@@ -400,7 +405,7 @@ struct MoveD {
     a.rates = ctx->rates;
     a.tx2 = ctx->fc.tx2;
     a.h2 = ctx->fc.h2;
-    a.floor_ = ctx->fc.zero_floor;
+    a.floor_ = fcur(ctx).zero_floor;
     a.part = ctx->d_move_part;
     // one launch for the rows outside S (with their Delta-ell terms) and the moved rows, one
     // CTA for the moved events' terms and the fixed-order sum (decide: the MH sweep's
@@ -413,7 +418,7 @@ struct MoveD {
     CHECK_LAUNCH();
     k_move_terms_final<<<1, MOVE_FINAL_THREADS, 0, ctx->stream>>>(ctx->rates, ctx->d_move_rows_part, nsplit,
                                                    ctx->d_move_idx, k, ctx->d_move_part, nb,
-                                                   ctx->fc.tx2, ctx->fc.h2, ctx->fc.zero_floor,
+                                                   ctx->fc.tx2, ctx->fc.h2, fcur(ctx).zero_floor,
                                                    ctx->d_move_rows, ctx->st, decide, ctx->d_mh_acc,
                                                    ctx->d_mh_la);
     CHECK_LAUNCH();
@@ -473,7 +478,7 @@ struct MhCoopD {
     a.c = ctx->pc;
     a.tx2 = ctx->fc.tx2;
     a.h2 = ctx->fc.h2;
-    a.floor_ = ctx->fc.zero_floor;
+    a.floor_ = fcur(ctx).zero_floor;
     a.st = ctx->st;
     a.acc_out = ctx->d_mh_acc;
     a.la_out = ctx->d_mh_la;

@@ -113,13 +113,19 @@ struct FinConst {
   double mu0, tau_t, theta, omega, tN;
   double scale_log2;      // pair sums carry 2^-scale_log2: -64 (fp64 path) or E (fp32 path)
   double zero_floor;      // Lambda' at or below this is lambda = 0 (fexp clamps at e^-707)
+  // fp32 range guard (reading R23): a Lambda' below this may have lost more than
+  // 2^-24 of its value to terms that ex2.approx.ftz flushed to 0 (each < 2^-126 in the
+  // kernels' scaled units, at most N of them per event); the evaluation is then redone by the
+  // fp64 kernels.  0 on the fp64 path.
+  double range_floor;
 };
 
 // kernel constants live in device memory so captured CUDA graphs survive set_params
 struct DevConsts {
   PassConst pc;
   PassConst32 pc32;
-  FinConst fc;
+  FinConst fc;     // constants of the context's precision
+  FinConst fc64;   // the fp64 kernels' (an fp32 context after its range guard tripped)
 };
 
 // device-side evaluation status (ell, flags, HMC / MH state), one per context
@@ -144,6 +150,7 @@ struct EvalStatus {
   int mh_block;         // next block of the sweep
   int mh_cur;           // block being processed
   int mh_prevk;         // proposal slots of the previous block still set (cleared by propose)
+  int range32;          // fp32 range guard tripped (FinConst::range_floor) in some evaluation
 };
 
 // lambda, rho' and ell_n of event i from its summed pass-1 partials (M', X'), then the
@@ -153,10 +160,11 @@ template <int D>
 __device__ __forceinline__ double fin1_event(int i, double M, double X, const double* __restrict__ rec,
                                            double* __restrict__ rl, double* __restrict__ rates,
                                            const FinConst& f, double* __restrict__ rec_rho,
-                                           float* __restrict__ rec32_rho) {
+                                           float* __restrict__ rec32_rho, int* __restrict__ range_flag) {
   using L = Layout<D>;
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
+  if (mu_s + xi_s < f.range_floor) *range_flag = 1;   // fp32 only (range_floor = 0 in fp64)
   const double Lp = (mu_s + xi_s > f.zero_floor) ? mu_s + xi_s : 0.0;
   const double rho = (Lp > 0.0) ? 1.0 / Lp : 0.0;
   const double sc = exp2(f.scale_log2);   // exact power of two
@@ -188,7 +196,8 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
                        const int* __restrict__ tiles, int N, const double* __restrict__ rec,
                        double* __restrict__ G1, double* __restrict__ rl,
                        double* __restrict__ rates, const FinConst* __restrict__ fcp,
-                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho) {
+                       double* __restrict__ rec_rho, float* __restrict__ rec32_rho,
+                       int* __restrict__ range_flag) {
   const int i = tiles[blockIdx.x] * RT + threadIdx.x;
   if (i >= N) return;
   double M = 0.0, X = 0.0, G[D];
@@ -207,7 +216,7 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
 #pragma unroll
     for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
   }
-  fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+  fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, range_flag);
 }
 
 // PAIRS finalizes (every event final on this process): one warp-lane per (event, component)
@@ -260,7 +269,8 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
   if (threadIdx.x < 32) {
     const double X = __shfl_down_sync(0xffffffffu, M, 1);
     double e = 0.0;
-    if (i < N && (threadIdx.x & 1) == 0) e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho);
+    if (i < N && (threadIdx.x & 1) == 0)
+      e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
     if (threadIdx.x == 0) {
@@ -303,10 +313,9 @@ __global__ void k_rho_to_rec(double* __restrict__ rec, float* __restrict__ rec32
                              const double* __restrict__ rl, int N) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  if (rec32)
-    rec32[(long long)i * Layout32<D>::REC + Layout32<D>::RHO] = (float)rl[2 * (long long)i];
-  else
-    rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
+  // both records: an fp32 context may evaluate with the fp64 kernels (range guard)
+  if (rec32) rec32[(long long)i * Layout32<D>::REC + Layout32<D>::RHO] = (float)rl[2 * (long long)i];
+  rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
 }
 
 // ---- HMC transition (Neal 2011): counter-based random numbers on the device.

@@ -9,7 +9,9 @@ static int lf_prepare(hawkes_ctx* ctx, int32_t mem, const double* inv_mass, cons
   const size_t n = (size_t)ctx->N * ctx->D;
   if (!ctx->lf_x) {
     int rc;
-    if ((rc = dalloc(ctx, &ctx->lf_x, n)) || (rc = dalloc(ctx, &ctx->lf_p, n))) return rc;
+    if ((rc = dalloc(ctx, &ctx->lf_x, n)) || (rc = dalloc(ctx, &ctx->lf_p, n)) ||
+        (rc = dalloc(ctx, &ctx->lf_x0, n)) || (rc = dalloc(ctx, &ctx->lf_p0, n)))
+      return rc;
   }
   if (inv_mass && !ctx->lf_minv) TRY(dalloc(ctx, &ctx->lf_minv, n));
   if (box_lo && !ctx->lf_lo) {
@@ -77,18 +79,22 @@ int hawkes_leapfrog(hawkes_ctx* ctx, double* x, double* p, int32_t mem, double s
         return set_err(ctx, HAWKES_ERR_NONFINITE, "x or p not finite at %zu", k);
   }
   TRY(lf_prepare(ctx, mem, inv_mass, box_lo, box_hi));
-  TRY(copy_in(ctx, ctx->lf_x, x, n, mem));
-  TRY(copy_in(ctx, ctx->lf_p, p, n, mem));
-  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+  TRY(copy_in(ctx, ctx->lf_x0, x, n, mem));
+  TRY(copy_in(ctx, ctx->lf_p0, p, n, mem));
   TRY(clear_move(ctx));
-  TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
-  ctx->have_x = true;
-  ctx->rates_valid = ctx->grad_valid = false;
-  TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [] { return HAWKES_OK; }));
-  CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-  TRY(copy_out(ctx, x, ctx->lf_x, n, mem));
-  TRY(copy_out(ctx, p, ctx->lf_p, n, mem));
-  TRY(fetch_status(ctx));
+  do {   // twice only if the fp32 range guard sent the context to fp64 during the trajectory
+    CU(cudaMemcpyAsync(ctx->lf_x, ctx->lf_x0, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->lf_p, ctx->lf_p0, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+    TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->lf_x));
+    ctx->have_x = true;
+    ctx->rates_valid = ctx->grad_valid = false;
+    TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [] { return HAWKES_OK; }));
+    CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    TRY(copy_out(ctx, x, ctx->lf_x, n, mem));
+    TRY(copy_out(ctx, p, ctx->lf_p, n, mem));
+    TRY(fetch_status(ctx));
+  } while (take_retry(ctx));
   if (out_ll) *out_ll = (use_h ? ctx->h_st->ell : 0.0) + (use_b ? ctx->h_st->bmds : 0.0);
   if (out_kin) *out_kin = ctx->h_st->kinetic;
   if (ctx->h_st->undefined)
@@ -116,30 +122,40 @@ int hawkes_hmc_step(hawkes_ctx* ctx, uint64_t seed, uint64_t iteration, double s
         return set_err(ctx, HAWKES_ERR_ARG, "inv_mass_diag must be finite and > 0");
   }
   TRY(fetch_status(ctx));   // surface a pending device-side validation failure of x0
+  take_retry(ctx);          // (a guard trip seen here only invalidates the cached rates)
   const size_t n = (size_t)ctx->N * ctx->D;
   TRY(lf_prepare(ctx, mem, inv_mass, box_lo, box_hi));
   TRY(clear_move(ctx));
   const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
-  // x0 = the context's state (records already hold it, so a cached gradient is reused)
-  CU(cudaMemcpyAsync(ctx->lf_x, ctx->xstage, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-  CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
-  const unsigned nq = (unsigned)((n + 1) / 2);
-  k_hmc_momenta<<<(nq + 255) / 256, 256, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr,
-                                                           (long long)n, key, iteration, 0);
-  CHECK_LAUNCH();
-  k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
-  CHECK_LAUNCH();
-  TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [&]() -> int {
-    k_hmc_begin<<<1, 1, 0, ctx->stream>>>(ctx->st, use_h, use_b);
+  // the chain's state, kept for an fp64 re-run of the transition (fp32 range guard)
+  CU(cudaMemcpyAsync(ctx->lf_x0, ctx->xstage, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  for (;;) {
+    // x0 = the context's state (records already hold it, so a cached gradient is reused)
+    CU(cudaMemcpyAsync(ctx->lf_x, ctx->xstage, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemsetAsync(&ctx->st->undefined, 0, sizeof(int), ctx->stream));
+    const unsigned nq = (unsigned)((n + 1) / 2);
+    k_hmc_momenta<<<(nq + 255) / 256, 256, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr,
+                                                             (long long)n, key, iteration, 0);
     CHECK_LAUNCH();
-    return HAWKES_OK;
-  }));
-  k_hmc_decide<<<1, 1, 0, ctx->stream>>>(ctx->st, ctx->bad, use_h, use_b, key, iteration);
-  CHECK_LAUNCH();
-  k_hmc_select<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->xstage, ctx->lf_x, (long long)n,
-                                                                      ctx->st);
-  CHECK_LAUNCH();
-  TRY(fetch_status(ctx));
+    k_kinetic<<<1, 1024, 0, ctx->stream>>>(ctx->lf_p, inv_mass ? ctx->lf_minv : nullptr, (long long)n, ctx->st);
+    CHECK_LAUNCH();
+    TRY(lf_core(ctx, step, n_steps, inv_mass != nullptr, box_lo != nullptr, [&]() -> int {
+      k_hmc_begin<<<1, 1, 0, ctx->stream>>>(ctx->st, use_h, use_b);
+      CHECK_LAUNCH();
+      return HAWKES_OK;
+    }));
+    k_hmc_decide<<<1, 1, 0, ctx->stream>>>(ctx->st, ctx->bad, use_h, use_b, key, iteration);
+    CHECK_LAUNCH();
+    k_hmc_select<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->xstage, ctx->lf_x, (long long)n,
+                                                                        ctx->st);
+    CHECK_LAUNCH();
+    TRY(fetch_status(ctx));
+    if (!take_retry(ctx)) break;
+    // the fp32 range guard tripped in the trajectory: the same transition (same momenta and
+    // uniform) again with the fp64 kernels, from the saved state
+    CU(cudaMemcpyAsync(ctx->xstage, ctx->lf_x0, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    TRY(dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage));
+  }
   const bool acc = ctx->h_st->accepted != 0;
   if (ctx->h_st->undef0) {
     ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
@@ -197,7 +213,8 @@ int hawkes_propose_move(hawkes_ctx* ctx, int32_t k, const int32_t* idx, const do
   TRY(clear_move(ctx));
   if (!ctx->lam_valid) {
     ctx->rates_valid = false;
-    TRY(run_rates(ctx));
+    // fp32: one host sync to check the range guard before the moves use these rates
+    TRY(use32(ctx) ? checked_rates(ctx) : run_rates(ctx));
     if (!ctx->pairs && !ctx->rates_exchanged) {
       TRY(exchange_rows(ctx, ctx->rates, 4));
       ctx->rates_exchanged = true;
@@ -317,7 +334,8 @@ int hawkes_mh_sweep(hawkes_ctx* ctx, int32_t n_blocks, int32_t k, const int32_t*
   CU(cudaMemcpyAsync(ctx->d_mh_blocks, blocks, total * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   if (!ctx->lam_valid) {
     ctx->rates_valid = false;
-    TRY(run_rates(ctx));
+    // fp32: one host sync to check the range guard before the moves use these rates
+    TRY(use32(ctx) ? checked_rates(ctx) : run_rates(ctx));
     if (!ctx->pairs && !ctx->rates_exchanged) {
       TRY(exchange_rows(ctx, ctx->rates, 4));
       ctx->rates_exchanged = true;

@@ -253,6 +253,14 @@ class HawkesContext:
         check(self._lib.hawkes_accept_move(self._h), self._h)
 
     # -- timing (CUDA events recorded by the library around the two pass kernels)
+    @property
+    def precision_in_use(self) -> str:
+        """hawkes_precision_in_use: "fp32", or "fp64" once an fp32 context's range guard
+        (reading R23) sent it to the fp64 kernels."""
+        v = ctypes.c_int32()
+        check(self._lib.hawkes_precision_in_use(self._h, ctypes.byref(v)), self._h)
+        return "fp32" if v.value == HAWKES_FP32 else "fp64"
+
     def enable_timing(self, enable: bool = True):
         check(self._lib.hawkes_enable_timing(self._h, int(bool(enable))), self._h)
 

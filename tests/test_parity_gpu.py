@@ -485,3 +485,72 @@ def test_largest_size_1m_sampled_rows_and_properties(precision):
             ctx.set_locations(x - eps * torch.from_numpy(V).cuda())
             lm = ctx.loglik()
             assert abs((lp - lm) / (2 * eps) - float(np.sum(g * V))) <= 1e-6 * np.sum(np.abs(g * V))
+
+
+def _fuzz_case(seed, case, nmax):
+    import importlib.util
+    import os
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "fuzz_parity.py")
+    spec = importlib.util.spec_from_file_location("fuzz_parity", p)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    rng = np.random.default_rng(seed)
+    for _ in range(case + 1):
+        out = mod.make_case(rng, nmax)
+    return out
+
+
+@pytest.mark.parametrize("algorithm", ["pairs", "rows"])
+def test_fp32_range_guard_falls_back_to_fp64(algorithm):
+    """Reading R23: round 1's one fuzz failure (seed 12, case 290: D = 7, lambda_n from 4e-35
+    to 6e-11) lost rate terms to the fp32 flush.  The range guard now detects it, the call is
+    redone by the fp64 kernels (precision_in_use reports fp64) and the result meets the fp32
+    gate -- in fact the fp64 one; set_params re-arms fp32.  A well-scaled catalog stays on fp32."""
+    from paper_2010_02994_b200 import HawkesContext
+    N, D, x, t, th, _, _, _ = _fuzz_case(12, 290, 4000)
+    ell_r, _, _, g_r, S = oracle_eval(x, t, th)
+    with HawkesContext(N, D, precision="fp32", algorithm=algorithm) as ctx:
+        ctx.set_times(t)
+        ctx.set_locations(x)
+        ctx.set_params(th)
+        assert ctx.precision_in_use == "fp32"
+        g, ell = ctx.grad_locations()
+        assert ctx.precision_in_use == "fp64"
+        assert_parity(ell, g.cpu().numpy(), ell_r, g_r, S, precision="fp64", what="guarded fp32")
+        ctx.set_params(th)
+        assert ctx.precision_in_use == "fp32"
+        assert ctx.loglik() == pytest.approx(ell_r, rel=1e-9)      # loglik alone trips it too
+        assert ctx.precision_in_use == "fp64"
+    c = synth.config("C3", 3000)
+    with HawkesContext(c.N, c.D, precision="fp32", algorithm=algorithm) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_locations(c.x)
+        ctx.set_params(c.theta)
+        g, ell = ctx.grad_locations()
+        assert ctx.precision_in_use == "fp32"
+    ell_r, _, _, g_r, S = oracle_eval(c.x, c.t, c.theta)
+    assert_parity(ell, g.cpu().numpy(), ell_r, g_r, S, precision="fp32", what="C3 fp32")
+
+
+def test_fp32_range_guard_in_leapfrog_and_hmc():
+    """The guarded catalog through the samplers: an fp32 leapfrog / HMC transition returns the
+    fp64 trajectory / decision (same as an fp64 context)."""
+    from paper_2010_02994_b200 import HawkesContext
+    N, D, x, t, th, _, _, _ = _fuzz_case(12, 290, 4000)
+    p0 = synth.momenta(N, D, seed=5)
+    res = {}
+    for prec in ("fp32", "fp64"):
+        with HawkesContext(N, D, precision=prec) as ctx:
+            ctx.set_times(t)
+            ctx.set_params(th)
+            xx = torch.from_numpy(x.copy()).cuda()
+            pp = torch.from_numpy(p0.copy()).cuda()
+            _, _, ell, kin = ctx.leapfrog(xx, pp, 1e-3, 3)
+            ctx.set_params(th)                       # re-arm fp32 for the HMC transition
+            ctx.set_locations(x)
+            acc, la = ctx.hmc_step(3, 1, 1e-3, 3)
+            res[prec] = (xx.cpu().numpy(), ell, kin, acc, la, ctx.precision_in_use)
+    assert res["fp32"][5] == "fp64"
+    assert np.allclose(res["fp32"][0], res["fp64"][0], rtol=0, atol=1e-12 * np.abs(x).max())
+    assert res["fp32"][1] == pytest.approx(res["fp64"][1], rel=1e-12)
+    assert res["fp32"][3] == res["fp64"][3] and res["fp32"][4] == pytest.approx(res["fp64"][4], abs=1e-9)

@@ -18,18 +18,9 @@ import numpy as np  # noqa: E402
 import oracle  # noqa: E402
 from tests.gpu_helpers import TOL, gpu_eval  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--cases", type=int, default=200)
-ap.add_argument("--seed", type=int, default=1)
-ap.add_argument("--nmax", type=int, default=2500)
-ap.add_argument("--only", type=int, default=-1, help="re-run one case (same random stream)")
-ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
-a = ap.parse_args()
-rng = np.random.default_rng(a.seed)
-fails = 0
-worst = {"fp64": 0.0, "fp32": 0.0}
-for case in range(a.cases):
-    N = int(rng.integers(2, a.nmax))
+def make_case(rng, nmax):
+    """One random case: (N, D, x, t, theta, precision, algorithm, emulated W)."""
+    N = int(rng.integers(2, nmax))
     D = int(rng.integers(1, 9))
     scale = float(10 ** rng.uniform(-2, 3))            # spatial units
     tscale = float(10 ** rng.uniform(-1, 3))           # time units
@@ -51,33 +42,49 @@ for case in range(a.cases):
     prec = "fp64" if rng.uniform() < 0.7 else "fp32"
     alg = ["auto", "pairs", "rows"][int(rng.integers(0, 3))]
     W = int(rng.choice([0, 0, 0, 2, 3]))
-    if a.only >= 0:
-        if case != a.only:
-            continue
-        alg = a.alg or alg
-    info = {"case": case, "N": N, "D": D, "prec": prec, "alg": alg, "W": W, "theta": th}
-    try:
-        ell_r, lam_r, _ = oracle.loglik(x, t, th)
-        if not np.isfinite(ell_r):
+    return N, D, x, t, th, prec, alg, W
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--nmax", type=int, default=2500)
+    ap.add_argument("--only", type=int, default=-1, help="re-run one case (same random stream)")
+    ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    fails = 0
+    worst = {"fp64": 0.0, "fp32": 0.0}
+    for case in range(a.cases):
+        N, D, x, t, th, prec, alg, W = make_case(rng, a.nmax)
+        if a.only >= 0:
+            if case != a.only:
+                continue
+            alg = a.alg or alg
+        info = {"case": case, "N": N, "D": D, "prec": prec, "alg": alg, "W": W, "theta": th}
+        try:
+            ell_r, lam_r, _ = oracle.loglik(x, t, th)
+            if not np.isfinite(ell_r):
+                ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
+                if prec == "fp64" and np.isfinite(ell):
+                    fails += 1
+                    print(json.dumps({**info, "fail": "oracle -inf, gpu finite", "ell": ell}), flush=True)
+                continue
+            g_r, S = oracle.grad(x, t, th, lam=lam_r)
             ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
-            if prec == "fp64" and np.isfinite(ell):
+            if prec == "fp32" and not np.isfinite(ell):
+                continue                                   # fp32 range (reading R23)
+            tol, floor = TOL[prec]
+            e_ell = abs(ell - ell_r) / abs(ell_r)
+            bound = tol * np.maximum(np.abs(g_r), floor * S)
+            ratio = float(np.max(np.abs(g - g_r) / np.maximum(bound, 1e-300))) if g is not None else math.inf
+            worst[prec] = max(worst[prec], ratio)
+            if e_ell > tol or ratio > 1.0:
                 fails += 1
-                print(json.dumps({**info, "fail": "oracle -inf, gpu finite", "ell": ell}), flush=True)
-            continue
-        g_r, S = oracle.grad(x, t, th, lam=lam_r)
-        ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
-        if prec == "fp32" and not np.isfinite(ell):
-            continue                                   # fp32 range (reading R23)
-        tol, floor = TOL[prec]
-        e_ell = abs(ell - ell_r) / abs(ell_r)
-        bound = tol * np.maximum(np.abs(g_r), floor * S)
-        ratio = float(np.max(np.abs(g - g_r) / np.maximum(bound, 1e-300))) if g is not None else math.inf
-        worst[prec] = max(worst[prec], ratio)
-        if e_ell > tol or ratio > 1.0:
+                print(json.dumps({**info, "fail": "tolerance", "ell_rel": e_ell, "grad_ratio": ratio}), flush=True)
+        except Exception as e:  # noqa: BLE001
             fails += 1
-            print(json.dumps({**info, "fail": "tolerance", "ell_rel": e_ell, "grad_ratio": ratio}), flush=True)
-    except Exception as e:  # noqa: BLE001
-        fails += 1
-        print(json.dumps({**info, "fail": "exception", "error": repr(e)[:300]}), flush=True)
-        traceback.print_exc()
-print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "worst_grad_ratio": worst}), flush=True)
+            print(json.dumps({**info, "fail": "exception", "error": repr(e)[:300]}), flush=True)
+            traceback.print_exc()
+    print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "worst_grad_ratio": worst}), flush=True)
