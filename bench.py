@@ -27,20 +27,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-8 B200"
-# FP64-pipe work per ordered pair (DESIGN.md §4 "Roofline"; tools/falg_count.py):
-#   F_IMPL  the unordered-pair algorithm as implemented: FP64 instructions of the shipped
-#           sym_kernel's unmasked hot loop / 8 (one step = 4 unordered pairs) -- the
-#           algorithmic work of this design, excluding masked / padding pairs (headline);
-#           the gradient pass's 8 I2F.F64 per step run on the conversion pipe, not counted
-#   F_UNO   SURVEY's method (naive per-pair bodies with libdevice exp) for unordered pairs
-#   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg
-F_IMPL = (12.5, 13.5)
+# Roofline basis (DESIGN.md §4 "Roofline"), per ORDERED pair, D = 2, (rate pass, gradient pass):
+#   F_ALG   frozen algorithmic FP64 work of the unordered-pair method with a u-accurate table
+#           exp costed at 7 FP64 operations (range reduction 3, degree-3 polynomial 3,
+#           reconstruction 1), per unordered pair: rate pass 10 (dx, dy, r^2 (2), dt, background
+#           exponent 3, self-excitation exponent 2) + 14 (two exps) + 3 (row mu, column mu, column
+#           xi sums) = 27; gradient pass 10 + 14 + 3 (c = rho_i mu + rho_j (mu + xi)) + 4 (two
+#           gradient updates) = 31.  It does not move when the shipped instruction count moves,
+#           so removing instructions raises frac (the headline).
+#   F_PIPE  FP64-pipe instructions per ordered pair of the shipped sym_kernel's unmasked hot loop
+#           (tools/falg_count.py --shipped): pipe utilisation, reported beside it.  The gradient
+#           pass's 8 I2F.F64 per step run on the conversion pipe and are not counted.
+#   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg (libdevice exp, ordered pairs): context.
+F_ALG = (13.5, 15.5)
+F_PIPE = (13.5, 14.0)
 # fp32 variant: FMA-pipe instructions per ordered pair of sym_kernel_f32's hot loop (packed
-# FFMA2 / FADD2 / FMUL2 = 1 per lane; tools/falg_count.py's method on its SASS); its peak is
-# one packed warp-instruction per 2 cycles per SMSP = 64 lanes/clk/SM, which reproduces ncu's
-# FMA-pipe utilisation of these kernels (profiles/r01_ncu_full_summary_fp32.txt: 76.7 / 74.2 %)
+# FFMA2 / FADD2 / FMUL2 = 1 per lane; SASS); its peak is one packed warp-instruction per 2
+# cycles per SMSP = 64 lanes/clk/SM.  MUFU: one ex2 per ordered pair per pass (two per unordered
+# pair), 16 / clk / SM.
 F_IMPL32 = (5.0, 6.0)
-F_UNO = (26.0, 28.5)
+MUFU_PER_SM = 16
 F_SURVEY = (34.5, 49.0)
 FP64_LANES_PER_SM = 64
 
@@ -404,7 +410,7 @@ def run_ours(args):
     fp32_pairs = ctx.algorithm in ("auto", "pairs") and args.precision == "fp32"
     if unordered:
         names = ("rate pass: sym_kernel<2,1,4,4>", "gradient pass: sym_kernel<2,2,4,4>")
-        F_impl = F_IMPL
+        F_impl = F_PIPE
     elif fp32_pairs:
         names = ("rate pass: sym_kernel_f32<2,1,4,1>", "gradient pass: sym_kernel_f32<2,2,4,1>")
         F_impl = F_IMPL32
@@ -414,10 +420,10 @@ def run_ours(args):
     pi = 1 if grad_avg >= rate_avg else 0
     dom, avg_ms = names[pi], (grad_avg if pi else rate_avg)
     props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak = props.multi_processor_count * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12   # T ops/s
-    rate_units = pairs_alg / (avg_ms * 1e-3) / 1e12      # T ordered pairs/s x ops
-    achieved = F_impl[pi] * rate_units
+    peak = sms * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12   # T lane-ops/s (FP64 pipe / FMA pipe)
+    rate_units = pairs_alg / (avg_ms * 1e-3) / 1e12      # T ordered pairs/s
     traffic = _ncu_traffic(dom.split(": ")[1]) if unordered else None
     try:
         dfma_peak = diag_fp64_peak() / 1e12
@@ -425,27 +431,42 @@ def run_ours(args):
         dfma_peak = None
 
     if fp32_pairs:
+        mufu_peak = sms * MUFU_PER_SM * sm_max * 1e6 / 1e12
+        achieved = F_impl[pi] * rate_units
         roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
                     "unit": "T FMA-pipe instructions/s (one per lane; packed FFMA2/FADD2/FMUL2 = 1)",
                     "frac": achieved / peak, "traffic": traffic,
-                    "peak_basis": f"{props.multi_processor_count} SMs x 64 lanes x {sm_max:.0f} MHz "
+                    "peak_basis": f"{sms} SMs x 64 lanes x {sm_max:.0f} MHz "
                                   "(one packed FP32 warp-instruction per 2 cycles per SMSP)",
                     "ops_per_pair": F_impl[pi],
                     "ops_per_pair_basis": "FMA-pipe instructions per ordered pair of the shipped "
-                                          "sym_kernel_f32's hot loop (SASS)"}
-    else:
+                                          "sym_kernel_f32's hot loop (SASS)",
+                    "mufu": {"achieved": rate_units, "peak": mufu_peak, "frac": rate_units / mufu_peak,
+                             "unit": "T ex2/s", "basis": f"1 MUFU ex2 per ordered pair; {sms} SMs x 16 "
+                                                         f"/clk x {sm_max:.0f} MHz"}}
+    elif unordered:
+        achieved = F_ALG[pi] * rate_units
         roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
-                    "unit": "T FP64-pipe instructions/s (one per lane; DFMA = 1)", "frac": achieved / peak,
+                    "unit": "T FP64 ops/s (algorithmic; DFMA = 1)", "frac": achieved / peak,
                     "traffic": traffic,
-                    "peak_basis": f"{props.multi_processor_count} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
-                    "ops_per_pair": F_impl[pi],
-                    "ops_per_pair_basis": "FP64 instructions per ordered pair of the shipped kernel's "
-                                          "unmasked hot loop (tools/falg_count.py --shipped)",
-                    "unordered_falg": {"ops_per_pair": F_UNO[pi], "frac": F_UNO[pi] * rate_units / peak,
-                                       "basis": "SURVEY's method (naive libdevice-exp bodies) for unordered pairs"},
+                    "peak_basis": f"{sms} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
+                    "ops_per_pair": F_ALG[pi],
+                    "ops_per_pair_basis": "frozen algorithmic FP64 operations per ordered pair of the "
+                                          "unordered-pair method with a u-accurate 7-op table exp "
+                                          "(DESIGN.md §4 Roofline)",
+                    "fp64_pipe": {"instr_per_pair": F_impl[pi], "frac": F_impl[pi] * rate_units / peak,
+                                  "basis": "FP64 instructions per ordered pair of the shipped hot loop "
+                                           "(tools/falg_count.py --shipped): pipe utilisation"},
                     "survey_falg": {"ops_per_pair": F_SURVEY[pi], "frac": F_SURVEY[pi] * rate_units / peak,
-                                    "basis": "SURVEY.md 8(d) ordered-pair F_alg (frozen)"},
+                                    "basis": "SURVEY.md 8(d) ordered-pair F_alg (frozen; libdevice exp, "
+                                             "ordered pairs)"},
                     "measured_dfma_peak": dfma_peak}
+    else:
+        achieved = F_impl[pi] * rate_units
+        roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "unit": "T FP64-pipe instructions/s (DFMA = 1)", "frac": achieved / peak,
+                    "traffic": None, "peak_basis": f"{sms} SMs x 64 FP64 lanes x {sm_max:.0f} MHz",
+                    "ops_per_pair": F_impl[pi], "ops_per_pair_basis": "ROWS kernel SASS count"}
     out = {
         "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,

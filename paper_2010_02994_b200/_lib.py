@@ -9,6 +9,8 @@ import ctypes
 import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhawkes_b200.so")
+# diagnostics only (tools/ab_builds.py): load an A/B build of the same sources instead
+LIB_PATH = os.environ.get("HAWKES_LIB_AB", LIB_PATH)
 
 HAWKES_OK = 0
 STATUS = {

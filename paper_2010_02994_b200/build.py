@@ -40,21 +40,24 @@ def sources():
                   + [os.path.join(ROOT, "include", "hawkes.h")])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Build the library (out: another path, with extra -D defines, for A/B builds)."""
     srcs = sources()
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+    lib = out or LIB
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(s) <= t for s in srcs):
-            return LIB
+            return lib
     cus = [s for s in srcs if s.endswith(".cu")]
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
            "-Xptxas", "-v" if verbose else "-O3", "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", _nccl_include(), *cus, "-o", LIB + ".tmp", "-ldl", "-lcudart"]
+           "-I", _nccl_include(), *[f"-D{d}" for d in defines], *cus, "-o", lib + ".tmp",
+           "-ldl", "-lcudart"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -117,10 +117,13 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   int rc;
   if ((rc = dalloc(ctx, &ctx->rec, (size_t)ctx->npad * REC)) ||
       (rc = dalloc(ctx, &ctx->gid, (size_t)ctx->npad)) ||
-      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nslots * ctx->npad * K1_of(D))) ||
+      // PAIRS' rate partials are (M', X') only (K1P = 2): half the memory at D = 2 that the
+      // ROWS layout (M', X', G1') takes -- 211 MB instead of 422 MB at N = 100k
+      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nslots * ctx->npad * (ctx->pairs ? K1P : K1_of(D)))) ||
       (rc = dalloc(ctx, &ctx->part2, (size_t)ctx->nslots * ctx->npad * K2_of(D))) ||
       (rc = dalloc(ctx, &ctx->G1, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->rl, (size_t)ctx->npad * 2)) ||
+      (rc = dalloc(ctx, &ctx->lrho, (size_t)ctx->npad)) ||
       (rc = dalloc(ctx, &ctx->rates, (size_t)ctx->npad * 4)) ||
       (rc = dalloc(ctx, &ctx->grad, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->xstage, (size_t)N * D)) ||
@@ -135,7 +138,8 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
       (rc = dalloc(ctx, &ctx->d_move_part, (size_t)(N + 255) / 256)) ||
       (rc = dalloc(ctx, &ctx->d_move_rows_part, (size_t)MOVE_MAX * 2 * MOVE_NSPLIT)))
     return fail(rc);
-  if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess)
+  if (cudaMemset(ctx->d_slot_of, 0xff, (size_t)N * sizeof(int)) != cudaSuccess ||
+      cudaMemset(ctx->lrho, 0, (size_t)ctx->npad * sizeof(double)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
   if (!ctx->multi && !getenv("HAWKES_NO_GRAPHS")) {
     if (cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) != cudaSuccess)
@@ -167,7 +171,7 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
     }
     if (ctx->multi) {
       const size_t copies = (size_t)ctx->W + 1;   // row 0: the sum; rows 1..W: per-rank sums
-      if ((rc = dalloc(ctx, &ctx->sums1, copies * ctx->npad * K1_of(D))) ||
+      if ((rc = dalloc(ctx, &ctx->sums1, copies * ctx->npad * K1P)) ||
           (rc = dalloc(ctx, &ctx->sums2, copies * ctx->npad * K2_of(D))))
         return fail(rc);
     }
@@ -251,7 +255,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamDestroy(ctx->gstream);
   }
   void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
-                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->rates,
+                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->lrho, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->ell_part, ctx->tab,
                   ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->lf_x0, ctx->lf_p0, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};

@@ -121,6 +121,7 @@ struct hawkes_ctx {
   double* part2 = nullptr; // nchunks x npad x K2
   double* G1 = nullptr;    // npad x D
   double* rl = nullptr;    // npad x 2 (rho', ell_n)
+  double* lrho = nullptr;  // npad: -ln lambda_n (PAIRS fp64 gradient pass; hawkes_kernels_sym.cuh)
   double* rates = nullptr; // npad x 4 (lambda, mu, xi, Lambda)
   double* grad = nullptr;  // npad x D
   double* xstage = nullptr;// N x D staging

@@ -358,6 +358,7 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   pc.omega = p.omega;
   pc.lnc_b = p.mu0 > 0 ? lnw_b + 64.0 * LN2 : -INFINITY;
   pc.lnc_s = p.theta > 0 ? lnw_s + 64.0 * LN2 : -INFINITY;
+  pc.lnc_sr = p.theta > 0 ? lnw_s : -INFINITY;
   if (!isfinite(pc.kx) || !isfinite(pc.kt) || !isfinite(pc.ks))
     return set_err(ctx, HAWKES_ERR_PARAM, "bandwidths too small for fp64");
   FinConst fc;

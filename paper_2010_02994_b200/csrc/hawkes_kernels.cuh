@@ -50,13 +50,15 @@ struct PassConst {
   double omega;
   double lnc_b;        // log(mu0/((2pi)^{(D+1)/2} tau_x^D tau_t) / tau_x^2 * 2^64)
   double lnc_s;        // log(theta omega/((2pi)^{D/2} h^D) / h^2 * 2^64)
+  double lnc_sr;       // lnc_s - 64 ln 2: the unordered-pair gradient pass folds -ln lambda_j
+                       // into the self-excitation exponent (hawkes_kernels_sym.cuh)
 };
 
-// ---------------------------------------------------------------- fast fp64 exp
+// ---------------------------------------------------------------- table fp64 exp
 // e^a for the pair kernels.  On sm_100 an FP64 instruction holds its SM sub-partition's
 // dispatch for two cycles and every other instruction for one (measured: the FP64 pipe
 // utilisation of a kernel tracks 2*n_fp64 / (2*n_fp64 + n_other)), so this exp is
-// built to minimise both: 6 FP64 instructions and 5 integer/shared-memory ones.
+// built to minimise both: 7 FP64 instructions and 5 integer/shared-memory ones.
 //   a' = max(a, AMIN)            one unsigned min on the high word (AMIN = -707: for
 //                                negative doubles a larger high word means a larger |a|;
 //                                positive a, high bit clear, pass through)
@@ -66,24 +68,18 @@ struct PassConst {
 //   T  = 2^(j/2048) from a 2048-entry (16 KB) shared table whose high words are
 //        pre-biased by -(j << 9), so that one integer multiply-add, hi + (k << 9), also
 //        adds m to the exponent field
-//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + c2 r)  (minimax, tools/fit_exp_poly.py 2048 2:
-//        |rel. err.| <= 8.1e-13 on |r| <= ln2/4096)
-// The 2048-entry table and degree 2 save one FP64 instruction per exp against a 256-entry
-// table with degree 3 (-DHK_EXP256, 2.4e-14): 4.7 % per evaluation at N = 100k
-// (profiles/r01_sym_variants.txt), and 8e-13 stays three orders of magnitude inside the
-// 1e-9 parity tolerance (reading R23).
+//   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + r (c2 + c3 r))  (minimax, tools/fit_exp_poly.py
+//        2048 3: |rel. err.| <= 5.9e-18 on |r| <= ln2/4096, so the result is within a few
+//        ulp of e^a': u-accurate, like the oracle's libm exp -- SURVEY.md §7 asks for
+//        <~1e-15 because gradient components cancel)
+// Round 1 shipped degree 2 (6 FP64, 8.1e-13; -DHK_EXP_FAST keeps it for A/B): its error
+// is systematic per table cell, so a gradient component's error reached ~7000 u S_nd and
+// the plain relative error exceeded 1e-9 from kappa ~ 8e3 (profiles/r02_plain_error_r01kernel.jsonl),
+// where a u-accurate sum stays below it up to kappa ~ 1e6.
 // Arguments below AMIN return e^(a') ~ e^-707 instead of a smaller number (callers treat
 // sums below N e^-700 as zero; reading R23).  Arguments must be < ~700
 // (guaranteed by the validated kernel constants).
-#ifndef HK_EXP256
-constexpr double EXP_K = 2954.639443740597;                 // 2048/ln2
-constexpr double EXP_C = 3.3845077175778579e-04;            // ln2/2048
-constexpr double EXP_C2 = 0.499999996420339;
-constexpr double EXP_C3 = 0.0;                              // unused
-constexpr int EXP_TABLE = 2048;
-constexpr int EXP_BIAS_SHIFT = 9;                           // 20 - log2(EXP_TABLE)
-constexpr int EXP_DEGREE = 2;
-#else   // the 256-entry, degree-3 exp (tools/fit_exp_poly.py 256 3: 2.4e-14)
+#if defined(HK_EXP256)   // the 256-entry, degree-3 exp (tools/fit_exp_poly.py 256 3: 2.4e-14)
 constexpr double EXP_K = 369.3299304675746;                // 256/ln2
 constexpr double EXP_C = 0.0027076061740622863;            // ln2/256
 constexpr double EXP_C2 = 0.5000000632802307;
@@ -91,6 +87,20 @@ constexpr double EXP_C3 = 0.1666666688540192;
 constexpr int EXP_TABLE = 256;
 constexpr int EXP_BIAS_SHIFT = 12;                          // 20 - log2(EXP_TABLE)
 constexpr int EXP_DEGREE = 3;
+#else
+constexpr double EXP_K = 2954.639443740597;                 // 2048/ln2
+constexpr double EXP_C = 3.3845077175778579e-04;            // ln2/2048
+constexpr int EXP_TABLE = 2048;
+constexpr int EXP_BIAS_SHIFT = 9;                           // 20 - log2(EXP_TABLE)
+#if defined(HK_EXP_FAST)  // round 1: degree 2, 8.1e-13
+constexpr double EXP_C2 = 0.499999996420339;
+constexpr double EXP_C3 = 0.0;                              // unused
+constexpr int EXP_DEGREE = 2;
+#else
+constexpr double EXP_C2 = 0.5000000009888816;               // 0x1.000000087e92ep-1
+constexpr double EXP_C3 = 0.16666666670097202;              // 0x1.5555555683162p-3
+constexpr int EXP_DEGREE = 3;
+#endif
 #endif
 constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
 constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
@@ -147,6 +157,23 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// two bulk copies completing on one barrier (one arrive with the summed byte count)
+__device__ __forceinline__ void tma_load_1d_x2(void* dst0, const void* src0, uint32_t bytes0, void* dst1,
+                                               const void* src1, uint32_t bytes1, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes0 + bytes1)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst0)),
+      "l"(src0), "r"(bytes0), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst1)),
+      "l"(src1), "r"(bytes1), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

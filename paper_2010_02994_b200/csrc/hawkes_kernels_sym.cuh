@@ -4,7 +4,10 @@
 // (P:L98-99), so one evaluation of the two exps of an unordered pair {i, j} (i earlier)
 // serves both events:
 //   pass 1  row i: M += mu'                 col j: M += mu', X += xi'   (rates only)
-//   pass 2  c = rho'_i mu' + rho'_j (mu' + xi'):   g_i += c dx,   g_j -= c dx
+//   pass 2  c = (rho'_i + rho'_j) mu' + rho'_j xi':   g_i += c dx,   g_j -= c dx
+//           where rho'_j xi' comes out of one exp: -ln lambda_j (per event, written by the
+//           rate finalize) is folded into the self-excitation exponent, so the coefficient
+//           costs one add and one fma
 // with dx = x_j - x_i and the scaled-domain terms of hawkes_kernels.cuh (mu' = alpha mu 2^64,
 // xi' = beta xi_ji 2^64).  App. A's coefficient of the pair is the same for both events
 // ((mu_ij/lambda_i + mu_ji/lambda_j)/tau_x^2 + (xi_ij/lambda_i + xi_ji/lambda_j)/h^2 with
@@ -43,6 +46,7 @@ constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : 2;
 
 struct SymArgs {
   const double* rec;
+  const double* lrho;    // pass 2: -ln lambda_j per event (npad), staged beside the records
   const int* gid;
   const int2* items;     // (a, b) chunk pairs, a < b
   int* counter;
@@ -90,7 +94,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
 
 template <int D, bool MASK, bool SELF, int TS>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
-                                          double crho, bool dead, double (&rG)[D],
+                                          double crho, double cL, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
                                           const int2* __restrict__ tab) {
   double dx[D];
@@ -101,16 +105,29 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
-  double eb = fexp<TS, (D <= 5)>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
-  double es = SELF ? fexp<TS, (D <= 5)>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+#ifdef HK_PASS2_NO_I2F
+  constexpr bool I2F = false;
+#else
+  constexpr bool I2F = D <= 5;
+#endif
+  double eb = fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+#ifndef HK_NO_FOLD
+  // rho'_j xi' = beta xi_ji / lambda_j: the column's cL = lnc_s - 64 ln 2 - ln lambda_j
+  double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, cL)), tab, lane_off) : 0.0;
+#else   // round 1's coefficient (A/B): xi' alone, weighted by rho'_j below
+  double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+#endif
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
   }
-  // the pair's App. A coefficient, the same for both events.  (Folding log rho'_j into the
-  // self-excitation exponent saves one FP64 instruction per pair but measured 2 % slower:
-  // the column's extra shared load sits on the exponent's dependency chain.)
+  // the pair's App. A coefficient, the same for both events
+#ifndef HK_NO_FOLD
+  const double rs = row.rho + crho;
+  const double cc = SELF ? fma(rs, eb, es) : rs * eb;
+#else
   const double cc = fma(row.rho, eb, crho * (SELF ? eb + es : eb));
+#endif
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     rG[d] = fma(cc, dx[d], rG[d]);
@@ -123,7 +140,8 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
 template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
-                                          const double* __restrict__ grp, int cg0, bool cvalid0,
+                                          const double* __restrict__ grp,
+                                          const double* __restrict__ lgrp, int cg0, bool cvalid0,
                                           int ridx0, int cidx0, bool diag,
                                           double (&rM)[SYM_R], double (&rG)[SYM_R][D],
                                           double (&cacc)[2 + D], const PassConst& c,
@@ -136,12 +154,13 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
     // column (l + s) mod 32 of this warp's group: from the staged tile (AoS records), or
     // from the warp's transposed copy (SOA: component pair p of column e at [p][e])
     double cx[D];
-    double ct, crho = 0.0;
-    if (SOA) {
+    double ct, crho = 0.0, cL = 0.0;
+    if (SOA) {   // pass 2: (x, t, rho', cL) of the column, cL in the pair after (x, t, rho')
       const double2* g2 = reinterpret_cast<const double2*>(grp);
-      double v[REC];
+      constexpr int NP = PASS == 2 ? (D + 4) / 2 : (D + 2) / 2;
+      double v[2 * NP];
 #pragma unroll
-      for (int p = 0; p < (PASS == 2 ? (D + 2 + 1) / 2 : (D + 1 + 1) / 2); ++p) {
+      for (int p = 0; p < NP; ++p) {
         const double2 w = g2[p * 32 + src];
         v[2 * p] = w.x;
         v[2 * p + 1] = w.y;
@@ -149,13 +168,19 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
 #pragma unroll
       for (int d = 0; d < D; ++d) cx[d] = v[d];
       ct = v[D];
-      if (PASS == 2) crho = v[D + 1];
+      if (PASS == 2) {
+        crho = v[D + 1];
+        cL = v[D + 2];
+      }
     } else {
       const double* rc = grp + src * REC;
 #pragma unroll
       for (int d = 0; d < D; ++d) cx[d] = rc[d];
       ct = rc[D];
-      if (PASS == 2) crho = rc[D + 1];
+      if (PASS == 2) {
+        crho = rc[D + 1];
+        cL = c.lnc_sr + lgrp[src];
+      }
     }
     int cg = 0;
     bool cv = true;
@@ -170,6 +195,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
         for (int d = 0; d < D; ++d) cx[d] = 0.0;
         ct = 0.0;
         crho = 0.0;
+        cL = 0.0;
       }
     }
     double cG[D];
@@ -184,7 +210,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       if (PASS == 1)
         sym_pair1<D, MASK, SELF, TS>(row[r], cx, ct, dead, rM[r], cacc[0], cacc[1], c, tab);
       else
-        sym_pair2<D, MASK, SELF, TS>(row[r], cx, ct, crho, dead, rG[r], cG, c, tab);
+        sym_pair2<D, MASK, SELF, TS>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -223,18 +249,32 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
   constexpr int KR = PASS == 1 ? 1 : D;       // row sums reduced over warps: M or G
   constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
   constexpr int TS = REPL ? TAB_COPIES : 1;
+  constexpr int LST = PASS == 2 ? TILE_J : 0;            // -ln lambda of the staged columns
+  constexpr int SOAW = PASS == 2 ? 2 * ((D + 4) / 2) : REC;   // doubles per column in the SoA copy
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage = reinterpret_cast<double*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(double));
+  double* lstage = stage + STAGES * TILE_J * REC;                 // [STAGES][LST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lstage + STAGES * LST);
   int2* tab = reinterpret_cast<int2*>(bars + STAGES);
   double* red = reinterpret_cast<double*>(tab + EXP_TABLE * TS);   // [4 warps][SYM_RT][KR]
-  double* soa = red + 4 * SYM_RT * KR;                            // [4 warps][REC][32] if SOA
+  double* soa = red + 4 * SYM_RT * KR;                            // [4 warps][SOAW][32] if SOA
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int q = tid; q < EXP_TABLE * TS; q += THREADS) tab[q] = a.tab[q / TS];
   const int2* mytab = tab;   // REPL: fexp or-s the lane's copy into the index
-  double* mysoa = soa + warp * 32 * REC;
+  double* mysoa = soa + warp * 32 * SOAW;
+  // stage s <- column tile [jt, jt + cnt): the records, and (pass 2) -ln lambda rounded up to
+  // an even count (16-byte bulk copies; lrho has npad >= N + 1 entries or N even)
+  auto load_stage = [&](int s, int jt, int cnt) {
+    if (PASS == 2)
+      tma_load_1d_x2(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
+                     (uint32_t)(cnt * REC * sizeof(double)), lstage + s * LST, a.lrho + jt,
+                     (uint32_t)(((cnt + 1) & ~1) * sizeof(double)), &bars[s]);
+    else
+      tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
+                  (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
+  };
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -264,9 +304,7 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
     if (tid == 0) {
       for (int s = 0; s < STAGES && prod.rt < n_rt; ++s, prod.next(n_ct, diag)) {
         const int jt = c0 + prod.ct * TILE_J;
-        const int cnt = min(TILE_J, c1 - jt);
-        tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
-                    (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
+        load_stage(s, jt, min(TILE_J, c1 - jt));
       }
     }
 
@@ -327,25 +365,41 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         // of this tile pair, the self-excitation exponent is <= lnc_s - omega dtmin and the
         // background one <= lnc_b + k_t dtmin^2; below the exp's clamp they add nothing
         const double dtmin = fmax(st[D] - t_rlast, 0.0);
-        const bool self_live = c.lnc_s - c.omega * dtmin > CULL_EXPONENT;
-        const bool bg_live = fma(c.kt * dtmin, dtmin, c.lnc_b) > CULL_EXPONENT;
         const double* grp = st + warp * 32 * REC;
-        if (SOA) {   // this lane's column record -> the warp's [pair][32] double2 buffer
+        const double* lgrp = lstage + s * LST + warp * 32;
+        // pass 2's self-excitation exponent carries the column's cL = lnc_s - 64 ln2 - ln
+        // lambda_j: its bound takes the largest cL of this warp's 32 columns
+        double self_bound = c.lnc_s;
+        if (PASS == 2) {
+          double cLmax = cvalid ? c.lnc_sr + lgrp[lane] : -INFINITY;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) cLmax = fmax(cLmax, __shfl_xor_sync(0xffffffffu, cLmax, o));
+          self_bound = cLmax;
+        }
+        const bool self_live = self_bound - c.omega * dtmin > CULL_EXPONENT;
+        const bool bg_live = fma(c.kt * dtmin, dtmin, c.lnc_b) > CULL_EXPONENT;
+        if (SOA) {   // this lane's column record (+ cL) -> the warp's [pair][32] double2 buffer
           const double* rc = grp + lane * REC;
           double2* g2 = reinterpret_cast<double2*>(mysoa);
+          double v[SOAW];
 #pragma unroll
-          for (int p = 0; p < REC / 2; ++p) g2[p * 32 + lane] = make_double2(rc[2 * p], rc[2 * p + 1]);
+          for (int q = 0; q < REC; ++q) v[q] = rc[q];
+          if constexpr (PASS == 2) v[D + 2] = c.lnc_sr + lgrp[lane];
+#pragma unroll
+          for (int q = (PASS == 2 ? D + 3 : REC); q < SOAW; ++q) v[q] = 0.0;
+#pragma unroll
+          for (int p = 0; p < SOAW / 2; ++p) g2[p * 32 + lane] = make_double2(v[2 * p], v[2 * p + 1]);
           __syncwarp();
           grp = mysoa;
         }
         if (!strict)
-          sym_group<D, PASS, true, SYM_R, true, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+          sym_group<D, PASS, true, SYM_R, true, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
                                                          jt + warp * 32, diag_tile, rM, rG, cacc, c, mytab);
         else if (self_live)
-          sym_group<D, PASS, false, SYM_R, true, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+          sym_group<D, PASS, false, SYM_R, true, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
                                                           jt + warp * 32, false, rM, rG, cacc, c, mytab);
         else if (bg_live)
-          sym_group<D, PASS, false, SYM_R, false, TS, SOA>(row, grp, cg, cvalid, row0 + lane,
+          sym_group<D, PASS, false, SYM_R, false, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
                                                            jt + warp * 32, false, rM, rG, cacc, c, mytab);
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
@@ -360,9 +414,7 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         __syncthreads();   // stage s fully consumed
         if (tid == 0 && prod.rt < n_rt) {
           const int jn = c0 + prod.ct * TILE_J;
-          const int cn = min(TILE_J, c1 - jn);
-          tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jn * REC,
-                      (uint32_t)(cn * REC * sizeof(double)), &bars[s]);
+          load_stage(s, jn, min(TILE_J, c1 - jn));
           prod.next(n_ct, diag);
         }
       }

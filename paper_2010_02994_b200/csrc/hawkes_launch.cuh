@@ -14,9 +14,11 @@ template <int D, int PASS, int R, int V>
 size_t sym_smem() {
   const int KR = PASS == 1 ? 1 : D;
   const int copies = (V & 2) ? TAB_COPIES : 1;
-  return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
+  const int soaw = PASS == 2 ? 2 * ((D + 4) / 2) : Layout<D>::REC;   // hawkes_kernels_sym.cuh
+  return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) +
+         (PASS == 2 ? (size_t)STAGES * TILE_J * sizeof(double) : 0) + STAGES * sizeof(uint64_t) +
          (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
-         ((V & 4) ? (size_t)4 * 32 * Layout<D>::REC * sizeof(double) : 0);
+         ((V & 4) ? (size_t)4 * 32 * soaw * sizeof(double) : 0);
 }
 
 // sym_kernel variants: R rows per lane; V1 / V2 = the pass-1 / pass-2 variant bits
@@ -232,6 +234,7 @@ struct PassD {
     if constexpr (D <= SYM_MAX_D) if (ctx->pairs && ctx->n_sym[rank] > 0) {
       SymArgs b;
       b.rec = ctx->rec;
+      b.lrho = ctx->lrho;
       b.gid = ctx->gid;
       b.items = ctx->d_sym[rank];
       b.counter = ctx->counters + 4 * rank + 2 + (pass - 1);
@@ -317,7 +320,7 @@ struct Fin1D {
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
-          ctx->counters + 4 * ctx->W, ctx->st);
+          ctx->counters + 4 * ctx->W, ctx->st, final_here ? ctx->lrho : nullptr);
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,

@@ -160,7 +160,8 @@ template <int D>
 __device__ __forceinline__ double fin1_event(int i, double M, double X, const double* __restrict__ rec,
                                            double* __restrict__ rl, double* __restrict__ rates,
                                            const FinConst& f, double* __restrict__ rec_rho,
-                                           float* __restrict__ rec32_rho, int* __restrict__ range_flag) {
+                                           float* __restrict__ rec32_rho, int* __restrict__ range_flag,
+                                           double* __restrict__ lrho) {
   using L = Layout<D>;
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
@@ -178,6 +179,13 @@ __device__ __forceinline__ double fin1_event(int i, double M, double X, const do
   const double ell = (Lp > 0.0) ? (log(Lp) + f.scale_log2 * LN2) - Lam : -INFINITY;
   rl[2 * (long long)i] = rho;
   rl[2 * (long long)i + 1] = ell;
+  // -ln lambda_i for the unordered-pair gradient pass (folded into its self-excitation
+  // exponent; -inf where rho' = 0).  lambda = Lambda' 2^scale is exact unless it underflows
+  if (lrho) {
+    const double lam = Lp * sc;
+    lrho[i] = !(Lp > 0.0) ? -INFINITY
+              : (lam >= 2.2250738585072014e-308 ? -log(lam) : -(log(Lp) + f.scale_log2 * LN2));
+  }
   // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
   if (rec_rho) rec_rho[(long long)i * L::REC] = rho;
   if (rec32_rho) rec32_rho[(long long)i * Layout32<D>::REC] = (float)rho;
@@ -216,7 +224,7 @@ __global__ void k_fin1(const double* __restrict__ part, long long npad, int nchu
 #pragma unroll
     for (int d = 0; d < D; ++d) G1[(long long)i * D + d] = G[d];
   }
-  fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, range_flag);
+  fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, range_flag, nullptr);
 }
 
 // PAIRS finalizes (every event final on this process): one warp-lane per (event, component)
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
                                                         double* __restrict__ rec_rho,
                                                         float* __restrict__ rec32_rho,
                                                         double* __restrict__ ell_part, int* ticket,
-                                                        EvalStatus* st) {
+                                                        EvalStatus* st, double* __restrict__ lrho) {
   const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, M' or X')
   const int i = (int)(q >> 1);
   // part[(c npad + i) K1P + k], K1P = 2
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
     const double X = __shfl_down_sync(0xffffffffu, M, 1);
     double e = 0.0;
     if (i < N && (threadIdx.x & 1) == 0)
-      e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32);
+      e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32, lrho);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
     if (threadIdx.x == 0) {
