@@ -40,7 +40,7 @@ METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-
 #           pass's 8 I2F.F64 per step run on the conversion pipe and are not counted.
 #   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg (libdevice exp, ordered pairs): context.
 F_ALG = (13.5, 15.5)
-F_PIPE = (13.5, 14.0)
+F_PIPE = (13.5, 14.5)
 # fp32 variant: FMA-pipe instructions per ordered pair of sym_kernel_f32's hot loop (packed
 # FFMA2 / FADD2 / FMUL2 = 1 per lane; SASS); its peak is one packed warp-instruction per 2
 # cycles per SMSP = 64 lanes/clk/SM.  MUFU: one ex2 per ordered pair per pass (two per unordered
@@ -53,8 +53,8 @@ FP64_LANES_PER_SM = 64
 
 def _ncu_traffic(kernel):
     """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed
-    ncu --set full capture (profiles/r01_ncu_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    ncu --set full capture (profiles/r02_ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     try:
         with open(path) as f:
             return json.load(f)[kernel]["bytes"]

@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing without a tool attached
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -249,7 +250,15 @@ int set_err(hawkes_ctx* c, int code, const char* fmt, ...) {
       return set_err(ctx, HAWKES_ERR_NCCL, "%s failed: %s", #call, g_nccl.errStr(r_));  \
   } while (0)
 
+// NVTX range over one ABI call (visible in an nsys / ncu timeline as "hawkes_<call>")
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define NVTX_CALL() NvtxRange nvtx_range_(__func__)
+
 #define ENTER(ctx)                                                                      \
+  NVTX_CALL();                                                                          \
   do {                                                                                  \
     if (!(ctx)) return HAWKES_ERR_ARG;                                                  \
     if ((ctx)->sticky != HAWKES_OK) return (ctx)->sticky;                               \

@@ -4,10 +4,7 @@
 // (P:L98-99), so one evaluation of the two exps of an unordered pair {i, j} (i earlier)
 // serves both events:
 //   pass 1  row i: M += mu'                 col j: M += mu', X += xi'   (rates only)
-//   pass 2  c = (rho'_i + rho'_j) mu' + rho'_j xi':   g_i += c dx,   g_j -= c dx
-//           where rho'_j xi' comes out of one exp: -ln lambda_j (per event, written by the
-//           rate finalize) is folded into the self-excitation exponent, so the coefficient
-//           costs one add and one fma
+//   pass 2  c = rho'_i mu' + rho'_j (mu' + xi'):   g_i += c dx,   g_j -= c dx
 // with dx = x_j - x_i and the scaled-domain terms of hawkes_kernels.cuh (mu' = alpha mu 2^64,
 // xi' = beta xi_ji 2^64).  App. A's coefficient of the pair is the same for both events
 // ((mu_ij/lambda_i + mu_ji/lambda_j)/tau_x^2 + (xi_ij/lambda_i + xi_ji/lambda_j)/h^2 with
@@ -33,6 +30,17 @@
 namespace hk {
 
 constexpr int SYM_RMAX = 4;               // largest rows-per-lane variant
+// -DHK_SYM_FOLD: pass 2 folds -ln lambda_j (staged beside the records) into the
+// self-excitation exponent, so rho'_j xi' comes out of one exp and the coefficient costs one
+// add and one fma instead of add, mul, fma: one FP64 instruction less per pair, but measured
+// 5 % SLOWER (11.39 vs 10.83 ms at N = 100k, profiles/r02_ab_fold.jsonl): the per-tile bound of
+// the staged -ln lambda (a warp max) makes the step loop's convergence non-uniform and the
+// column's extra shared load sits on the exponent's dependency chain.  Off by default.
+#ifdef HK_SYM_FOLD
+constexpr bool SYM_FOLD = true;
+#else
+constexpr bool SYM_FOLD = false;
+#endif
 constexpr int K1P = 2;                    // pass-1 partials of the unordered-pair kernels: M', X' 
 // a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
 // treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
@@ -81,8 +89,13 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;   // >= 0: the column is the later event
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
-  double eb = fexp<TS>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
-  double es = SELF ? fexp<TS>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+#ifdef HK_PASS1_I2F   // A/B: the exp's k -> double on the conversion pipe in pass 1 too
+  constexpr bool I2F1 = D <= 5;
+#else
+  constexpr bool I2F1 = false;
+#endif
+  double eb = fexp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+  double es = SELF ? fexp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
@@ -111,7 +124,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   constexpr bool I2F = D <= 5;
 #endif
   double eb = fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
-#ifndef HK_NO_FOLD
+#ifdef HK_SYM_FOLD
   // rho'_j xi' = beta xi_ji / lambda_j: the column's cL = lnc_s - 64 ln 2 - ln lambda_j
   double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, cL)), tab, lane_off) : 0.0;
 #else   // round 1's coefficient (A/B): xi' alone, weighted by rho'_j below
@@ -122,7 +135,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
     es = dead ? 0.0 : es;
   }
   // the pair's App. A coefficient, the same for both events
-#ifndef HK_NO_FOLD
+#ifdef HK_SYM_FOLD
   const double rs = row.rho + crho;
   const double cc = SELF ? fma(rs, eb, es) : rs * eb;
 #else
@@ -148,7 +161,10 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const int2* __restrict__ tab) {
   constexpr int REC = Layout<D>::REC;
   const int lane = threadIdx.x & 31;
-#pragma unroll 1   // unrolling by 2 halves the loop overhead but measured 1 % slower
+  // unrolling by 2: pass 1 -2.8 %, pass 2 +1.4 % (N = 100k, accurate exp;
+  // profiles/r02_ab_unroll.jsonl)
+  constexpr int UNR = PASS == 1 ? 2 : 1;
+#pragma unroll UNR
   for (int s = 0; s < 32; ++s) {
     const int src = (lane + s) & 31;
     // column (l + s) mod 32 of this warp's group: from the staged tile (AoS records), or
@@ -157,7 +173,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
     double ct, crho = 0.0, cL = 0.0;
     if (SOA) {   // pass 2: (x, t, rho', cL) of the column, cL in the pair after (x, t, rho')
       const double2* g2 = reinterpret_cast<const double2*>(grp);
-      constexpr int NP = PASS == 2 ? (D + 4) / 2 : (D + 2) / 2;
+      constexpr int NP = (PASS == 2 && SYM_FOLD) ? (D + 4) / 2 : (PASS == 2 ? (D + 3) / 2 : (D + 2) / 2);
       double v[2 * NP];
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
@@ -170,7 +186,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       ct = v[D];
       if (PASS == 2) {
         crho = v[D + 1];
-        cL = v[D + 2];
+        if constexpr (SYM_FOLD) cL = v[D + 2];
       }
     } else {
       const double* rc = grp + src * REC;
@@ -179,7 +195,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       ct = rc[D];
       if (PASS == 2) {
         crho = rc[D + 1];
-        cL = c.lnc_sr + lgrp[src];
+        if constexpr (SYM_FOLD) cL = c.lnc_sr + lgrp[src];
       }
     }
     int cg = 0;
@@ -249,8 +265,9 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
   constexpr int KR = PASS == 1 ? 1 : D;       // row sums reduced over warps: M or G
   constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
   constexpr int TS = REPL ? TAB_COPIES : 1;
-  constexpr int LST = PASS == 2 ? TILE_J : 0;            // -ln lambda of the staged columns
-  constexpr int SOAW = PASS == 2 ? 2 * ((D + 4) / 2) : REC;   // doubles per column in the SoA copy
+  constexpr bool FOLD = PASS == 2 && SYM_FOLD;
+  constexpr int LST = FOLD ? TILE_J : 0;                  // -ln lambda of the staged columns
+  constexpr int SOAW = FOLD ? 2 * ((D + 4) / 2) : REC;    // doubles per column in the SoA copy
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* stage = reinterpret_cast<double*>(smem_raw);
   double* lstage = stage + STAGES * TILE_J * REC;                 // [STAGES][LST]
@@ -267,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
   // stage s <- column tile [jt, jt + cnt): the records, and (pass 2) -ln lambda rounded up to
   // an even count (16-byte bulk copies; lrho has npad >= N + 1 entries or N even)
   auto load_stage = [&](int s, int jt, int cnt) {
-    if (PASS == 2)
+    if (FOLD)
       tma_load_1d_x2(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
                      (uint32_t)(cnt * REC * sizeof(double)), lstage + s * LST, a.lrho + jt,
                      (uint32_t)(((cnt + 1) & ~1) * sizeof(double)), &bars[s]);
@@ -370,7 +387,7 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
         // pass 2's self-excitation exponent carries the column's cL = lnc_s - 64 ln2 - ln
         // lambda_j: its bound takes the largest cL of this warp's 32 columns
         double self_bound = c.lnc_s;
-        if (PASS == 2) {
+        if (FOLD) {
           double cLmax = cvalid ? c.lnc_sr + lgrp[lane] : -INFINITY;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) cLmax = fmax(cLmax, __shfl_xor_sync(0xffffffffu, cLmax, o));
@@ -384,9 +401,9 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
           double v[SOAW];
 #pragma unroll
           for (int q = 0; q < REC; ++q) v[q] = rc[q];
-          if constexpr (PASS == 2) v[D + 2] = c.lnc_sr + lgrp[lane];
+          if constexpr (FOLD) v[D + 2] = c.lnc_sr + lgrp[lane];
 #pragma unroll
-          for (int q = (PASS == 2 ? D + 3 : REC); q < SOAW; ++q) v[q] = 0.0;
+          for (int q = (FOLD ? D + 3 : REC); q < SOAW; ++q) v[q] = 0.0;
 #pragma unroll
           for (int p = 0; p < SOAW / 2; ++p) g2[p * 32 + lane] = make_double2(v[2 * p], v[2 * p + 1]);
           __syncwarp();

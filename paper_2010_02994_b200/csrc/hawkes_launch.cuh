@@ -14,9 +14,10 @@ template <int D, int PASS, int R, int V>
 size_t sym_smem() {
   const int KR = PASS == 1 ? 1 : D;
   const int copies = (V & 2) ? TAB_COPIES : 1;
-  const int soaw = PASS == 2 ? 2 * ((D + 4) / 2) : Layout<D>::REC;   // hawkes_kernels_sym.cuh
+  const bool fold = PASS == 2 && SYM_FOLD;
+  const int soaw = fold ? 2 * ((D + 4) / 2) : Layout<D>::REC;   // hawkes_kernels_sym.cuh
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) +
-         (PASS == 2 ? (size_t)STAGES * TILE_J * sizeof(double) : 0) + STAGES * sizeof(uint64_t) +
+         (fold ? (size_t)STAGES * TILE_J * sizeof(double) : 0) + STAGES * sizeof(uint64_t) +
          (size_t)EXP_TABLE * copies * sizeof(int2) + (size_t)4 * 32 * R * KR * sizeof(double) +
          ((V & 4) ? (size_t)4 * 32 * soaw * sizeof(double) : 0);
 }
@@ -320,7 +321,7 @@ struct Fin1D {
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
-          ctx->counters + 4 * ctx->W, ctx->st, final_here ? ctx->lrho : nullptr);
+          ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr);
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,

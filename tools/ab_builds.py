@@ -27,7 +27,10 @@ def do_build(spec):
 
 
 def time_one(name, n, precision, reps):
-    lib = "" if name == "base" else os.path.join(ALT, f"lib_{name}.so")
+    """name = BUILD[@ENV=VALUE[@ENV=VALUE]]: a build (base = the in-tree library) and runtime
+    environment switches (e.g. base@HAWKES_SYM_V=6)."""
+    build, *envs = name.split("@")
+    lib = "" if build == "base" else os.path.join(ALT, f"lib_{build}.so")
     code = f"""
 import json, sys, torch
 sys.path.insert(0, {ROOT!r})
@@ -46,6 +49,9 @@ kt = ctx.kernel_times()
 print(json.dumps({{"rate_ms": kt["rate_ms"] / kt["rate_launches"], "grad_ms": kt["grad_ms"] / kt["grad_launches"]}}))
 """
     env = dict(os.environ)
+    for e in envs:
+        k, _, v = e.partition("=")
+        env[k] = v
     if lib:
         env["HAWKES_LIB_AB"] = lib
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
