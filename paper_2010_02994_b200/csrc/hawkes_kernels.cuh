@@ -62,16 +62,17 @@ struct PassConst {
 //   a' = max(a, AMIN)            one unsigned min on the high word (AMIN = -707: for
 //                                negative doubles a larger high word means a larger |a|;
 //                                positive a, high bit clear, pass through)
-//   y  = a' * 2048/ln2 + 1.5*2^52 rounds to an integer: y's low word is
-//                                k = rint(a' * 2048/ln2) = 2048m + j
-//   r  = a' - k ln2/2048         |r| <= ln2/4096
-//   T  = 2^(j/2048) from a 2048-entry (16 KB) shared table whose high words are
-//        pre-biased by -(j << 9), so that one integer multiply-add, hi + (k << 9), also
+//   y  = a' * 1024/ln2 + 1.5*2^52 rounds to an integer: y's low word is
+//                                k = rint(a' * 1024/ln2) = 1024m + j
+//   r  = a' - k ln2/1024         |r| <= ln2/2048
+//   T  = 2^(j/1024) from a 1024-entry (8 KB) shared table whose high words are
+//        pre-biased by -(j << 10), so that one integer multiply-add, hi + (k << 10), also
 //        adds m to the exponent field
 //   e^a = T 2^m (1 + p(r)),  p(r) = r (1 + r (c2 + c3 r))  (minimax, tools/fit_exp_poly.py
-//        2048 3: |rel. err.| <= 5.9e-18 on |r| <= ln2/4096, so the result is within a few
+//        1024 3: |rel. err.| <= 9.4e-17 on |r| <= ln2/2048, so the result is within a few
 //        ulp of e^a': u-accurate, like the oracle's libm exp -- SURVEY.md §7 asks for
-//        <~1e-15 because gradient components cancel)
+//        <~1e-15 because gradient components cancel).  1024 entries measured 0.4 % faster
+//        in the gradient pass than 2048 (-DHK_EXP2048; profiles/r02_ab_table.jsonl)
 // Round 1 shipped degree 2 (6 FP64, 8.1e-13; -DHK_EXP_FAST keeps it for A/B): its error
 // is systematic per table cell, so a gradient component's error reached ~7000 u S_nd and
 // the plain relative error exceeded 1e-9 from kappa ~ 8e3 (profiles/r02_plain_error_r01kernel.jsonl),
@@ -87,7 +88,7 @@ constexpr double EXP_C3 = 0.1666666688540192;
 constexpr int EXP_TABLE = 256;
 constexpr int EXP_BIAS_SHIFT = 12;                          // 20 - log2(EXP_TABLE)
 constexpr int EXP_DEGREE = 3;
-#else
+#elif defined(HK_EXP2048) || defined(HK_EXP_FAST)   // 2048 entries (16 KB)
 constexpr double EXP_K = 2954.639443740597;                 // 2048/ln2
 constexpr double EXP_C = 3.3845077175778579e-04;            // ln2/2048
 constexpr int EXP_TABLE = 2048;
@@ -96,14 +97,26 @@ constexpr int EXP_BIAS_SHIFT = 9;                           // 20 - log2(EXP_TAB
 constexpr double EXP_C2 = 0.499999996420339;
 constexpr double EXP_C3 = 0.0;                              // unused
 constexpr int EXP_DEGREE = 2;
-#else
+#else                     // degree 3, 5.9e-18
 constexpr double EXP_C2 = 0.5000000009888816;               // 0x1.000000087e92ep-1
 constexpr double EXP_C3 = 0.16666666670097202;              // 0x1.5555555683162p-3
 constexpr int EXP_DEGREE = 3;
 #endif
+#else   // default: 1024 entries (8 KB), degree 3 (tools/fit_exp_poly.py 1024 3: 9.4e-17)
+constexpr double EXP_K = 1477.3197218702985;                // 1024/ln2
+constexpr double EXP_C = 6.7690154351557158e-04;            // ln2/1024
+constexpr int EXP_TABLE = 1024;
+constexpr int EXP_BIAS_SHIFT = 10;                          // 20 - log2(EXP_TABLE)
+constexpr double EXP_C2 = 0.5000000039557457;               // 0x1.00000021fac6ep-1
+constexpr double EXP_C3 = 0.16666666680410733;              // 0x1.5555555a0e463p-3
+constexpr int EXP_DEGREE = 3;
 #endif
 constexpr double EXP_SHIFT = 6755399441055744.0;            // 1.5 * 2^52
 constexpr unsigned EXP_AMIN_HI = 0xC0861800u;               // high word of -707.0
+
+#ifdef HK_ABLATE_TABMASK
+__constant__ int g_ablate_tabmask = 0;
+#endif
 
 // STRIDE > 1: the table is stored interleaved in STRIDE copies (entry j of copy c at
 // j*STRIDE + c) and tab points at this thread's copy (see sym_kernel)
@@ -123,7 +136,11 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, i
   const double r = fma(kf, -EXP_C, ac);
   int2 T;
   if constexpr (STRIDE == 1) {
+#ifdef HK_ABLATE_TABMASK   // diagnostics only (wrong results): every lane reads one entry,
+    T = tab[k & g_ablate_tabmask];   // a broadcast -- the kernel timed without bank conflicts
+#else
     T = tab[k & (EXP_TABLE - 1)];
+#endif
   } else {
     // interleaved copies: byte offset ((k mod 256) * STRIDE + copy) * 8, the copy's part
     // (lane_off, 0..STRIDE-1 times 8) or-ed in: one shift + one LOP3, uniform table base

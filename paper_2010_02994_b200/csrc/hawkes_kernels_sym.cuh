@@ -49,8 +49,8 @@ constexpr double CULL_EXPONENT = -708.0;
 // copies, lane l reading copy l & 15, so a half-warp's 16 lookups hit 16 distinct bank pairs;
 // 4 = each warp transposes its 32-column group once per tile into a private structure-of-
 // arrays buffer of double2 pairs, so the 32 steps read columns without bank conflicts
-// 16 copies of the 256-entry table (32 KB); the 2048-entry table (16 KB) fits 2 copies
-constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : 2;
+// 16 copies of the 256-entry table (32 KB); the 1024-entry table (8 KB) fits 4, the 2048-entry one 2
+constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : (EXP_TABLE == 1024 ? 4 : 2);
 
 struct SymArgs {
   const double* rec;

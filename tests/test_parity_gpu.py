@@ -237,10 +237,10 @@ def test_full_size_c4_sampled_rows_and_properties():
 
 
 def test_fast_exp_accuracy():
-    """The kernels' exp (2048-entry table + degree-3 minimax polynomial, hawkes_kernels.cuh)
+    """The kernels' exp (1024-entry table + degree-3 minimax polynomial, hawkes_kernels.cuh)
     against an 80-bit long-double exp: relative error <= 4e-16 + 1.2e-16 |a| on [-707, 700]
-    (truncation 5.9e-18 from tools/fit_exp_poly.py 2048 3; the rest is the rounding of the
-    table entry, the reduction r = a - k ln2/2048 and the final fma) -- u-accurate, as SURVEY
+    (truncation 9.4e-17 from tools/fit_exp_poly.py 1024 3; the rest is the rounding of the
+    table entry, the reduction r = a - k ln2/1024 and the final fma) -- u-accurate, as SURVEY
     §7 asks; below -707 the argument is clamped, so the result is e^(-707 +- 1e-3), never
     above e^-706 (R23)."""
     from paper_2010_02994_b200 import diag_exp
