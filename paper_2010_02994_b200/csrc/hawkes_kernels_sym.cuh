@@ -255,32 +255,82 @@ struct TileWalk {
   }
 };
 
-template <int D, int PASS, int SYM_R, int V>
-__global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a) {
+// Shared-memory layout of the pass kernels: the column-tile stages (records, and the staged
+// -ln lambda of -DHK_SYM_FOLD), the stage barriers, the exp table (TS interleaved copies),
+// the 4 warps' row-sum buffers (KR per row) and the per-warp SoA column copies (SOAW doubles
+// per column).  The fused small-N kernel (sym_eval_fused) takes the larger of both passes.
+template <int D, int TS, int KR, int SOAW, int LST>
+struct SymSmem {
+  static constexpr int REC = Layout<D>::REC;
+  static constexpr size_t bytes() {
+    return (size_t)STAGES * TILE_J * REC * sizeof(double) + (size_t)STAGES * LST * sizeof(double) +
+           STAGES * sizeof(uint64_t) + (size_t)EXP_TABLE * TS * sizeof(int2) +
+           (size_t)4 * TILE_J * KR * sizeof(double) + (size_t)4 * 32 * SOAW * sizeof(double);
+  }
+  double* stage;
+  double* lstage;
+  uint64_t* bars;
+  int2* tab;
+  double* red;
+  double* soa;
+  __device__ __forceinline__ explicit SymSmem(unsigned char* raw) {
+    stage = reinterpret_cast<double*>(raw);
+    lstage = stage + STAGES * TILE_J * REC;
+    bars = reinterpret_cast<uint64_t*>(lstage + STAGES * LST);
+    tab = reinterpret_cast<int2*>(bars + STAGES);
+    red = reinterpret_cast<double*>(tab + EXP_TABLE * TS);
+    soa = red + 4 * TILE_J * KR;
+  }
+};
+
+template <int D, int PASS, int V>
+struct SymCfg {
+  static constexpr bool FOLD = PASS == 2 && SYM_FOLD;
+  static constexpr int TS = (V & 2) ? TAB_COPIES : 1;
+  static constexpr int KR = PASS == 1 ? 1 : D;           // row sums reduced over warps: M or G
+  static constexpr int LST = FOLD ? TILE_J : 0;          // -ln lambda of the staged columns
+  static constexpr int SOAW = FOLD ? 2 * ((D + 4) / 2) : Layout<D>::REC;   // doubles per column
+  using Smem = SymSmem<D, TS, KR, (V & 4) ? SOAW : 0, LST>;
+};
+
+// kernel prologue: the exp table into shared memory (TS copies), the stage barriers
+template <int TS>
+__device__ __forceinline__ void sym_prologue(const int2* __restrict__ gtab, int2* tab, uint64_t* bars) {
+  const int tid = threadIdx.x;
+  for (int q = tid; q < EXP_TABLE * TS; q += THREADS) tab[q] = gtab[q / TS];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// One pass over the work items of a.counter (chunk pairs), pulled until exhausted; the
+// shared-memory pointers come from the caller's layout, parity carries the stage barriers'
+// phases across calls (every issued stage is consumed before this returns).
+template <int D, int PASS, int SYM_R, int V, class Sm>
+__device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s_item_p,
+                                          uint32_t& parity) {
   static_assert(32 * SYM_R == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SYM_RT = 32 * SYM_R;
   using L = Layout<D>;
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? K1P : L::K2;
-  constexpr int KR = PASS == 1 ? 1 : D;       // row sums reduced over warps: M or G
-  constexpr bool REPL = (V & 2) != 0, SOA = (V & 4) != 0;
-  constexpr int TS = REPL ? TAB_COPIES : 1;
-  constexpr bool FOLD = PASS == 2 && SYM_FOLD;
-  constexpr int LST = FOLD ? TILE_J : 0;                  // -ln lambda of the staged columns
-  constexpr int SOAW = FOLD ? 2 * ((D + 4) / 2) : REC;    // doubles per column in the SoA copy
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* stage = reinterpret_cast<double*>(smem_raw);
-  double* lstage = stage + STAGES * TILE_J * REC;                 // [STAGES][LST]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lstage + STAGES * LST);
-  int2* tab = reinterpret_cast<int2*>(bars + STAGES);
-  double* red = reinterpret_cast<double*>(tab + EXP_TABLE * TS);   // [4 warps][SYM_RT][KR]
-  double* soa = red + 4 * SYM_RT * KR;                            // [4 warps][SOAW][32] if SOA
-  __shared__ int s_item;
-
+  using Cfg = SymCfg<D, PASS, V>;
+  constexpr int KR = Cfg::KR;
+  constexpr bool SOA = (V & 4) != 0;
+  constexpr int TS = Cfg::TS;
+  constexpr bool FOLD = Cfg::FOLD;
+  constexpr int LST = Cfg::LST;
+  constexpr int SOAW = Cfg::SOAW;
+  double* stage = sm.stage;
+  double* lstage = sm.lstage;
+  uint64_t* bars = sm.bars;
+  double* red = sm.red;
+  int& s_item = *s_item_p;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int q = tid; q < EXP_TABLE * TS; q += THREADS) tab[q] = a.tab[q / TS];
-  const int2* mytab = tab;   // REPL: fexp or-s the lane's copy into the index
-  double* mysoa = soa + warp * 32 * SOAW;
+  const int2* mytab = sm.tab;   // REPL: fexp or-s the lane's copy into the index
+  double* mysoa = sm.soa + warp * 32 * SOAW;
   // stage s <- column tile [jt, jt + cnt): the records, and (pass 2) -ln lambda rounded up to
   // an even count (16-byte bulk copies; lrho has npad >= N + 1 entries or N even)
   auto load_stage = [&](int s, int jt, int cnt) {
@@ -292,12 +342,6 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
       tma_load_1d(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
                   (uint32_t)(cnt * REC * sizeof(double)), &bars[s]);
   };
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t parity = 0;
   const PassConst c = a.c;
   const int N = a.N;
 
@@ -465,6 +509,17 @@ __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a)
       __syncthreads();
     }
   }
+}
+
+template <int D, int PASS, int SYM_R, int V>
+__global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a) {
+  using Cfg = SymCfg<D, PASS, V>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const typename Cfg::Smem sm(smem_raw);
+  __shared__ int s_item;
+  sym_prologue<Cfg::TS>(a.tab, sm.tab, sm.bars);
+  uint32_t parity = 0;
+  sym_items<D, PASS, SYM_R, V>(a, sm, &s_item, parity);
 }
 
 }  // namespace hk

@@ -244,7 +244,7 @@ __device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, lo
   double acc = 0.0;
   if (live) {
 #pragma unroll 4
-    for (int c = c0; c < c1; ++c) acc += p[c * stride];
+    for (int c = c0; c < c1; ++c) acc += __ldcg(p + c * stride);   // L2: written by other CTAs
   }
   __shared__ double sh[FINP_SPLIT][32];
   sh[w][threadIdx.x & 31] = acc;
@@ -260,15 +260,14 @@ __device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, lo
 // k: blocks k, k + 128, ...; then a fixed shared-memory tree) into st->ell and re-arms the
 // ticket.  Replaces k_ell_reduce (one launch and a one-CTA pass over N) on the PAIRS path.
 template <int D>
-__global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
-                                                        int nslots, int N, const double* __restrict__ rec,
-                                                        double* __restrict__ rl, double* __restrict__ rates,
-                                                        const FinConst* __restrict__ fcp,
-                                                        double* __restrict__ rec_rho,
-                                                        float* __restrict__ rec32_rho,
-                                                        double* __restrict__ ell_part, int* ticket,
-                                                        EvalStatus* st, double* __restrict__ lrho) {
-  const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, M' or X')
+__device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __restrict__ part,
+                                            long long npad, int nslots, int N,
+                                            const double* __restrict__ rec, double* __restrict__ rl,
+                                            double* __restrict__ rates, const FinConst* __restrict__ fcp,
+                                            double* __restrict__ rec_rho, float* __restrict__ rec32_rho,
+                                            double* __restrict__ ell_part, int* ticket, EvalStatus* st,
+                                            double* __restrict__ lrho) {
+  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (event, M' or X')
   const int i = (int)(q >> 1);
   // part[(c npad + i) K1P + k], K1P = 2
   const double M = finp_slot_sum(part + q, npad * 2, nslots, i < N);
@@ -282,38 +281,60 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
     if (threadIdx.x == 0) {
-      ell_part[blockIdx.x] = e;
+      ell_part[blk] = e;
       __threadfence();
-      last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+      last = atomicAdd(ticket, 1) == nblk - 1;
     }
   }
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double s = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += FINP_THREADS) s += __ldcg(ell_part + b);
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = FINP_THREADS / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+  if (last) {   // CTA-uniform
+    __threadfence();
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += FINP_THREADS) s += __ldcg(ell_part + b);
+    red[threadIdx.x] = s;
     __syncthreads();
+    for (int w = FINP_THREADS / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      st->ell = red[0];
+      if (!(red[0] > -INFINITY)) st->undefined = 1;
+      *ticket = 0;
+    }
   }
-  if (threadIdx.x == 0) {
-    st->ell = red[0];
-    if (!(red[0] > -INFINITY)) st->undefined = 1;
-    *ticket = 0;
-  }
+  __syncthreads();   // last / red reused by the caller's next block
+}
+
+template <int D>
+__global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
+                                                        int nslots, int N, const double* __restrict__ rec,
+                                                        double* __restrict__ rl, double* __restrict__ rates,
+                                                        const FinConst* __restrict__ fcp,
+                                                        double* __restrict__ rec_rho,
+                                                        float* __restrict__ rec32_rho,
+                                                        double* __restrict__ ell_part, int* ticket,
+                                                        EvalStatus* st, double* __restrict__ lrho) {
+  fin1p_block<D>(blockIdx.x, gridDim.x, part, npad, nslots, N, rec, rl, rates, fcp, rec_rho, rec32_rho,
+                 ell_part, ticket, st, lrho);
+}
+
+template <int D>
+__device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ part, long long npad,
+                                            int nslots, int N, double* __restrict__ grad) {
+  constexpr int K = Layout<D>::K2;
+  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (event, d)
+  const bool live = q < (long long)N * D;
+  const int i = (int)(q / D), d = (int)(q % D);
+  const double g = finp_slot_sum(part + (long long)i * K + d, npad * K, nslots, live);
+  if (threadIdx.x < 32 && live) grad[q] = g;
+  __syncthreads();   // finp_slot_sum's shared buffer is reused by the next block
 }
 
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, long long npad,
                                                         int nslots, int N, double* __restrict__ grad) {
-  constexpr int K = Layout<D>::K2;
-  const long long q = (long long)blockIdx.x * 32 + (threadIdx.x & 31);   // (event, d)
-  const bool live = q < (long long)N * D;
-  const int i = (int)(q / D), d = (int)(q % D);
-  const double g = finp_slot_sum(part + (long long)i * K + d, npad * K, nslots, live);
-  if (threadIdx.x < 32 && live) grad[q] = g;
+  fin2p_block<D>(blockIdx.x, part, npad, nslots, N, grad);
 }
 
 template <int D>

@@ -52,12 +52,14 @@ if __name__ == "__main__":
     ap.add_argument("--nmax", type=int, default=2500)
     ap.add_argument("--only", type=int, default=-1, help="re-run one case (same random stream)")
     ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
+    ap.add_argument("--precision", default=None, help="force fp64 or fp32 for every case")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     fails = 0
     worst = {"fp64": 0.0, "fp32": 0.0}
     for case in range(a.cases):
         N, D, x, t, th, prec, alg, W = make_case(rng, a.nmax)
+        prec = a.precision or prec
         if a.only >= 0:
             if case != a.only:
                 continue
@@ -87,4 +89,5 @@ if __name__ == "__main__":
             fails += 1
             print(json.dumps({**info, "fail": "exception", "error": repr(e)[:300]}), flush=True)
             traceback.print_exc()
-    print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "worst_grad_ratio": worst}), flush=True)
+    print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "seed": a.seed, "nmax": a.nmax,
+                      "precision": a.precision or "mixed", "worst_grad_ratio": worst}), flush=True)
