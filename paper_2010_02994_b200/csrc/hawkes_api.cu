@@ -365,8 +365,7 @@ int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_grad_locations");
   TRY(check_ready(ctx));
   do {   // twice only if the fp32 range guard sent the context to fp64
-    TRY(run_rates(ctx));
-    TRY(run_grad(ctx));
+    TRY(run_grad(ctx));   // (with the rate pass first when it is due)
     TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
     TRY(fetch_status(ctx));
   } while (take_retry(ctx));

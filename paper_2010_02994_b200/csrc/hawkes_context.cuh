@@ -26,7 +26,6 @@
 #include "hawkes_moves.cuh"
 #include "hawkes_bmds.cuh"
 #include "hawkes_ops.cuh"
-#include "hawkes_fused.cuh"
 #include "hawkes_mh.cuh"
 #include "hawkes_mh_coop.cuh"
 #include "hawkes_plan.h"
@@ -167,7 +166,6 @@ struct hawkes_ctx {
   int grid1 = 0, grid2 = 0;
   int grid_s1 = 0, grid_s2 = 0;
   int grid32_1 = 0, grid32_2 = 0, grid32_s1 = 0, grid32_s2 = 0;   // fp32 kernels
-  int grid_fused = 0;      // co-resident CTAs of sym_eval_fused (0: not available)
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;

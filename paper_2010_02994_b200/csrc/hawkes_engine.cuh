@@ -170,27 +170,8 @@ int run_rates(hawkes_ctx* ctx) {
   return HAWKES_OK;
 }
 
-// the fused small-N evaluation (hawkes_fused.cuh): one process, fp64 PAIRS, rates and
-// gradient both due, N up to HAWKES_FUSED_MAX_N (default FUSED_MAX_N; 0 disables)
-constexpr long long FUSED_MAX_N = 40000;
-bool use_fused(const hawkes_ctx* ctx) {
-  static const long long max_n = [] {
-    const char* e = getenv("HAWKES_FUSED_MAX_N");
-    return e ? atoll(e) : FUSED_MAX_N;
-  }();
-  return ctx->pairs && !ctx->multi && !use32(ctx) && ctx->grid_fused > 0 && ctx->N <= max_n &&
-         !ctx->timing && !ctx->rates_valid && ctx->D <= SYM_MAX_D && ctx->N >= 2;
-}
-
 int run_grad(hawkes_ctx* ctx) {
   if (ctx->grad_valid) return HAWKES_OK;
-  if (use_fused(ctx)) {
-    CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1), ctx->stream));
-    TRY(dispatchD<FusedD>(ctx->D, ctx));
-    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = true;
-    ctx->rates_exchanged = false;
-    return HAWKES_OK;
-  }
   if (!ctx->capturing && !ctx->rates_valid) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, ctx->rates_valid ? 2 : 1));

@@ -258,7 +258,7 @@ struct TileWalk {
 // Shared-memory layout of the pass kernels: the column-tile stages (records, and the staged
 // -ln lambda of -DHK_SYM_FOLD), the stage barriers, the exp table (TS interleaved copies),
 // the 4 warps' row-sum buffers (KR per row) and the per-warp SoA column copies (SOAW doubles
-// per column).  The fused small-N kernel (sym_eval_fused) takes the larger of both passes.
+// per column).
 template <int D, int TS, int KR, int SOAW, int LST>
 struct SymSmem {
   static constexpr int REC = Layout<D>::REC;

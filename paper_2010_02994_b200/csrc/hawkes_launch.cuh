@@ -64,14 +64,6 @@ template <int D, int V1, int V2>
 int sym_call_v(hawkes_ctx* ctx, int pass, const SymArgs* b) {
   if (pass) return SymOps<D, 4, V1, V2>::launch(ctx, pass, *b);
   TRY((SymOps<D, 4, V1, V2>::setup(ctx)));
-  if constexpr (V1 == 4 && V2 == 4) {   // the fused small-N evaluation (hawkes_fused.cuh)
-    auto kf = sym_eval_fused<D, 4>;
-    const size_t sm = SymCfg<D, 2, 4>::Smem::bytes();
-    CU(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int per = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, THREADS, sm));
-    ctx->grid_fused = ctx->coop_ok ? per * ctx->sms : 0;
-  }
   return HAWKES_OK;
 }
 
@@ -548,50 +540,6 @@ struct DriftD {
         box ? ctx->lf_hi : nullptr, n, eps, ctx->bad);
     CHECK_LAUNCH();
     return dispatchD<PackXD>(D, ctx, (const double*)ctx->lf_x);
-  }
-};
-
-// one cooperative launch for rate pass + finalize + gradient pass + finalize (W = 1, fp64 PAIRS)
-template <int D>
-struct FusedD {
-  static SymArgs args(hawkes_ctx* ctx, int pass) {
-    SymArgs b;
-    b.rec = ctx->rec;
-    b.lrho = ctx->lrho;
-    b.gid = ctx->gid;
-    b.items = ctx->d_sym[0];
-    b.counter = ctx->counters + 2 + (pass - 1);
-    b.part = pass == 1 ? ctx->part1 : ctx->part2;
-    b.tab = ctx->tab;
-    b.npad = ctx->npad;
-    b.N = (int)ctx->N;
-    b.n_items = ctx->n_sym[0];
-    b.chunk = ctx->chunk;
-    b.nchunks = ctx->nchunks;
-    b.c = ctx->pc;
-    return b;
-  }
-  static int run(hawkes_ctx* ctx) {
-    FusedArgs f;
-    f.s1 = args(ctx, 1);
-    f.s2 = args(ctx, 2);
-    f.nslots = ctx->nslots;
-    f.fcp = &ctx->d_consts->fc64;
-    f.rl = ctx->rl;
-    f.rates = ctx->rates;
-    f.rec_rho = ctx->rec + Layout<D>::RHO;
-    f.rec32_rho = ctx->rec32 ? ctx->rec32 + Layout32<D>::RHO : nullptr;
-    f.ell_part = ctx->ell_part;
-    f.ticket = ctx->counters + 4 * ctx->W;
-    f.st = ctx->st;
-    f.lrho = SYM_FOLD ? ctx->lrho : nullptr;
-    f.grad = ctx->grad;
-    const int grid = std::min(ctx->grid_fused, std::max(f.s1.n_items, (int)((2 * ctx->N + 31) / 32)));
-    void* kargs[] = {&f};
-    CU(cudaLaunchCooperativeKernel((const void*)sym_eval_fused<D, 4>, dim3(grid), dim3(THREADS), kargs,
-                                   SymCfg<D, 2, 4>::Smem::bytes(), ctx->stream));
-    CHECK_LAUNCH();
-    return HAWKES_OK;
   }
 };
 

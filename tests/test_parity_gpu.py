@@ -555,30 +555,3 @@ def test_fp32_range_guard_in_leapfrog_and_hmc():
     assert np.allclose(res["fp32"][0], res["fp64"][0], rtol=0, atol=1e-12 * np.abs(x).max())
     assert res["fp32"][1] == pytest.approx(res["fp64"][1], rel=1e-12)
     assert res["fp32"][3] == res["fp64"][3] and res["fp32"][4] == pytest.approx(res["fp64"][4], abs=1e-9)
-
-
-@pytest.mark.parametrize("name,N", [("C1", 500), ("C2", 5000), ("C3", 20000)])
-def test_fused_small_n_evaluation_is_bitwise_the_separate_launches(name, N):
-    """hawkes_fused.cuh: at N <= 40k a grad_locations call with both passes due runs as ONE
-    cooperative launch (rate pass | finalize | gradient pass | finalize).  It must give bitwise
-    the results of the separate launches (loglik first, then the gradient pass alone), and
-    match the oracle."""
-    from paper_2010_02994_b200 import HawkesContext
-    c = synth.config(name, N)
-    out = []
-    for split in (False, True):
-        with HawkesContext(c.N, c.D) as ctx:
-            ctx.set_times(c.t)
-            ctx.set_locations(c.x)
-            ctx.set_params(c.theta)
-            if split:
-                ctx.loglik()
-            n_before = ctx.kernel_times()["total_launches"]
-            g, ell = ctx.grad_locations()
-            launches = ctx.kernel_times()["total_launches"] - n_before
-            out.append((ell, g.cpu().numpy(), ctx.get_rates()["lambda"], launches))
-    (e0, g0, l0, n0), (e1, g1, l1, n1) = out
-    assert n0 == 1 and n1 == 2          # one fused launch; pass 2 + its finalize
-    assert e0 == e1 and np.array_equal(g0, g1) and np.array_equal(l0, l1)
-    ell_r, _, _, g_r, S = oracle_eval(c.x, c.t, c.theta)
-    assert_parity(e0, g0, ell_r, g_r, S, what=f"fused {name}")
