@@ -81,10 +81,26 @@ typedef enum { HAWKES_MEM_HOST = 0, HAWKES_MEM_DEVICE = 1 } hawkes_mem;
  *           passes; results are bitwise identical for every W.
  *  PAIRS -- unordered pairs: chunk pairs (a < b) evaluate each pair's two exps once and
  *           feed both events (2 exps per ordered pair over both
- *           passes); W > 1 shards chunk pairs and allreduces per-event partial sums;
- *           results are deterministic for a fixed W.  Every D (1..8).
+ *           passes); W > 1 shards chunk pairs and allgathers per-event partial sums,
+ *           added in rank order; results are bitwise reproducible for a fixed W.  Every D
+ *           (1..8).
  *  AUTO  -- PAIRS (about 2x ROWS at N ~ 5k, ahead or level at 20k for every D). */
 typedef enum { HAWKES_ALGO_AUTO = 0, HAWKES_ALGO_ROWS = 1, HAWKES_ALGO_PAIRS = 2 } hawkes_algorithm;
+
+/* Walk order of the PAIRS fp64 kernels (hawkes_set_ordering):
+ *  TIME  -- events in time order: chunk pairs and tiles are time ranges (exact temporal
+ *           culling of tile pairs whose time gap puts both terms below the exp's clamp).
+ *  SPACE -- events in a Morton (Z-order) permutation of their locations, fixed when chosen:
+ *           tiles are compact in space and tile pairs / chunk pairs whose bounding boxes (in
+ *           space and time) put both terms below the clamp are skipped -- the same exact
+ *           culling rule, which pays on catalogs many bandwidths wide (the DC shape).
+ *  AUTO  -- SPACE when a box-based work estimate of both orders (hawkes_plan.h walk_cost) is
+ *           > 10 % lower for it, decided at the first evaluation after hawkes_set_times /
+ *           hawkes_set_ordering from the locations and Theta of that evaluation (kept
+ *           through later set_locations / set_params: the choice affects speed and summation
+ *           order, never which terms are summed).  fp32 contexts, ROWS and D > 4 walk in time
+ *           order. */
+typedef enum { HAWKES_ORDER_AUTO = 0, HAWKES_ORDER_TIME = 1, HAWKES_ORDER_SPACE = 2 } hawkes_ordering;
 
 typedef struct {
   int32_t device;            /* CUDA device ordinal                                           */
@@ -209,6 +225,14 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
  * the context stays on fp64 until the next hawkes_set_times / hawkes_set_params.
  * Errors: HAWKES_ERR_ARG. */
 int hawkes_precision_in_use(const hawkes_ctx* ctx, int32_t* out);
+
+/* Walk order (hawkes_ordering) of the PAIRS fp64 kernels; takes effect at the next
+ * evaluation (the permutation is built then from its locations).  hawkes_ordering_in_use
+ * writes the order the last evaluation used (HAWKES_ORDER_TIME or _SPACE) and, when
+ * out_cost is non-NULL, the decision's two work estimates (time, space; 0 if not estimated).
+ * Errors: HAWKES_ERR_ARG. */
+int hawkes_set_ordering(hawkes_ctx* ctx, int32_t mode);
+int hawkes_ordering_in_use(const hawkes_ctx* ctx, int32_t* out, double* out_cost);
 
 /* Bayesian MDS: the flu application's second O(N^2)
  * term.  hawkes_set_bmds copies the N*N row-major dissimilarity matrix Y (host or device per

@@ -255,7 +255,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamDestroy(ctx->gstream);
   }
   void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
-                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->lrho, ctx->rates,
+                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->lrho, ctx->d_perm, ctx->d_gid_p, ctx->rec_p, ctx->d_boxes, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->ell_part, ctx->tab,
                   ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->lf_x0, ctx->lf_p0, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};
@@ -304,6 +304,10 @@ int hawkes_set_times(hawkes_ctx* ctx, const double* t, int32_t mem) {
   TRY(upload_consts(ctx));
   ctx->have_t = true;
   ctx->fb64 = false;   // a new catalog: the fp32 range guard decides again
+  ctx->h_t.swap(h);
+  ctx->ties = false;
+  for (int64_t i = 1; i < N; ++i) ctx->ties |= ctx->h_t[i] == ctx->h_t[i - 1];
+  ctx->order_decided = false;   // and the walk order
   ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
   TRY(clear_move(ctx));
   return HAWKES_OK;
@@ -399,6 +403,27 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
       memcpy(outs[k], col.data(), N * sizeof(double));
     else
       CU(cudaMemcpy(outs[k], col.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return HAWKES_OK;
+}
+
+int hawkes_set_ordering(hawkes_ctx* ctx, int32_t mode) {
+  ENTER(ctx);
+  if (mode != HAWKES_ORDER_AUTO && mode != HAWKES_ORDER_TIME && mode != HAWKES_ORDER_SPACE)
+    return set_err(ctx, HAWKES_ERR_ARG, "bad ordering mode %d", mode);
+  ctx->order_req = mode;
+  ctx->order_decided = false;
+  drop_graphs(ctx);
+  ctx->rates_valid = ctx->grad_valid = false;
+  return HAWKES_OK;
+}
+
+int hawkes_ordering_in_use(const hawkes_ctx* ctx, int32_t* out, double* out_cost) {
+  if (!ctx || !out) return HAWKES_ERR_ARG;
+  *out = ctx->spatial ? HAWKES_ORDER_SPACE : HAWKES_ORDER_TIME;
+  if (out_cost) {
+    out_cost[0] = ctx->order_cost[0];
+    out_cost[1] = ctx->order_cost[1];
   }
   return HAWKES_OK;
 }

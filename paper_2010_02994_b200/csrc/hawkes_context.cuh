@@ -123,6 +123,18 @@ struct hawkes_ctx {
   double* G1 = nullptr;    // npad x D
   double* rl = nullptr;    // npad x 2 (rho', ell_n)
   double* lrho = nullptr;  // npad: -ln lambda_n (PAIRS fp64 gradient pass; hawkes_kernels_sym.cuh)
+  // walk order of the PAIRS fp64 kernels (hawkes_plan.h): time (records as they are) or
+  // spatial (a Morton permutation; rec_p gathered per evaluation, with 128-event tile boxes)
+  int order_req = 0;          // HAWKES_ORDER_AUTO / _TIME / _SPACE (hawkes_set_ordering)
+  bool order_decided = false; // decided at the first evaluation after set_times / set_ordering
+  bool spatial = false;       // the walk is spatial
+  double order_cost[2] = {0.0, 0.0};   // walk_cost estimates (time, space) of the decision
+  bool ties = false;          // the catalog has equal times
+  std::vector<double> h_t;    // host copy of the times (order decision, tie groups)
+  int* d_perm = nullptr;      // npad: walk position -> event
+  int* d_gid_p = nullptr;     // npad: tie-group ids in walk order
+  double* rec_p = nullptr;    // npad x REC: records in walk order
+  double* d_boxes = nullptr;  // npad/128 x (2D + 2): tile boxes in walk order
   double* rates = nullptr; // npad x 4 (lambda, mu, xi, Lambda)
   double* grad = nullptr;  // npad x D
   double* xstage = nullptr;// N x D staging
@@ -166,6 +178,7 @@ struct hawkes_ctx {
   int grid1 = 0, grid2 = 0;
   int grid_s1 = 0, grid_s2 = 0;
   int grid32_1 = 0, grid32_2 = 0, grid32_s1 = 0, grid32_s2 = 0;   // fp32 kernels
+  int grid_g1 = 0, grid_g2 = 0;   // spatial-walk (GEN) sym kernels
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;

@@ -135,8 +135,60 @@ int replay(hawkes_ctx* ctx, int which) {
   return HAWKES_OK;
 }
 
+// The PAIRS fp64 walk order (hawkes_plan.h, include/hawkes.h hawkes_ordering), decided at the
+// first evaluation after set_times / set_ordering from that evaluation's locations and Theta.
+int decide_order(hawkes_ctx* ctx) {
+  ctx->order_decided = true;
+  ctx->order_cost[0] = ctx->order_cost[1] = 0.0;
+  const int N = (int)ctx->N, D = ctx->D;
+  const bool eligible = ctx->pairs && !ctx->rec32 && D <= SPACE_MAX_D && N >= 2 * TILE_J &&
+                        ctx->order_req != HAWKES_ORDER_TIME;
+  bool want = false;
+  std::vector<int> perm;
+  if (eligible) {
+    std::vector<double> hx((size_t)N * D);
+    CU(cudaMemcpyAsync(hx.data(), ctx->xstage, hx.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    TRY(wait_stream(ctx));
+    perm = morton_order(hx.data(), N, D);
+    if (ctx->order_req == HAWKES_ORDER_SPACE) {
+      want = true;
+    } else {
+      ctx->order_cost[0] = walk_cost(hx.data(), ctx->h_t.data(), nullptr, N, D, ctx->pc, false);
+      ctx->order_cost[1] = walk_cost(hx.data(), ctx->h_t.data(), perm.data(), N, D, ctx->pc, true);
+      want = ctx->order_cost[1] < 0.9 * ctx->order_cost[0];
+    }
+  }
+  if (want != ctx->spatial) drop_graphs(ctx);
+  ctx->spatial = want;
+  if (!want) return HAWKES_OK;
+  const int REC = REC_of(D);
+  if (!ctx->d_perm) {
+    int rc;
+    if ((rc = dalloc(ctx, &ctx->d_perm, (size_t)ctx->npad)) ||
+        (rc = dalloc(ctx, &ctx->d_gid_p, (size_t)ctx->npad)) ||
+        (rc = dalloc(ctx, &ctx->rec_p, (size_t)ctx->npad * REC)) ||
+        (rc = dalloc(ctx, &ctx->d_boxes, (size_t)(ctx->npad / TILE_J) * (2 * D + 2))))
+      return rc;
+    CU(cudaMemsetAsync(ctx->rec_p, 0, (size_t)ctx->npad * REC * sizeof(double), ctx->stream));
+  }
+  // tie-group ids (first event with the same time) in walk order
+  std::vector<int> g(N), gp(ctx->npad);
+  for (int i = 0; i < N; ++i) g[i] = (i && ctx->h_t[i] == ctx->h_t[i - 1]) ? g[i - 1] : i;
+  std::vector<int> hp(ctx->npad);
+  for (int p = 0; p < ctx->npad; ++p) {
+    hp[p] = perm[std::min(p, N - 1)];
+    gp[p] = g[hp[p]];
+  }
+  CU(cudaMemcpyAsync(ctx->d_perm, hp.data(), hp.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_gid_p, gp.data(), gp.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  TRY(wait_stream(ctx));   // the host vectors go out of scope
+  return HAWKES_OK;
+}
+
 int run_rates(hawkes_ctx* ctx) {
   if (ctx->rates_valid) return HAWKES_OK;
+  if (!ctx->order_decided && !ctx->capturing) TRY(decide_order(ctx));
   if (!ctx->capturing) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, 0));
@@ -148,6 +200,7 @@ int run_rates(hawkes_ctx* ctx) {
   }
   CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1), ctx->stream));
   if (ctx->pairs) {
+    if (ctx->spatial) TRY(dispatchD<WalkD>(ctx->D, ctx));
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
     if (ctx->multi) TRY(reduce_pair_partials(ctx, ctx->part1, ctx->sums1, K1P));
     TRY(dispatchD<Fin1D>(ctx->D, ctx, 0));
@@ -172,6 +225,7 @@ int run_rates(hawkes_ctx* ctx) {
 
 int run_grad(hawkes_ctx* ctx) {
   if (ctx->grad_valid) return HAWKES_OK;
+  if (!ctx->order_decided && !ctx->capturing) TRY(decide_order(ctx));
   if (!ctx->capturing && !ctx->rates_valid) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, ctx->rates_valid ? 2 : 1));

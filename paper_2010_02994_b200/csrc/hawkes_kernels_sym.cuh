@@ -53,7 +53,9 @@ constexpr double CULL_EXPONENT = -708.0;
 constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : (EXP_TABLE == 1024 ? 4 : 2);
 
 struct SymArgs {
-  const double* rec;
+  const double* rec;     // records in the item walk's order (time order, or spatial: rec_p)
+  const double* boxes;   // GEN: per 128-event tile {lo[D], hi[D], tmin, tmax} (spatial order)
+  int ties;              // GEN: the catalog has equal times (every tile pair takes the masked path)
   const double* lrho;    // pass 2: -ln lambda_j per event (npad), staged beside the records
   const int* gid;
   const int2* items;     // (a, b) chunk pairs, a < b
@@ -76,10 +78,13 @@ struct SymRow {
   int g;
 };
 
-// one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution
-template <int D, bool MASK, bool SELF, int TS>
+// one unordered pair, pass 1; MASK: tie (same time) or padding column -> no contribution.
+// GEN (spatial order, hawkes_plan.h): the column may be earlier or later than the row; the
+// self-excitation term is that of the later event, exponent k_s r^2 - omega |dt|, added to
+// the row's X (row later) or the column's (column later).
+template <int D, bool MASK, bool SELF, int TS, bool GEN = false>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
-                                          bool dead, double& rM, double& cM, double& cX,
+                                          bool dead, double& rM, double& rX, double& cM, double& cX,
                                           const PassConst& c, const int2* __restrict__ tab) {
   double dx[D];
 #pragma unroll
@@ -95,17 +100,26 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   constexpr bool I2F1 = false;
 #endif
   double eb = fexp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
-  double es = SELF ? fexp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+  double es = SELF ? fexp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off)
+                   : 0.0;
   if (MASK) {
     eb = dead ? 0.0 : eb;
     es = dead ? 0.0 : es;
   }
   rM += eb;
   cM += eb;
-  if (SELF) cX += es;
+  if (SELF) {
+    if (GEN) {   // the later event takes xi (dt != 0 here: ties are masked)
+      const bool row_later = __double2hiint(dt) < 0;
+      rX += row_later ? es : 0.0;
+      cX += row_later ? 0.0 : es;
+    } else {
+      cX += es;
+    }
+  }
 }
 
-template <int D, bool MASK, bool SELF, int TS>
+template <int D, bool MASK, bool SELF, int TS, bool GEN = false>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           double crho, double cL, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
@@ -127,8 +141,9 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 #ifdef HK_SYM_FOLD
   // rho'_j xi' = beta xi_ji / lambda_j: the column's cL = lnc_s - 64 ln 2 - ln lambda_j
   double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, cL)), tab, lane_off) : 0.0;
-#else   // round 1's coefficient (A/B): xi' alone, weighted by rho'_j below
-  double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, c.lnc_s)), tab, lane_off) : 0.0;
+#else   // xi' alone, weighted by rho' of the later event below
+  double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off)
+                   : 0.0;
 #endif
   if (MASK) {
     eb = dead ? 0.0 : eb;
@@ -139,7 +154,13 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   const double rs = row.rho + crho;
   const double cc = SELF ? fma(rs, eb, es) : rs * eb;
 #else
-  const double cc = fma(row.rho, eb, crho * (SELF ? eb + es : eb));
+  double cc;
+  if (GEN) {   // rho'_i mu' + rho'_j mu' + rho'_later xi'
+    const double rlater = __double2hiint(dt) < 0 ? row.rho : crho;
+    cc = SELF ? fma(row.rho + crho, eb, rlater * es) : (row.rho + crho) * eb;
+  } else {
+    cc = fma(row.rho, eb, crho * (SELF ? eb + es : eb));
+  }
 #endif
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -151,12 +172,12 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA>
+template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA, bool GEN>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp,
                                           const double* __restrict__ lgrp, int cg0, bool cvalid0,
                                           int ridx0, int cidx0, bool diag,
-                                          double (&rM)[SYM_R], double (&rG)[SYM_R][D],
+                                          double (&rM)[SYM_R], double (&rX)[SYM_R], double (&rG)[SYM_R][D],
                                           double (&cacc)[2 + D], const PassConst& c,
                                           const int2* __restrict__ tab) {
   constexpr int REC = Layout<D>::REC;
@@ -224,9 +245,9 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
                                  (diag && cidx0 + src <= ridx0 + 32 * r));
       if (PASS == 1)
-        sym_pair1<D, MASK, SELF, TS>(row[r], cx, ct, dead, rM[r], cacc[0], cacc[1], c, tab);
+        sym_pair1<D, MASK, SELF, TS, GEN>(row[r], cx, ct, dead, rM[r], rX[r], cacc[0], cacc[1], c, tab);
       else
-        sym_pair2<D, MASK, SELF, TS>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
+        sym_pair2<D, MASK, SELF, TS, GEN>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -241,6 +262,36 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       for (int d = 0; d < D; ++d) cacc[2 + d] = shfl(cacc[2 + d], nxt);
     }
   }
+}
+
+// Smallest squared distance and time gap between two boxes {lo[D], tlo} / {hi[D], thi} and a
+// tile box b = {lo[D], hi[D], tmin, tmax}.
+template <int D>
+__device__ __forceinline__ void box_gaps(const double (&lo)[D + 1], const double (&hi)[D + 1],
+                                         const double* __restrict__ b, double& r2min, double& dtmin) {
+  r2min = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double g = fmax(0.0, fmax(b[d] - hi[d], lo[d] - b[D + d]));
+    r2min = fma(g, g, r2min);
+  }
+  dtmin = fmax(0.0, fmax(b[2 * D] - hi[D], lo[D] - b[2 * D + 1]));
+}
+
+// Can any pair of the two boxes (space D + time) have a term above the exp's clamp?
+template <int D>
+__device__ __forceinline__ bool box_pair_live(const double (&lo_a)[D + 1], const double (&hi_a)[D + 1],
+                                              const double (&lo_b)[D + 1], const double (&hi_b)[D + 1],
+                                              const PassConst& c) {
+  double r2min = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double g = fmax(0.0, fmax(lo_b[d] - hi_a[d], lo_a[d] - hi_b[d]));
+    r2min = fma(g, g, r2min);
+  }
+  const double dtmin = fmax(0.0, fmax(lo_b[D] - hi_a[D], lo_a[D] - hi_b[D]));
+  return fma(c.kx, r2min, fma(c.kt * dtmin, dtmin, c.lnc_b)) > CULL_EXPONENT ||
+         fma(c.ks, r2min, c.lnc_s - c.omega * dtmin) > CULL_EXPONENT;
 }
 
 // Tile walk of one item: row tiles rt = 0..n_rt-1, column tiles ct = (diag ? rt : 0)..n_ct-1
@@ -283,11 +334,13 @@ struct SymSmem {
   }
 };
 
-template <int D, int PASS, int V>
+template <int D, int PASS, int V, bool GEN = false>
 struct SymCfg {
   static constexpr bool FOLD = PASS == 2 && SYM_FOLD;
   static constexpr int TS = (V & 2) ? TAB_COPIES : 1;
-  static constexpr int KR = PASS == 1 ? 1 : D;           // row sums reduced over warps: M or G
+  // row sums reduced over warps: M (time order: a row is never the later event of its pairs),
+  // M and X (GEN), or G
+  static constexpr int KR = PASS == 1 ? (GEN ? 2 : 1) : D;
   static constexpr int LST = FOLD ? TILE_J : 0;          // -ln lambda of the staged columns
   static constexpr int SOAW = FOLD ? 2 * ((D + 4) / 2) : Layout<D>::REC;   // doubles per column
   using Smem = SymSmem<D, TS, KR, (V & 4) ? SOAW : 0, LST>;
@@ -308,7 +361,10 @@ __device__ __forceinline__ void sym_prologue(const int2* __restrict__ gtab, int2
 // One pass over the work items of a.counter (chunk pairs), pulled until exhausted; the
 // shared-memory pointers come from the caller's layout, parity carries the stage barriers'
 // phases across calls (every issued stage is consumed before this returns).
-template <int D, int PASS, int SYM_R, int V, class Sm>
+// GEN: spatial order (hawkes_plan.h morton_order): no time order between or inside chunks,
+// so the general-direction pair bodies; tile pairs and whole items are culled by the
+// bounding boxes of their tiles (a.boxes) in space and time.
+template <int D, int PASS, int SYM_R, int V, bool GEN, class Sm>
 __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s_item_p,
                                           uint32_t& parity) {
   static_assert(32 * SYM_R == TILE_J, "row tiles and column tiles must coincide");
@@ -316,7 +372,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
   using L = Layout<D>;
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? K1P : L::K2;
-  using Cfg = SymCfg<D, PASS, V>;
+  using Cfg = SymCfg<D, PASS, V, GEN>;
   constexpr int KR = Cfg::KR;
   constexpr bool SOA = (V & 4) != 0;
   constexpr int TS = Cfg::TS;
@@ -360,6 +416,44 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
     const int n_rt = (r1 - r0 + SYM_RT - 1) / SYM_RT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
     const int cslot = diag ? a.nchunks : w.x;     // column-role slot of this item
+    if (GEN && !diag) {
+      // item-level cull: the union boxes of the two chunks; a dead item still owns its
+      // slots (row role: slot b of chunk a's events; column role: slot a of chunk b's)
+      const double* bx = a.boxes;
+      double lo_a[D + 1], hi_a[D + 1], lo_b[D + 1], hi_b[D + 1];
+#pragma unroll
+      for (int d = 0; d <= D; ++d) {
+        lo_a[d] = lo_b[d] = INFINITY;
+        hi_a[d] = hi_b[d] = -INFINITY;
+      }
+      for (int q = 0; q < n_rt; ++q) {
+        const double* b = bx + (long long)(r0 / TILE_J + q) * (2 * D + 2);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          lo_a[d] = fmin(lo_a[d], b[d]);
+          hi_a[d] = fmax(hi_a[d], b[D + d]);
+        }
+        lo_a[D] = fmin(lo_a[D], b[2 * D]);
+        hi_a[D] = fmax(hi_a[D], b[2 * D + 1]);
+      }
+      for (int q = 0; q < n_ct; ++q) {
+        const double* b = bx + (long long)(c0 / TILE_J + q) * (2 * D + 2);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          lo_b[d] = fmin(lo_b[d], b[d]);
+          hi_b[d] = fmax(hi_b[d], b[D + d]);
+        }
+        lo_b[D] = fmin(lo_b[D], b[2 * D]);
+        hi_b[D] = fmax(hi_b[D], b[2 * D + 1]);
+      }
+      if (!box_pair_live<D>(lo_a, hi_a, lo_b, hi_b, c)) {
+        for (int q = tid; q < (r1 - r0) * K; q += THREADS)
+          a.part[((long long)w.y * a.npad + r0) * K + q] = 0.0;
+        for (int q = tid; q < (c1 - c0) * K; q += THREADS)
+          a.part[((long long)cslot * a.npad + c0) * K + q] = 0.0;
+        continue;   // (the next item fetch synchronises the CTA)
+      }
+    }
 
     TileWalk prod{0, 0};
     if (tid == 0) {
@@ -374,7 +468,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
       const int row0 = r0 + rt * SYM_RT;
       const bool rows_full = row0 + SYM_RT <= r1;
       SymRow<D> row[SYM_R];
-      double rM[SYM_R], rG[SYM_R][D];
+      double rM[SYM_R], rX[SYM_R], rG[SYM_R][D];
 #pragma unroll
       for (int r = 0; r < SYM_R; ++r) {
         const int i = row0 + lane + 32 * r;
@@ -385,8 +479,21 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         row[r].rho = ri[D + 1];
         row[r].g = i < N ? a.gid[i] : -1;   // -1: padding row (masked)
         rM[r] = 0.0;
+        rX[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
+      }
+      // GEN: this row tile's box (tiles are TILE_J-aligned in the walk's order)
+      double rlo[D + 1], rhi[D + 1];
+      if (GEN) {
+        const double* b = a.boxes + (long long)(row0 / TILE_J) * (2 * D + 2);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          rlo[d] = b[d];
+          rhi[d] = b[D + d];
+        }
+        rlo[D] = b[2 * D];
+        rhi[D] = b[2 * D + 1];
       }
       const int rlast = min(row0 + SYM_RT, r1) - 1;
       const int g_rlast = a.gid[rlast];
@@ -421,11 +528,19 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
           for (int d = 0; d < D; ++d) cacc[2 + d] = cpart[d];
         }
         const bool diag_tile = diag && ct == rt;
-        const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
+        const bool strict = !diag_tile && rows_full && cnt == TILE_J &&
+                            (GEN ? !a.ties : g_rlast < a.gid[jt]);
         // temporal culling (NEXT-2 on time-compact tiles): with dt >= dtmin for every pair
         // of this tile pair, the self-excitation exponent is <= lnc_s - omega dtmin and the
-        // background one <= lnc_b + k_t dtmin^2; below the exp's clamp they add nothing
-        const double dtmin = fmax(st[D] - t_rlast, 0.0);
+        // background one <= lnc_b + k_t dtmin^2; below the exp's clamp they add nothing.
+        // GEN: the same bounds from the two tiles' boxes, with r^2 >= r2min as well.
+        double dtmin, r2min = 0.0;
+        if (GEN) {
+          const double* b = a.boxes + (long long)(jt / TILE_J) * (2 * D + 2);
+          box_gaps<D>(rlo, rhi, b, r2min, dtmin);
+        } else {
+          dtmin = fmax(st[D] - t_rlast, 0.0);
+        }
         const double* grp = st + warp * 32 * REC;
         const double* lgrp = lstage + s * LST + warp * 32;
         // pass 2's self-excitation exponent carries the column's cL = lnc_s - 64 ln2 - ln
@@ -437,8 +552,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
           for (int o = 16; o > 0; o >>= 1) cLmax = fmax(cLmax, __shfl_xor_sync(0xffffffffu, cLmax, o));
           self_bound = cLmax;
         }
-        const bool self_live = self_bound - c.omega * dtmin > CULL_EXPONENT;
-        const bool bg_live = fma(c.kt * dtmin, dtmin, c.lnc_b) > CULL_EXPONENT;
+        const bool self_live = fma(c.ks, r2min, self_bound - c.omega * dtmin) > CULL_EXPONENT;
+        const bool bg_live = fma(c.kx, r2min, fma(c.kt * dtmin, dtmin, c.lnc_b)) > CULL_EXPONENT;
         if (SOA) {   // this lane's column record (+ cL) -> the warp's [pair][32] double2 buffer
           const double* rc = grp + lane * REC;
           double2* g2 = reinterpret_cast<double2*>(mysoa);
@@ -454,14 +569,17 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
           grp = mysoa;
         }
         if (!strict)
-          sym_group<D, PASS, true, SYM_R, true, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                         jt + warp * 32, diag_tile, rM, rG, cacc, c, mytab);
+          sym_group<D, PASS, true, SYM_R, true, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                              jt + warp * 32, diag_tile, rM, rX, rG, cacc, c,
+                                                              mytab);
         else if (self_live)
-          sym_group<D, PASS, false, SYM_R, true, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                          jt + warp * 32, false, rM, rG, cacc, c, mytab);
+          sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                               jt + warp * 32, false, rM, rX, rG, cacc, c,
+                                                               mytab);
         else if (bg_live)
-          sym_group<D, PASS, false, SYM_R, false, TS, SOA>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                           jt + warp * 32, false, rM, rG, cacc, c, mytab);
+          sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                                jt + warp * 32, false, rM, rX, rG, cacc, c,
+                                                                mytab);
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {
@@ -485,6 +603,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         double* o = red + ((long long)warp * SYM_RT + lane + 32 * r) * KR;
         if (PASS == 1) {
           o[0] = rM[r];
+          if (GEN) o[1] = rX[r];
         } else {
 #pragma unroll
           for (int d = 0; d < D; ++d) o[d] = rG[r][d];
@@ -499,11 +618,11 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         v += red[(2 * SYM_RT + rr) * KR + kk];
         v += red[(3 * SYM_RT + rr) * KR + kk];
         double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;   // slot b
-        if (PASS == 1) {
+        if (PASS == 1 && !GEN) {
           o[0] = v;      // M
           o[1] = 0.0;    // X: xi_ij = 0 for a later j
         } else {
-          o[kk] = v;
+          o[kk] = v;     // (GEN pass 1: M and X)
         }
       }
       __syncthreads();
@@ -511,15 +630,15 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
   }
 }
 
-template <int D, int PASS, int SYM_R, int V>
+template <int D, int PASS, int SYM_R, int V, bool GEN = false>
 __global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a) {
-  using Cfg = SymCfg<D, PASS, V>;
+  using Cfg = SymCfg<D, PASS, V, GEN>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const typename Cfg::Smem sm(smem_raw);
   __shared__ int s_item;
   sym_prologue<Cfg::TS>(a.tab, sm.tab, sm.bars);
   uint32_t parity = 0;
-  sym_items<D, PASS, SYM_R, V>(a, sm, &s_item, parity);
+  sym_items<D, PASS, SYM_R, V, GEN>(a, sm, &s_item, parity);
 }
 
 }  // namespace hk

@@ -45,6 +45,35 @@ struct SymOps {
   }
 };
 
+// the spatial-walk (GEN) kernels: V = 4, D <= SPACE_MAX_D
+template <int D>
+struct SymGen {
+  static size_t smem(int pass) {
+    return pass == 1 ? SymCfg<D, 1, 4, true>::Smem::bytes() : SymCfg<D, 2, 4, true>::Smem::bytes();
+  }
+  static int setup(hawkes_ctx* ctx) {
+    auto g1 = sym_kernel<D, 1, 4, 4, true>;
+    auto g2 = sym_kernel<D, 2, 4, 4, true>;
+    CU(cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+    CU(cudaFuncSetAttribute(g2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(2)));
+    int b1 = 0, b2 = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, g1, THREADS, smem(1)));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, g2, THREADS, smem(2)));
+    ctx->grid_g1 = std::max(1, b1) * ctx->sms;
+    ctx->grid_g2 = std::max(1, b2) * ctx->sms;
+    return HAWKES_OK;
+  }
+  static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
+    const int grid = std::min(pass == 1 ? ctx->grid_g1 : ctx->grid_g2, b.n_items);
+    if (pass == 1)
+      sym_kernel<D, 1, 4, 4, true><<<grid, THREADS, smem(1), ctx->stream>>>(b);
+    else
+      sym_kernel<D, 2, 4, 4, true><<<grid, THREADS, smem(2), ctx->stream>>>(b);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
+  }
+};
+
 // default: V = 4 (SoA columns) in both passes.  The interleaved exp-table copies (V bit 2)
 // cut pass 1's bank conflicts while pass 1 also accumulated the row-local gradient (-1.6 %
 // with 2 copies of the 2048-entry table, -3.4 % with 16 copies of the -DHK_EXP256 table);
@@ -69,6 +98,10 @@ int sym_call_v(hawkes_ctx* ctx, int pass, const SymArgs* b) {
 
 template <int D>
 int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
+  if constexpr (D <= SPACE_MAX_D) {
+    if (pass == 0) TRY(SymGen<D>::setup(ctx));
+    else if (ctx->spatial) return SymGen<D>::launch(ctx, pass, *b);
+  }
   const int v = sym_variant();
   if (v == 0) return sym_call_v<D, 0, 0>(ctx, pass, b);
   if constexpr (D == 2) {
@@ -230,9 +263,11 @@ struct PassD {
     }
     if constexpr (D <= SYM_MAX_D) if (ctx->pairs && ctx->n_sym[rank] > 0) {
       SymArgs b;
-      b.rec = ctx->rec;
+      b.rec = ctx->spatial ? ctx->rec_p : ctx->rec;
       b.lrho = ctx->lrho;
-      b.gid = ctx->gid;
+      b.gid = ctx->spatial ? ctx->d_gid_p : ctx->gid;
+      b.boxes = ctx->d_boxes;
+      b.ties = ctx->ties ? 1 : 0;
       b.items = ctx->d_sym[rank];
       b.counter = ctx->counters + 4 * rank + 2 + (pass - 1);
       b.part = pass == 1 ? ctx->part1 : ctx->part2;
@@ -317,7 +352,8 @@ struct Fin1D {
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
           sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
-          ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr);
+          ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr,
+          ctx->spatial ? WalkMap{ctx->d_perm, ctx->rec_p + Layout<D>::RHO} : WalkMap{nullptr, nullptr});
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,
@@ -338,7 +374,8 @@ struct Fin2D {
     if (all) {
       const long long n = ctx->N * D;
       k_fin2p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
-          sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->grad);
+          sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->grad,
+          ctx->spatial ? ctx->d_perm : nullptr);
     } else {
       k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,
                                                            ctx->d_tiles[rank], (int)ctx->N, ctx->G1,
@@ -540,6 +577,17 @@ struct DriftD {
         box ? ctx->lf_hi : nullptr, n, eps, ctx->bad);
     CHECK_LAUNCH();
     return dispatchD<PackXD>(D, ctx, (const double*)ctx->lf_x);
+  }
+};
+
+// spatial walk: gather the records in walk order and the tile boxes (every evaluation)
+template <int D>
+struct WalkD {
+  static int run(hawkes_ctx* ctx) {
+    k_walk_records<D><<<(unsigned)(ctx->npad / 128), 128, 0, ctx->stream>>>(
+        ctx->rec, ctx->d_perm, (int)ctx->N, ctx->npad, ctx->rec_p, ctx->d_boxes);
+    CHECK_LAUNCH();
+    return HAWKES_OK;
   }
 };
 

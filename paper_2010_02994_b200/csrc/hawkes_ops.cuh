@@ -16,6 +16,7 @@ namespace hk {
 constexpr int R_ROWS = 2;                    // rows per thread
 constexpr int SYM_MAX_D = 8;                 // unordered-pair kernels are built for every D
 constexpr int SYM_AUTO_MAX_D = 8;            // ... and chosen by HAWKES_ALGO_AUTO up to this D
+constexpr int SPACE_MAX_D = 4;               // spatial walk order (GEN kernels) built for D <= 4
                                              // (2x ROWS at N = 4733, >= ROWS at 20k for D <= 7;
                                              // profiles/r01_ab_algo.jsonl)
 constexpr int RT = THREADS * R_ROWS;         // rows per row tile
@@ -153,16 +154,24 @@ struct EvalStatus {
   int range32;          // fp32 range guard tripped (FinConst::range_floor) in some evaluation
 };
 
-// lambda, rho' and ell_n of event i from its summed pass-1 partials (M', X'), then the
-// stores: rl[i] = (rho'_i, ell_i); rates[i] = (lambda, mu, xi, Lambda); rho' into the records;
-// returns ell_i
+// Where the pair kernels walked the events in spatial order (hawkes_plan.h), the per-event
+// partial slots are indexed by walk position p and perm[p] is the event; nullptr: identity.
+struct WalkMap {
+  const int* perm;       // p -> event
+  double* recp_rho;      // rho' of the walk-order records (pass 2 reads them), or nullptr
+};
+
+// lambda, rho' and ell_n of the event at walk position p from its summed pass-1 partials
+// (M', X'), then the stores (event i = perm[p]): rl[i] = (rho'_i, ell_i); rates[i] = (lambda,
+// mu, xi, Lambda); rho' into the records; returns ell_i
 template <int D>
-__device__ __forceinline__ double fin1_event(int i, double M, double X, const double* __restrict__ rec,
+__device__ __forceinline__ double fin1_event(int p, double M, double X, const double* __restrict__ rec,
                                            double* __restrict__ rl, double* __restrict__ rates,
                                            const FinConst& f, double* __restrict__ rec_rho,
                                            float* __restrict__ rec32_rho, int* __restrict__ range_flag,
-                                           double* __restrict__ lrho) {
+                                           double* __restrict__ lrho, WalkMap wm = WalkMap{nullptr, nullptr}) {
   using L = Layout<D>;
+  const int i = wm.perm ? wm.perm[p] : p;
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
   if (mu_s + xi_s < f.range_floor) *range_flag = 1;   // fp32 only (range_floor = 0 in fp64)
@@ -183,11 +192,12 @@ __device__ __forceinline__ double fin1_event(int i, double M, double X, const do
   // exponent; -inf where rho' = 0).  lambda = Lambda' 2^scale is exact unless it underflows
   if (lrho) {
     const double lam = Lp * sc;
-    lrho[i] = !(Lp > 0.0) ? -INFINITY
+    lrho[p] = !(Lp > 0.0) ? -INFINITY
               : (lam >= 2.2250738585072014e-308 ? -log(lam) : -(log(Lp) + f.scale_log2 * LN2));
   }
   // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
   if (rec_rho) rec_rho[(long long)i * L::REC] = rho;
+  if (wm.recp_rho) wm.recp_rho[(long long)p * L::REC] = rho;
   if (rec32_rho) rec32_rho[(long long)i * Layout32<D>::REC] = (float)rho;
   rates[4 * (long long)i] = Lp * sc;
   rates[4 * (long long)i + 1] = mu_s * sc;
@@ -266,8 +276,8 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
                                             double* __restrict__ rates, const FinConst* __restrict__ fcp,
                                             double* __restrict__ rec_rho, float* __restrict__ rec32_rho,
                                             double* __restrict__ ell_part, int* ticket, EvalStatus* st,
-                                            double* __restrict__ lrho) {
-  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (event, M' or X')
+                                            double* __restrict__ lrho, WalkMap wm) {
+  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, M' or X')
   const int i = (int)(q >> 1);
   // part[(c npad + i) K1P + k], K1P = 2
   const double M = finp_slot_sum(part + q, npad * 2, nslots, i < N);
@@ -277,7 +287,7 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
     const double X = __shfl_down_sync(0xffffffffu, M, 1);
     double e = 0.0;
     if (i < N && (threadIdx.x & 1) == 0)
-      e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32, lrho);
+      e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32, lrho, wm);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
     if (threadIdx.x == 0) {
@@ -314,27 +324,30 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
                                                         double* __restrict__ rec_rho,
                                                         float* __restrict__ rec32_rho,
                                                         double* __restrict__ ell_part, int* ticket,
-                                                        EvalStatus* st, double* __restrict__ lrho) {
+                                                        EvalStatus* st, double* __restrict__ lrho,
+                                                        WalkMap wm) {
   fin1p_block<D>(blockIdx.x, gridDim.x, part, npad, nslots, N, rec, rl, rates, fcp, rec_rho, rec32_rho,
-                 ell_part, ticket, st, lrho);
+                 ell_part, ticket, st, lrho, wm);
 }
 
 template <int D>
 __device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ part, long long npad,
-                                            int nslots, int N, double* __restrict__ grad) {
+                                            int nslots, int N, double* __restrict__ grad,
+                                            const int* __restrict__ perm) {
   constexpr int K = Layout<D>::K2;
-  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (event, d)
+  const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, d)
   const bool live = q < (long long)N * D;
-  const int i = (int)(q / D), d = (int)(q % D);
-  const double g = finp_slot_sum(part + (long long)i * K + d, npad * K, nslots, live);
-  if (threadIdx.x < 32 && live) grad[q] = g;
+  const int p = (int)(q / D), d = (int)(q % D);
+  const double g = finp_slot_sum(part + (long long)p * K + d, npad * K, nslots, live);
+  if (threadIdx.x < 32 && live) grad[(perm ? (long long)perm[p] * D + d : q)] = g;
   __syncthreads();   // finp_slot_sum's shared buffer is reused by the next block
 }
 
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, long long npad,
-                                                        int nslots, int N, double* __restrict__ grad) {
-  fin2p_block<D>(blockIdx.x, part, npad, nslots, N, grad);
+                                                        int nslots, int N, double* __restrict__ grad,
+                                                        const int* __restrict__ perm) {
+  fin2p_block<D>(blockIdx.x, part, npad, nslots, N, grad, perm);
 }
 
 template <int D>
@@ -345,6 +358,57 @@ __global__ void k_rho_to_rec(double* __restrict__ rec, float* __restrict__ rec32
   // both records: an fp32 context may evaluate with the fp64 kernels (range guard)
   if (rec32) rec32[(long long)i * Layout32<D>::REC + Layout32<D>::RHO] = (float)rl[2 * (long long)i];
   rec[(long long)i * Layout<D>::REC + Layout<D>::RHO] = rl[2 * (long long)i];
+}
+
+// Spatial walk order (hawkes_plan.h): the records the pair kernels stream, gathered in walk
+// order, rec_p[p] = rec[perm[p]] (x, t; rho' is written by the rate finalize), and each
+// 128-event tile's box {lo[D], hi[D], tmin, tmax} for the kernels' culling.  One CTA per tile,
+// once per evaluation (the locations move between evaluations).
+template <int D>
+__global__ void __launch_bounds__(128) k_walk_records(const double* __restrict__ rec,
+                                                      const int* __restrict__ perm, int N, int npad,
+                                                      double* __restrict__ rec_p,
+                                                      double* __restrict__ boxes) {
+  using L = Layout<D>;
+  const int p = blockIdx.x * 128 + threadIdx.x;
+  const bool live = p < N;
+  double v[D + 1];
+  const int i = perm[min(p, N - 1)];
+#pragma unroll
+  for (int d = 0; d <= D; ++d) v[d] = rec[(long long)i * L::REC + d];
+  if (p < npad) {
+#pragma unroll
+    for (int d = 0; d <= D; ++d) rec_p[(long long)p * L::REC + d] = v[d];
+  }
+  __shared__ double lo[4][D + 1], hi[4][D + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d <= D; ++d) {
+    double a = live ? v[d] : INFINITY, b = live ? v[d] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      lo[w][d] = a;
+      hi[w][d] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x <= D) {
+    const int d = threadIdx.x;
+    const double a = fmin(fmin(lo[0][d], lo[1][d]), fmin(lo[2][d], lo[3][d]));
+    const double b = fmax(fmax(hi[0][d], hi[1][d]), fmax(hi[2][d], hi[3][d]));
+    double* o = boxes + (long long)blockIdx.x * (2 * D + 2);
+    if (d < D) {
+      o[d] = a;
+      o[D + d] = b;
+    } else {
+      o[2 * D] = a;
+      o[2 * D + 1] = b;
+    }
+  }
 }
 
 // ---- HMC transition (Neal 2011): counter-based random numbers on the device.

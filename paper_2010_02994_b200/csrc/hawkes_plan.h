@@ -3,6 +3,7 @@
 // greedy deal of PAIRS' chunk pairs.  Included by hawkes_api.cu only.
 #pragma once
 #include <math.h>
+#include <cmath>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -67,6 +68,91 @@ std::vector<int> pair_owners(long long N, int chunk, int W) {
 int owner_of_tile(int k, int W) {
   const int pos = k % (2 * W);
   return pos < W ? pos : 2 * W - 1 - pos;
+}
+
+}  // namespace hk
+
+// ------------------------------------------------------------- spatial walk order (NEXT-2)
+// The PAIRS kernels walk the events in time order by default: chunk pairs and tiles are
+// time ranges, which makes the temporal culling exact and cheap.  Where the catalog's
+// spatial extent is many bandwidths wide (the DC shape: 16 km across, a 3.7 km
+// background cutoff), a spatial walk order instead makes tiles compact in space, so whole
+// tile pairs and chunk pairs fall outside every kernel's reach and are skipped by their
+// bounding boxes.  The order is a Morton (Z-order) sort of the locations quantised on their
+// bounding box (64 / D bits per dimension), ties broken by index.
+namespace hk {
+
+inline std::vector<int> morton_order(const double* x, int N, int D) {
+  const int bits = std::min(21, 64 / D);
+  std::vector<double> lo(D, INFINITY), hi(D, -INFINITY);
+  for (int i = 0; i < N; ++i)
+    for (int d = 0; d < D; ++d) {
+      lo[d] = std::min(lo[d], x[(size_t)i * D + d]);
+      hi[d] = std::max(hi[d], x[(size_t)i * D + d]);
+    }
+  const double scale = (double)((1ULL << bits) - 1);
+  std::vector<std::pair<unsigned long long, int>> key(N);
+  for (int i = 0; i < N; ++i) {
+    unsigned long long k = 0;
+    for (int d = 0; d < D; ++d) {
+      const double w = hi[d] > lo[d] ? (x[(size_t)i * D + d] - lo[d]) / (hi[d] - lo[d]) : 0.0;
+      const unsigned long long q = (unsigned long long)std::llround(std::min(1.0, std::max(0.0, w)) * scale);
+      for (int b = 0; b < bits; ++b) k |= ((q >> b) & 1ULL) << (b * D + d);
+    }
+    key[i] = {k, i};
+  }
+  std::sort(key.begin(), key.end());
+  std::vector<int> perm(N);
+  for (int i = 0; i < N; ++i) perm[i] = key[i].second;
+  return perm;
+}
+
+// Work estimate of a walk order: over the unordered tile pairs (128-event tiles of the order,
+// diagonal pairs at half weight), the number of pair terms (background, self-excitation)
+// whose bound from the two tiles' boxes can exceed the exp's clamp.  spatial_boxes = false
+// mirrors the time-order kernel, which bounds by the time gap alone.  Large N: a strided
+// sample of the tile pairs (the estimate only chooses between two orders).
+inline double walk_cost(const double* x, const double* t, const int* order, int N, int D,
+                        const PassConst& c, bool spatial_boxes) {
+  const int nt = (N + TILE_J - 1) / TILE_J;
+  std::vector<double> box((size_t)nt * (2 * D + 2));
+  for (int k = 0; k < nt; ++k) {
+    double* b = &box[(size_t)k * (2 * D + 2)];
+    for (int d = 0; d <= D; ++d) {
+      b[d < D ? d : 2 * D] = INFINITY;
+      b[d < D ? D + d : 2 * D + 1] = -INFINITY;
+    }
+    for (int p = k * TILE_J; p < std::min(N, (k + 1) * TILE_J); ++p) {
+      const int i = order ? order[p] : p;
+      for (int d = 0; d < D; ++d) {
+        b[d] = std::min(b[d], x[(size_t)i * D + d]);
+        b[D + d] = std::max(b[D + d], x[(size_t)i * D + d]);
+      }
+      b[2 * D] = std::min(b[2 * D], t[i]);
+      b[2 * D + 1] = std::max(b[2 * D + 1], t[i]);
+    }
+  }
+  const long long pairs = (long long)nt * (nt + 1) / 2;
+  const long long stride = std::max<long long>(1, pairs / 4000000);
+  double cost = 0.0;
+  long long q = 0;
+  for (int a = 0; a < nt; ++a)
+    for (int b = a; b < nt; ++b, ++q) {
+      if (q % stride) continue;
+      const double* A = &box[(size_t)a * (2 * D + 2)];
+      const double* B = &box[(size_t)b * (2 * D + 2)];
+      double r2 = 0.0;
+      if (spatial_boxes)
+        for (int d = 0; d < D; ++d) {
+          const double g = std::max(0.0, std::max(B[d] - A[D + d], A[d] - B[D + d]));
+          r2 += g * g;
+        }
+      const double dt = std::max(0.0, std::max(B[2 * D] - A[2 * D + 1], A[2 * D] - B[2 * D + 1]));
+      const double w = a == b ? 0.5 : 1.0;
+      if (c.kx * r2 + c.kt * dt * dt + c.lnc_b > CULL_EXPONENT) cost += w;
+      if (c.ks * r2 - c.omega * dt + c.lnc_s > CULL_EXPONENT) cost += w;
+    }
+  return cost * (double)stride;
 }
 
 }  // namespace hk

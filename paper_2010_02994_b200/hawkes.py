@@ -261,6 +261,19 @@ class HawkesContext:
         check(self._lib.hawkes_precision_in_use(self._h, ctypes.byref(v)), self._h)
         return "fp32" if v.value == HAWKES_FP32 else "fp64"
 
+    def set_ordering(self, mode: str = "auto"):
+        """hawkes_set_ordering: walk order of the PAIRS fp64 kernels, "auto" | "time" | "space"
+        (include/hawkes.h hawkes_ordering)."""
+        check(self._lib.hawkes_set_ordering(self._h, _lib.ORDERINGS[mode]), self._h)
+
+    @property
+    def ordering_in_use(self) -> Tuple[str, Tuple[float, float]]:
+        """hawkes_ordering_in_use: ("time" | "space", (time-order cost, space-order cost))."""
+        v = ctypes.c_int32()
+        cost = (ctypes.c_double * 2)()
+        check(self._lib.hawkes_ordering_in_use(self._h, ctypes.byref(v), cost), self._h)
+        return ("space" if v.value == 2 else "time"), (cost[0], cost[1])
+
     def enable_timing(self, enable: bool = True):
         check(self._lib.hawkes_enable_timing(self._h, int(bool(enable))), self._h)
 

@@ -15,11 +15,12 @@ TOL = {"fp64": (1e-9, 1e-3), "fp32": (1e-4, 1.0)}
 
 
 def gpu_eval(x, t, theta, precision="fp64", emulate_world=0, with_rates=True, device=0,
-             algorithm="auto"):
+             algorithm="auto", ordering="auto"):
     from paper_2010_02994_b200 import HawkesContext
     N, D = x.shape
     with HawkesContext(N, D, device=device, precision=precision, emulate_world=emulate_world,
                        algorithm=algorithm) as ctx:
+        ctx.set_ordering(ordering)
         ctx.set_times(torch.from_numpy(np.ascontiguousarray(t)).cuda(device))
         ctx.set_locations(torch.from_numpy(np.ascontiguousarray(x)).cuda(device))
         ctx.set_params(theta)
