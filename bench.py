@@ -407,6 +407,43 @@ def run_ours(args):
                         "acceptance": float(acc.mean())}
             mctx.close()
 
+    # ---- the paper's catalog shapes at N = 100k (SURVEY §8(d) C2 / C3 recipes): the walk
+    # order AUTO picks (spatial for the DC shape: exact box culling, NEXT-2) and its time
+    shaped = None
+    if not args.no_hmc and args.precision == "fp64":
+        shaped = {}
+        for name in ("C2", "C3"):
+            cs = synth.config(name, N=N)
+            sctx = (init_distributed_context(N, D, precision=args.precision, algorithm=args.algorithm)
+                    if world > 1 else HawkesContext(N, D, device=local, precision=args.precision,
+                                                     algorithm=args.algorithm))
+            xs = torch.from_numpy(cs.x).to(dev)
+            sctx.set_times(torch.from_numpy(cs.t).to(dev))
+            sctx.set_params(cs.theta)
+            gs = torch.empty_like(xs)
+            for _ in range(3):
+                sctx.set_locations(xs)
+                sctx.grad_locations(gs)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(sctx.stream)
+            for _ in range(5):
+                sctx.set_locations(xs)
+                sctx.grad_locations(gs)
+            s1.record(sctx.stream)
+            torch.cuda.synchronize()
+            sms_ = torch.tensor([s0.elapsed_time(s1) / 5], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(sms_, op=dist.ReduceOp.MAX)
+            order, cost = sctx.ordering_in_use
+            shaped[name] = {"config": f"{name}-shaped N={N} D=2 fp64", "ms_per_eval": float(sms_.item()),
+                            "pairs_per_s": N * (N - 1) / (float(sms_.item()) * 1e-3), "walk_order": order,
+                            "walk_cost_time_space": cost,
+                            "note": "effective pairs/s: culled pairs (exact, below the exp clamp) counted"}
+            sctx.close()
+
     # ---- per-rank pass-kernel time (library CUDA events): the load balance of the plan
     pass_ms = [float(kt["rate_ms"] + kt["grad_ms"]) / max(1, kt["rate_launches"])]
     if world > 1:
@@ -509,6 +546,7 @@ def run_ours(args):
         "loglik_only": loglik_only,
         "hmc": hmc,
         "mh_sweep": mh,
+        "shaped": shaped,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline()

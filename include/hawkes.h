@@ -337,6 +337,15 @@ int hawkes_plan(int64_t N, int32_t world, int32_t rank, int32_t* tiles_out, int3
 int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out,
                       int32_t* n_items, int32_t* chunk);
 
+/* Spatial walk order of the PAIRS kernels (host only, the logic hawkes_ordering AUTO uses):
+ * perm_out (nullable, N) receives the walk (Hilbert order of the locations for D = 2, Morton
+ * for other D), cost_out (nullable, 2) the work estimates of the time and the spatial walk
+ * (live (tile pair, term) counts from the tiles' bounding boxes under Theta; AUTO takes the
+ * spatial walk when cost_out[1] < 0.9 cost_out[0]).  x: N*D row-major, t: N non-decreasing.
+ * Errors: HAWKES_ERR_ARG. */
+int hawkes_plan_walk(const double* x, const double* t, int64_t N, int32_t D, const hawkes_params* p,
+                     int32_t* perm_out, double* cost_out);
+
 /* Diagnostics (not part of the numerical contract; used by the tests and bench.py):
  * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak
  * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */

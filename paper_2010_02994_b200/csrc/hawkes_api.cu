@@ -497,6 +497,20 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
   return HAWKES_OK;
 }
 
+int hawkes_plan_walk(const double* x, const double* t, int64_t N, int32_t D, const hawkes_params* p,
+                     int32_t* perm_out, double* cost_out) {
+  if (!x || !t || !p || N < 1 || N > (1LL << 30) || D < 1 || D > HAWKES_MAX_D)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan_walk");
+  const std::vector<int> perm = morton_order(x, (int)N, D);
+  if (perm_out) memcpy(perm_out, perm.data(), N * sizeof(int32_t));
+  if (cost_out) {
+    const PassConst pc = make_pass_const(*p, D, nullptr, nullptr);
+    cost_out[0] = walk_cost(x, t, nullptr, (int)N, D, pc, false);
+    cost_out[1] = walk_cost(x, t, perm.data(), (int)N, D, pc, true);
+  }
+  return HAWKES_OK;
+}
+
 int hawkes_nccl_unique_id(void* out) {
   if (!out) return set_err(nullptr, HAWKES_ERR_ARG, "out is NULL");
   std::string e;

@@ -392,9 +392,9 @@ int upload_consts(hawkes_ctx* ctx) {
   return HAWKES_OK;
 }
 
-// Kernel constants for Theta; written to ctx only when every check passes.
-int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
-  const int D = ctx->D;
+// The fp64 pass kernels' folded constants for Theta (lnw_b / lnw_s: the log kernel weights
+// times alpha / beta, returned for the range checks)
+PassConst make_pass_const(const hawkes_params& p, int D, double* lnw_b_out, double* lnw_s_out) {
   const double two_pi = 6.283185307179586476925286766559;
   // background weight mu0/((2pi)^{D/2} tau_x^D * sqrt(2pi) tau_t), times alpha = 1/tau_x^2
   const double lnw_b = log(p.mu0) - 0.5 * (D + 1) * log(two_pi) - D * log(p.tau_x) - log(p.tau_t) -
@@ -402,9 +402,6 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   // self-excitation weight theta omega/((2pi)^{D/2} h^D), times beta = 1/h^2
   const double lnw_s = log(p.theta) + log(p.omega) - 0.5 * D * log(two_pi) - D * log(p.sigma_x) -
                        2.0 * log(p.sigma_x);
-  if ((p.mu0 > 0 && !(fabs(lnw_b) < 600.0)) || (p.theta > 0 && !(fabs(lnw_s) < 600.0)))
-    return set_err(ctx, HAWKES_ERR_PARAM,
-                   "Theta puts the kernel constants outside the fp64 exp range (|log w| >= 600)");
   PassConst pc;
   pc.kx = -0.5 / (p.tau_x * p.tau_x);
   pc.kt = -0.5 / (p.tau_t * p.tau_t);
@@ -413,6 +410,19 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
   pc.lnc_b = p.mu0 > 0 ? lnw_b + 64.0 * LN2 : -INFINITY;
   pc.lnc_s = p.theta > 0 ? lnw_s + 64.0 * LN2 : -INFINITY;
   pc.lnc_sr = p.theta > 0 ? lnw_s : -INFINITY;
+  if (lnw_b_out) *lnw_b_out = lnw_b;
+  if (lnw_s_out) *lnw_s_out = lnw_s;
+  return pc;
+}
+
+// Kernel constants for Theta; written to ctx only when every check passes.
+int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
+  const int D = ctx->D;
+  double lnw_b = 0.0, lnw_s = 0.0;
+  const PassConst pc = make_pass_const(p, D, &lnw_b, &lnw_s);
+  if ((p.mu0 > 0 && !(fabs(lnw_b) < 600.0)) || (p.theta > 0 && !(fabs(lnw_s) < 600.0)))
+    return set_err(ctx, HAWKES_ERR_PARAM,
+                   "Theta puts the kernel constants outside the fp64 exp range (|log w| >= 600)");
   if (!isfinite(pc.kx) || !isfinite(pc.kt) || !isfinite(pc.ks))
     return set_err(ctx, HAWKES_ERR_PARAM, "bandwidths too small for fp64");
   FinConst fc;

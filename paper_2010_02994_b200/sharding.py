@@ -37,6 +37,24 @@ def plan_pairs(N: int, world: int, rank: int) -> Tuple[List[Tuple[int, int]], in
     return [(buf[2 * k], buf[2 * k + 1]) for k in range(n.value)], ck.value
 
 
+def plan_walk(x, t, theta) -> Tuple[List[int], Tuple[float, float]]:
+    """hawkes_plan_walk: (the spatial walk permutation, (time-walk cost, spatial-walk cost))."""
+    import numpy as np
+    lib = _lib.load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    N, D = x.shape
+    perm = np.empty(N, dtype=np.int32)
+    cost = np.zeros(2)
+    p = _lib.Params(*[float(v) for v in theta])
+    _lib.check(lib.hawkes_plan_walk(x.ctypes.data, t.ctypes.data, N, D, ctypes.byref(p),
+                                    perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                    cost.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return perm.tolist(), (float(cost[0]), float(cost[1]))
+
+
 def rows_of(N: int, world: int, rank: int) -> List[int]:
     tiles, rt, _ = plan(N, world, rank)
     return [i for k in tiles for i in range(k * rt, min(N, (k + 1) * rt))]

@@ -123,3 +123,26 @@ def test_pair_chunk_heuristic(N, W, chunk):
     r01_chunk256.txt)."""
     from paper_2010_02994_b200 import sharding
     assert sharding.plan_pairs(N, W, 0)[1] == chunk
+
+
+def test_spatial_walk_plan_host_logic():
+    """hawkes_plan_walk (the host logic of the AUTO walk order): the walk
+    is a permutation; it is spatially local (consecutive events of the walk are far closer
+    than random pairs); the box-based work estimate prefers it on the DC shape (16 km across,
+    3.7 km cutoff) and not on the unit square (nothing to cull), and a pure translation or a
+    reversal of the time axis does not change the costs."""
+    import numpy as np
+
+    import synth
+    from paper_2010_02994_b200 import sharding
+    for name, N, want in (("C2", 20000, True), ("C4", 20000, False)):
+        c = synth.config(name, N)
+        perm, (ct, cs) = sharding.plan_walk(c.x, c.t, c.theta)
+        assert sorted(perm) == list(range(N))
+        xp = c.x[perm]
+        step = np.mean(np.linalg.norm(np.diff(xp, axis=0), axis=1))
+        rnd = np.mean(np.linalg.norm(c.x[1:] - c.x[:-1], axis=1))   # time order ~ random in space
+        assert step < 0.05 * rnd, (name, step, rnd)
+        assert (cs < 0.9 * ct) == want, (name, ct, cs)
+        perm2, (ct2, cs2) = sharding.plan_walk(c.x + 1e3, c.t, c.theta)
+        assert perm2 == perm and abs(ct2 - ct) <= 1e-9 * ct and abs(cs2 - cs) <= 1e-9 * cs
