@@ -32,6 +32,25 @@
 
 namespace hk {
 
+// -DHK_CHECKED (tools/checked_run.sh): device-side bounds checks on the pass kernels' item
+// decode, bulk-copy ranges, partial-slot stores and walk permutation -- compute-sanitizer is
+// closed on the GPU pool, so the checked build runs the GPU test-suite instead.  A failed check
+// prints its site and traps (the launch then fails with an error).
+#ifdef HK_CHECKED
+#define HK_CHECK(cond)                                                                    \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("HK_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,      \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define HK_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int THREADS = 128;
 constexpr int TILE_J = 128;
 constexpr int STAGES = 4;

@@ -390,6 +390,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
   // stage s <- column tile [jt, jt + cnt): the records, and (pass 2) -ln lambda rounded up to
   // an even count (16-byte bulk copies; lrho has npad >= N + 1 entries or N even)
   auto load_stage = [&](int s, int jt, int cnt) {
+    HK_CHECK(s >= 0 && s < STAGES && cnt >= 1 && cnt <= TILE_J && jt >= 0 && jt + cnt <= a.npad &&
+             jt % TILE_J == 0);
     if (FOLD)
       tma_load_1d_x2(stage + s * TILE_J * REC, a.rec + (long long)jt * REC,
                      (uint32_t)(cnt * REC * sizeof(double)), lstage + s * LST, a.lrho + jt,
@@ -408,6 +410,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
     __syncthreads();
     if (it >= a.n_items) break;
     const int2 w = a.items[it];
+    HK_CHECK(w.x >= 0 && w.x <= w.y && w.y < a.nchunks);
     const bool diag = w.x == w.y;
     const int r0 = w.x * a.chunk;                 // chunk a: rows
     const int r1 = min(N, r0 + a.chunk);
@@ -513,6 +516,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         const int cj = jt + min(cl, cnt - 1);
         const int cg = a.gid[cj];
         // column sums: accumulated over this item's row tiles in its own slot
+        HK_CHECK(cslot >= 0 && cslot <= a.nchunks && cj >= 0 && cj < a.N);
         double* cpart = a.part + ((long long)cslot * a.npad + cj) * K;
         const bool first = rt == 0;   // every column tile is first visited by row tile 0
         double cacc[2 + D];
@@ -617,6 +621,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         v += red[(1 * SYM_RT + rr) * KR + kk];
         v += red[(2 * SYM_RT + rr) * KR + kk];
         v += red[(3 * SYM_RT + rr) * KR + kk];
+        HK_CHECK(row0 + rr < a.N && w.y < a.nchunks && kk < K);
         double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;   // slot b
         if (PASS == 1 && !GEN) {
           o[0] = v;      // M

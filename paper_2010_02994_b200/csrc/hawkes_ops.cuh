@@ -172,6 +172,7 @@ __device__ __forceinline__ double fin1_event(int p, double M, double X, const do
                                            double* __restrict__ lrho, WalkMap wm = WalkMap{nullptr, nullptr}) {
   using L = Layout<D>;
   const int i = wm.perm ? wm.perm[p] : p;
+  HK_CHECK(i >= 0 && p >= 0);
   // Lambda' = 2^64 lambda = M' tau_x^2 + X' h^2 (undo the alpha / beta folded into the exps)
   const double mu_s = M * f.tx2, xi_s = X * f.h2;
   if (mu_s + xi_s < f.range_floor) *range_flag = 1;   // fp32 only (range_floor = 0 in fp64)
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(128) k_walk_records(const double* __restrict__
   const bool live = p < N;
   double v[D + 1];
   const int i = perm[min(p, N - 1)];
+  HK_CHECK(i >= 0 && i < N);
 #pragma unroll
   for (int d = 0; d <= D; ++d) v[d] = rec[(long long)i * L::REC + d];
   if (p < npad) {
