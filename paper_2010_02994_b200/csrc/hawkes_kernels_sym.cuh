@@ -635,8 +635,21 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
   }
 }
 
+// CTAs per SM: 4 (<= 128 registers) for the D <= 2 time-walk gradient pass, 3 (<= 168) for
+// the other D <= 4 kernels, 2 above.  At N = 100k the gradient pass at 128 registers has no
+// spills and runs 1.5 % faster (more warps hide its dependency latency), the rate pass 1.2 %
+// slower (profiles/r02_ab_occ4.jsonl) and the spatial-walk gradient pass 2 % slower (DC shape);
+// -DHK_SYM_OCC4 asks for 4 everywhere (A/B).
+template <int D, int PASS, bool GEN>
+constexpr int sym_min_ctas() {
+#ifdef HK_SYM_OCC4
+  return D <= 4 ? 4 : 2;
+#else
+  return (D <= 2 && PASS == 2 && !GEN) ? 4 : (D <= 4 ? 3 : 2);
+#endif
+}
 template <int D, int PASS, int SYM_R, int V, bool GEN = false>
-__global__ void __launch_bounds__(THREADS, D <= 4 ? 3 : 2) sym_kernel(SymArgs a) {
+__global__ void __launch_bounds__(THREADS, sym_min_ctas<D, PASS, GEN>()) sym_kernel(SymArgs a) {
   using Cfg = SymCfg<D, PASS, V, GEN>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const typename Cfg::Smem sm(smem_raw);
