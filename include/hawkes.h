@@ -346,6 +346,14 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
 int hawkes_plan_walk(const double* x, const double* t, int64_t N, int32_t D, const hawkes_params* p,
                      int32_t* perm_out, double* cost_out);
 
+/* Partial-slot footprint of HAWKES_ALGO_PAIRS on one rank (host only): the events of the
+ * compact, item-indexed slot blocks rank `rank` of `world` allocates (one block of chunk
+ * events per (chunk, slot id) its chunk pairs write; device memory = slot_events * 8 *
+ * (2 + K2) bytes), and in *max_events (nullable) the largest over all ranks.  At world = 1
+ * it is (C + 1) C chunk; the ranks together hold the same blocks, so each holds ~1/world.
+ * Errors: HAWKES_ERR_ARG. */
+int hawkes_plan_slots(int64_t N, int32_t world, int32_t rank, int64_t* slot_events, int64_t* max_events);
+
 /* Diagnostics (not part of the numerical contract; used by the tests and bench.py):
  * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak
  * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */

@@ -106,21 +106,27 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   else
     for (int r = 0; r < ctx->W; ++r) ctx->my_ranks.push_back(r);
 
-  std::vector<std::vector<int2>> it1, it2, sym;
+  std::vector<std::vector<int2>> it1, it2;
+  std::vector<std::vector<PairItem>> sym;
+  std::vector<std::vector<long long>> coff;
+  std::vector<std::vector<int>> cn;
   std::vector<int> own;
   if (ctx->pairs)
-    build_plan_pairs(ctx, it1, it2, sym, own);
+    build_plan_pairs(ctx, it1, it2, sym, own, coff, cn);
   else
     build_plan(ctx, it1, it2);
+  // partial slots: PAIRS item-indexed and compact per rank (slot_events x K), ROWS
+  // [nchunks][npad][K]
+  const size_t slots1 = ctx->pairs ? (size_t)ctx->slot_events * K1P : (size_t)ctx->nslots * ctx->npad * K1_of(D);
+  const size_t slots2 = ctx->pairs ? (size_t)ctx->slot_events * K2_of(D) : (size_t)ctx->nslots * ctx->npad * K2_of(D);
 
   const int REC = REC_of(D);
   int rc;
   if ((rc = dalloc(ctx, &ctx->rec, (size_t)ctx->npad * REC)) ||
       (rc = dalloc(ctx, &ctx->gid, (size_t)ctx->npad)) ||
       // PAIRS' rate partials are (M', X') only (K1P = 2): half the memory at D = 2 that the
-      // ROWS layout (M', X', G1') takes -- 211 MB instead of 422 MB at N = 100k
-      (rc = dalloc(ctx, &ctx->part1, (size_t)ctx->nslots * ctx->npad * (ctx->pairs ? K1P : K1_of(D)))) ||
-      (rc = dalloc(ctx, &ctx->part2, (size_t)ctx->nslots * ctx->npad * K2_of(D))) ||
+      // ROWS layout (M', X', G1') takes -- 211 MB instead of 422 MB at N = 100k, W = 1
+      (rc = dalloc(ctx, &ctx->part1, slots1)) || (rc = dalloc(ctx, &ctx->part2, slots2)) ||
       (rc = dalloc(ctx, &ctx->G1, (size_t)ctx->npad * D)) ||
       (rc = dalloc(ctx, &ctx->rl, (size_t)ctx->npad * 2)) ||
       (rc = dalloc(ctx, &ctx->lrho, (size_t)ctx->npad)) ||
@@ -161,12 +167,18 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
         cudaMemcpy(ctx->d_own, own.data(), own.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair plan failed"));
     ctx->d_sym.assign(ctx->W, nullptr);
+    ctx->d_coff.assign(ctx->W, nullptr);
+    ctx->d_cn.assign(ctx->W, nullptr);
     ctx->n_sym.assign(ctx->W, 0);
     for (int r = 0; r < ctx->W; ++r) {
       ctx->n_sym[r] = (int)sym[r].size();
-      if ((rc = dalloc(ctx, &ctx->d_sym[r], sym[r].size()))) return fail(rc);
-      if (!sym[r].empty() &&
-          cudaMemcpy(ctx->d_sym[r], sym[r].data(), sym[r].size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess)
+      if ((rc = dalloc(ctx, &ctx->d_sym[r], sym[r].size())) ||
+          (rc = dalloc(ctx, &ctx->d_coff[r], coff[r].size())) || (rc = dalloc(ctx, &ctx->d_cn[r], cn[r].size())))
+        return fail(rc);
+      if ((!sym[r].empty() &&
+           cudaMemcpy(ctx->d_sym[r], sym[r].data(), sym[r].size() * sizeof(PairItem), cudaMemcpyHostToDevice) != cudaSuccess) ||
+          cudaMemcpy(ctx->d_coff[r], coff[r].data(), coff[r].size() * sizeof(long long), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(ctx->d_cn[r], cn[r].data(), cn[r].size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(set_err(ctx, HAWKES_ERR_CUDA, "copy of the pair items failed"));
     }
     if (ctx->multi) {
@@ -264,6 +276,8 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   for (auto* p : ctx->d_items1) if (p) cudaFree(p);
   for (auto* p : ctx->d_items2) if (p) cudaFree(p);
   for (auto* p : ctx->d_sym) if (p) cudaFree(p);
+  for (auto* p : ctx->d_coff) if (p) cudaFree(p);
+  for (auto* p : ctx->d_cn) if (p) cudaFree(p);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   for (auto& pr : ctx->ev_rate) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto& pr : ctx->ev_grad) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -507,6 +521,24 @@ int hawkes_plan_walk(const double* x, const double* t, int64_t N, int32_t D, con
     const PassConst pc = make_pass_const(*p, D, nullptr, nullptr);
     cost_out[0] = walk_cost(x, t, nullptr, (int)N, D, pc, false);
     cost_out[1] = walk_cost(x, t, perm.data(), (int)N, D, pc, true);
+  }
+  return HAWKES_OK;
+}
+
+int hawkes_plan_slots(int64_t N, int32_t world, int32_t rank, int64_t* slot_events, int64_t* max_events) {
+  if (N < 1 || N > (1LL << 30) || world < 1 || rank < 0 || rank >= world || !slot_events)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan_slots");
+  const int ck = chunk_pairs_of(N, world);
+  const PairsLayout L = pairs_layout(N, ck, world, {rank});
+  *slot_events = L.slot_events;
+  if (max_events) {   // every rank's, for the balance
+    long long mx = 0;
+    for (int r = 0; r < world; ++r) {
+      long long s = 0;
+      for (int c : L.cn[r]) s += (long long)c * ck;
+      mx = std::max(mx, s);
+    }
+    *max_events = mx;
   }
   return HAWKES_OK;
 }

@@ -105,8 +105,11 @@ struct hawkes_ctx {
   ncclComm_t comm = nullptr;
   // HAWKES_ALGO_PAIRS
   bool pairs = false;
-  std::vector<int2*> d_sym;                 // per rank: off-diagonal chunk pairs
+  std::vector<PairItem*> d_sym;             // per rank: chunk pairs (a <= b) and slot blocks
   std::vector<int> n_sym;
+  std::vector<long long*> d_coff;           // per rank: [nchunks] slot-block event offsets
+  std::vector<int*> d_cn;                   // per rank: [nchunks] slot blocks per chunk
+  long long slot_events = 0;                // events of all slot blocks this process holds
   int* d_own = nullptr;                     // [nchunks][nchunks] owner rank of pair (a <= b)
   int* d_every_tile = nullptr;              // all row tiles 0..ntiles-1
   bool multi = false;                       // W > 1 (real or emulated) or an NCCL communicator:

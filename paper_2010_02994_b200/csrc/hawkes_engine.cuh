@@ -47,8 +47,7 @@ int reduce_pair_partials(hawkes_ctx* ctx, const double* part, double* sums, int 
   const long long stride = (long long)ctx->npad * K;
   for (int r : ctx->my_ranks) {
     k_slot_sum<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
-        part, ctx->npad, ctx->nchunks, ctx->chunk, K, ctx->d_own, r, (int)ctx->N,
-        sums + (1 + r) * stride);
+        part, SlotView{ctx->d_coff[r], ctx->d_cn[r], ctx->chunk}, K, (int)ctx->N, sums + (1 + r) * stride);
     CHECK_LAUNCH();
   }
   if (ctx->comm) {
@@ -314,31 +313,23 @@ int check_ready(hawkes_ctx* ctx) {
   return HAWKES_OK;
 }
 
+// PAIRS plan (hawkes_plan.h pairs_layout): each rank's chunk pairs (heaviest first) and its
+// compact slot layout; ROWS' tile lists stay empty.
 void build_plan_pairs(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
-                      std::vector<std::vector<int2>>& it2, std::vector<std::vector<int2>>& sym,
-                      std::vector<int>& own) {
-  const int W = ctx->W, C = ctx->nchunks, N = (int)ctx->N;
-  own = pair_owners(N, ctx->chunk, W);
+                      std::vector<std::vector<int2>>& it2, std::vector<std::vector<PairItem>>& sym,
+                      std::vector<int>& own, std::vector<std::vector<long long>>& coff,
+                      std::vector<std::vector<int>>& cn) {
+  const int W = ctx->W;
+  own = pair_owners(ctx->N, ctx->chunk, W);
   ctx->tiles_of.assign(W, {});
   ctx->max_tiles = 0;
   it1.assign(W, {});
   it2.assign(W, {});
-  sym.assign(W, {});
-  for (int r = 0; r < W; ++r) {
-    std::vector<std::pair<double, int2>> items;   // (pair count, (a, b)); heaviest first
-    for (int a = 0; a < C; ++a)
-      for (int b = a; b < C; ++b) {
-        if (own[(size_t)a * C + b] != r) continue;
-        const double na = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)a * ctx->chunk);
-        const double nb = (double)std::min<long long>(ctx->chunk, (long long)N - (long long)b * ctx->chunk);
-        items.push_back({a == b ? 0.5 * na * na : na * nb, make_int2(a, b)});
-      }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const std::pair<double, int2>& x, const std::pair<double, int2>& y) {
-                       return x.first > y.first;
-                     });
-    for (auto& e : items) sym[r].push_back(e.second);
-  }
+  PairsLayout lay = pairs_layout(ctx->N, ctx->chunk, W, ctx->my_ranks);
+  sym.swap(lay.items);
+  coff.swap(lay.coff);
+  cn.swap(lay.cn);
+  ctx->slot_events = lay.slot_events;
 }
 
 void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,

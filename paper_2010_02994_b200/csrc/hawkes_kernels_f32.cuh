@@ -422,7 +422,7 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
 struct SymArgs32 {
   const float* rec;
   const int* gid;
-  const int2* items;
+  const PairItem* items;   // chunk pairs and their slot blocks (hawkes_kernels_sym.cuh)
   int* counter;
   double* part;
   long long npad;
@@ -466,15 +466,14 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
     const int it = s_item;
     __syncthreads();
     if (it >= a.n_items) break;
-    const int2 w = a.items[it];
-    const bool diag = w.x == w.y;
-    const int r0 = w.x * a.chunk;
+    const PairItem w = a.items[it];
+    const bool diag = w.a == w.b;
+    const int r0 = w.a * a.chunk;
     const int r1 = min(N, r0 + a.chunk);
-    const int c0 = w.y * a.chunk;
+    const int c0 = w.b * a.chunk;
     const int c1 = min(N, c0 + a.chunk);
     const int n_rt = (r1 - r0 + SRT - 1) / SRT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
-    const int cslot = diag ? a.nchunks : w.x;
 
     TileWalk prod{0, 0};
     if (tid == 0) {
@@ -530,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         const bool cvalid = cl < cnt;
         const int cj = jt + min(cl, cnt - 1);
         const int cg = a.gid[cj];
-        double* cpart = a.part + ((long long)cslot * a.npad + cj) * K;
+        double* cpart = a.part + (w.co + (cj - c0)) * K;
         float cacc[2 + D];
 #pragma unroll
         for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.f;
@@ -612,7 +611,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         v += red[(1 * SRT + rr) * KR + kk];
         v += red[(2 * SRT + rr) * KR + kk];
         v += red[(3 * SRT + rr) * KR + kk];
-        double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;
+        double* o = a.part + (w.ro + (row0 + rr - r0)) * K;
         if (PASS == 1) {
           o[0] = v;
           o[1] = 0.0;

@@ -52,15 +52,28 @@ constexpr double CULL_EXPONENT = -708.0;
 // 16 copies of the 256-entry table (32 KB); the 1024-entry table (8 KB) fits 4, the 2048-entry one 2
 constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : (EXP_TABLE == 1024 ? 4 : 2);
 
+// One work item of the unordered-pair kernels: chunk pair (a, b), a <= b, and where its
+// partial sums go.  The slot arrays are item-indexed and compact per rank (hawkes_engine.cuh
+// build_plan_pairs): for each chunk c, one block of `chunk` events per slot that this rank's
+// items write for c's events, the slots in ascending slot id (row role of item (c, b): slot b;
+// column role of item (a, c), a < c: slot a; column role of the diagonal item (c, c): slot C),
+// so a rank holds ~1/W of the partials and the finalize adds them in the same fixed order for
+// every W.  ro / co: the event offsets of this item's row block (chunk a's events) and column
+// block (chunk b's events) in the slot array.
+struct PairItem {
+  int a, b;
+  long long ro, co;
+};
+
 struct SymArgs {
   const double* rec;     // records in the item walk's order (time order, or spatial: rec_p)
   const double* boxes;   // GEN: per 128-event tile {lo[D], hi[D], tmin, tmax} (spatial order)
   int ties;              // GEN: the catalog has equal times (every tile pair takes the masked path)
   const double* lrho;    // pass 2: -ln lambda_j per event (npad), staged beside the records
   const int* gid;
-  const int2* items;     // (a, b) chunk pairs, a < b
+  const PairItem* items; // chunk pairs and their slot blocks
   int* counter;
-  double* part;          // [chunks][Npad][K]
+  double* part;          // item-indexed slot blocks (PairItem), K per event
   const int2* tab;
   long long npad;
   int N;
@@ -409,16 +422,15 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
     const int it = s_item;
     __syncthreads();
     if (it >= a.n_items) break;
-    const int2 w = a.items[it];
-    HK_CHECK(w.x >= 0 && w.x <= w.y && w.y < a.nchunks);
-    const bool diag = w.x == w.y;
-    const int r0 = w.x * a.chunk;                 // chunk a: rows
+    const PairItem w = a.items[it];
+    HK_CHECK(w.a >= 0 && w.a <= w.b && w.b < a.nchunks && w.ro >= 0 && w.co >= 0);
+    const bool diag = w.a == w.b;
+    const int r0 = w.a * a.chunk;                 // chunk a: rows
     const int r1 = min(N, r0 + a.chunk);
-    const int c0 = w.y * a.chunk;                 // chunk b: columns
+    const int c0 = w.b * a.chunk;                 // chunk b: columns
     const int c1 = min(N, c0 + a.chunk);
     const int n_rt = (r1 - r0 + SYM_RT - 1) / SYM_RT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
-    const int cslot = diag ? a.nchunks : w.x;     // column-role slot of this item
     if (GEN && !diag) {
       // item-level cull: the union boxes of the two chunks; a dead item still owns its
       // slots (row role: slot b of chunk a's events; column role: slot a of chunk b's)
@@ -450,10 +462,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         hi_b[D] = fmax(hi_b[D], b[2 * D + 1]);
       }
       if (!box_pair_live<D>(lo_a, hi_a, lo_b, hi_b, c)) {
-        for (int q = tid; q < (r1 - r0) * K; q += THREADS)
-          a.part[((long long)w.y * a.npad + r0) * K + q] = 0.0;
-        for (int q = tid; q < (c1 - c0) * K; q += THREADS)
-          a.part[((long long)cslot * a.npad + c0) * K + q] = 0.0;
+        for (int q = tid; q < (r1 - r0) * K; q += THREADS) a.part[w.ro * K + q] = 0.0;
+        for (int q = tid; q < (c1 - c0) * K; q += THREADS) a.part[w.co * K + q] = 0.0;
         continue;   // (the next item fetch synchronises the CTA)
       }
     }
@@ -516,8 +526,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         const int cj = jt + min(cl, cnt - 1);
         const int cg = a.gid[cj];
         // column sums: accumulated over this item's row tiles in its own slot
-        HK_CHECK(cslot >= 0 && cslot <= a.nchunks && cj >= 0 && cj < a.N);
-        double* cpart = a.part + ((long long)cslot * a.npad + cj) * K;
+        HK_CHECK(cj >= c0 && cj < c1);
+        double* cpart = a.part + (w.co + (cj - c0)) * K;
         const bool first = rt == 0;   // every column tile is first visited by row tile 0
         double cacc[2 + D];
         if (first || !cvalid) {
@@ -621,8 +631,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         v += red[(1 * SYM_RT + rr) * KR + kk];
         v += red[(2 * SYM_RT + rr) * KR + kk];
         v += red[(3 * SYM_RT + rr) * KR + kk];
-        HK_CHECK(row0 + rr < a.N && w.y < a.nchunks && kk < K);
-        double* o = a.part + ((long long)w.y * a.npad + row0 + rr) * K;   // slot b
+        HK_CHECK(row0 + rr < a.N && kk < K);
+        double* o = a.part + (w.ro + (row0 + rr - r0)) * K;   // row block (slot b)
         if (PASS == 1 && !GEN) {
           o[0] = v;      // M
           o[1] = 0.0;    // X: xi_ij = 0 for a later j

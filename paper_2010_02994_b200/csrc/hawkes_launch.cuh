@@ -350,7 +350,9 @@ struct Fin1D {
       static_assert(K1P == 2, "k_fin1p pairs (M', X') lanes");
       const long long n = 2 * ctx->N;
       k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
-          sums ? ctx->sums1 : ctx->part1, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->rec,
+          sums ? ctx->sums1 : ctx->part1,
+          sums ? SlotView{nullptr, nullptr, ctx->chunk} : SlotView{ctx->d_coff[0], ctx->d_cn[0], ctx->chunk},
+          (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
           ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr,
           ctx->spatial ? WalkMap{ctx->d_perm, ctx->rec_p + Layout<D>::RHO} : WalkMap{nullptr, nullptr});
@@ -374,7 +376,9 @@ struct Fin2D {
     if (all) {
       const long long n = ctx->N * D;
       k_fin2p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
-          sums ? ctx->sums2 : ctx->part2, ctx->npad, sums ? 1 : ctx->nslots, (int)ctx->N, ctx->grad,
+          sums ? ctx->sums2 : ctx->part2,
+          sums ? SlotView{nullptr, nullptr, ctx->chunk} : SlotView{ctx->d_coff[0], ctx->d_cn[0], ctx->chunk},
+          (int)ctx->N, ctx->grad,
           ctx->spatial ? ctx->d_perm : nullptr);
     } else {
       k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,

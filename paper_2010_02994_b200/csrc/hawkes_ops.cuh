@@ -81,21 +81,26 @@ __global__ void k_pack_t32(float* __restrict__ rec, const double* __restrict__ t
   for (int k = L::RHO; k < L::REC; ++k) rec[(long long)i * L::REC + k] = 0.f;
 }
 
-// PAIRS with W > 1: per event, fixed-order sum of the partial slots this rank computed.
-// Slot s of event i (chunk c) comes from chunk pair (min(s, c), max(s, c)).
-// Slot nchunks (the diagonal items' column role) comes from pair (c, c).
-__global__ void k_slot_sum(const double* __restrict__ part, long long npad, int nchunks, int chunk,
-                           int K, const int* __restrict__ own, int rank, int N,
+// The slot blocks of event i's chunk c in a rank's compact slot array (PairItem): cn[c] blocks
+// of `chunk` events from event offset coff[c], in ascending slot id.  coff == nullptr: one
+// event-major slot (the exchanged per-event sums of W > 1).
+struct SlotView {
+  const long long* coff;
+  const int* cn;
+  int chunk;
+};
+
+// PAIRS with W > 1: per event, the fixed-order sum of the slots this rank computed.
+__global__ void k_slot_sum(const double* __restrict__ part, SlotView sv, int K, int N,
                            double* __restrict__ out) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)N * K) return;
   const int i = (int)(idx / K), k = (int)(idx % K);
-  const int c = i / chunk;
+  const int c = i / sv.chunk;
+  const double* p = part + (sv.coff[c] + (i - c * sv.chunk)) * K + k;
+  const long long stride = (long long)sv.chunk * K;
   double v = 0.0;
-  for (int sl = 0; sl <= nchunks; ++sl) {
-    const int a = sl == nchunks ? c : min(sl, c), b = sl == nchunks ? c : max(sl, c);
-    if (own[a * nchunks + b] == rank) v += part[((long long)sl * npad + i) * K + k];
-  }
+  for (int s = 0; s < sv.cn[c]; ++s) v += p[s * stride];
   out[idx] = v;
 }
 
@@ -272,7 +277,7 @@ __device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, lo
 // ticket.  Replaces k_ell_reduce (one launch and a one-CTA pass over N) on the PAIRS path.
 template <int D>
 __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __restrict__ part,
-                                            long long npad, int nslots, int N,
+                                            SlotView sv, int N,
                                             const double* __restrict__ rec, double* __restrict__ rl,
                                             double* __restrict__ rates, const FinConst* __restrict__ fcp,
                                             double* __restrict__ rec_rho, float* __restrict__ rec32_rho,
@@ -280,8 +285,17 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
                                             double* __restrict__ lrho, WalkMap wm) {
   const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, M' or X')
   const int i = (int)(q >> 1);
-  // part[(c npad + i) K1P + k], K1P = 2
-  const double M = finp_slot_sum(part + q, npad * 2, nslots, i < N);
+  // K1P = 2 partials per event
+  const double* p0 = part + q;
+  long long stride = 0;
+  int nslots = 1;
+  if (sv.coff) {
+    const int c = min(i, N - 1) / sv.chunk;
+    p0 = part + (sv.coff[c] + (i - c * sv.chunk)) * 2 + (q & 1);
+    stride = (long long)sv.chunk * 2;
+    nslots = sv.cn[c];
+  }
+  const double M = finp_slot_sum(p0, stride, nslots, i < N);
   __shared__ int last;
   __shared__ double red[FINP_THREADS];
   if (threadIdx.x < 32) {
@@ -318,8 +332,8 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
 }
 
 template <int D>
-__global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, long long npad,
-                                                        int nslots, int N, const double* __restrict__ rec,
+__global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict__ part, SlotView sv,
+                                                        int N, const double* __restrict__ rec,
                                                         double* __restrict__ rl, double* __restrict__ rates,
                                                         const FinConst* __restrict__ fcp,
                                                         double* __restrict__ rec_rho,
@@ -327,28 +341,37 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
                                                         double* __restrict__ ell_part, int* ticket,
                                                         EvalStatus* st, double* __restrict__ lrho,
                                                         WalkMap wm) {
-  fin1p_block<D>(blockIdx.x, gridDim.x, part, npad, nslots, N, rec, rl, rates, fcp, rec_rho, rec32_rho,
+  fin1p_block<D>(blockIdx.x, gridDim.x, part, sv, N, rec, rl, rates, fcp, rec_rho, rec32_rho,
                  ell_part, ticket, st, lrho, wm);
 }
 
 template <int D>
-__device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ part, long long npad,
-                                            int nslots, int N, double* __restrict__ grad,
+__device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ part, SlotView sv,
+                                            int N, double* __restrict__ grad,
                                             const int* __restrict__ perm) {
   constexpr int K = Layout<D>::K2;
   const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, d)
   const bool live = q < (long long)N * D;
   const int p = (int)(q / D), d = (int)(q % D);
-  const double g = finp_slot_sum(part + (long long)p * K + d, npad * K, nslots, live);
+  const double* p0 = part + (long long)p * K + d;
+  long long stride = 0;
+  int nslots = 1;
+  if (sv.coff) {
+    const int c = min(p, N - 1) / sv.chunk;
+    p0 = part + (sv.coff[c] + (p - c * sv.chunk)) * K + d;
+    stride = (long long)sv.chunk * K;
+    nslots = sv.cn[c];
+  }
+  const double g = finp_slot_sum(p0, stride, nslots, live);
   if (threadIdx.x < 32 && live) grad[(perm ? (long long)perm[p] * D + d : q)] = g;
   __syncthreads();   // finp_slot_sum's shared buffer is reused by the next block
 }
 
 template <int D>
-__global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, long long npad,
-                                                        int nslots, int N, double* __restrict__ grad,
+__global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, SlotView sv,
+                                                        int N, double* __restrict__ grad,
                                                         const int* __restrict__ perm) {
-  fin2p_block<D>(blockIdx.x, part, npad, nslots, N, grad, perm);
+  fin2p_block<D>(blockIdx.x, part, sv, N, grad, perm);
 }
 
 template <int D>

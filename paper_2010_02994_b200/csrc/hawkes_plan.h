@@ -65,6 +65,71 @@ std::vector<int> pair_owners(long long N, int chunk, int W) {
   return own;
 }
 
+// PAIRS work items and compact slot layout of every rank (hawkes_kernels_sym.cuh PairItem):
+// rank r's chunk pairs, heaviest first (dynamic scheduling takes them in this order); for every
+// chunk c the ascending slot ids r's items write for c's events (row role of (c, b): b;
+// column role of (a, c), a < c: a; of (c, c): C), one block of `chunk` events per slot id,
+// chunk after chunk.  The ranks in `mine` (this process) are laid out one after another in one
+// array of slot_events events; the others' offsets start at 0 (not allocated here).  At W = 1
+// every chunk has C + 1 slots in slot-id order, the order the finalize sums them in.
+struct PairsLayout {
+  std::vector<std::vector<PairItem>> items;
+  std::vector<std::vector<long long>> coff;
+  std::vector<std::vector<int>> cn;
+  long long slot_events = 0;
+};
+
+inline PairsLayout pairs_layout(long long N, int chunk, int W, const std::vector<int>& mine) {
+  const int C = (int)((N + chunk - 1) / chunk);
+  const std::vector<int> own = pair_owners(N, chunk, W);
+  PairsLayout L;
+  L.items.assign(W, {});
+  L.coff.assign(W, {});
+  L.cn.assign(W, {});
+  long long base = 0;
+  for (int r = 0; r < W; ++r) {
+    const bool is_mine = std::find(mine.begin(), mine.end(), r) != mine.end();
+    std::vector<std::pair<double, int2>> items;   // (pair count, (a, b)); heaviest first
+    for (int a = 0; a < C; ++a)
+      for (int b = a; b < C; ++b) {
+        if (own[(size_t)a * C + b] != r) continue;
+        const double na = (double)std::min<long long>(chunk, N - (long long)a * chunk);
+        const double nb = (double)std::min<long long>(chunk, N - (long long)b * chunk);
+        items.push_back({a == b ? 0.5 * na * na : na * nb, make_int2(a, b)});
+      }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<double, int2>& x, const std::pair<double, int2>& y) {
+                       return x.first > y.first;
+                     });
+    std::vector<std::vector<int>> ids(C);
+    for (auto& e : items) {
+      const int a = e.second.x, b = e.second.y;
+      ids[a].push_back(b);
+      ids[b].push_back(a == b ? C : a);
+    }
+    L.coff[r].assign(C, 0);
+    L.cn[r].assign(C, 0);
+    long long off = is_mine ? base : 0;
+    for (int c = 0; c < C; ++c) {
+      std::sort(ids[c].begin(), ids[c].end());
+      L.coff[r][c] = off;
+      L.cn[r][c] = (int)ids[c].size();
+      off += (long long)ids[c].size() * chunk;
+    }
+    auto block = [&](int c, int id) {
+      const auto it = std::lower_bound(ids[c].begin(), ids[c].end(), id);
+      return L.coff[r][c] + (long long)(it - ids[c].begin()) * chunk;
+    };
+    for (auto& e : items) {
+      const int a = e.second.x, b = e.second.y;
+      L.items[r].push_back(PairItem{a, b, block(a, b), block(b, a == b ? C : a)});
+    }
+    if (is_mine) base = off;
+  }
+  L.slot_events = base;
+  return L;
+}
+
 int owner_of_tile(int k, int W) {
   const int pos = k % (2 * W);
   return pos < W ? pos : 2 * W - 1 - pos;

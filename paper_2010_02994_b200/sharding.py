@@ -37,6 +37,14 @@ def plan_pairs(N: int, world: int, rank: int) -> Tuple[List[Tuple[int, int]], in
     return [(buf[2 * k], buf[2 * k + 1]) for k in range(n.value)], ck.value
 
 
+def plan_slots(N: int, world: int, rank: int) -> Tuple[int, int]:
+    """hawkes_plan_slots: (this rank's partial-slot events, the largest over the ranks)."""
+    lib = _lib.load()
+    s, m = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(lib.hawkes_plan_slots(N, world, rank, ctypes.byref(s), ctypes.byref(m)))
+    return s.value, m.value
+
+
 def plan_walk(x, t, theta) -> Tuple[List[int], Tuple[float, float]]:
     """hawkes_plan_walk: (the spatial walk permutation, (time-walk cost, spatial-walk cost))."""
     import numpy as np

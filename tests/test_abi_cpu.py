@@ -146,3 +146,20 @@ def test_spatial_walk_plan_host_logic():
         assert (cs < 0.9 * ct) == want, (name, ct, cs)
         perm2, (ct2, cs2) = sharding.plan_walk(c.x + 1e3, c.t, c.theta)
         assert perm2 == perm and abs(ct2 - ct) <= 1e-9 * ct and abs(cs2 - cs) <= 1e-9 * cs
+
+
+@pytest.mark.parametrize("N", [5000, 100_000, 1_000_000])
+def test_compact_slot_layout_footprint(N):
+    """hawkes_plan_slots: PAIRS' item-indexed slot blocks.  At W = 1 a rank holds (C + 1) C
+    chunk events (every chunk has C + 1 slots); at W ranks the blocks are split without overlap
+    (the ranks' counts add up to the same total for that W's chunk) and each rank holds about
+    1/W of them (the full [C+1][Npad][K] arrays on every rank were ~12 GB at
+    N = 1M, W = 8)."""
+    from paper_2010_02994_b200 import sharding
+    for W in (1, 2, 4, 8):
+        _, chunk = sharding.plan_pairs(N, W, 0)
+        C = (N + chunk - 1) // chunk
+        per = [sharding.plan_slots(N, W, r)[0] for r in range(W)]
+        assert sum(per) == (C + 1) * C * chunk
+        assert sharding.plan_slots(N, W, 0)[1] == max(per)
+        assert max(per) <= 1.35 * (C + 1) * C * chunk / W + 4 * chunk * (C + 1), (W, per)
