@@ -98,8 +98,8 @@ typedef enum { HAWKES_ALGO_AUTO = 0, HAWKES_ALGO_ROWS = 1, HAWKES_ALGO_PAIRS = 2
  *           > 10 % lower for it, decided at the first evaluation after hawkes_set_times /
  *           hawkes_set_ordering from the locations and Theta of that evaluation (kept
  *           through later set_locations / set_params: the choice affects speed and summation
- *           order, never which terms are summed).  fp32 contexts, ROWS and D > 4 walk in time
- *           order. */
+ *           order, never which terms are summed).  ROWS and D > 4 walk in time order; fp32
+ *           contexts take the spatial walk too (their bounds against the fp32 flush). */
 typedef enum { HAWKES_ORDER_AUTO = 0, HAWKES_ORDER_TIME = 1, HAWKES_ORDER_SPACE = 2 } hawkes_ordering;
 
 typedef struct {

@@ -267,7 +267,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
     cudaStreamDestroy(ctx->gstream);
   }
   void* bufs[] = {ctx->d_mh_stamp, ctx->d_reg_c, ctx->d_reg_s, ctx->d_mh_blocks, ctx->d_mh_acc, ctx->d_mh_la, ctx->d_Y, ctx->d_bgrad, ctx->d_brow, ctx->d_bpart, ctx->d_move_rows_part, ctx->d_move_part, ctx->d_slot_of, ctx->d_move_idx, ctx->d_move_x, ctx->d_move_delta, ctx->d_move_rows,
-                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->lrho, ctx->d_perm, ctx->d_gid_p, ctx->rec_p, ctx->d_boxes, ctx->rates,
+                  ctx->d_consts, ctx->rec, ctx->rec32, ctx->gid, ctx->part1, ctx->part2, ctx->G1, ctx->rl, ctx->lrho, ctx->d_perm, ctx->d_gid_p, ctx->rec_p, ctx->rec32_p, ctx->d_boxes, ctx->rates,
                   ctx->grad, ctx->xstage, ctx->sendbuf, ctx->recvbuf, ctx->counters, ctx->ell_part, ctx->tab,
                   ctx->st, ctx->d_all_tiles, ctx->lf_x, ctx->lf_p, ctx->lf_minv,
                   ctx->lf_lo, ctx->lf_hi, ctx->lf_x0, ctx->lf_p0, ctx->d_own, ctx->d_every_tile, ctx->sums1, ctx->sums2};

@@ -137,6 +137,7 @@ struct hawkes_ctx {
   int* d_perm = nullptr;      // npad: walk position -> event
   int* d_gid_p = nullptr;     // npad: tie-group ids in walk order
   double* rec_p = nullptr;    // npad x REC: records in walk order
+  float* rec32_p = nullptr;   // npad x REC32: fp32 records in walk order (fp32 contexts)
   double* d_boxes = nullptr;  // npad/128 x (2D + 2): tile boxes in walk order
   double* rates = nullptr; // npad x 4 (lambda, mu, xi, Lambda)
   double* grad = nullptr;  // npad x D
@@ -182,6 +183,7 @@ struct hawkes_ctx {
   int grid_s1 = 0, grid_s2 = 0;
   int grid32_1 = 0, grid32_2 = 0, grid32_s1 = 0, grid32_s2 = 0;   // fp32 kernels
   int grid_g1 = 0, grid_g2 = 0;   // spatial-walk (GEN) sym kernels
+  int grid32_g1 = 0, grid32_g2 = 0;
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;

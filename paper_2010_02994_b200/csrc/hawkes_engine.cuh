@@ -140,7 +140,7 @@ int decide_order(hawkes_ctx* ctx) {
   ctx->order_decided = true;
   ctx->order_cost[0] = ctx->order_cost[1] = 0.0;
   const int N = (int)ctx->N, D = ctx->D;
-  const bool eligible = ctx->pairs && !ctx->rec32 && D <= SPACE_MAX_D && N >= 2 * TILE_J &&
+  const bool eligible = ctx->pairs && D <= SPACE_MAX_D && N >= 2 * TILE_J &&
                         ctx->order_req != HAWKES_ORDER_TIME;
   bool want = false;
   std::vector<int> perm;
@@ -170,6 +170,10 @@ int decide_order(hawkes_ctx* ctx) {
         (rc = dalloc(ctx, &ctx->d_boxes, (size_t)(ctx->npad / TILE_J) * (2 * D + 2))))
       return rc;
     CU(cudaMemsetAsync(ctx->rec_p, 0, (size_t)ctx->npad * REC * sizeof(double), ctx->stream));
+    if (ctx->rec32) {
+      TRY(dalloc(ctx, &ctx->rec32_p, (size_t)ctx->npad * Layout32Rec(D)));
+      CU(cudaMemsetAsync(ctx->rec32_p, 0, (size_t)ctx->npad * Layout32Rec(D) * sizeof(float), ctx->stream));
+    }
   }
   // tie-group ids (first event with the same time) in walk order
   std::vector<int> g(N), gp(ctx->npad);

@@ -294,11 +294,14 @@ struct RowPair32 {
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
-template <int D, int PASS, bool MASK, bool SELF>
+// GEN (spatial walk, as in the fp64 kernels): either event may be the later one; the
+// self-excitation term uses |dt| and goes to the later event (pass 1: the row's X or the
+// column's; pass 2: rho' of the later event in the coefficient).
+template <int D, int PASS, bool MASK, bool SELF, bool GEN = false>
 __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float (&cxh)[D],
                                             const float (&cxl)[D], float cth, float ctl,
                                             float crho, bool dead_a, bool dead_b, float2& rM,
-                                            float2 (&rG)[D], float2& cM, float2& cX,
+                                            float2& rX, float2 (&rG)[D], float2& cM, float2& cX,
                                             float2 (&cG)[D], const PassConst32& c) {
   float2 dx[D];
 #pragma unroll
@@ -309,7 +312,8 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
   const float2 dt = __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
   const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
-  const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), dt, f2(c.cs)))
+  const float2 adt = GEN ? make_float2(fabsf(dt.x), fabsf(dt.y)) : dt;
+  const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), adt, f2(c.cs)))
                          : make_float2(0.f, 0.f);
   float2 eb = make_float2(ex2f(ab.x), ex2f(ab.y));
   float2 es = SELF ? make_float2(ex2f(as.x), ex2f(as.y)) : make_float2(0.f, 0.f);
@@ -322,10 +326,27 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   if (PASS == 1) {   // rates only (the gradient comes out of pass 2)
     rM = __fadd2_rn(rM, eb);
     cM = __fadd2_rn(cM, eb);
-    if (SELF) cX = __fadd2_rn(cX, es);
+    if (SELF) {
+      if (GEN) {
+        const bool la = __float_as_int(dt.x) < 0, lb = __float_as_int(dt.y) < 0;   // row later
+        rX = __fadd2_rn(rX, make_float2(la ? es.x : 0.f, lb ? es.y : 0.f));
+        cX = __fadd2_rn(cX, make_float2(la ? 0.f : es.x, lb ? 0.f : es.y));
+      } else {
+        cX = __fadd2_rn(cX, es);
+      }
+    }
   } else {
     // the pair's App. A coefficient rho'_i mu' + rho'_j (mu' + xi'), the same for both events
-    const float2 cc = __ffma2_rn(rp.rho, eb, __fmul2_rn(f2(crho), SELF ? __fadd2_rn(eb, es) : eb));
+    // (GEN: rho'_i mu' + rho'_j mu' + rho'_later xi')
+    float2 cc;
+    if (GEN) {
+      const float2 rl = make_float2(__float_as_int(dt.x) < 0 ? rp.rho.x : crho,
+                                    __float_as_int(dt.y) < 0 ? rp.rho.y : crho);
+      const float2 rs = __fadd2_rn(rp.rho, f2(crho));
+      cc = SELF ? __ffma2_rn(rs, eb, __fmul2_rn(rl, es)) : __fmul2_rn(rs, eb);
+    } else {
+      cc = __ffma2_rn(rp.rho, eb, __fmul2_rn(f2(crho), SELF ? __fadd2_rn(eb, es) : eb));
+    }
     const float2 ncc = make_float2(-cc.x, -cc.y);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -335,11 +356,12 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA>
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN>
 __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag,
-                                            float2 (&rM)[SR / 2], float2 (&rG)[SR / 2][D],
+                                            float2 (&rM)[SR / 2], float2 (&rX)[SR / 2],
+                                            float2 (&rG)[SR / 2][D],
                                             float (&cacc)[2 + D], const PassConst32& c) {
   using L = Layout32<D>;
   constexpr int REC = L::REC;
@@ -398,8 +420,8 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
         da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
         db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
       }
-      sym32_pair2<D, PASS, MASK, SELF>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h], rG[h], cM,
-                                       cX, cG, c);
+      sym32_pair2<D, PASS, MASK, SELF, GEN>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h], rX[h],
+                                            rG[h], cM, cX, cG, c);
     }
     if (PASS == 1) {
       cacc[0] = cM.x + cM.y;
@@ -420,7 +442,9 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
 }
 
 struct SymArgs32 {
-  const float* rec;
+  const float* rec;          // records in the walk's order (time order, or spatial: rec32_p)
+  const double* boxes;       // GEN: per 128-event tile {lo[D], hi[D], tmin, tmax} (fp64)
+  int ties;                  // GEN: the catalog has equal times
   const int* gid;
   const PairItem* items;   // chunk pairs and their slot blocks (hawkes_kernels_sym.cuh)
   int* counter;
@@ -433,7 +457,24 @@ struct SymArgs32 {
   PassConst32 c;
 };
 
-template <int D, int PASS, int SR, bool SOA>
+// box bounds in the fp32 kernels' log2 domain (the 2^-E scale folded into cb, cs): a term
+// whose bound is below -127 is flushed by ex2.approx.ftz
+template <int D>
+__device__ __forceinline__ void box_bounds32(const double* lo_a, const double* hi_a, const double* lo_b,
+                                             const double* hi_b, const PassConst32& c, bool& bg, bool& self) {
+  double r2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double g = fmax(0.0, fmax(lo_b[d] - hi_a[d], lo_a[d] - hi_b[d]));
+    r2 = fma(g, g, r2);
+  }
+  const float dt = (float)fmax(0.0, fmax(lo_b[D] - hi_a[D], lo_a[D] - hi_b[D]));
+  const float r2f = (float)r2;
+  bg = fmaf(c.kx, r2f, fmaf(c.kt * dt, dt, c.cb)) > -127.f;
+  self = fmaf(c.ks, r2f, c.cs - c.omega * dt) > -127.f;
+}
+
+template <int D, int PASS, int SR, bool SOA, bool GEN = false>
 __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_kernel_f32(SymArgs32 a) {
   static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
@@ -441,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
   using L64 = Layout<D>;
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? K1P : L64::K2;
-  constexpr int KR = PASS == 1 ? 1 : D;
+  constexpr int KR = PASS == 1 ? (GEN ? 2 : 1) : D;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
@@ -474,6 +515,34 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
     const int c1 = min(N, c0 + a.chunk);
     const int n_rt = (r1 - r0 + SRT - 1) / SRT;
     const int n_ct = (c1 - c0 + TILE_J - 1) / TILE_J;
+    if (GEN && !diag) {   // item-level cull by the chunks' union boxes (see sym_items)
+      double lo_a[D + 1], hi_a[D + 1], lo_b[D + 1], hi_b[D + 1];
+#pragma unroll
+      for (int d = 0; d <= D; ++d) {
+        lo_a[d] = lo_b[d] = INFINITY;
+        hi_a[d] = hi_b[d] = -INFINITY;
+      }
+      for (int q = 0; q < n_rt + n_ct; ++q) {
+        const bool ra = q < n_rt;
+        const double* b = a.boxes + (long long)((ra ? r0 : c0) / TILE_J + (ra ? q : q - n_rt)) * (2 * D + 2);
+        double* lo = ra ? lo_a : lo_b;
+        double* hi = ra ? hi_a : hi_b;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          lo[d] = fmin(lo[d], b[d]);
+          hi[d] = fmax(hi[d], b[D + d]);
+        }
+        lo[D] = fmin(lo[D], b[2 * D]);
+        hi[D] = fmax(hi[D], b[2 * D + 1]);
+      }
+      bool bg, self;
+      box_bounds32<D>(lo_a, hi_a, lo_b, hi_b, c, bg, self);
+      if (!bg && !self) {
+        for (int q = tid; q < (r1 - r0) * K; q += THREADS) a.part[w.ro * K + q] = 0.0;
+        for (int q = tid; q < (c1 - c0) * K; q += THREADS) a.part[w.co * K + q] = 0.0;
+        continue;
+      }
+    }
 
     TileWalk prod{0, 0};
     if (tid == 0) {
@@ -490,7 +559,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
       const int row0 = r0 + rt * SRT;
       const bool rows_full = row0 + SRT <= r1;
       RowPair32<D> rp[SR / 2];
-      double rM[SR], rG[SR][D];
+      double rM[SR], rX[SR], rG[SR][D];
 #pragma unroll
       for (int h = 0; h < SR / 2; ++h) {
         const int ia = row0 + lane + 32 * (2 * h), ib = ia + 32;
@@ -510,9 +579,11 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
 #pragma unroll
       for (int r = 0; r < SR; ++r) {
         rM[r] = 0.0;
+        rX[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) rG[r][d] = 0.0;
       }
+      const double* rbox = GEN ? a.boxes + (long long)(row0 / TILE_J) * (2 * D + 2) : nullptr;
       const int rlast = min(row0 + SRT, r1) - 1;
       const int g_rlast = a.gid[rlast];
       const float th_rlast = a.rec[(long long)rlast * REC + L::TH];
@@ -533,20 +604,40 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         float cacc[2 + D];
 #pragma unroll
         for (int q = 0; q < 2 + D; ++q) cacc[q] = 0.f;
-        float2 rM32[SR / 2], rG32[SR / 2][D];
+        float2 rM32[SR / 2], rX32[SR / 2], rG32[SR / 2][D];
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM32[h] = make_float2(0.f, 0.f);
+          rX32[h] = make_float2(0.f, 0.f);
 #pragma unroll
           for (int d = 0; d < D; ++d) rG32[h][d] = make_float2(0.f, 0.f);
         }
         const bool diag_tile = diag && ct == rt;
-        const bool strict = !diag_tile && rows_full && cnt == TILE_J && g_rlast < a.gid[jt];
+        const bool strict = !diag_tile && rows_full && cnt == TILE_J && (GEN ? !a.ties : g_rlast < a.gid[jt]);
         // temporal culling as in the fp64 kernel, in the log2 domain: ex2.approx.ftz
-        // returns 0 below 2^-126 (with the 2^-E scale already folded into cb, cs)
-        const float dtmin = fmaxf((st[L::TH] - th_rlast) + (st[L::TL] - tl_rlast), 0.f);
-        const bool self_live = c.cs - c.omega * dtmin > -127.f;
-        const bool bg_live = fmaf(c.kt * dtmin, dtmin, c.cb) > -127.f;
+        // returns 0 below 2^-126 (with the 2^-E scale already folded into cb, cs); GEN: the
+        // two tiles' boxes in space and time
+        bool self_live, bg_live;
+        if (GEN) {
+          const double* cb = a.boxes + (long long)(jt / TILE_J) * (2 * D + 2);
+          double lo_r[D + 1], hi_r[D + 1], lo_c[D + 1], hi_c[D + 1];
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            lo_r[d] = rbox[d];
+            hi_r[d] = rbox[D + d];
+            lo_c[d] = cb[d];
+            hi_c[d] = cb[D + d];
+          }
+          lo_r[D] = rbox[2 * D];
+          hi_r[D] = rbox[2 * D + 1];
+          lo_c[D] = cb[2 * D];
+          hi_c[D] = cb[2 * D + 1];
+          box_bounds32<D>(lo_r, hi_r, lo_c, hi_c, c, bg_live, self_live);
+        } else {
+          const float dtmin = fmaxf((st[L::TH] - th_rlast) + (st[L::TL] - tl_rlast), 0.f);
+          self_live = c.cs - c.omega * dtmin > -127.f;
+          bg_live = fmaf(c.kt * dtmin, dtmin, c.cb) > -127.f;
+        }
         const float* grp = st + warp * 32 * REC;
         if (SOA) {   // this lane's column record -> the warp's [unit][32] float4 buffer
           const float4* rc4 = reinterpret_cast<const float4*>(grp + lane * REC);
@@ -557,18 +648,22 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           grp = mysoa;
         }
         if (!strict)
-          sym32_group<D, PASS, true, SR, true, SOA>(rp, grp, cg, cvalid, row0 + lane,
-                                                    jt + warp * 32, diag_tile, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, true, SR, true, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
+                                                         jt + warp * 32, diag_tile, rM32, rX32, rG32, cacc, c);
         else if (self_live)
-          sym32_group<D, PASS, false, SR, true, SOA>(rp, grp, cg, cvalid, row0 + lane,
-                                                     jt + warp * 32, false, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, true, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
+                                                          jt + warp * 32, false, rM32, rX32, rG32, cacc, c);
         else if (bg_live)
-          sym32_group<D, PASS, false, SR, false, SOA>(rp, grp, cg, cvalid, row0 + lane,
-                                                      jt + warp * 32, false, rM32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, false, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
+                                                           jt + warp * 32, false, rM32, rX32, rG32, cacc, c);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;
           rM[2 * h + 1] += (double)rM32[h].y;
+          if (GEN && PASS == 1) {
+            rX[2 * h] += (double)rX32[h].x;
+            rX[2 * h + 1] += (double)rX32[h].y;
+          }
 #pragma unroll
           for (int d = 0; d < D; ++d) {
             rG[2 * h][d] += (double)rG32[h][d].x;
@@ -598,6 +693,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         double* o = red + ((long long)warp * SRT + lane + 32 * r) * KR;
         if (PASS == 1) {
           o[0] = rM[r];
+          if (GEN) o[1] = rX[r];
         } else {
 #pragma unroll
           for (int d = 0; d < D; ++d) o[d] = rG[r][d];
@@ -612,7 +708,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
         v += red[(2 * SRT + rr) * KR + kk];
         v += red[(3 * SRT + rr) * KR + kk];
         double* o = a.part + (w.ro + (row0 + rr - r0)) * K;
-        if (PASS == 1) {
+        if (PASS == 1 && !GEN) {
           o[0] = v;
           o[1] = 0.0;
         } else {

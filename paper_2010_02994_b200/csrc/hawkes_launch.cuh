@@ -113,9 +113,9 @@ int sym_call(hawkes_ctx* ctx, int pass, const SymArgs* b) {
 }
 
 constexpr int SYM32_R = 4;
-template <int D, int PASS>
+template <int D, int PASS, bool GEN = false>
 size_t sym32_smem() {
-  const int KR = PASS == 1 ? 1 : D;
+  const int KR = PASS == 1 ? (GEN ? 2 : 1) : D;
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t) +
          (size_t)4 * 32 * SYM32_R * KR * sizeof(double) +
          (size_t)4 * 32 * Layout32<D>::REC * sizeof(float);   // per-warp SoA column buffers
@@ -131,27 +131,29 @@ static bool sym32_soa() {
   return v;
 }
 
-template <int D, bool SOA>
+template <int D, bool SOA, bool GEN = false>
 int sym32_setup(hawkes_ctx* ctx) {
-  auto s1 = sym_kernel_f32<D, 1, SYM32_R, SOA>;
-  auto s2 = sym_kernel_f32<D, 2, SYM32_R, SOA>;
-  CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1>()));
-  CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2>()));
+  auto s1 = sym_kernel_f32<D, 1, SYM32_R, SOA, GEN>;
+  auto s2 = sym_kernel_f32<D, 2, SYM32_R, SOA, GEN>;
+  CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1, GEN>()));
+  CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2, GEN>()));
   int b1 = 0, b2 = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1>()));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2>()));
-  ctx->grid32_s1 = std::max(1, b1) * ctx->sms;
-  ctx->grid32_s2 = std::max(1, b2) * ctx->sms;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1, GEN>()));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2, GEN>()));
+  (GEN ? ctx->grid32_g1 : ctx->grid32_s1) = std::max(1, b1) * ctx->sms;
+  (GEN ? ctx->grid32_g2 : ctx->grid32_s2) = std::max(1, b2) * ctx->sms;
   return HAWKES_OK;
 }
 
-template <int D, bool SOA>
+template <int D, bool SOA, bool GEN = false>
 int sym32_launch(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
-  const int grid = std::min(pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2, b.n_items);
+  const int grid = std::min(GEN ? (pass == 1 ? ctx->grid32_g1 : ctx->grid32_g2)
+                                : (pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2),
+                            b.n_items);
   if (pass == 1)
-    sym_kernel_f32<D, 1, SYM32_R, SOA><<<grid, THREADS, sym32_smem<D, 1>(), ctx->stream>>>(b);
+    sym_kernel_f32<D, 1, SYM32_R, SOA, GEN><<<grid, THREADS, sym32_smem<D, 1, GEN>(), ctx->stream>>>(b);
   else
-    sym_kernel_f32<D, 2, SYM32_R, SOA><<<grid, THREADS, sym32_smem<D, 2>(), ctx->stream>>>(b);
+    sym_kernel_f32<D, 2, SYM32_R, SOA, GEN><<<grid, THREADS, sym32_smem<D, 2, GEN>(), ctx->stream>>>(b);
   CHECK_LAUNCH();
   return HAWKES_OK;
 }
@@ -184,6 +186,10 @@ struct SetupD {
         if (soa) rc = sym32_setup<D, true>(ctx);
         else if constexpr (D == 2) rc = sym32_setup<D, false>(ctx);
         if (rc != HAWKES_OK) return rc;
+        if constexpr (D <= SPACE_MAX_D) {   // the spatial walk's fp32 kernels
+          rc = sym32_setup<D, true, true>(ctx);
+          if (rc != HAWKES_OK) return rc;
+        }
       }
       // and the fp64 kernels below: the fp32 range guard can send this context to them
     }
@@ -307,8 +313,10 @@ struct PassD {
     }
     if constexpr (D <= SYM_MAX_D) if (ctx->pairs && ctx->n_sym[rank] > 0) {
       SymArgs32 b;
-      b.rec = ctx->rec32;
-      b.gid = ctx->gid;
+      b.rec = ctx->spatial ? ctx->rec32_p : ctx->rec32;
+      b.boxes = ctx->d_boxes;
+      b.ties = ctx->ties ? 1 : 0;
+      b.gid = ctx->spatial ? ctx->d_gid_p : ctx->gid;
       b.items = ctx->d_sym[rank];
       b.counter = ctx->counters + 4 * rank + 2 + (pass - 1);
       b.part = pass == 1 ? ctx->part1 : ctx->part2;
@@ -321,7 +329,9 @@ struct PassD {
       bool soa = true;
       if constexpr (D == 2) soa = sym32_soa();
       int rc = HAWKES_OK;
-      if (soa)
+      if (ctx->spatial) {
+        if constexpr (D <= SPACE_MAX_D) rc = sym32_launch<D, true, true>(ctx, pass, b);
+      } else if (soa)
         rc = sym32_launch<D, true>(ctx, pass, b);
       else if constexpr (D == 2)
         rc = sym32_launch<D, false>(ctx, pass, b);
@@ -355,7 +365,9 @@ struct Fin1D {
           (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
           ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr,
-          ctx->spatial ? WalkMap{ctx->d_perm, ctx->rec_p + Layout<D>::RHO} : WalkMap{nullptr, nullptr});
+          ctx->spatial ? WalkMap{ctx->d_perm, ctx->rec_p + Layout<D>::RHO,
+                                 ctx->rec32_p ? ctx->rec32_p + Layout32<D>::RHO : nullptr}
+                       : WalkMap{nullptr, nullptr, nullptr});
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,
@@ -591,6 +603,11 @@ struct WalkD {
     k_walk_records<D><<<(unsigned)(ctx->npad / 128), 128, 0, ctx->stream>>>(
         ctx->rec, ctx->d_perm, (int)ctx->N, ctx->npad, ctx->rec_p, ctx->d_boxes);
     CHECK_LAUNCH();
+    if (ctx->rec32_p) {
+      k_walk_records32<D><<<(unsigned)(ctx->npad / 128), 128, 0, ctx->stream>>>(
+          ctx->rec32, ctx->d_perm, (int)ctx->N, ctx->npad, ctx->rec32_p);
+      CHECK_LAUNCH();
+    }
     return HAWKES_OK;
   }
 };

@@ -164,6 +164,7 @@ struct EvalStatus {
 struct WalkMap {
   const int* perm;       // p -> event
   double* recp_rho;      // rho' of the walk-order records (pass 2 reads them), or nullptr
+  float* recp32_rho;     // and of the fp32 walk-order records, or nullptr
 };
 
 // lambda, rho' and ell_n of the event at walk position p from its summed pass-1 partials
@@ -174,7 +175,7 @@ __device__ __forceinline__ double fin1_event(int p, double M, double X, const do
                                            double* __restrict__ rl, double* __restrict__ rates,
                                            const FinConst& f, double* __restrict__ rec_rho,
                                            float* __restrict__ rec32_rho, int* __restrict__ range_flag,
-                                           double* __restrict__ lrho, WalkMap wm = WalkMap{nullptr, nullptr}) {
+                                           double* __restrict__ lrho, WalkMap wm = WalkMap{nullptr, nullptr, nullptr}) {
   using L = Layout<D>;
   const int i = wm.perm ? wm.perm[p] : p;
   HK_CHECK(i >= 0 && p >= 0);
@@ -204,6 +205,7 @@ __device__ __forceinline__ double fin1_event(int p, double M, double X, const do
   // every row is final on this process (W = 1 or PAIRS): write rho' into the records here
   if (rec_rho) rec_rho[(long long)i * L::REC] = rho;
   if (wm.recp_rho) wm.recp_rho[(long long)p * L::REC] = rho;
+  if (wm.recp32_rho) wm.recp32_rho[(long long)p * Layout32<D>::REC] = (float)rho;
   if (rec32_rho) rec32_rho[(long long)i * Layout32<D>::REC] = (float)rho;
   rates[4 * (long long)i] = Lp * sc;
   rates[4 * (long long)i + 1] = mu_s * sc;
@@ -434,6 +436,20 @@ __global__ void __launch_bounds__(128) k_walk_records(const double* __restrict__
       o[2 * D + 1] = b;
     }
   }
+}
+
+// the fp32 records in walk order (their rho' is written by the rate finalize)
+template <int D>
+__global__ void __launch_bounds__(128) k_walk_records32(const float* __restrict__ rec32,
+                                                        const int* __restrict__ perm, int N, int npad,
+                                                        float* __restrict__ rec32_p) {
+  using L = Layout32<D>;
+  const int p = blockIdx.x * 128 + threadIdx.x;
+  if (p >= npad) return;
+  const int i = perm[min(p, N - 1)];
+  HK_CHECK(i >= 0 && i < N);
+#pragma unroll
+  for (int q = 0; q < L::RHO; ++q) rec32_p[(long long)p * L::REC + q] = rec32[(long long)i * L::REC + q];
 }
 
 // ---- HMC transition (Neal 2011): counter-based random numbers on the device.

@@ -95,3 +95,13 @@ def test_auto_ordering_choice_and_samplers():
     np.testing.assert_allclose(res["space"][1], res["time"][1], rtol=1e-9, atol=1e-9)
     assert res["space"][2] == res["time"][2] and abs(res["space"][3] - res["time"][3]) <= 1e-8
     np.testing.assert_allclose(res["space"][4], res["time"][4], rtol=0, atol=1e-8)
+
+
+@pytest.mark.parametrize("name,N", [("C2", 6000), ("C3", 6000), ("C1", 3001)])
+def test_space_order_fp32(name, N):
+    """The fp32 kernels on the spatial walk (hawkes_kernels_f32.cuh GEN) under the fp32 gate."""
+    c = synth.config(name, N)
+    ell, g, rates = gpu_eval(c.x, c.t, c.theta, precision="fp32", ordering="space")
+    ell_r, lam_r, _, g_r, S = oracle_eval(c.x, c.t, c.theta)
+    np.testing.assert_allclose(rates["lambda"], lam_r, rtol=1e-4)
+    assert_parity(ell, g, ell_r, g_r, S, precision="fp32", what=f"space fp32 {name}")

@@ -53,6 +53,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", type=int, default=-1, help="re-run one case (same random stream)")
     ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
     ap.add_argument("--precision", default=None, help="force fp64 or fp32 for every case")
+    ap.add_argument("--ordering", default="auto", help="walk order of the PAIRS fp64 kernels: auto | time | space")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     fails = 0
@@ -69,7 +70,7 @@ if __name__ == "__main__":
         try:
             ell_r, lam_r, _ = oracle.loglik(x, t, th)
             if not np.isfinite(ell_r):
-                ell, g, rates = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg)
+                ell, g, rates = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, ordering=a.ordering)
                 if prec == "fp64" and np.isfinite(ell):
                     # reading R23: the oracle evaluates each term unscaled, so an event whose
                     # every term is below 2^-1075 gets lambda = 0 there although its true rate
@@ -86,7 +87,8 @@ if __name__ == "__main__":
                                       "gpu_min_lambda": lam_min}), flush=True)
                 continue
             g_r, S = oracle.grad(x, t, th, lam=lam_r)
-            ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False)
+            ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False,
+                                 ordering=a.ordering)
             if prec == "fp32" and not np.isfinite(ell):
                 continue                                   # fp32 range (reading R23)
             tol, floor = TOL[prec]
@@ -103,4 +105,5 @@ if __name__ == "__main__":
             traceback.print_exc()
     print(json.dumps({"summary": True, "cases": a.cases, "fails": fails, "r23_underflow": underflow,
                       "seed": a.seed, "nmax": a.nmax,
-                      "precision": a.precision or "mixed", "worst_grad_ratio": worst}), flush=True)
+                      "precision": a.precision or "mixed", "ordering": a.ordering,
+                      "worst_grad_ratio": worst}), flush=True)

@@ -15,13 +15,14 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_2010_02994_b200 import HawkesContext  # noqa: E402
 
-SIZES = [a.split(":") for a in sys.argv[1:]] or [["C2", "5000"], ["C2", "20000"], ["C2", "100000"],
+PREC = "fp32" if "--fp32" in sys.argv else "fp64"
+SIZES = [a.split(":") for a in sys.argv[1:] if a != "--fp32"] or [["C2", "5000"], ["C2", "20000"], ["C2", "100000"],
                                                   ["C3", "20000"], ["C3", "100000"], ["C4", "100000"]]
 for name, n in SIZES:
     c = synth.config(name, int(n))
     x = torch.from_numpy(c.x).cuda()
     for mode in ("time", "space", "auto"):
-        ctx = HawkesContext(c.N, c.D)
+        ctx = HawkesContext(c.N, c.D, precision=PREC)
         ctx.set_ordering(mode)
         ctx.set_times(torch.from_numpy(c.t).cuda())
         ctx.set_params(c.theta)
@@ -41,7 +42,7 @@ for name, n in SIZES:
             ts.append(e0.elapsed_time(e1))
         ts.sort()
         order, cost = ctx.ordering_in_use
-        print(json.dumps({"config": name, "N": c.N, "mode": mode, "order": order, "ms": ts[len(ts) // 2],
+        print(json.dumps({"config": name, "N": c.N, "precision": PREC, "mode": mode, "order": order, "ms": ts[len(ts) // 2],
                           "pairs_per_s": c.N * (c.N - 1) / (ts[len(ts) // 2] * 1e-3),
                           "cost_time": cost[0], "cost_space": cost[1], "ell": ell}), flush=True)
         ctx.close()
