@@ -410,7 +410,7 @@ def run_ours(args):
     # ---- the paper's catalog shapes at N = 100k (SURVEY §8(d) C2 / C3 recipes): the walk
     # order AUTO picks (spatial for the DC shape: exact box culling, NEXT-2) and its time
     shaped = None
-    if not args.no_hmc and args.precision == "fp64":
+    if not args.no_hmc:
         shaped = {}
         for name in ("C2", "C3"):
             cs = synth.config(name, N=N)
@@ -438,7 +438,7 @@ def run_ours(args):
             if world > 1:
                 dist.all_reduce(sms_, op=dist.ReduceOp.MAX)
             order, cost = sctx.ordering_in_use
-            shaped[name] = {"config": f"{name}-shaped N={N} D=2 fp64", "ms_per_eval": float(sms_.item()),
+            shaped[name] = {"config": f"{name}-shaped N={N} D=2 {args.precision}", "ms_per_eval": float(sms_.item()),
                             "pairs_per_s": N * (N - 1) / (float(sms_.item()) * 1e-3), "walk_order": order,
                             "walk_cost_time_space": cost,
                             "note": "effective pairs/s: culled pairs (exact, below the exp clamp) counted"}
