@@ -196,6 +196,11 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   {
     cudaError_t e = cudaMallocHost((void**)&ctx->h_st, sizeof(EvalStatus));
     if (e != cudaSuccess) return fail(set_err(ctx, HAWKES_ERR_OOM, "cudaMallocHost failed"));
+    e = cudaHostAlloc((void**)&ctx->h_mirror, sizeof(EvalStatus), cudaHostAllocMapped);
+    if (e != cudaSuccess) return fail(set_err(ctx, HAWKES_ERR_OOM, "cudaHostAlloc failed"));
+    memset((void*)ctx->h_mirror, 0, sizeof(EvalStatus));
+    if (cudaHostGetDevicePointer((void**)&ctx->d_mirror, ctx->h_mirror, 0) != cudaSuccess)
+      return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaHostGetDevicePointer failed"));
   }
   // tile lists / items
   {
@@ -230,8 +235,10 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   }
   ctx->bad = &ctx->st->nonfinite;
   if (cudaMemset(ctx->st, 0, sizeof(EvalStatus)) != cudaSuccess ||
+      cudaMemset(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1)) != cudaSuccess ||
       cudaMemset(ctx->rec, 0, (size_t)ctx->npad * REC * sizeof(double)) != cudaSuccess)
     return fail(set_err(ctx, HAWKES_ERR_CUDA, "cudaMemset failed"));
+  ctx->counters_armed = true;
   if ((rc = dispatchD<SetupD>(D, ctx))) return fail(rc);
   if (o.nccl_unique_id) {
     std::string e;
@@ -279,6 +286,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   for (auto* p : ctx->d_coff) if (p) cudaFree(p);
   for (auto* p : ctx->d_cn) if (p) cudaFree(p);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  if (ctx->h_mirror) cudaFreeHost(ctx->h_mirror);
   for (auto& pr : ctx->ev_rate) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto& pr : ctx->ev_grad) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -372,7 +380,8 @@ int hawkes_loglik(hawkes_ctx* ctx, double* out) {
   ENTER(ctx);
   if (!out) return set_err(ctx, HAWKES_ERR_ARG, "out_loglik is NULL");
   TRY(check_ready(ctx));
-  TRY(checked_rates(ctx));
+  ctx->mirror_fresh = false;
+  TRY(checked_rates(ctx, true));
   *out = ctx->h_st->ell;
   return HAWKES_OK;
 }
@@ -382,10 +391,11 @@ int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double
   if (!out_grad || (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE))
     return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_grad_locations");
   TRY(check_ready(ctx));
+  ctx->mirror_fresh = false;
   do {   // twice only if the fp32 range guard sent the context to fp64
     TRY(run_grad(ctx));   // (with the rate pass first when it is due)
     TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
-    TRY(fetch_status(ctx));
+    TRY(fetch_status(ctx, true));
   } while (take_retry(ctx));
   if (out_ll) *out_ll = ctx->h_st->ell;
   if (!(ctx->h_st->ell > -INFINITY))
@@ -399,7 +409,8 @@ int hawkes_get_rates(hawkes_ctx* ctx, double* lambda, double* mu, double* xi, do
   if (mem != HAWKES_MEM_HOST && mem != HAWKES_MEM_DEVICE)
     return set_err(ctx, HAWKES_ERR_ARG, "bad mem");
   TRY(check_ready(ctx));
-  TRY(checked_rates(ctx));
+  ctx->mirror_fresh = false;
+  TRY(checked_rates(ctx, true));
   if (!ctx->rates_exchanged && !ctx->pairs) {
     TRY(exchange_rows(ctx, ctx->rates, 4));
     ctx->rates_exchanged = true;

@@ -150,6 +150,13 @@ struct hawkes_ctx {
   int* bad = nullptr;      // device-side input validation flag: &st->nonfinite
   EvalStatus* st = nullptr;
   EvalStatus* h_st = nullptr;  // pinned
+  // small-call path (hawkes_loglik / hawkes_grad_locations / hawkes_get_rates): k_fin1p's last
+  // CTA copies the status into the mapped, pinned h_mirror (device view d_mirror), so those
+  // calls need no device-to-host status copy after the evaluation
+  EvalStatus* h_mirror = nullptr;
+  EvalStatus* d_mirror = nullptr;
+  bool mirror_fresh = false;   // a k_fin1p was enqueued since the last fetch_status
+  bool counters_armed = false; // PAIRS item counters are zero (re-armed by the finalizes)
   // leapfrog state
   double *lf_x = nullptr, *lf_p = nullptr, *lf_minv = nullptr, *lf_lo = nullptr, *lf_hi = nullptr;
   double *lf_x0 = nullptr, *lf_p0 = nullptr;   // start of the trajectory (fp64 re-run)

@@ -195,13 +195,17 @@ int run_rates(hawkes_ctx* ctx) {
   if (!ctx->capturing) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
     TRY(replay(ctx, 0));
+    if (ctx->pairs) ctx->mirror_fresh = true;
     ctx->rates_valid = true;
     ctx->rates_exchanged = false;
     ctx->grad_valid = false;
     ctx->lam_valid = true;
     return HAWKES_OK;
   }
-  CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1), ctx->stream));
+  // PAIRS: the finalizes re-arm the item counters they follow (k_fin1p / k_fin2p), so the
+  // captured evaluation starts with the pass kernel instead of a memset node
+  if (!ctx->pairs || !ctx->counters_armed)
+    CU(cudaMemsetAsync(ctx->counters, 0, sizeof(int) * (4 * ctx->W + 1), ctx->stream));
   if (ctx->pairs) {
     if (ctx->spatial) TRY(dispatchD<WalkD>(ctx->D, ctx));
     for (int r : ctx->my_ranks) TRY(dispatchD<PassD>(ctx->D, ctx, 1, r));
@@ -231,6 +235,7 @@ int run_grad(hawkes_ctx* ctx) {
   if (!ctx->order_decided && !ctx->capturing) TRY(decide_order(ctx));
   if (!ctx->capturing && !ctx->rates_valid) ++ctx->evals_same_consts;
   if (use_graph(ctx)) {
+    if (!ctx->rates_valid && ctx->pairs) ctx->mirror_fresh = true;
     TRY(replay(ctx, ctx->rates_valid ? 2 : 1));
     if (!ctx->rates_valid) ctx->rates_exchanged = false;
     ctx->rates_valid = ctx->grad_valid = true;
@@ -253,11 +258,17 @@ int run_grad(hawkes_ctx* ctx) {
   return HAWKES_OK;
 }
 
-int fetch_status(hawkes_ctx* ctx) {
+// mirror_ok: the caller enqueued nothing but evaluations since the last fetch, so when one of
+// them ran k_fin1p (which writes the status into h_st) no copy is needed
+int fetch_status(hawkes_ctx* ctx, bool mirror_ok = false) {
   // (ctx->bad is st->nonfinite: one copy brings the flags and the results)
-  CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  const bool mirror = mirror_ok && ctx->mirror_fresh;
+  if (!mirror)
+    CU(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(EvalStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->mirror_fresh = false;
   int bad = 0;
   TRY(wait_stream(ctx));
+  if (mirror) memcpy((void*)ctx->h_st, (const void*)ctx->h_mirror, sizeof(EvalStatus));
   bad = ctx->h_st->nonfinite;
   if (ctx->h_st->range32) {
     CU(cudaMemsetAsync(&ctx->st->range32, 0, sizeof(int), ctx->stream));
@@ -292,10 +303,10 @@ bool take_retry(hawkes_ctx* ctx) {
 }
 
 // rates for the current state, checked against the fp32 range guard (one host sync)
-int checked_rates(hawkes_ctx* ctx) {
+int checked_rates(hawkes_ctx* ctx, bool mirror_ok = false) {
   for (;;) {
     TRY(run_rates(ctx));
-    TRY(fetch_status(ctx));
+    TRY(fetch_status(ctx, mirror_ok));
     if (!take_retry(ctx)) return HAWKES_OK;
   }
 }

@@ -173,6 +173,18 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, i
   return fma(Tm, p, Tm);
 }
 
+// --------------------------------------------------------------- programmatic dependent launch
+// The evaluation's kernels after the first (PAIRS: pass 1 -> finalize 1 -> pass 2 -> finalize
+// 2) are launched with programmatic stream serialization (hawkes_launch.cuh launch_pdl): each
+// lets its dependent grid launch at its start (pdl_trigger), and the dependent runs whatever
+// reads no earlier kernel's output (exp-table copy into shared memory, barrier init) before
+// pdl_wait, which returns once every prerequisite grid has completed and its memory is
+// visible.  Both are no-ops in a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // --------------------------------------------------------------- TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

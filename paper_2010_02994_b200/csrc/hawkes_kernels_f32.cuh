@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   uint32_t parity = 0;
   const PassConst32 c = a.c;
   const int N = a.N;
@@ -718,6 +719,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
       __syncthreads();
     }
   }
+  pdl_trigger();   // out of items (as sym_kernel)
 }
 
 }  // namespace hk

@@ -664,9 +664,14 @@ __global__ void __launch_bounds__(THREADS, sym_min_ctas<D, PASS, GEN>()) sym_ker
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const typename Cfg::Smem sm(smem_raw);
   __shared__ int s_item;
-  sym_prologue<Cfg::TS>(a.tab, sm.tab, sm.bars);
+  sym_prologue<Cfg::TS>(a.tab, sm.tab, sm.bars);   // the table is written at creation
+  pdl_wait();
   uint32_t parity = 0;
   sym_items<D, PASS, SYM_R, V, GEN>(a, sm, &s_item, parity);
+  // the dependent grid launches once every CTA is out of items: triggering at the start lets
+  // its CTAs take SM slots while this grid still runs, which at small N (grid < 148) packs
+  // the next pass's CTAs onto busy SMs (N = 2000: +11 us per call)
+  pdl_trigger();
 }
 
 }  // namespace hk

@@ -4,10 +4,50 @@
 #pragma once
 namespace {
 
+// Launch with programmatic stream serialization (hawkes_kernels.cuh pdl_trigger / pdl_wait):
+// the kernel's launch and prologue overlap the previous kernel's tail; under stream capture the
+// edge becomes a programmatic graph edge.  Only kernels that pdl_wait before touching earlier
+// kernels' output go through here.  HAWKES_PDL=0 launches them plainly (A/B).
+static bool pdl_enabled() {
+  static bool v = [] {
+    const char* e = getenv("HAWKES_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 template <int D, int PASS>
 size_t pass_smem() {
   return (size_t)STAGES * TILE_J * Layout<D>::REC * sizeof(double) + STAGES * sizeof(uint64_t) +
          EXP_TABLE * sizeof(int2);
+}
+
+// diagnostics: HAWKES_SYM_CPS1 / HAWKES_SYM_CPS2 cap the sym kernels' CTAs per SM (A/B of
+// the grid at small N, where the items come in few rounds)
+static int sym_cps(int pass) {
+  static int v[2] = {[] { const char* e = getenv("HAWKES_SYM_CPS1"); return e ? atoi(e) : 0; }(),
+                     [] { const char* e = getenv("HAWKES_SYM_CPS2"); return e ? atoi(e) : 0; }()};
+  return v[pass - 1];
+}
+static int sym_grid(const hawkes_ctx* ctx, int pass, int resident, int n_items) {
+  int g = std::min(resident, n_items);
+  if (sym_cps(pass) > 0) g = std::min(g, sym_cps(pass) * ctx->sms);
+  return std::max(1, g);
 }
 
 template <int D, int PASS, int R, int V>
@@ -35,11 +75,11 @@ struct SymOps {
     return HAWKES_OK;
   }
   static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
-    const int grid = std::min(pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
     if (pass == 1)
-      sym_kernel<D, 1, R, V1><<<grid, THREADS, sym_smem<D, 1, R, V1>(), ctx->stream>>>(b);
+      CU(launch_pdl(sym_kernel<D, 1, R, V1>, grid, THREADS, sym_smem<D, 1, R, V1>(), ctx->stream, b));
     else
-      sym_kernel<D, 2, R, V2><<<grid, THREADS, sym_smem<D, 2, R, V2>(), ctx->stream>>>(b);
+      CU(launch_pdl(sym_kernel<D, 2, R, V2>, grid, THREADS, sym_smem<D, 2, R, V2>(), ctx->stream, b));
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -64,11 +104,11 @@ struct SymGen {
     return HAWKES_OK;
   }
   static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
-    const int grid = std::min(pass == 1 ? ctx->grid_g1 : ctx->grid_g2, b.n_items);
+    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_g1 : ctx->grid_g2, b.n_items);
     if (pass == 1)
-      sym_kernel<D, 1, 4, 4, true><<<grid, THREADS, smem(1), ctx->stream>>>(b);
+      CU(launch_pdl(sym_kernel<D, 1, 4, 4, true>, grid, THREADS, smem(1), ctx->stream, b));
     else
-      sym_kernel<D, 2, 4, 4, true><<<grid, THREADS, smem(2), ctx->stream>>>(b);
+      CU(launch_pdl(sym_kernel<D, 2, 4, 4, true>, grid, THREADS, smem(2), ctx->stream, b));
     CHECK_LAUNCH();
     return HAWKES_OK;
   }
@@ -151,9 +191,9 @@ int sym32_launch(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
                                 : (pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2),
                             b.n_items);
   if (pass == 1)
-    sym_kernel_f32<D, 1, SYM32_R, SOA, GEN><<<grid, THREADS, sym32_smem<D, 1, GEN>(), ctx->stream>>>(b);
+    CU(launch_pdl(sym_kernel_f32<D, 1, SYM32_R, SOA, GEN>, grid, THREADS, sym32_smem<D, 1, GEN>(), ctx->stream, b));
   else
-    sym_kernel_f32<D, 2, SYM32_R, SOA, GEN><<<grid, THREADS, sym32_smem<D, 2, GEN>(), ctx->stream>>>(b);
+    CU(launch_pdl(sym_kernel_f32<D, 2, SYM32_R, SOA, GEN>, grid, THREADS, sym32_smem<D, 2, GEN>(), ctx->stream, b));
   CHECK_LAUNCH();
   return HAWKES_OK;
 }
@@ -342,6 +382,16 @@ struct PassD {
   }
 };
 
+// k_fin1p lets the gradient pass launch at its start when that pass's grid is the full
+// resident grid on every rank of this process (its items fill all SM slots)
+static bool early_pass2(const hawkes_ctx* ctx) {
+  const int resident = use32(ctx) ? (ctx->spatial ? ctx->grid32_g2 : ctx->grid32_s2)
+                                  : (ctx->spatial ? ctx->grid_g2 : ctx->grid_s2);
+  for (int r : ctx->my_ranks)
+    if (ctx->n_sym[r] < resident) return false;
+  return resident > 0;
+}
+
 template <int D>
 struct Fin1D {
   // ROWS: this rank's row tiles from the chunk partials.  PAIRS: every row, from the chunk
@@ -359,15 +409,17 @@ struct Fin1D {
     if (all) {   // PAIRS: (M', X') partials, gradient from pass 2 alone
       static_assert(K1P == 2, "k_fin1p pairs (M', X') lanes");
       const long long n = 2 * ctx->N;
-      k_fin1p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
-          sums ? ctx->sums1 : ctx->part1,
+      CU(launch_pdl(k_fin1p<D>, (unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream,
+          (const double*)(sums ? ctx->sums1 : ctx->part1),
           sums ? SlotView{nullptr, nullptr, ctx->chunk} : SlotView{ctx->d_coff[0], ctx->d_cn[0], ctx->chunk},
           (int)ctx->N, ctx->rec,
           ctx->rl, ctx->rates, fcp, rr, rr32, ctx->ell_part,
           ctx->counters + 4 * ctx->W, ctx->st, (final_here && SYM_FOLD) ? ctx->lrho : nullptr,
           ctx->spatial ? WalkMap{ctx->d_perm, ctx->rec_p + Layout<D>::RHO,
                                  ctx->rec32_p ? ctx->rec32_p + Layout32<D>::RHO : nullptr}
-                       : WalkMap{nullptr, nullptr, nullptr});
+                       : WalkMap{nullptr, nullptr, nullptr},
+          ctx->d_mirror, ctx->counters, ctx->W, early_pass2(ctx) ? 1 : 0));
+      ctx->mirror_fresh = true;
     } else {     // ROWS: (M', X', G1') partials of this rank's row tiles
       k_fin1<D, Layout<D>::K1, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(
           ctx->part1, ctx->npad, ctx->nslots, ctx->d_tiles[rank], (int)ctx->N, ctx->rec, ctx->G1,
@@ -387,11 +439,11 @@ struct Fin2D {
     const bool sums = all && ctx->multi;
     if (all) {
       const long long n = ctx->N * D;
-      k_fin2p<D><<<(unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream>>>(
-          sums ? ctx->sums2 : ctx->part2,
+      CU(launch_pdl(k_fin2p<D>, (unsigned)((n + 31) / 32), FINP_THREADS, 0, ctx->stream,
+          (const double*)(sums ? ctx->sums2 : ctx->part2),
           sums ? SlotView{nullptr, nullptr, ctx->chunk} : SlotView{ctx->d_coff[0], ctx->d_cn[0], ctx->chunk},
           (int)ctx->N, ctx->grad,
-          ctx->spatial ? ctx->d_perm : nullptr);
+          (const int*)(ctx->spatial ? ctx->d_perm : nullptr), ctx->counters, ctx->W));
     } else {
       k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,
                                                            ctx->d_tiles[rank], (int)ctx->N, ctx->G1,

@@ -284,7 +284,8 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
                                             double* __restrict__ rates, const FinConst* __restrict__ fcp,
                                             double* __restrict__ rec_rho, float* __restrict__ rec32_rho,
                                             double* __restrict__ ell_part, int* ticket, EvalStatus* st,
-                                            double* __restrict__ lrho, WalkMap wm) {
+                                            double* __restrict__ lrho, WalkMap wm,
+                                            EvalStatus* mirror = nullptr) {
   const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, M' or X')
   const int i = (int)(q >> 1);
   // K1P = 2 partials per event
@@ -307,6 +308,8 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
       e = fin1_event<D>(i, M, X, rec, rl, rates, *fcp, rec_rho, rec32_rho, &st->range32, lrho, wm);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
+    __threadfence();   // every lane: its range flag before the ticket (the mirror reads it)
+    __syncwarp();
     if (threadIdx.x == 0) {
       ell_part[blk] = e;
       __threadfence();
@@ -328,6 +331,16 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
       st->ell = red[0];
       if (!(red[0] > -INFINITY)) st->undefined = 1;
       *ticket = 0;
+      __threadfence();
+    }
+    if (mirror) {   // the status into the caller's pinned host copy (no device-to-host copy)
+      __syncthreads();
+      constexpr int NW = (int)(sizeof(EvalStatus) / sizeof(int));
+      static_assert(sizeof(EvalStatus) % sizeof(int) == 0, "EvalStatus is copied in words");
+      const int* src = reinterpret_cast<const int*>(st);
+      volatile int* dst = reinterpret_cast<volatile int*>(mirror);
+      for (int k = threadIdx.x; k < NW; k += FINP_THREADS) dst[k] = __ldcg(src + k);
+      __threadfence_system();
     }
   }
   __syncthreads();   // last / red reused by the caller's next block
@@ -342,9 +355,19 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
                                                         float* __restrict__ rec32_rho,
                                                         double* __restrict__ ell_part, int* ticket,
                                                         EvalStatus* st, double* __restrict__ lrho,
-                                                        WalkMap wm) {
+                                                        WalkMap wm, EvalStatus* mirror,
+                                                        int* counters, int W, int early) {
+  // early: the gradient pass's grid fills every SM slot, so its CTAs may launch (and stage
+  // the exp table) while this kernel runs; else at the end (a small grid launched early gets
+  // packed onto busy SMs: N = 2000, +11 us per call)
+  if (early) pdl_trigger();
+  pdl_wait();
+  // re-arm the pass-1 item counters of the W logical ranks (hawkes_engine.cuh run_rates: the
+  // PAIRS path has no counter memset; pass 1 is complete here, pass 2's counters untouched)
+  if (counters && blockIdx.x == 0 && threadIdx.x < W) counters[4 * threadIdx.x + 2] = 0;
   fin1p_block<D>(blockIdx.x, gridDim.x, part, sv, N, rec, rl, rates, fcp, rec_rho, rec32_rho,
-                 ell_part, ticket, st, lrho, wm);
+                 ell_part, ticket, st, lrho, wm, mirror);
+  if (!early) pdl_trigger();
 }
 
 template <int D>
@@ -372,7 +395,11 @@ __device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ 
 template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, SlotView sv,
                                                         int N, double* __restrict__ grad,
-                                                        const int* __restrict__ perm) {
+                                                        const int* __restrict__ perm,
+                                                        int* counters, int W) {
+  pdl_wait();
+  // re-arm the pass-2 item counters (as k_fin1p does pass 1's)
+  if (counters && blockIdx.x == 0 && threadIdx.x < W) counters[4 * threadIdx.x + 3] = 0;
   fin2p_block<D>(blockIdx.x, part, sv, N, grad, perm);
 }
 

@@ -387,6 +387,64 @@ def test_graph_replay_matches_fresh_contexts():
             assert np.array_equal(g.cpu().numpy(), gf)
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_call_sequences_status_mirror_and_counter_rearm(precision):
+    """The small-call path: the PAIRS finalizes re-arm the item counters (no
+    memset in the captured evaluation) and k_fin1p writes the status into mapped host memory,
+    read instead of a device-to-host copy only when this call ran k_fin1p.  Every order of
+    calls -- gradient with and without a rate pass first, repeated calls, rates, an input
+    error and recovery, a committed block move (which updates ell on the device without
+    k_fin1p) -- must give a fresh context's results."""
+    from paper_2010_02994_b200 import HawkesContext, HawkesError
+    c = synth.unit_square(1500, config=29)
+    x2 = c.x + 0.002
+    xbad = c.x.copy()
+    xbad[7, 1] = np.nan
+
+    def fresh(x):
+        with HawkesContext(c.N, c.D, precision=precision) as f:
+            f.set_times(c.t)
+            f.set_locations(x)
+            f.set_params(c.theta)
+            g, e = f.grad_locations()
+            return e, g.cpu().numpy(), f.get_rates()["lambda"]
+
+    e1, g1, l1 = fresh(c.x)
+    e2, g2, l2 = fresh(x2)
+    with HawkesContext(c.N, c.D, precision=precision) as ctx:
+        ctx.set_times(c.t)
+        ctx.set_params(c.theta)
+        for rep in range(3):   # plain launches first, then graph replays
+            ctx.set_locations(c.x)
+            g, e = ctx.grad_locations()                      # rate + gradient pass
+            assert e == e1 and np.array_equal(g.cpu().numpy(), g1)
+            g, e = ctx.grad_locations()                      # gradient already held
+            assert e == e1 and np.array_equal(g.cpu().numpy(), g1)
+            ctx.set_locations(x2)
+            assert np.array_equal(ctx.get_rates()["lambda"], l2)   # rate pass only
+            assert ctx.loglik() == e2                        # rates held: no evaluation
+            g, e = ctx.grad_locations()                      # gradient pass only
+            assert e == e2 and np.array_equal(g.cpu().numpy(), g2)
+            ctx.set_locations(torch.from_numpy(xbad).cuda())   # validated on the device
+            with pytest.raises(HawkesError):
+                ctx.grad_locations()
+            ctx.set_locations(c.x)
+            assert ctx.loglik() == e1
+            assert np.array_equal(ctx.get_rates()["lambda"], l1)
+        # a committed move updates ell on the device; loglik must not return the last mirror
+        idx = np.array([3, 400], dtype=np.int32)
+        new = c.x[idx] + 0.01
+        d = ctx.propose_move(idx, new)
+        ctx.accept_move()
+        xm = c.x.copy()
+        xm[idx] = new
+        em, gm, _ = fresh(xm)
+        assert ctx.loglik() == pytest.approx(e1 + d, rel=1e-12)
+        assert ctx.loglik() == pytest.approx(em, rel=1e-9 if precision == "fp64" else 1e-5)
+        g, e = ctx.grad_locations()
+        assert e == pytest.approx(em, rel=1e-9 if precision == "fp64" else 1e-5)
+
+
 def test_full_size_c4_gradient_rows_vs_oracle():
     """BASELINE configs[3] at N = 100k in the bench's launch configuration: the oracle's
     rates for all events (O(N^2), ~30 s on the host cores), then its App. A gradient for
