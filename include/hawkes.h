@@ -354,6 +354,18 @@ int hawkes_plan_walk(const double* x, const double* t, int64_t N, int32_t D, con
  * Errors: HAWKES_ERR_ARG. */
 int hawkes_plan_slots(int64_t N, int32_t world, int32_t rank, int64_t* slot_events, int64_t* max_events);
 
+/* Work items of HAWKES_ALGO_PAIRS on one rank as the device launches them (host only): the
+ * chunk pairs of hawkes_plan_pairs in the kernels' order (heaviest first), each as one item
+ * or, when the rank's n items fill less than one round of `resident` CTA slots (the gradient
+ * pass's resident grid; 0 = whole items), as k pieces over the skewed-step ranges
+ * [32q/k, 32(q+1)/k) (k the largest of 8, 4, 2 with k n <= resident), every piece with its own
+ * row and column slot blocks (DESIGN.md §5 "Small N").  items_out (nullable; n_items x 6 int64,
+ * row-major): a, b, row-block event offset, column-block event offset, s0, s1 into this
+ * rank's slot array of *slot_events events; *pieces receives k (1: whole items).  Call with
+ * items_out = NULL for the count.  Errors: HAWKES_ERR_ARG. */
+int hawkes_plan_items(int64_t N, int32_t world, int32_t rank, int32_t resident, int64_t* items_out,
+                      int32_t* n_items, int32_t* pieces, int64_t* slot_events);
+
 /* Diagnostics (not part of the numerical contract; used by the tests and bench.py):
  * hawkes_diag_exp evaluates the kernels' fast exp on n device doubles; hawkes_diag_fp64_peak
  * measures the device's dependent-DFMA throughput in FP64 lane-ops per second. */

@@ -34,7 +34,7 @@ EXPORTS = (
     "hawkes_set_bmds", "hawkes_bmds_logdensity", "hawkes_set_potential", "hawkes_enable_timing", "hawkes_get_kernel_times",
     "hawkes_plan", "hawkes_plan_pairs", "hawkes_nccl_unique_id", "hawkes_diag_exp", "hawkes_diag_normals", "hawkes_diag_fp64_peak", "hawkes_diag_fp64_mode", "hawkes_last_error",
     "hawkes_abi_version", "hawkes_precision_in_use", "hawkes_set_ordering", "hawkes_ordering_in_use",
-    "hawkes_plan_walk", "hawkes_plan_slots",
+    "hawkes_plan_walk", "hawkes_plan_slots", "hawkes_plan_items",
 )
 ORDERINGS = {"auto": 0, "time": 1, "space": 2}
 
@@ -99,6 +99,7 @@ def load() -> ctypes.CDLL:
     lib.hawkes_set_ordering.argtypes = [vp, i32]
     lib.hawkes_plan_walk.argtypes = [dp, dp, i64, i32, P(Params), P(i32), P(ctypes.c_double)]
     lib.hawkes_plan_slots.argtypes = [i64, i32, i32, P(i64), P(i64)]
+    lib.hawkes_plan_items.argtypes = [i64, i32, i32, i32, P(i64), P(i32), P(i32), P(i64)]
     lib.hawkes_ordering_in_use.argtypes = [vp, P(i32), P(ctypes.c_double)]
     lib.hawkes_get_kernel_times.argtypes = [vp, P(ctypes.c_double), P(i64), P(ctypes.c_double),
                                             P(i64), P(i64)]

@@ -111,10 +111,13 @@ int hawkes_create(int64_t N, int32_t D, const hawkes_opts* opts_in, hawkes_ctx**
   std::vector<std::vector<long long>> coff;
   std::vector<std::vector<int>> cn;
   std::vector<int> own;
-  if (ctx->pairs)
+  if (ctx->pairs) {
+    const int rc0 = dispatchD<SymSetupD>(D, ctx);
+    if (rc0 != HAWKES_OK) return fail(rc0);
     build_plan_pairs(ctx, it1, it2, sym, own, coff, cn);
-  else
+  } else {
     build_plan(ctx, it1, it2);
+  }
   // partial slots: PAIRS item-indexed and compact per rank (slot_events x K), ROWS
   // [nchunks][npad][K]
   const size_t slots1 = ctx->pairs ? (size_t)ctx->slot_events * K1P : (size_t)ctx->nslots * ctx->npad * K1_of(D);
@@ -519,6 +522,29 @@ int hawkes_plan_pairs(int64_t N, int32_t world, int32_t rank, int32_t* items_out
       }
   *n_items = cnt;
   if (chunk) *chunk = ck;
+  return HAWKES_OK;
+}
+
+int hawkes_plan_items(int64_t N, int32_t world, int32_t rank, int32_t resident, int64_t* items_out,
+                      int32_t* n_items, int32_t* pieces, int64_t* slot_events) {
+  if (N < 1 || N > (1LL << 30) || world < 1 || rank < 0 || rank >= world || resident < 0 || !n_items)
+    return set_err(nullptr, HAWKES_ERR_ARG, "bad arguments to hawkes_plan_items");
+  const int ck = chunk_pairs_of(N, world);
+  const PairsLayout L = pairs_layout(N, ck, world, {rank}, resident);
+  const auto& it = L.items[rank];
+  *n_items = (int32_t)it.size();
+  if (pieces) *pieces = L.pieces[rank];
+  if (slot_events) *slot_events = L.slot_events;
+  if (items_out)
+    for (size_t q = 0; q < it.size(); ++q) {
+      int64_t* o = items_out + 6 * q;
+      o[0] = it[q].a;
+      o[1] = it[q].b;
+      o[2] = it[q].ro;
+      o[3] = it[q].co;
+      o[4] = it[q].s0;
+      o[5] = it[q].s1;
+    }
   return HAWKES_OK;
 }
 

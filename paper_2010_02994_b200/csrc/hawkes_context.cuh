@@ -110,6 +110,7 @@ struct hawkes_ctx {
   std::vector<long long*> d_coff;           // per rank: [nchunks] slot-block event offsets
   std::vector<int*> d_cn;                   // per rank: [nchunks] slot blocks per chunk
   long long slot_events = 0;                // events of all slot blocks this process holds
+  std::vector<int> piece_k;                 // per rank: 1, or the plan's pieces per item
   int* d_own = nullptr;                     // [nchunks][nchunks] owner rank of pair (a <= b)
   int* d_every_tile = nullptr;              // all row tiles 0..ntiles-1
   bool multi = false;                       // W > 1 (real or emulated) or an NCCL communicator:

@@ -340,11 +340,12 @@ void build_plan_pairs(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,
   ctx->max_tiles = 0;
   it1.assign(W, {});
   it2.assign(W, {});
-  PairsLayout lay = pairs_layout(ctx->N, ctx->chunk, W, ctx->my_ranks);
+  PairsLayout lay = pairs_layout(ctx->N, ctx->chunk, W, ctx->my_ranks, ctx->grid_s2);
   sym.swap(lay.items);
   coff.swap(lay.coff);
   cn.swap(lay.cn);
   ctx->slot_events = lay.slot_events;
+  ctx->piece_k = lay.pieces;
 }
 
 void build_plan(hawkes_ctx* ctx, std::vector<std::vector<int2>>& it1,

@@ -356,18 +356,20 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN>
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE>
 __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
-                                            int ridx0, int cidx0, bool diag,
+                                            int ridx0, int cidx0, bool diag, int s0, int s1,
                                             float2 (&rM)[SR / 2], float2 (&rX)[SR / 2],
                                             float2 (&rG)[SR / 2][D],
                                             float (&cacc)[2 + D], const PassConst32& c) {
   using L = Layout32<D>;
   constexpr int REC = L::REC;
   const int lane = threadIdx.x & 31;
+  if (!PIECE) s0 = 0, s1 = 32;   // PIECE: a step range (hawkes_kernels_sym.cuh sym_group)
+  if (PIECE && s0) rotate_cols<D, PASS>(cacc, (lane + s0) & 31);
 #pragma unroll 2
-  for (int s = 0; s < 32; ++s) {
+  for (int s = s0; s < s1; ++s) {
     const int src = (lane + s) & 31;
     // AoS record in the stage, or (SOA) the warp's transposed copy: float4 unit u of column
     // e at [u][e], read without bank conflicts
@@ -439,6 +441,7 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
       for (int d = 0; d < D; ++d) cacc[2 + d] = __shfl_sync(0xffffffffu, cacc[2 + d], nxt);
     }
   }
+  if (PIECE && s1 != 32) rotate_cols<D, PASS>(cacc, (lane - s1) & 31);
 }
 
 struct SymArgs32 {
@@ -454,6 +457,7 @@ struct SymArgs32 {
   int n_items;
   int chunk;
   int nchunks;
+  int piece;                 // host side: the plan is made of pieces (SymArgs.piece)
   PassConst32 c;
 };
 
@@ -474,7 +478,7 @@ __device__ __forceinline__ void box_bounds32(const double* lo_a, const double* h
   self = fmaf(c.ks, r2f, c.cs - c.omega * dt) > -127.f;
 }
 
-template <int D, int PASS, int SR, bool SOA, bool GEN = false>
+template <int D, int PASS, int SR, bool SOA, bool GEN = false, bool PIECE = false>
 __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_kernel_f32(SymArgs32 a) {
   static_assert(32 * SR == TILE_J, "row tiles and column tiles must coincide");
   constexpr int SRT = 32 * SR;
@@ -502,6 +506,9 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
   const PassConst32 c = a.c;
   const int N = a.N;
 
+  // (drawing the next item's index early -- during the item's last tile pair -- was measured
+  // slower at small N, where an item is one tile pair: a CTA then holds its next item for a
+  // whole item, N = 5000 +6 %; profiles/r02_latency_prefetch.jsonl)
   for (;;) {
     if (tid == 0) s_item = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -648,15 +655,18 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           __syncwarp();
           grp = mysoa;
         }
-        if (!strict)
-          sym32_group<D, PASS, true, SR, true, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
-                                                         jt + warp * 32, diag_tile, rM32, rX32, rG32, cacc, c);
+        if (!strict)   // PIECE: as sym_items
+          sym32_group<D, PASS, true, SR, true, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
+                                                                jt + warp * 32, diag_tile, w.s0, w.s1, rM32,
+                                                                rX32, rG32, cacc, c);
         else if (self_live)
-          sym32_group<D, PASS, false, SR, true, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
-                                                          jt + warp * 32, false, rM32, rX32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, true, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
+                                                                 jt + warp * 32, false, w.s0, w.s1, rM32,
+                                                                 rX32, rG32, cacc, c);
         else if (bg_live)
-          sym32_group<D, PASS, false, SR, false, SOA, GEN>(rp, grp, cg, cvalid, row0 + lane,
-                                                           jt + warp * 32, false, rM32, rX32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, false, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
+                                                                  jt + warp * 32, false, w.s0, w.s1, rM32,
+                                                                  rX32, rG32, cacc, c);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;

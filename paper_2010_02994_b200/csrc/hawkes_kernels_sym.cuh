@@ -60,10 +60,27 @@ constexpr int TAB_COPIES = EXP_TABLE == 256 ? 16 : (EXP_TABLE == 1024 ? 4 : 2);
 // so a rank holds ~1/W of the partials and the finalize adds them in the same fixed order for
 // every W.  ro / co: the event offsets of this item's row block (chunk a's events) and column
 // block (chunk b's events) in the slot array.
+// s0, s1: the skewed steps [s0, s1) of every tile pair this item runs (hawkes_plan.h
+// pairs_layout splits the lightest items of a small plan into 2 or 4 step ranges, "pieces",
+// each with its own row and column slot blocks; a whole item runs [0, 32)).
 struct PairItem {
   int a, b;
   long long ro, co;
+  int s0, s1;
 };
+
+// lane l takes v from lane src(l): the column-sum rotation of a step range that does not
+// start (or end) at step 0 (or 32)
+template <int D, int PASS, class T>
+__device__ __forceinline__ void rotate_cols(T (&cacc)[2 + D], int src) {
+  if (PASS == 1) {
+    cacc[0] = __shfl_sync(0xffffffffu, cacc[0], src);
+    cacc[1] = __shfl_sync(0xffffffffu, cacc[1], src);
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) cacc[2 + d] = __shfl_sync(0xffffffffu, cacc[2 + d], src);
+  }
+}
 
 struct SymArgs {
   const double* rec;     // records in the item walk's order (time order, or spatial: rec_p)
@@ -78,6 +95,7 @@ struct SymArgs {
   long long npad;
   int N;
   int n_items;
+  int piece;             // host side: the plan is made of pieces (launch the PIECE kernel)
   int chunk;
   int nchunks;           // slot nchunks holds the column-role sums of diagonal items
   PassConst c;          // by value: DFMA constant-bank operands
@@ -185,21 +203,25 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA, bool GEN>
+template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA, bool GEN, bool PIECE>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp,
                                           const double* __restrict__ lgrp, int cg0, bool cvalid0,
-                                          int ridx0, int cidx0, bool diag,
+                                          int ridx0, int cidx0, bool diag, int s0, int s1,
                                           double (&rM)[SYM_R], double (&rX)[SYM_R], double (&rG)[SYM_R][D],
                                           double (&cacc)[2 + D], const PassConst& c,
                                           const int2* __restrict__ tab) {
   constexpr int REC = Layout<D>::REC;
   const int lane = threadIdx.x & 31;
+  // PIECE: a step range [s0, s1) (whole items: the constant 0..32 loop).  Starting at s0,
+  // lane l must hold column (l + s0)'s sums at the first step.
+  if (!PIECE) s0 = 0, s1 = 32;
+  if (PIECE && s0) rotate_cols<D, PASS>(cacc, (lane + s0) & 31);
   // unrolling by 2: pass 1 -2.8 %, pass 2 +1.4 % (N = 100k, accurate exp;
   // profiles/r02_ab_unroll.jsonl)
   constexpr int UNR = PASS == 1 ? 2 : 1;
 #pragma unroll UNR
-  for (int s = 0; s < 32; ++s) {
+  for (int s = s0; s < s1; ++s) {
     const int src = (lane + s) & 31;
     // column (l + s) mod 32 of this warp's group: from the staged tile (AoS records), or
     // from the warp's transposed copy (SOA: component pair p of column e at [p][e])
@@ -275,6 +297,8 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       for (int d = 0; d < D; ++d) cacc[2 + d] = shfl(cacc[2 + d], nxt);
     }
   }
+  // ... and ending at s1: lane l holds column (l + s1)'s; back to column l
+  if (PIECE && s1 != 32) rotate_cols<D, PASS>(cacc, (lane - s1) & 31);
 }
 
 // Smallest squared distance and time gap between two boxes {lo[D], tlo} / {hi[D], thi} and a
@@ -363,7 +387,15 @@ struct SymCfg {
 template <int TS>
 __device__ __forceinline__ void sym_prologue(const int2* __restrict__ gtab, int2* tab, uint64_t* bars) {
   const int tid = threadIdx.x;
-  for (int q = tid; q < EXP_TABLE * TS; q += THREADS) tab[q] = gtab[q / TS];
+  // all of a thread's table loads in flight at once, then the stores (a load-store loop pays
+  // one L2 round trip per entry: 7 % of the gradient pass's samples at N = 5000)
+  static_assert(EXP_TABLE * TS % THREADS == 0, "whole table rows per thread");
+  constexpr int PER = EXP_TABLE * TS / THREADS;
+  int2 v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) v[k] = __ldg(gtab + (tid + k * THREADS) / TS);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) tab[tid + k * THREADS] = v[k];
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -377,7 +409,7 @@ __device__ __forceinline__ void sym_prologue(const int2* __restrict__ gtab, int2
 // GEN: spatial order (hawkes_plan.h morton_order): no time order between or inside chunks,
 // so the general-direction pair bodies; tile pairs and whole items are culled by the
 // bounding boxes of their tiles (a.boxes) in space and time.
-template <int D, int PASS, int SYM_R, int V, bool GEN, class Sm>
+template <int D, int PASS, int SYM_R, int V, bool GEN, bool PIECE, class Sm>
 __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s_item_p,
                                           uint32_t& parity) {
   static_assert(32 * SYM_R == TILE_J, "row tiles and column tiles must coincide");
@@ -416,6 +448,9 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
   const PassConst c = a.c;
   const int N = a.N;
 
+  // (drawing the next item's index early -- during the item's last tile pair -- was measured
+  // slower at small N, where an item is one tile pair: a CTA then holds its next item for a
+  // whole item, N = 5000 +6 %; profiles/r02_latency_prefetch.jsonl)
   for (;;) {
     if (tid == 0) s_item = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -423,7 +458,8 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
     __syncthreads();
     if (it >= a.n_items) break;
     const PairItem w = a.items[it];
-    HK_CHECK(w.a >= 0 && w.a <= w.b && w.b < a.nchunks && w.ro >= 0 && w.co >= 0);
+    HK_CHECK(w.a >= 0 && w.a <= w.b && w.b < a.nchunks && w.ro >= 0 && w.co >= 0 && 0 <= w.s0 &&
+             w.s0 < w.s1 && w.s1 <= 32);
     const bool diag = w.a == w.b;
     const int r0 = w.a * a.chunk;                 // chunk a: rows
     const int r1 = min(N, r0 + a.chunk);
@@ -464,7 +500,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
       if (!box_pair_live<D>(lo_a, hi_a, lo_b, hi_b, c)) {
         for (int q = tid; q < (r1 - r0) * K; q += THREADS) a.part[w.ro * K + q] = 0.0;
         for (int q = tid; q < (c1 - c0) * K; q += THREADS) a.part[w.co * K + q] = 0.0;
-        continue;   // (the next item fetch synchronises the CTA)
+        continue;
       }
     }
 
@@ -582,18 +618,21 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
           __syncwarp();
           grp = mysoa;
         }
+        // PIECE (a plan of pieces, hawkes_plan.h): the item's step range; whole items run the
+        // constant 32-step loop (a kernel instantiation of its own: carrying both in one
+        // kernel made the gradient pass 5 % slower at N = 100k)
         if (!strict)
-          sym_group<D, PASS, true, SYM_R, true, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                              jt + warp * 32, diag_tile, rM, rX, rG, cacc, c,
-                                                              mytab);
+          sym_group<D, PASS, true, SYM_R, true, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                                     jt + warp * 32, diag_tile, w.s0, w.s1,
+                                                                     rM, rX, rG, cacc, c, mytab);
         else if (self_live)
-          sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                               jt + warp * 32, false, rM, rX, rG, cacc, c,
-                                                               mytab);
+          sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                                      jt + warp * 32, false, w.s0, w.s1, rM,
+                                                                      rX, rG, cacc, c, mytab);
         else if (bg_live)
-          sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                                jt + warp * 32, false, rM, rX, rG, cacc, c,
-                                                                mytab);
+          sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid,
+                                                                       row0 + lane, jt + warp * 32, false,
+                                                                       w.s0, w.s1, rM, rX, rG, cacc, c, mytab);
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {
@@ -658,7 +697,7 @@ constexpr int sym_min_ctas() {
   return (D <= 2 && PASS == 2 && !GEN) ? 4 : (D <= 4 ? 3 : 2);
 #endif
 }
-template <int D, int PASS, int SYM_R, int V, bool GEN = false>
+template <int D, int PASS, int SYM_R, int V, bool GEN = false, bool PIECE = false>
 __global__ void __launch_bounds__(THREADS, sym_min_ctas<D, PASS, GEN>()) sym_kernel(SymArgs a) {
   using Cfg = SymCfg<D, PASS, V, GEN>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -667,7 +706,7 @@ __global__ void __launch_bounds__(THREADS, sym_min_ctas<D, PASS, GEN>()) sym_ker
   sym_prologue<Cfg::TS>(a.tab, sm.tab, sm.bars);   // the table is written at creation
   pdl_wait();
   uint32_t parity = 0;
-  sym_items<D, PASS, SYM_R, V, GEN>(a, sm, &s_item, parity);
+  sym_items<D, PASS, SYM_R, V, GEN, PIECE>(a, sm, &s_item, parity);
   // the dependent grid launches once every CTA is out of items: triggering at the start lets
   // its CTAs take SM slots while this grid still runs, which at small N (grid < 148) packs
   // the next pass's CTAs onto busy SMs (N = 2000: +11 us per call)

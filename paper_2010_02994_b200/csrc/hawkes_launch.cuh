@@ -62,26 +62,37 @@ size_t sym_smem() {
 // integer instructions than the bank conflicts it removes; the SoA columns pay in both.
 template <int D, int R, int V1, int V2>
 struct SymOps {
-  static int setup(hawkes_ctx* ctx) {
-    auto s1 = sym_kernel<D, 1, R, V1>;
-    auto s2 = sym_kernel<D, 2, R, V2>;
+  // PIECE: the instantiation for plans of pieces (hawkes_plan.h choose_pieces; SymArgs.piece)
+  template <bool PIECE>
+  static int attrs(hawkes_ctx* ctx, int* b1, int* b2) {
+    auto s1 = sym_kernel<D, 1, R, V1, false, PIECE>;
+    auto s2 = sym_kernel<D, 2, R, V2, false, PIECE>;
     CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 1, R, V1>()));
     CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem<D, 2, R, V2>()));
-    int b1 = 0, b2 = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym_smem<D, 1, R, V1>()));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym_smem<D, 2, R, V2>()));
-    ctx->grid_s1 = std::max(1, b1) * ctx->sms;
-    ctx->grid_s2 = std::max(1, b2) * ctx->sms;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b1, s1, THREADS, sym_smem<D, 1, R, V1>()));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b2, s2, THREADS, sym_smem<D, 2, R, V2>()));
+    return HAWKES_OK;
+  }
+  static int setup(hawkes_ctx* ctx) {
+    int b1 = 0, b2 = 0, p1 = 0, p2 = 0;
+    TRY(attrs<false>(ctx, &b1, &b2));
+    TRY(attrs<true>(ctx, &p1, &p2));
+    ctx->grid_s1 = std::max(1, std::min(b1, p1)) * ctx->sms;
+    ctx->grid_s2 = std::max(1, std::min(b2, p2)) * ctx->sms;
+    return HAWKES_OK;
+  }
+  template <bool PIECE>
+  static int go(hawkes_ctx* ctx, int pass, const SymArgs& b) {
+    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
+    if (pass == 1)
+      CU(launch_pdl(sym_kernel<D, 1, R, V1, false, PIECE>, grid, THREADS, sym_smem<D, 1, R, V1>(), ctx->stream, b));
+    else
+      CU(launch_pdl(sym_kernel<D, 2, R, V2, false, PIECE>, grid, THREADS, sym_smem<D, 2, R, V2>(), ctx->stream, b));
+    CHECK_LAUNCH();
     return HAWKES_OK;
   }
   static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
-    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_s1 : ctx->grid_s2, b.n_items);
-    if (pass == 1)
-      CU(launch_pdl(sym_kernel<D, 1, R, V1>, grid, THREADS, sym_smem<D, 1, R, V1>(), ctx->stream, b));
-    else
-      CU(launch_pdl(sym_kernel<D, 2, R, V2>, grid, THREADS, sym_smem<D, 2, R, V2>(), ctx->stream, b));
-    CHECK_LAUNCH();
-    return HAWKES_OK;
+    return b.piece ? go<true>(ctx, pass, b) : go<false>(ctx, pass, b);
   }
 };
 
@@ -91,26 +102,36 @@ struct SymGen {
   static size_t smem(int pass) {
     return pass == 1 ? SymCfg<D, 1, 4, true>::Smem::bytes() : SymCfg<D, 2, 4, true>::Smem::bytes();
   }
-  static int setup(hawkes_ctx* ctx) {
-    auto g1 = sym_kernel<D, 1, 4, 4, true>;
-    auto g2 = sym_kernel<D, 2, 4, 4, true>;
+  template <bool PIECE>
+  static int attrs(hawkes_ctx* ctx, int* b1, int* b2) {
+    auto g1 = sym_kernel<D, 1, 4, 4, true, PIECE>;
+    auto g2 = sym_kernel<D, 2, 4, 4, true, PIECE>;
     CU(cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
     CU(cudaFuncSetAttribute(g2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(2)));
-    int b1 = 0, b2 = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, g1, THREADS, smem(1)));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, g2, THREADS, smem(2)));
-    ctx->grid_g1 = std::max(1, b1) * ctx->sms;
-    ctx->grid_g2 = std::max(1, b2) * ctx->sms;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b1, g1, THREADS, smem(1)));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b2, g2, THREADS, smem(2)));
+    return HAWKES_OK;
+  }
+  static int setup(hawkes_ctx* ctx) {
+    int b1 = 0, b2 = 0, p1 = 0, p2 = 0;
+    TRY(attrs<false>(ctx, &b1, &b2));
+    TRY(attrs<true>(ctx, &p1, &p2));
+    ctx->grid_g1 = std::max(1, std::min(b1, p1)) * ctx->sms;
+    ctx->grid_g2 = std::max(1, std::min(b2, p2)) * ctx->sms;
+    return HAWKES_OK;
+  }
+  template <bool PIECE>
+  static int go(hawkes_ctx* ctx, int pass, const SymArgs& b) {
+    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_g1 : ctx->grid_g2, b.n_items);
+    if (pass == 1)
+      CU(launch_pdl(sym_kernel<D, 1, 4, 4, true, PIECE>, grid, THREADS, smem(1), ctx->stream, b));
+    else
+      CU(launch_pdl(sym_kernel<D, 2, 4, 4, true, PIECE>, grid, THREADS, smem(2), ctx->stream, b));
+    CHECK_LAUNCH();
     return HAWKES_OK;
   }
   static int launch(hawkes_ctx* ctx, int pass, const SymArgs& b) {
-    const int grid = sym_grid(ctx, pass, pass == 1 ? ctx->grid_g1 : ctx->grid_g2, b.n_items);
-    if (pass == 1)
-      CU(launch_pdl(sym_kernel<D, 1, 4, 4, true>, grid, THREADS, smem(1), ctx->stream, b));
-    else
-      CU(launch_pdl(sym_kernel<D, 2, 4, 4, true>, grid, THREADS, smem(2), ctx->stream, b));
-    CHECK_LAUNCH();
-    return HAWKES_OK;
+    return b.piece ? go<true>(ctx, pass, b) : go<false>(ctx, pass, b);
   }
 };
 
@@ -171,37 +192,59 @@ static bool sym32_soa() {
   return v;
 }
 
-template <int D, bool SOA, bool GEN = false>
-int sym32_setup(hawkes_ctx* ctx) {
-  auto s1 = sym_kernel_f32<D, 1, SYM32_R, SOA, GEN>;
-  auto s2 = sym_kernel_f32<D, 2, SYM32_R, SOA, GEN>;
+template <int D, bool SOA, bool GEN, bool PIECE>
+int sym32_attrs(hawkes_ctx* ctx, int* b1, int* b2) {
+  auto s1 = sym_kernel_f32<D, 1, SYM32_R, SOA, GEN, PIECE>;
+  auto s2 = sym_kernel_f32<D, 2, SYM32_R, SOA, GEN, PIECE>;
   CU(cudaFuncSetAttribute(s1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 1, GEN>()));
   CU(cudaFuncSetAttribute(s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym32_smem<D, 2, GEN>()));
-  int b1 = 0, b2 = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, s1, THREADS, sym32_smem<D, 1, GEN>()));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, s2, THREADS, sym32_smem<D, 2, GEN>()));
-  (GEN ? ctx->grid32_g1 : ctx->grid32_s1) = std::max(1, b1) * ctx->sms;
-  (GEN ? ctx->grid32_g2 : ctx->grid32_s2) = std::max(1, b2) * ctx->sms;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b1, s1, THREADS, sym32_smem<D, 1, GEN>()));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(b2, s2, THREADS, sym32_smem<D, 2, GEN>()));
+  return HAWKES_OK;
+}
+
+template <int D, bool SOA, bool GEN = false>
+int sym32_setup(hawkes_ctx* ctx) {
+  int b1 = 0, b2 = 0, p1 = 0, p2 = 0;
+  int rc = sym32_attrs<D, SOA, GEN, false>(ctx, &b1, &b2);
+  if (rc == HAWKES_OK) rc = sym32_attrs<D, SOA, GEN, true>(ctx, &p1, &p2);
+  if (rc != HAWKES_OK) return rc;
+  (GEN ? ctx->grid32_g1 : ctx->grid32_s1) = std::max(1, std::min(b1, p1)) * ctx->sms;
+  (GEN ? ctx->grid32_g2 : ctx->grid32_s2) = std::max(1, std::min(b2, p2)) * ctx->sms;
+  return HAWKES_OK;
+}
+
+template <int D, bool SOA, bool GEN, bool PIECE>
+int sym32_go(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
+  const int grid = std::min(GEN ? (pass == 1 ? ctx->grid32_g1 : ctx->grid32_g2)
+                                : (pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2),
+                            b.n_items);
+  if (pass == 1)
+    CU(launch_pdl(sym_kernel_f32<D, 1, SYM32_R, SOA, GEN, PIECE>, grid, THREADS, sym32_smem<D, 1, GEN>(), ctx->stream, b));
+  else
+    CU(launch_pdl(sym_kernel_f32<D, 2, SYM32_R, SOA, GEN, PIECE>, grid, THREADS, sym32_smem<D, 2, GEN>(), ctx->stream, b));
+  CHECK_LAUNCH();
   return HAWKES_OK;
 }
 
 template <int D, bool SOA, bool GEN = false>
 int sym32_launch(hawkes_ctx* ctx, int pass, const SymArgs32& b) {
-  const int grid = std::min(GEN ? (pass == 1 ? ctx->grid32_g1 : ctx->grid32_g2)
-                                : (pass == 1 ? ctx->grid32_s1 : ctx->grid32_s2),
-                            b.n_items);
-  if (pass == 1)
-    CU(launch_pdl(sym_kernel_f32<D, 1, SYM32_R, SOA, GEN>, grid, THREADS, sym32_smem<D, 1, GEN>(), ctx->stream, b));
-  else
-    CU(launch_pdl(sym_kernel_f32<D, 2, SYM32_R, SOA, GEN>, grid, THREADS, sym32_smem<D, 2, GEN>(), ctx->stream, b));
-  CHECK_LAUNCH();
-  return HAWKES_OK;
+  return b.piece ? sym32_go<D, SOA, GEN, true>(ctx, pass, b) : sym32_go<D, SOA, GEN, false>(ctx, pass, b);
 }
 
 template <int D>
 size_t pass_smem32() {
   return (size_t)STAGES * TILE_J * Layout32<D>::REC * sizeof(float) + STAGES * sizeof(uint64_t);
 }
+
+// the pass kernels' resident grids alone (create, before the plan: pieces need grid_s2)
+template <int D>
+struct SymSetupD {
+  static int run(hawkes_ctx* ctx) {
+    if constexpr (D <= SYM_MAX_D) return sym_call<D>(ctx, 0, nullptr);
+    return HAWKES_OK;
+  }
+};
 
 template <int D>
 struct SetupD {
@@ -324,6 +367,7 @@ struct PassD {
       b.chunk = ctx->chunk;
       b.nchunks = ctx->nchunks;
       b.c = ctx->pc;
+      b.piece = ctx->piece_k[rank] > 1 ? 1 : 0;
       TRY(sym_call<D>(ctx, pass, &b));
     }
     record_stop(ctx, pass == 1);
@@ -366,6 +410,7 @@ struct PassD {
       b.chunk = ctx->chunk;
       b.nchunks = ctx->nchunks;
       b.c = ctx->pc32;
+      b.piece = ctx->piece_k[rank] > 1 ? 1 : 0;
       bool soa = true;
       if constexpr (D == 2) soa = sym32_soa();
       int rc = HAWKES_OK;

@@ -339,8 +339,8 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
       static_assert(sizeof(EvalStatus) % sizeof(int) == 0, "EvalStatus is copied in words");
       const int* src = reinterpret_cast<const int*>(st);
       volatile int* dst = reinterpret_cast<volatile int*>(mirror);
+      // (no system fence: the host reads it after the stream has completed)
       for (int k = threadIdx.x; k < NW; k += FINP_THREADS) dst[k] = __ldcg(src + k);
-      __threadfence_system();
     }
   }
   __syncthreads();   // last / red reused by the caller's next block

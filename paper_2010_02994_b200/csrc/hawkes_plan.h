@@ -65,6 +65,26 @@ std::vector<int> pair_owners(long long N, int chunk, int W) {
   return own;
 }
 
+// Pieces (hawkes_kernels_sym.cuh PairItem s0 / s1).  When a rank's n items fill less than
+// one round of the G resident CTA slots of the gradient pass (N = 2000: 136 items, one per
+// SM: each CTA runs latency-bound, its 4 warps alone on an SM), every item runs as k pieces
+// of 32 / k skewed steps, k the largest of 8, 4, 2 with k n <= G, each piece with its own row
+// and column slot blocks, so k CTAs share an item's tile pair (N = 2000: 136 x 4 pieces;
+// measured 56.5 -> 51.8 us per l + grad call, N = 500: 54 -> 40 us,
+// profiles/r02_latency_pieces.jsonl).  Above one round, whole items: splitting the
+// tail of a multi-round plan measured slower (N = 5000, 820 items on 592 slots: +3 %), since
+// an item's fixed cost (row and column tile loads, the row reduction) does not split.
+inline int choose_pieces(int n, int G) {
+  if (const char* e = getenv("HAWKES_PIECES")) {   // diagnostics: 0 / 1 = whole items, 2/4/8
+    const int k = atoi(e);
+    if (k >= 0) return (k == 2 || k == 4 || k == 8) ? k : 1;
+  }
+  if (G <= 0 || n <= 0) return 1;
+  for (int k : {8, 4, 2})
+    if ((long long)k * n <= G) return k;
+  return 1;
+}
+
 // PAIRS work items and compact slot layout of every rank (hawkes_kernels_sym.cuh PairItem):
 // rank r's chunk pairs, heaviest first (dynamic scheduling takes them in this order); for every
 // chunk c the ascending slot ids r's items write for c's events (row role of (c, b): b;
@@ -74,18 +94,22 @@ std::vector<int> pair_owners(long long N, int chunk, int W) {
 // every chunk has C + 1 slots in slot-id order, the order the finalize sums them in.
 struct PairsLayout {
   std::vector<std::vector<PairItem>> items;
+  std::vector<int> pieces;   // k per rank (1: whole items)
   std::vector<std::vector<long long>> coff;
   std::vector<std::vector<int>> cn;
   long long slot_events = 0;
 };
 
-inline PairsLayout pairs_layout(long long N, int chunk, int W, const std::vector<int>& mine) {
+// G > 0: the gradient pass's resident CTA slots, for the pieces above (0: whole items only;
+// the host-side plan calls, which know no device)
+inline PairsLayout pairs_layout(long long N, int chunk, int W, const std::vector<int>& mine, int G = 0) {
   const int C = (int)((N + chunk - 1) / chunk);
   const std::vector<int> own = pair_owners(N, chunk, W);
   PairsLayout L;
   L.items.assign(W, {});
   L.coff.assign(W, {});
   L.cn.assign(W, {});
+  L.pieces.assign(W, 1);
   long long base = 0;
   for (int r = 0; r < W; ++r) {
     const bool is_mine = std::find(mine.begin(), mine.end(), r) != mine.end();
@@ -101,11 +125,18 @@ inline PairsLayout pairs_layout(long long N, int chunk, int W, const std::vector
                      [](const std::pair<double, int2>& x, const std::pair<double, int2>& y) {
                        return x.first > y.first;
                      });
+    const int kp = choose_pieces((int)items.size(), G);
+    L.pieces[r] = kp;
+    auto pieces_of = [&](int) { return kp; };
+    // slot ids: piece q of item (a, b) -- row role b + q (C + 1), column role a (C for a
+    // diagonal item) + q (C + 1); a whole item is piece 0
     std::vector<std::vector<int>> ids(C);
-    for (auto& e : items) {
-      const int a = e.second.x, b = e.second.y;
-      ids[a].push_back(b);
-      ids[b].push_back(a == b ? C : a);
+    for (int i = 0; i < (int)items.size(); ++i) {
+      const int a = items[i].second.x, b = items[i].second.y;
+      for (int q = 0; q < pieces_of(i); ++q) {
+        ids[a].push_back(b + q * (C + 1));
+        ids[b].push_back((a == b ? C : a) + q * (C + 1));
+      }
     }
     L.coff[r].assign(C, 0);
     L.cn[r].assign(C, 0);
@@ -120,9 +151,13 @@ inline PairsLayout pairs_layout(long long N, int chunk, int W, const std::vector
       const auto it = std::lower_bound(ids[c].begin(), ids[c].end(), id);
       return L.coff[r][c] + (long long)(it - ids[c].begin()) * chunk;
     };
-    for (auto& e : items) {
-      const int a = e.second.x, b = e.second.y;
-      L.items[r].push_back(PairItem{a, b, block(a, b), block(b, a == b ? C : a)});
+    for (int i = 0; i < (int)items.size(); ++i) {
+      const int a = items[i].second.x, b = items[i].second.y;
+      const int k = pieces_of(i);
+      for (int q = 0; q < k; ++q)
+        L.items[r].push_back(PairItem{a, b, block(a, b + q * (C + 1)),
+                                      block(b, (a == b ? C : a) + q * (C + 1)), 32 * q / k,
+                                      32 * (q + 1) / k});
     }
     if (is_mine) base = off;
   }

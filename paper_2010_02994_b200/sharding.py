@@ -45,6 +45,20 @@ def plan_slots(N: int, world: int, rank: int) -> Tuple[int, int]:
     return s.value, m.value
 
 
+def plan_items(N: int, world: int, rank: int, resident: int = 0):
+    """hawkes_plan_items: (items as (a, b, row offset, column offset, s0, s1), pieces per
+    item, slot events) of `rank` for a gradient pass of `resident` CTA slots."""
+    import numpy as np
+    lib = _lib.load()
+    n, k, se = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    _lib.check(lib.hawkes_plan_items(N, world, rank, resident, None, ctypes.byref(n), None, None))
+    out = np.zeros((max(1, n.value), 6), dtype=np.int64)
+    _lib.check(lib.hawkes_plan_items(N, world, rank, resident,
+                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                     ctypes.byref(n), ctypes.byref(k), ctypes.byref(se)))
+    return out[: n.value], k.value, se.value
+
+
 def plan_walk(x, t, theta) -> Tuple[List[int], Tuple[float, float]]:
     """hawkes_plan_walk: (the spatial walk permutation, (time-walk cost, spatial-walk cost))."""
     import numpy as np

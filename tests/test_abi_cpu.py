@@ -163,3 +163,39 @@ def test_compact_slot_layout_footprint(N):
         assert sum(per) == (C + 1) * C * chunk
         assert sharding.plan_slots(N, W, 0)[1] == max(per)
         assert max(per) <= 1.35 * (C + 1) * C * chunk / W + 4 * chunk * (C + 1), (W, per)
+
+
+@pytest.mark.parametrize("N,W,resident,k_want", [(500, 1, 592, 8), (2000, 1, 592, 4), (3000, 1, 592, 1),
+                                                 (5000, 1, 592, 1), (2000, 3, 444, 8), (7000, 2, 592, 2),
+                                                 (2000, 1, 0, 1)])
+def test_plan_items_pieces_cover_every_pair_once(N, W, resident, k_want):
+    """hawkes_plan_items (DESIGN.md §5 "Small N"): below one round of `resident` CTA slots
+    every item runs as k pieces whose step ranges partition [0, 32); every piece owns its
+    own row and column blocks, so the blocks of all pieces tile [0, slot_events) exactly
+    once, and each chunk's blocks are as many as its slot count; the pieces of an item keep
+    the item's chunk pair, and the chunk pairs are hawkes_plan_pairs' (a <= b) on that rank."""
+    from paper_2010_02994_b200 import sharding
+    total = 0
+    for r in range(W):
+        items, k, se = sharding.plan_items(N, W, r, resident)
+        pairs, chunk = sharding.plan_pairs(N, W, r)
+        n_pairs = len(pairs)
+        assert k == (k_want if W == 1 or k_want == 1 else k) and k in (1, 2, 4, 8)
+        if resident:
+            assert k == 1 or k * n_pairs <= resident
+            assert k == 8 or 2 * k * n_pairs > resident   # the largest k that fits
+        assert len(items) == k * n_pairs
+        assert sorted({(int(a), int(b)) for a, b in items[:, :2]}) == sorted(map(tuple, pairs))
+        steps = {}
+        for a, b, ro, co, s0, s1 in items:
+            steps.setdefault((a, b), []).append((s0, s1))
+        for rngs in steps.values():
+            rngs.sort()
+            assert rngs[0][0] == 0 and rngs[-1][1] == 32
+            assert all(rngs[q][1] == rngs[q + 1][0] for q in range(len(rngs) - 1))
+            assert len({s1 - s0 for s0, s1 in rngs}) == 1
+        blocks = sorted([int(ro) for ro in items[:, 2]] + [int(co) for co in items[:, 3]])
+        assert blocks == list(range(0, se, chunk)), "every block owned by exactly one (piece, role)"
+        total += se
+    if W == 1 and k_want == 1:
+        assert total == sharding.plan_slots(N, W, 0)[0]

@@ -179,7 +179,9 @@ def test_emulated_world_other_dimensions(D, precision):
     ell_ref, _, _, g_ref, S = oracle_eval(c.x, c.t, c.theta)
     e1, g1, r1 = gpu_eval(c.x, c.t, c.theta, precision=precision, algorithm="pairs")
     e3, g3, r3 = gpu_eval(c.x, c.t, c.theta, precision=precision, emulate_world=3, algorithm="pairs")
-    tol = 1e-13 if precision == "fp64" else 1e-9
+    # fp32: the plan's pieces (hawkes_plan.h choose_pieces) depend on W, and each piece sums
+    # its terms in fp32 before they meet in fp64: W = 3 regroups fp32 partial sums
+    tol = 1e-13 if precision == "fp64" else 4e-6
     assert abs(e3 - e1) <= tol * abs(e1)
     assert np.all(np.abs(g3 - g1) <= tol * (np.abs(g1) + S))
     assert_parity(e3, g3, ell_ref, g_ref, S, precision=precision, what=f"PAIRS W=3 D={D} {precision}")
@@ -439,7 +441,8 @@ def test_call_sequences_status_mirror_and_counter_rearm(precision):
         xm = c.x.copy()
         xm[idx] = new
         em, gm, _ = fresh(xm)
-        assert ctx.loglik() == pytest.approx(e1 + d, rel=1e-12)
+        # (fp32 contexts: the committed rates and ell come from the move kernels' own sums)
+        assert ctx.loglik() == pytest.approx(e1 + d, rel=1e-12 if precision == "fp64" else 1e-9)
         assert ctx.loglik() == pytest.approx(em, rel=1e-9 if precision == "fp64" else 1e-5)
         g, e = ctx.grad_locations()
         assert e == pytest.approx(em, rel=1e-9 if precision == "fp64" else 1e-5)
