@@ -166,6 +166,19 @@ int hawkes_loglik(hawkes_ctx* ctx, double* out_loglik);
  * Errors: as hawkes_loglik, plus HAWKES_ERR_GRAD_UNDEFINED when ell = -inf. */
 int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double* out_loglik);
 
+/* ell and d ell / d x (Eq. 1, App. A: P:L96-101) at new locations in one call: the
+ * same results as hawkes_set_locations(ctx, x, HAWKES_MEM_DEVICE) followed by
+ * hawkes_grad_locations(ctx, out_grad, HAWKES_MEM_DEVICE, out_loglik), bit for bit.  x
+ * (N*D, row-major) and out_grad (N*D) are DEVICE arrays; x is read (and copied) by the call's
+ * first kernel, so the caller may overwrite it once the call has returned.  The small-catalog
+ * path (the paper's N ~ 3-5k evaluated millions of times): once the constants have
+ * been used for two evaluations (W = 1, the unordered-pair algorithm, timing off) the packing,
+ * both passes and both finalizes run as ONE CUDA-graph launch whose first and last nodes take
+ * x and out_grad (no separate packing launch, no gradient copy); otherwise the two calls above
+ * are made.  Errors: as hawkes_set_locations (device input) and hawkes_grad_locations;
+ * HAWKES_ERR_STATE without set_times and set_params. */
+int hawkes_grad_at(hawkes_ctx* ctx, const double* x, double* out_grad, double* out_loglik);
+
 /* HMC leapfrog over X (potential U = -ell): starting from (x, p), n_steps steps
  *   p += (step/2) grad ell(x);  x += step * Minv * p;  [reflect into [box_lo, box_hi]];
  *   p += (step/2) grad ell(x)

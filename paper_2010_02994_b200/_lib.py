@@ -29,6 +29,7 @@ REGIONS = {"square": 1, "disc": 2}
 EXPORTS = (
     "hawkes_default_opts", "hawkes_create", "hawkes_destroy", "hawkes_set_times",
     "hawkes_set_locations", "hawkes_set_params", "hawkes_loglik", "hawkes_grad_locations",
+    "hawkes_grad_at",
     "hawkes_leapfrog", "hawkes_hmc_step", "hawkes_get_rates", "hawkes_propose_move", "hawkes_accept_move",
     "hawkes_set_regions", "hawkes_mh_sweep", "hawkes_get_locations",
     "hawkes_set_bmds", "hawkes_bmds_logdensity", "hawkes_set_potential", "hawkes_enable_timing", "hawkes_get_kernel_times",
@@ -78,6 +79,7 @@ def load() -> ctypes.CDLL:
     lib.hawkes_set_params.argtypes = [vp, P(Params)]
     lib.hawkes_loglik.argtypes = [vp, P(ctypes.c_double)]
     lib.hawkes_grad_locations.argtypes = [vp, dp, i32, P(ctypes.c_double)]
+    lib.hawkes_grad_at.argtypes = [vp, dp, dp, P(ctypes.c_double)]
     lib.hawkes_leapfrog.argtypes = [vp, dp, dp, i32, ctypes.c_double, i32, dp, dp, dp,
                                     P(ctypes.c_double), P(ctypes.c_double)]
     u64 = ctypes.c_uint64

@@ -265,6 +265,7 @@ int hawkes_destroy(hawkes_ctx* ctx) {
   if (ctx->comm && g_nccl.commDestroy) g_nccl.commDestroy(ctx->comm);
   for (auto& ge : ctx->gexec)
     if (ge) cudaGraphExecDestroy(ge);
+  if (ctx->g_at) cudaGraphDestroy(ctx->g_at);
   if (ctx->mh_gexec) cudaGraphExecDestroy(ctx->mh_gexec);
   if (ctx->mh_ev0) cudaEventDestroy(ctx->mh_ev0);
   if (ctx->mh_ev1) cudaEventDestroy(ctx->mh_ev1);
@@ -400,6 +401,41 @@ int hawkes_grad_locations(hawkes_ctx* ctx, double* out_grad, int32_t mem, double
     TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, mem));
     TRY(fetch_status(ctx, true));
   } while (take_retry(ctx));
+  if (out_ll) *out_ll = ctx->h_st->ell;
+  if (!(ctx->h_st->ell > -INFINITY))
+    return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "some lambda_n = 0: ell = -inf, gradient undefined");
+  return HAWKES_OK;
+}
+
+int hawkes_grad_at(hawkes_ctx* ctx, const double* x, double* out_grad, double* out_ll) {
+  ENTER(ctx);
+  if (!x || !out_grad) return set_err(ctx, HAWKES_ERR_ARG, "bad arguments to hawkes_grad_at");
+  if (!ctx->have_t || !ctx->have_p)
+    return set_err(ctx, HAWKES_ERR_STATE, "set_times and set_params are required");
+  TRY(clear_move(ctx));
+  ctx->mirror_fresh = false;
+  bool done = false;
+  // the captured path counts the evaluation as run_grad would (use_graph: same constants for
+  // >= 2 evaluations); the plain path below counts it itself
+  ++ctx->evals_same_consts;
+  TRY(grad_at_graph(ctx, x, out_grad, &done));
+  if (done) {
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = true;
+    ctx->rates_exchanged = false;
+  } else {
+    --ctx->evals_same_consts;
+    TRY(dispatchD<PackXD>(ctx->D, ctx, x, ctx->xstage));
+    ctx->have_x = true;
+    ctx->rates_valid = ctx->grad_valid = ctx->lam_valid = false;
+    TRY(run_grad(ctx));
+    TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, HAWKES_MEM_DEVICE));
+  }
+  TRY(fetch_status(ctx, true));
+  while (take_retry(ctx)) {   // the fp32 range guard sent the context to fp64
+    TRY(run_grad(ctx));
+    TRY(copy_out(ctx, out_grad, ctx->grad, (size_t)ctx->N * ctx->D, HAWKES_MEM_DEVICE));
+    TRY(fetch_status(ctx, true));
+  }
   if (out_ll) *out_ll = ctx->h_st->ell;
   if (!(ctx->h_st->ell > -INFINITY))
     return set_err(ctx, HAWKES_ERR_GRAD_UNDEFINED, "some lambda_n = 0: ell = -inf, gradient undefined");

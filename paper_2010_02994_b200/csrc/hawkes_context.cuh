@@ -195,10 +195,14 @@ struct hawkes_ctx {
   DevConsts* d_consts = nullptr;
   // CUDA graphs of one evaluation (single process, W = 1, timing off)
   cudaStream_t gstream = nullptr;
-  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};   // rates, rates+grad, grad only
+  // rates, rates+grad, grad only, and (3) hawkes_grad_at: pack + rates + grad, whose pack and
+  // gradient-finalize nodes take the caller's x / gradient pointers per launch
+  cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraph_t g_at = nullptr;                 // kept: its nodes address the exec's params
+  cudaGraphNode_t at_pack = nullptr, at_pack32 = nullptr, at_fin2 = nullptr;
   bool graphs = false;
   bool capturing = false;
-  int64_t graph_launches[3] = {0, 0, 0};
+  int64_t graph_launches[4] = {0, 0, 0, 0};
   int evals_same_consts = 0;   // evaluations since the last constants change
   // block moves (hawkes_propose_move / hawkes_accept_move)
   int* d_slot_of = nullptr;    // N, -1 or the event's index in the pending proposal

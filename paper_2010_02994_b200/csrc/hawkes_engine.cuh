@@ -84,12 +84,16 @@ void drop_graphs(hawkes_ctx* ctx) {
       cudaGraphExecDestroy(ge);
       ge = nullptr;
     }
+  if (ctx->g_at) cudaGraphDestroy(ctx->g_at);
+  ctx->g_at = nullptr;
+  ctx->at_pack = ctx->at_pack32 = ctx->at_fin2 = nullptr;
   ctx->evals_same_consts = 0;
   drop_mh_graph(ctx);   // its launches carry the folded constants by value
 }
 
 // Capture one evaluation sequence (0: rate pass; 1: rate + gradient pass; 2: gradient pass
-// with cached rates) on the context's own stream and instantiate it.
+// with cached rates; 3: location packing + rate + gradient pass, hawkes_grad_at) on the
+// context's own stream and instantiate it.
 int capture(hawkes_ctx* ctx, int which) {
   cudaStream_t user = ctx->stream;
   const bool rv = ctx->rates_valid, gv = ctx->grad_valid;
@@ -101,7 +105,9 @@ int capture(hawkes_ctx* ctx, int which) {
   if (e == cudaSuccess) {
     ctx->rates_valid = which == 2;
     ctx->grad_valid = false;
-    rc = which == 0 ? run_rates(ctx) : run_grad(ctx);
+    // (3: packed from xstage in place; each launch points the pack nodes at the caller's x)
+    if (which == 3) rc = dispatchD<PackXD>(ctx->D, ctx, (const double*)ctx->xstage, ctx->xstage);
+    if (rc == HAWKES_OK) rc = which == 0 ? run_rates(ctx) : run_grad(ctx);
   }
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(ctx->gstream, &g);
@@ -117,11 +123,33 @@ int capture(hawkes_ctx* ctx, int which) {
     return set_err(ctx, HAWKES_ERR_CUDA, "graph capture failed: %s",
                    cudaGetErrorString(e != cudaSuccess ? e : e2));
   cudaError_t e3 = cudaGraphInstantiate(&ctx->gexec[which], g, 0);
-  cudaGraphDestroy(g);
+  if (which == 3 && e3 == cudaSuccess) {
+    ctx->g_at = g;
+    TRY(dispatchD<AtNodesD>(ctx->D, ctx));
+    if (!ctx->at_pack || !ctx->at_fin2 || (ctx->rec32 && !ctx->at_pack32))
+      return set_err(ctx, HAWKES_ERR_CUDA, "grad_at graph: packing / finalize nodes not found");
+  } else {
+    cudaGraphDestroy(g);
+  }
   if (e3 != cudaSuccess)
     return set_err(ctx, HAWKES_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e3));
   ctx->graph_launches[which] = ctx->launches - l0;
   ctx->launches = l0;
+  return HAWKES_OK;
+}
+
+// Point one kernel node of the grad_at exec at a new value of argument `arg` (a pointer): the
+// other arguments keep the values captured in g_at.
+int set_node_ptr(hawkes_ctx* ctx, cudaGraphNode_t nd, int arg, int nargs, const void* const* val) {
+  cudaKernelNodeParams kp;
+  CU(cudaGraphKernelNodeGetParams(nd, &kp));
+  void* args[16];
+  if (nargs > 16) return set_err(ctx, HAWKES_ERR_CUDA, "set_node_ptr: too many arguments");
+  for (int k = 0; k < nargs; ++k) args[k] = kp.kernelParams[k];
+  args[arg] = const_cast<void*>(static_cast<const void*>(val));
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  CU(cudaGraphExecKernelNodeSetParams(ctx->gexec[3], nd, &kp));
   return HAWKES_OK;
 }
 
@@ -255,6 +283,27 @@ int run_grad(hawkes_ctx* ctx) {
     TRY(exchange_rows(ctx, ctx->grad, ctx->D));
   }
   ctx->grad_valid = true;
+  return HAWKES_OK;
+}
+
+// hawkes_grad_at: one launch of the captured pack + rate + gradient evaluation (gexec[3]) at
+// the caller's device locations x, the gradient finalize also writing the caller's out_grad.
+// Takes the graph path when the plain one would (use_graph: W = 1, same constants for >= 2
+// evaluations, timing off); returns false (nothing enqueued) otherwise.
+int grad_at_graph(hawkes_ctx* ctx, const double* x, double* out_grad, bool* done) {
+  *done = false;
+  if (ctx->multi || !ctx->pairs || !ctx->order_decided || !ctx->have_x || !use_graph(ctx))
+    return HAWKES_OK;
+  if (!ctx->gexec[3]) TRY(capture(ctx, 3));
+  // k_pack_x(rec, x, N, npad, bad, xcopy); k_pack_x32(rec32, x, N, npad);
+  // k_fin2p(part, sv, N, grad, perm, counters, W, grad2)
+  TRY(set_node_ptr(ctx, ctx->at_pack, 1, 6, (const void* const*)&x));
+  if (ctx->at_pack32) TRY(set_node_ptr(ctx, ctx->at_pack32, 1, 4, (const void* const*)&x));
+  TRY(set_node_ptr(ctx, ctx->at_fin2, 7, 8, (const void* const*)&out_grad));
+  CU(cudaGraphLaunch(ctx->gexec[3], ctx->stream));
+  ctx->launches += ctx->graph_launches[3];
+  ctx->mirror_fresh = true;
+  *done = true;
   return HAWKES_OK;
 }
 

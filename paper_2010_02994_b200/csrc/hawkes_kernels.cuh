@@ -173,6 +173,39 @@ __device__ __forceinline__ double fexp(double a, const int2* __restrict__ tab, i
   return fma(Tm, p, Tm);
 }
 
+// The same exp as a product e^a = Tm * P, P = 1 + r (1 + r (c2 + c3 r)) = e^r (one rounding
+// more than fexp's Tm + Tm (e^r - 1): still within ~1 ulp), for callers that only accumulate
+// e^a: each sum += e^a becomes one fma(Tm, P, sum), so the exp's final multiply disappears
+// into the accumulations (the unordered-pair kernels: one FP64 instruction less per term in
+// pass 1, one per pair in pass 2).  A caller masks a term by zeroing Tm (P is
+// finite for every finite a).
+template <int STRIDE = 1, bool KF_I2F = false>
+__device__ __forceinline__ void fexp_tp(double a, const int2* __restrict__ tab, int lane_off,
+                                        double& Tm, double& P) {
+  static_assert(STRIDE == 1 || STRIDE == 2 || STRIDE == 4 || STRIDE == 16, "interleaved copies");
+  static_assert(EXP_DEGREE == 3, "the product form follows the degree-3 polynomial");
+  const unsigned ahi = min((unsigned)__double2hiint(a), EXP_AMIN_HI);
+  const double ac = __hiloint2double((int)ahi, __double2loint(a));
+  const double y = fma(ac, EXP_K, EXP_SHIFT);
+  const int k = __double2loint(y);
+  const double kf = KF_I2F ? __int2double_rn(k) : y - EXP_SHIFT;
+  const double r = fma(kf, -EXP_C, ac);
+  int2 T;
+  if constexpr (STRIDE == 1) {
+#ifdef HK_ABLATE_TABMASK
+    T = tab[k & g_ablate_tabmask];
+#else
+    T = tab[k & (EXP_TABLE - 1)];
+#endif
+  } else {
+    constexpr int SH = 3 + (STRIDE == 2 ? 1 : STRIDE == 4 ? 2 : 4);
+    T = *reinterpret_cast<const int2*>(reinterpret_cast<const char*>(tab) +
+                                       (((k << SH) & ((EXP_TABLE - 1) << SH)) | lane_off));
+  }
+  P = fma(fma(fma(EXP_C3, r, EXP_C2), r, 1.0), r, 1.0);
+  Tm = __hiloint2double(T.y + k * (1 << EXP_BIAS_SHIFT), T.x);
+}
+
 // --------------------------------------------------------------- programmatic dependent launch
 // The evaluation's kernels after the first (PAIRS: pass 1 -> finalize 1 -> pass 2 -> finalize
 // 2) are launched with programmatic stream serialization (hawkes_launch.cuh launch_pdl): each

@@ -130,6 +130,31 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
 #else
   constexpr bool I2F1 = false;
 #endif
+#ifndef HK_NO_EXPFMA
+  // product-form exps (fexp_tp): each accumulation is one fma(Tm, P, sum) -- 25 FP64
+  // instructions per unordered pair instead of 27 (100 + 51.5 other per 4-pair step), measured
+  // 9.00 -> 8.85 ms at N = 100k (profiles/r02_ab_expfma.jsonl; -DHK_NO_EXPFMA: the old form)
+  double Tb, Pb, Ts = 0.0, Ps = 0.0;
+  fexp_tp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+  if (SELF)
+    fexp_tp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+  if (MASK) {
+    Tb = dead ? 0.0 : Tb;
+    Ts = dead ? 0.0 : Ts;
+  }
+  rM = fma(Tb, Pb, rM);
+  cM = fma(Tb, Pb, cM);
+  if (SELF) {
+    if (GEN) {   // the later event takes xi (dt != 0 here: ties are masked)
+      const bool row_later = __double2hiint(dt) < 0;
+      rX = fma(row_later ? Ts : 0.0, Ps, rX);
+      cX = fma(row_later ? 0.0 : Ts, Ps, cX);
+    } else {
+      cX = fma(Ts, Ps, cX);
+    }
+  }
+  return;
+#endif
   double eb = fexp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
   double es = SELF ? fexp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off)
                    : 0.0;
@@ -167,6 +192,47 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   constexpr bool I2F = false;
 #else
   constexpr bool I2F = D <= 5;
+#endif
+#if defined(HK_PASS2_EXPFMA) && !defined(HK_SYM_FOLD)
+  // A/B only: product-form exps (fexp_tp) in pass 2 too -- mu' = Tb Pb once (it is needed
+  // twice), mu' + xi' as one fma: 4 FP64 instructions fewer per 4-pair step, but measured 0.9 %
+  // SLOWER at N = 100k (10.62 vs 10.52 ms; the 128-register build rematerialises two exp
+  // constants per step, and at 3 CTAs/SM, without them, 10.98 ms; profiles/r02_ab_expfma.jsonl)
+  {
+    double Ts = 0.0, Ps = 0.0;
+#ifdef HK_EXPFMA_MIX   // mu' by fexp (it is needed as a value), xi' in product form
+    double eb = fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+    if (SELF)
+      fexp_tp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+    if (MASK) {
+      eb = dead ? 0.0 : eb;
+      Ts = dead ? 0.0 : Ts;
+    }
+#else
+    double Tb, Pb;
+    fexp_tp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+    if (SELF)
+      fexp_tp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+    if (MASK) {
+      Tb = dead ? 0.0 : Tb;
+      Ts = dead ? 0.0 : Ts;
+    }
+    const double eb = Tb * Pb;
+#endif
+    double cc;
+    if (GEN) {   // rho'_i mu' + rho'_j mu' + rho'_later xi'
+      const double rlater = __double2hiint(dt) < 0 ? row.rho : crho;
+      cc = SELF ? fma(row.rho + crho, eb, (rlater * Ts) * Ps) : (row.rho + crho) * eb;
+    } else {
+      cc = fma(row.rho, eb, crho * (SELF ? fma(Ts, Ps, eb) : eb));
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      rG[d] = fma(cc, dx[d], rG[d]);
+      cG[d] = fma(-cc, dx[d], cG[d]);
+    }
+    return;
+  }
 #endif
   double eb = fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
 #ifdef HK_SYM_FOLD
@@ -691,8 +757,10 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
 // -DHK_SYM_OCC4 asks for 4 everywhere (A/B).
 template <int D, int PASS, bool GEN>
 constexpr int sym_min_ctas() {
-#ifdef HK_SYM_OCC4
+#if defined(HK_SYM_OCC4)
   return D <= 4 ? 4 : 2;
+#elif defined(HK_SYM_GRAD_OCC3)   // A/B: the D <= 2 gradient pass at 3 CTAs/SM as well
+  return D <= 4 ? 3 : 2;
 #else
   return (D <= 2 && PASS == 2 && !GEN) ? 4 : (D <= 4 ? 3 : 2);
 #endif

@@ -488,7 +488,7 @@ struct Fin2D {
           (const double*)(sums ? ctx->sums2 : ctx->part2),
           sums ? SlotView{nullptr, nullptr, ctx->chunk} : SlotView{ctx->d_coff[0], ctx->d_cn[0], ctx->chunk},
           (int)ctx->N, ctx->grad,
-          (const int*)(ctx->spatial ? ctx->d_perm : nullptr), ctx->counters, ctx->W));
+          (const int*)(ctx->spatial ? ctx->d_perm : nullptr), ctx->counters, ctx->W, (double*)nullptr));
     } else {
       k_fin2<D, true><<<nt, FIN_THREADS, 0, ctx->stream>>>(ctx->part2, ctx->npad, ctx->nslots,
                                                            ctx->d_tiles[rank], (int)ctx->N, ctx->G1,
@@ -519,6 +519,29 @@ struct PackXD {
       k_pack_x32<D><<<(ctx->npad + 255) / 256, 256, 0, ctx->stream>>>(ctx->rec32, xdev,
                                                                       (int)ctx->N, ctx->npad);
       CHECK_LAUNCH();
+    }
+    return HAWKES_OK;
+  }
+};
+
+// hawkes_grad_at's graph (hawkes_engine.cuh capture, which = 3): its location-packing and
+// gradient-finalize kernel nodes, found by kernel function
+template <int D>
+struct AtNodesD {
+  static int run(hawkes_ctx* ctx) {
+    size_t n = 0;
+    CU(cudaGraphGetNodes(ctx->g_at, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CU(cudaGraphGetNodes(ctx->g_at, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      CU(cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      CU(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == (void*)k_pack_x<D>) ctx->at_pack = nd;
+      else if (kp.func == (void*)k_pack_x32<D>) ctx->at_pack32 = nd;
+      else if (kp.func == (void*)k_fin2p<D>) ctx->at_fin2 = nd;
     }
     return HAWKES_OK;
   }

@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(FINP_THREADS) k_fin1p(const double* __restrict
 template <int D>
 __device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ part, SlotView sv,
                                             int N, double* __restrict__ grad,
-                                            const int* __restrict__ perm) {
+                                            const int* __restrict__ perm,
+                                            double* __restrict__ grad2 = nullptr) {
   constexpr int K = Layout<D>::K2;
   const long long q = (long long)blk * 32 + (threadIdx.x & 31);   // (walk position, d)
   const bool live = q < (long long)N * D;
@@ -388,7 +389,11 @@ __device__ __forceinline__ void fin2p_block(int blk, const double* __restrict__ 
     nslots = sv.cn[c];
   }
   const double g = finp_slot_sum(p0, stride, nslots, live);
-  if (threadIdx.x < 32 && live) grad[(perm ? (long long)perm[p] * D + d : q)] = g;
+  if (threadIdx.x < 32 && live) {
+    const long long o = perm ? (long long)perm[p] * D + d : q;
+    grad[o] = g;
+    if (grad2) grad2[o] = g;   // hawkes_grad_at: the caller's array as well (no copy launch)
+  }
   __syncthreads();   // finp_slot_sum's shared buffer is reused by the next block
 }
 
@@ -396,11 +401,12 @@ template <int D>
 __global__ void __launch_bounds__(FINP_THREADS) k_fin2p(const double* __restrict__ part, SlotView sv,
                                                         int N, double* __restrict__ grad,
                                                         const int* __restrict__ perm,
-                                                        int* counters, int W) {
+                                                        int* counters, int W,
+                                                        double* __restrict__ grad2) {
   pdl_wait();
   // re-arm the pass-2 item counters (as k_fin1p does pass 1's)
   if (counters && blockIdx.x == 0 && threadIdx.x < W) counters[4 * threadIdx.x + 3] = 0;
-  fin2p_block<D>(blockIdx.x, part, sv, N, grad, perm);
+  fin2p_block<D>(blockIdx.x, part, sv, N, grad, perm, grad2);
 }
 
 template <int D>

@@ -121,6 +121,19 @@ class HawkesContext:
         check(self._lib.hawkes_grad_locations(self._h, p, mem, ctypes.byref(ll)), self._h)
         return out, ll.value
 
+    def grad_at(self, x, out=None) -> Tuple[object, float]:
+        """set_locations(x) + grad_locations(out) in one call (hawkes_grad_at): x and out are
+        float64 CUDA tensors (N x D); returns (out, ell)."""
+        if out is None:
+            out = torch.empty((self.N, self.D), dtype=torch.float64, device=f"cuda:{self.device}")
+        px, memx, kx = _ptr_mem(x)
+        po, memo, ko = _ptr_mem(out)
+        if memx != HAWKES_MEM_DEVICE or memo != HAWKES_MEM_DEVICE:
+            raise ValueError("grad_at takes device arrays (float64 CUDA tensors)")
+        ll = ctypes.c_double()
+        check(self._lib.hawkes_grad_at(self._h, px, po, ctypes.byref(ll)), self._h)
+        return out, ll.value
+
     def get_rates(self) -> dict:
         """lambda_n, mu_n, xi_n, Lambda_n of the current state (numpy, host)."""
         arrs = {k: np.empty(self.N) for k in ("lambda", "mu", "xi", "Lambda")}

@@ -1,7 +1,9 @@
 """Per-call latency of ell + gradient at small N (the paper's catalogs are N ~ 3-5k, called
 millions of times by MCMC): device-input set_locations + grad_locations, host sync each call.
 
-    python tools/latency.py [--sizes 500,2000,5000,20000]
+    python tools/latency.py [--sizes 500,2000,5000,20000] [--at]
+
+--at: the one-call hawkes_grad_at (set_locations + grad_locations as one graph launch) as well.
 """
 import argparse
 import json
@@ -20,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="500,2000,5000,20000")
 ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--precision", default="fp64")
+ap.add_argument("--at", action="store_true")
 a = ap.parse_args()
 for N in [int(s) for s in a.sizes.split(",")]:
     c = synth.unit_square(N, config=4)
@@ -42,6 +45,15 @@ for N in [int(s) for s in a.sizes.split(",")]:
         ctx.set_locations(x)
         ell = ctx.loglik()
     dl = (time.perf_counter() - t0) / a.reps
-    print(json.dumps({"N": N, "grad_us": dt * 1e6, "loglik_us": dl * 1e6,
-                      "pairs_per_s": N * (N - 1) / dt}), flush=True)
+    rec = {"N": N, "grad_us": dt * 1e6, "loglik_us": dl * 1e6, "pairs_per_s": N * (N - 1) / dt}
+    if a.at:
+        for _ in range(5):
+            ctx.grad_at(x, g)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.reps):
+            _, ell = ctx.grad_at(x, g)      # one call, one sync
+        da = (time.perf_counter() - t0) / a.reps
+        rec.update(grad_at_us=da * 1e6, grad_at_pairs_per_s=N * (N - 1) / da)
+    print(json.dumps(rec), flush=True)
     ctx.close()
