@@ -289,6 +289,7 @@ template <int D>
 struct RowPair32 {
   float2 nxh[D], nxl[D];
   float2 nth, ntl, rho;
+  float2 nrt;   // TREB: -(t - T0) of the two rows, T0 the current column tile's first time
   int ga, gb;
 };
 
@@ -297,7 +298,9 @@ __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 // GEN (spatial walk, as in the fp64 kernels): either event may be the later one; the
 // self-excitation term uses |dt| and goes to the later event (pass 1: the row's X or the
 // column's; pass 2: rho' of the later event in the coefficient).
-template <int D, int PASS, bool MASK, bool SELF, bool GEN = false>
+// TREB (time walk): the column's time arrives as t_j - T0 and the rows' as -(t_i - T0), T0
+// the column tile's first time (sym_kernel_f32), so dt is one packed add instead of three
+template <int D, int PASS, bool MASK, bool SELF, bool GEN = false, bool TREB = false>
 __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float (&cxh)[D],
                                             const float (&cxl)[D], float cth, float ctl,
                                             float crho, bool dead_a, bool dead_b, float2& rM,
@@ -310,7 +313,8 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   float2 r2 = __fmul2_rn(dx[0], dx[0]);
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
-  const float2 dt = __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
+  const float2 dt = TREB ? __fadd2_rn(f2(cth), rp.nrt)
+                         : __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
   const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
   const float2 adt = GEN ? make_float2(fabsf(dt.x), fabsf(dt.y)) : dt;
   const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), adt, f2(c.cs)))
@@ -356,8 +360,8 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE>
-__device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, bool TREB = false>
+__device__ __forceinline__ void sym32_group_t(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag, int s0, int s1,
                                             float2 (&rM)[SR / 2], float2 (&rX)[SR / 2],
@@ -422,8 +426,8 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
         da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
         db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
       }
-      sym32_pair2<D, PASS, MASK, SELF, GEN>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h], rX[h],
-                                            rG[h], cM, cX, cG, c);
+      sym32_pair2<D, PASS, MASK, SELF, GEN, TREB>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h],
+                                                  rX[h], rG[h], cM, cX, cG, c);
     }
     if (PASS == 1) {
       cacc[0] = cM.x + cM.y;
@@ -442,6 +446,23 @@ __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
     }
   }
   if (PIECE && s1 != 32) rotate_cols<D, PASS>(cacc, (lane - s1) & 31);
+}
+
+// TREB kernels: the unmasked tile pairs whose column tile passed the span test take the
+// rebased times (treb), the others -- and every masked tile pair -- the hi/lo differences
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, bool TREB>
+__device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
+                                            const float* __restrict__ grp, int cg0, bool cvalid0,
+                                            int ridx0, int cidx0, bool diag, int s0, int s1,
+                                            float2 (&rM)[SR / 2], float2 (&rX)[SR / 2],
+                                            float2 (&rG)[SR / 2][D],
+                                            float (&cacc)[2 + D], const PassConst32& c, bool treb) {
+  if (TREB && !MASK && treb)
+    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, true>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
+                                                                  s0, s1, rM, rX, rG, cacc, c);
+  else
+    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, false>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
+                                                                   s0, s1, rM, rX, rG, cacc, c);
 }
 
 struct SymArgs32 {
@@ -487,6 +508,11 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? K1P : L64::K2;
   constexpr int KR = PASS == 1 ? (GEN ? 2 : 1) : D;
+#ifdef HK_NO_TREB   // A/B: hi/lo time differences in every pair
+  constexpr bool TREB = false;
+#else
+  constexpr bool TREB = SOA && !GEN;   // time walk: times relative to the column tile (below)
+#endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
@@ -647,26 +673,64 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           bg_live = fmaf(c.kt * dtmin, dtmin, c.cb) > -127.f;
         }
         const float* grp = st + warp * 32 * REC;
+        // TREB (time walk: tiles are time ranges): times relative to T0 = this column tile's
+        // first time -- the column's t_j - T0 replaces its t_hi in the transposed copy, the
+        // rows' -(t_i - T0) is formed here, so each pair's dt is one packed add.  The rounding
+        // of t - T0 is u32 |t - T0| <= u32 (|dt| + span of the tile), against u32 |dt| for the
+        // hi/lo difference: the same order for every pair whose terms survive the flush
+        // ... only where the column tile's time span is short against the time scales: its
+        // rounding adds u32 (omega log2e span) to the self-excitation exponent and u32 (2 |k_t|
+        // dt span) to the background one, so omega log2e span <= 64 and |k_t| span^2 <= 64 keep
+        // both within the hi/lo form's error class (a sparse-in-time catalog with a large omega
+        // keeps the hi/lo differences: fuzz seed 44 without this guard, 1.5x the fp32 gate)
+        bool treb = false;
+        if (TREB && strict) {   // (masked tile pairs read the hi/lo times)
+          const float* lastc = st + (cnt - 1) * REC;
+          const float span = (lastc[L::TH] - st[L::TH]) + (lastc[L::TL] - st[L::TL]);
+          treb = c.omega * span <= 64.f && c.kt * span * span >= -64.f;
+        }
+        if (treb) {
+          const float T0h = st[L::TH], T0l = st[L::TL];
+#pragma unroll
+          for (int h = 0; h < SR / 2; ++h)
+            rp[h].nrt = __fadd2_rn(__fadd2_rn(rp[h].nth, f2(T0h)), __fadd2_rn(rp[h].ntl, f2(T0l)));
+        }
         if (SOA) {   // this lane's column record -> the warp's [unit][32] float4 buffer
           const float4* rc4 = reinterpret_cast<const float4*>(grp + lane * REC);
           float4* g4 = reinterpret_cast<float4*>(mysoa);
+          if (treb) {
+            float v[REC];
 #pragma unroll
-          for (int u = 0; u < REC / 4; ++u) g4[u * 32 + lane] = rc4[u];
+            for (int u = 0; u < REC / 4; ++u) {
+              const float4 w4 = rc4[u];
+              v[4 * u] = w4.x;
+              v[4 * u + 1] = w4.y;
+              v[4 * u + 2] = w4.z;
+              v[4 * u + 3] = w4.w;
+            }
+            v[L::TH] = (v[L::TH] - st[L::TH]) + (v[L::TL] - st[L::TL]);
+#pragma unroll
+            for (int u = 0; u < REC / 4; ++u)
+              g4[u * 32 + lane] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < REC / 4; ++u) g4[u * 32 + lane] = rc4[u];
+          }
           __syncwarp();
           grp = mysoa;
         }
-        if (!strict)   // PIECE: as sym_items
-          sym32_group<D, PASS, true, SR, true, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
-                                                                jt + warp * 32, diag_tile, w.s0, w.s1, rM32,
-                                                                rX32, rG32, cacc, c);
+        if (!strict)   // PIECE: as sym_items; the masked tiles keep the hi/lo differences
+          sym32_group<D, PASS, true, SR, true, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+                                                                      jt + warp * 32, diag_tile, w.s0, w.s1,
+                                                                      rM32, rX32, rG32, cacc, c, treb);
         else if (self_live)
-          sym32_group<D, PASS, false, SR, true, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
-                                                                 jt + warp * 32, false, w.s0, w.s1, rM32,
-                                                                 rX32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, true, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+                                                                       jt + warp * 32, false, w.s0, w.s1,
+                                                                       rM32, rX32, rG32, cacc, c, treb);
         else if (bg_live)
-          sym32_group<D, PASS, false, SR, false, SOA, GEN, PIECE>(rp, grp, cg, cvalid, row0 + lane,
-                                                                  jt + warp * 32, false, w.s0, w.s1, rM32,
-                                                                  rX32, rG32, cacc, c);
+          sym32_group<D, PASS, false, SR, false, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+                                                                        jt + warp * 32, false, w.s0, w.s1,
+                                                                        rM32, rX32, rG32, cacc, c, treb);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;

@@ -125,3 +125,21 @@ def test_grad_at_after_params_change():
             g_ref, ell_ref = ref.grad_locations()
             g_at, ell_at = at.grad_at(x)
             assert ell_at == ell_ref and torch.equal(g_at, g_ref), f"call {k}"
+
+
+def test_grad_at_fp32_range_guard():
+    """The fp32 range guard (reading R23) inside grad_at: round 1's failing fuzz catalog is
+    redone by the fp64 kernels on the first call, and the following (captured) calls stay on
+    fp64 and meet the fp64 gate."""
+    from paper_2010_02994_b200 import HawkesContext
+    from tests.test_parity_gpu import _fuzz_case
+    N, D, x, t, th, _, _, _ = _fuzz_case(12, 290, 4000)
+    ell_r, _, _, g_r, S = oracle_eval(x, t, th)
+    with HawkesContext(N, D, precision="fp32") as ctx:
+        ctx.set_times(t)
+        ctx.set_params(th)
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        for k in range(4):
+            g, ell = ctx.grad_at(xd)
+            assert ctx.precision_in_use == "fp64", f"call {k}"
+            assert_parity(ell, g.cpu().numpy(), ell_r, g_r, S, precision="fp64", what=f"guarded grad_at {k}")

@@ -54,6 +54,7 @@ if __name__ == "__main__":
     ap.add_argument("--alg", default=None, help="with --only: override the algorithm")
     ap.add_argument("--precision", default=None, help="force fp64 or fp32 for every case")
     ap.add_argument("--ordering", default="auto", help="walk order of the PAIRS fp64 kernels: auto | time | space")
+    ap.add_argument("--show", type=float, default=None, help="also print passing cases whose gradient error exceeds this share of the bound")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     fails = 0
@@ -89,6 +90,19 @@ if __name__ == "__main__":
             g_r, S = oracle.grad(x, t, th, lam=lam_r)
             ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False,
                                  ordering=a.ordering)
+            # reading R23, subnormal side: an oracle rate below 2^-1022 is a sum of subnormal
+            # terms, each rounded to a multiple of 2^-1074, so the oracle's own lambda (and every
+            # gradient term divided by it) carries relative errors far above the gate; the GPU
+            # works in the 2^64-scaled domain.  Such a case is checked only where the oracle is
+            # accurate (its fp64 arithmetic stays normal) and is counted apart.  Evidence: seed
+            # 41 case 602 (lambda_min = 1.7e-310) against a 30-digit App. A evaluation
+            # (tools/mp_check_case.py, profiles/r02_fuzz_case602_mp.txt): oracle 300x over the
+            # gate, the GPU kernels 0.005 of it
+            if prec == "fp64" and float(np.min(lam_r)) < 2.2250738585072014e-308:
+                underflow += 1
+                print(json.dumps({**info, "r23_underflow": "oracle rates subnormal", "oracle_min_lambda":
+                                  float(np.min(lam_r))}), flush=True)
+                continue
             if prec == "fp32" and not np.isfinite(ell):
                 continue                                   # fp32 range (reading R23)
             tol, floor = TOL[prec]
@@ -99,6 +113,8 @@ if __name__ == "__main__":
             if e_ell > tol or ratio > 1.0:
                 fails += 1
                 print(json.dumps({**info, "fail": "tolerance", "ell_rel": e_ell, "grad_ratio": ratio}), flush=True)
+            elif a.show is not None and ratio > a.show:
+                print(json.dumps({**info, "pass": True, "ell_rel": e_ell, "grad_ratio": ratio}), flush=True)
         except Exception as e:  # noqa: BLE001
             fails += 1
             print(json.dumps({**info, "fail": "exception", "error": repr(e)[:300]}), flush=True)
