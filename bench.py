@@ -62,12 +62,14 @@ def _ncu_traffic(kernel):
         return None
     if kernel in caps:
         return caps[kernel]["bytes"]
-    # the capture names every template argument; bench names the leading ones (the trailing
-    # GEN / PIECE flags of the time-walk whole-item kernels are 0)
+    # the capture names every template argument; bench names the leading ones
+    # (GEN, PIECE, NW) = (0, 0, 4): the time-walk whole-item 4-warp kernel
     stem = kernel[:-1] + ","
     for k, v in caps.items():
-        if k.startswith(stem) and all(a.strip() == "0" for a in k[len(stem):-1].split(",")):
-            return v["bytes"]
+        if k.startswith(stem):
+            rest = [a.strip() for a in k[len(stem):-1].split(",")]
+            if rest == ["0", "0", "4"][:len(rest)]:
+                return v["bytes"]
     return None
 
 

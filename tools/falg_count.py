@@ -56,7 +56,7 @@ def shipped():
     sass = subprocess.check_output(["cuobjdump", "-sass", lib], text=True, stderr=subprocess.DEVNULL)
     for f in re.split(r"\n\s+Function : ", sass)[1:]:
         name = f.split("\n")[0].strip()
-        m = re.match(r"_ZN2hk10sym_kernelILi2ELi([12])ELi4ELi(\d)ELb0ELb0EEEvNS_7SymArgsE", name)
+        m = re.match(r"_ZN2hk10sym_kernelILi2ELi([12])ELi4ELi(\d)ELb0ELb0E(?:Li4E)?EEvNS_7SymArgsE", name)
         if not m:
             continue
         ins = [(int(a, 16), b) for a, b in
