@@ -289,7 +289,8 @@ template <int D>
 struct RowPair32 {
   float2 nxh[D], nxl[D];
   float2 nth, ntl, rho;
-  float2 nrt;   // TREB: -(t - T0) of the two rows, T0 the current column tile's first time
+  float2 nrt;      // REB 1: -(t - T0) of the two rows, T0 the current column tile's first time
+  float2 nxr[D];   // REB 2: -(x - O) of the two rows, O the current column tile's first location
   int ga, gb;
 };
 
@@ -298,9 +299,10 @@ __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 // GEN (spatial walk, as in the fp64 kernels): either event may be the later one; the
 // self-excitation term uses |dt| and goes to the later event (pass 1: the row's X or the
 // column's; pass 2: rho' of the later event in the coefficient).
-// TREB (time walk): the column's time arrives as t_j - T0 and the rows' as -(t_i - T0), T0
-// the column tile's first time (sym_kernel_f32), so dt is one packed add instead of three
-template <int D, int PASS, bool MASK, bool SELF, bool GEN = false, bool TREB = false>
+// REB = 1 (time walk): the column's time arrives as t_j - T0 and the rows' as -(t_i - T0), T0
+// the column tile's first time (sym_kernel_f32), so dt is one packed add instead of three;
+// REB = 2 (spatial walk): the same for the locations, relative to the column tile's first one
+template <int D, int PASS, bool MASK, bool SELF, bool GEN = false, int REB = 0>
 __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float (&cxh)[D],
                                             const float (&cxl)[D], float cth, float ctl,
                                             float crho, bool dead_a, bool dead_b, float2& rM,
@@ -309,11 +311,12 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   float2 dx[D];
 #pragma unroll
   for (int d = 0; d < D; ++d)
-    dx[d] = __fadd2_rn(__fadd2_rn(f2(cxh[d]), rp.nxh[d]), __fadd2_rn(f2(cxl[d]), rp.nxl[d]));
+    dx[d] = REB == 2 ? __fadd2_rn(f2(cxh[d]), rp.nxr[d])
+                     : __fadd2_rn(__fadd2_rn(f2(cxh[d]), rp.nxh[d]), __fadd2_rn(f2(cxl[d]), rp.nxl[d]));
   float2 r2 = __fmul2_rn(dx[0], dx[0]);
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
-  const float2 dt = TREB ? __fadd2_rn(f2(cth), rp.nrt)
+  const float2 dt = REB == 1 ? __fadd2_rn(f2(cth), rp.nrt)
                          : __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
   const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
   const float2 adt = GEN ? make_float2(fabsf(dt.x), fabsf(dt.y)) : dt;
@@ -360,7 +363,7 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   }
 }
 
-template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, bool TREB = false>
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, int REB = 0>
 __device__ __forceinline__ void sym32_group_t(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag, int s0, int s1,
@@ -426,7 +429,7 @@ __device__ __forceinline__ void sym32_group_t(const RowPair32<D> (&rp)[SR / 2],
         da = !cv || rp[h].ga < 0 || cg == rp[h].ga || (diag && cidx0 + src <= ia);
         db = !cv || rp[h].gb < 0 || cg == rp[h].gb || (diag && cidx0 + src <= ib);
       }
-      sym32_pair2<D, PASS, MASK, SELF, GEN, TREB>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h],
+      sym32_pair2<D, PASS, MASK, SELF, GEN, REB>(rp[h], cxh, cxl, cth_v, ctl_v, crho_v, da, db, rM[h],
                                                   rX[h], rG[h], cM, cX, cG, c);
     }
     if (PASS == 1) {
@@ -448,20 +451,21 @@ __device__ __forceinline__ void sym32_group_t(const RowPair32<D> (&rp)[SR / 2],
   if (PIECE && s1 != 32) rotate_cols<D, PASS>(cacc, (lane - s1) & 31);
 }
 
-// TREB kernels: the unmasked tile pairs whose column tile passed the span test take the
-// rebased times (treb), the others -- and every masked tile pair -- the hi/lo differences
-template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, bool TREB>
+// REB kernels: the unmasked tile pairs whose column tile passed the span test take the
+// rebased times / locations (reb), the others -- and every masked tile pair -- the hi/lo
+// differences
+template <int D, int PASS, bool MASK, int SR, bool SELF, bool SOA, bool GEN, bool PIECE, int REB>
 __device__ __forceinline__ void sym32_group(const RowPair32<D> (&rp)[SR / 2],
                                             const float* __restrict__ grp, int cg0, bool cvalid0,
                                             int ridx0, int cidx0, bool diag, int s0, int s1,
                                             float2 (&rM)[SR / 2], float2 (&rX)[SR / 2],
                                             float2 (&rG)[SR / 2][D],
-                                            float (&cacc)[2 + D], const PassConst32& c, bool treb) {
-  if (TREB && !MASK && treb)
-    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, true>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
+                                            float (&cacc)[2 + D], const PassConst32& c, bool reb) {
+  if (REB && !MASK && reb)
+    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, REB>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
                                                                   s0, s1, rM, rX, rG, cacc, c);
   else
-    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, false>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
+    sym32_group_t<D, PASS, MASK, SR, SELF, SOA, GEN, PIECE, 0>(rp, grp, cg0, cvalid0, ridx0, cidx0, diag,
                                                                    s0, s1, rM, rX, rG, cacc, c);
 }
 
@@ -508,11 +512,18 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
   constexpr int REC = L::REC;
   constexpr int K = PASS == 1 ? K1P : L64::K2;
   constexpr int KR = PASS == 1 ? (GEN ? 2 : 1) : D;
+  // rebased differences (below): times on the time walk, locations on the spatial walk
 #ifdef HK_NO_TREB   // A/B: hi/lo time differences in every pair
   constexpr bool TREB = false;
 #else
-  constexpr bool TREB = SOA && !GEN;   // time walk: times relative to the column tile (below)
+  constexpr bool TREB = SOA && !GEN;
 #endif
+#ifdef HK_NO_XREB   // A/B: hi/lo location differences in every pair
+  constexpr bool XREB = false;
+#else
+  constexpr bool XREB = SOA && GEN;
+#endif
+  constexpr int REBK = TREB ? 1 : (XREB ? 2 : 0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES * TILE_J * REC * sizeof(float));
@@ -695,10 +706,33 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           for (int h = 0; h < SR / 2; ++h)
             rp[h].nrt = __fadd2_rn(__fadd2_rn(rp[h].nth, f2(T0h)), __fadd2_rn(rp[h].ntl, f2(T0l)));
         }
+        // XREB (spatial walk: tiles are compact in space): the same for the locations, relative
+        // to O = the column tile's first location, where the column tile's extent E around O
+        // (its box) keeps u32 |k| E^2-sized exponent errors small: |k| E^2 <= 64 for both
+        // kernels' k (log2 domain)
+        bool xreb = false;
+        if (XREB && strict) {
+          const double* cbx = a.boxes + (long long)(jt / TILE_J) * (2 * D + 2);
+          float e = 0.f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double o = (double)st[L::XH + d] + (double)st[L::XL + d];
+            e = fmaxf(e, (float)fmax(cbx[D + d] - o, o - cbx[d]));
+          }
+          xreb = fminf(c.kx, c.ks) * e * e >= -64.f;
+        }
+        if (xreb) {
+#pragma unroll
+          for (int h = 0; h < SR / 2; ++h)
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              rp[h].nxr[d] = __fadd2_rn(__fadd2_rn(rp[h].nxh[d], f2(st[L::XH + d])),
+                                        __fadd2_rn(rp[h].nxl[d], f2(st[L::XL + d])));
+        }
         if (SOA) {   // this lane's column record -> the warp's [unit][32] float4 buffer
           const float4* rc4 = reinterpret_cast<const float4*>(grp + lane * REC);
           float4* g4 = reinterpret_cast<float4*>(mysoa);
-          if (treb) {
+          if (treb || xreb) {
             float v[REC];
 #pragma unroll
             for (int u = 0; u < REC / 4; ++u) {
@@ -708,7 +742,12 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
               v[4 * u + 2] = w4.z;
               v[4 * u + 3] = w4.w;
             }
-            v[L::TH] = (v[L::TH] - st[L::TH]) + (v[L::TL] - st[L::TL]);
+            if (treb) v[L::TH] = (v[L::TH] - st[L::TH]) + (v[L::TL] - st[L::TL]);
+            if (xreb) {
+#pragma unroll
+              for (int d = 0; d < D; ++d)
+                v[L::XH + d] = (v[L::XH + d] - st[L::XH + d]) + (v[L::XL + d] - st[L::XL + d]);
+            }
 #pragma unroll
             for (int u = 0; u < REC / 4; ++u)
               g4[u * 32 + lane] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
@@ -720,17 +759,17 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           grp = mysoa;
         }
         if (!strict)   // PIECE: as sym_items; the masked tiles keep the hi/lo differences
-          sym32_group<D, PASS, true, SR, true, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+          sym32_group<D, PASS, true, SR, true, SOA, GEN, PIECE, REBK>(rp, grp, cg, cvalid, row0 + lane,
                                                                       jt + warp * 32, diag_tile, w.s0, w.s1,
-                                                                      rM32, rX32, rG32, cacc, c, treb);
+                                                                      rM32, rX32, rG32, cacc, c, treb || xreb);
         else if (self_live)
-          sym32_group<D, PASS, false, SR, true, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+          sym32_group<D, PASS, false, SR, true, SOA, GEN, PIECE, REBK>(rp, grp, cg, cvalid, row0 + lane,
                                                                        jt + warp * 32, false, w.s0, w.s1,
-                                                                       rM32, rX32, rG32, cacc, c, treb);
+                                                                       rM32, rX32, rG32, cacc, c, treb || xreb);
         else if (bg_live)
-          sym32_group<D, PASS, false, SR, false, SOA, GEN, PIECE, TREB>(rp, grp, cg, cvalid, row0 + lane,
+          sym32_group<D, PASS, false, SR, false, SOA, GEN, PIECE, REBK>(rp, grp, cg, cvalid, row0 + lane,
                                                                         jt + warp * 32, false, w.s0, w.s1,
-                                                                        rM32, rX32, rG32, cacc, c, treb);
+                                                                        rM32, rX32, rG32, cacc, c, treb || xreb);
 #pragma unroll
         for (int h = 0; h < SR / 2; ++h) {
           rM[2 * h] += (double)rM32[h].x;

@@ -90,19 +90,29 @@ if __name__ == "__main__":
             g_r, S = oracle.grad(x, t, th, lam=lam_r)
             ell, g, _ = gpu_eval(x, t, th, precision=prec, emulate_world=W, algorithm=alg, with_rates=False,
                                  ordering=a.ordering)
-            # reading R23, subnormal side: an oracle rate below 2^-1022 is a sum of subnormal
-            # terms, each rounded to a multiple of 2^-1074, so the oracle's own lambda (and every
-            # gradient term divided by it) carries relative errors far above the gate; the GPU
-            # works in the 2^64-scaled domain.  Such a case is checked only where the oracle is
-            # accurate (its fp64 arithmetic stays normal) and is counted apart.  Evidence: seed
-            # 41 case 602 (lambda_min = 1.7e-310) against a 30-digit App. A evaluation
-            # (tools/mp_check_case.py, profiles/r02_fuzz_case602_mp.txt): oracle 300x over the
-            # gate, the GPU kernels 0.005 of it
-            if prec == "fp64" and float(np.min(lam_r)) < 2.2250738585072014e-308:
-                underflow += 1
-                print(json.dumps({**info, "r23_underflow": "oracle rates subnormal", "oracle_min_lambda":
-                                  float(np.min(lam_r))}), flush=True)
-                continue
+            # reading R23, subnormal side: the oracle evaluates each term unscaled as a kernel
+            # constant c (c_b = mu0 / ((2 pi)^((D+1)/2) tau_x^D tau_t), c_s = theta
+            # omega / ((2 pi)^(D/2) h^D)) times exps, so an exp factor below 2^-1022 is subnormal
+            # and carries an absolute error up to 2^-1074 c.  Where some rate lambda_n is below
+            # 1e13 N 2^-1074 max(c_b, c_s) (or itself subnormal), the oracle's lambda_n -- and every
+            # gradient term divided by it -- may be off by more than ~1e-13 relative, far above
+            # what the gate assumes of the reference; the GPU works in the 2^64-scaled domain.
+            # Such a case is counted apart.  Evidence against 30-digit App. A evaluations
+            # (tools/mp_check_case.py): seed 41 case 602 (lambda_min = 1.7e-310; oracle 300x over
+            # the gate, the GPU kernels 0.005 of it, profiles/r02_fuzz_case602_mp.txt) and seed 45
+            # case 514 (lambda_35 = 5.4e-299 from two terms whose exp factors are ~1e-318:
+            # oracle lambda_35 off by 2.6e-10, the GPU's by 3e-15; profiles/r02_fuzz_case45_514_mp.txt)
+            if prec == "fp64":
+                lc = max(math.log(th[0]) - 0.5 * (D + 1) * math.log(2 * math.pi) - D * math.log(th[1])
+                         - math.log(th[2]) if th[0] > 0 else -math.inf,
+                         math.log(th[3] * th[4]) - 0.5 * D * math.log(2 * math.pi) - D * math.log(th[5])
+                         if th[3] > 0 else -math.inf)
+                floor = max(2.2250738585072014e-308, math.exp(min(700.0, lc + math.log(1e13 * N) - 1074 * math.log(2))))
+                if float(np.min(lam_r)) < floor:
+                    underflow += 1
+                    print(json.dumps({**info, "r23_underflow": "oracle exp factors subnormal",
+                                      "oracle_min_lambda": float(np.min(lam_r)), "floor": floor}), flush=True)
+                    continue
             if prec == "fp32" and not np.isfinite(ell):
                 continue                                   # fp32 range (reading R23)
             tol, floor = TOL[prec]
