@@ -125,10 +125,16 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
   const double dt = ct - row.t;   // >= 0: the column is the later event
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
-#ifdef HK_PASS1_I2F   // A/B: the exp's k -> double on the conversion pipe in pass 1 too
+  // the exp's k -> double on the conversion pipe (I2F.F64) in pass 1 as well: with the product
+  // form's fewer FP64 instructions it pays at D = 2 (N = 100k 8.84 -> 8.81 ms, Alaska-shaped
+  // time walk -1.2 %, DC-shaped spatial walk -0.3 %; profiles/r02_ab_final_variants.jsonl); it
+  // cost 0.6-2.6 % before, and D >= 3 is unmeasured, so it stays off there
+#if defined(HK_PASS1_I2F)      // A/B: for every D <= 5
   constexpr bool I2F1 = D <= 5;
-#else
+#elif defined(HK_PASS1_NO_I2F)   // A/B: off
   constexpr bool I2F1 = false;
+#else
+  constexpr bool I2F1 = D <= 2;
 #endif
 #ifndef HK_NO_EXPFMA
   // product-form exps (fexp_tp): each accumulation is one fma(Tm, P, sum) -- 25 FP64
@@ -285,7 +291,11 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
   if (PIECE && s0) rotate_cols<D, PASS>(cacc, (lane + s0) & 31);
   // unrolling by 2: pass 1 -2.8 %, pass 2 +1.4 % (N = 100k, accurate exp;
   // profiles/r02_ab_unroll.jsonl)
+#ifdef HK_PASS2_UNR2   // A/B: pass 2 unrolled by 2 as well
+  constexpr int UNR = 2;
+#else
   constexpr int UNR = PASS == 1 ? 2 : 1;
+#endif
 #pragma unroll UNR
   for (int s = s0; s < s1; ++s) {
     const int src = (lane + s) & 31;
