@@ -455,6 +455,35 @@ def run_ours(args):
                             "note": "effective pairs/s: culled pairs (exact, below the exp clamp) counted"}
             sctx.close()
 
+    # ---- the paper's catalog sizes (BASELINE configs[1] DC-shaped N = 5000, configs[2]
+    # Alaska-shaped N = 20k): per call of hawkes_grad_at (new locations + ell + gradient, one
+    # graph launch) with the host synchronised on ell every call, as an MCMC driver calls it;
+    # one process (rank 0), 1 GPU
+    paper_sized = None
+    if not args.no_hmc and rank == 0:
+        paper_sized = {}
+        for name, Nc in (("C2", 5000), ("C3", 20000)):
+            cc = synth.config(name, N=Nc)
+            pctx = HawkesContext(Nc, D, device=local, precision=args.precision, algorithm=args.algorithm)
+            xc = torch.from_numpy(cc.x).to(dev)
+            pctx.set_times(torch.from_numpy(cc.t).to(dev))
+            pctx.set_params(cc.theta)
+            gc = torch.empty_like(xc)
+            for _ in range(10):
+                pctx.grad_at(xc, gc)
+            torch.cuda.synchronize()
+            reps = 400 if Nc <= 5000 else 100
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                pctx.grad_at(xc, gc)
+            dt_call = (time.perf_counter() - t0) / reps
+            order, _ = pctx.ordering_in_use
+            paper_sized[name] = {"config": f"{name}-shaped N={Nc} D=2 {args.precision} (BASELINE configs[{1 if name == 'C2' else 2}])",
+                                 "us_per_call": dt_call * 1e6, "calls_per_s": 1.0 / dt_call,
+                                 "pairs_per_s": Nc * (Nc - 1) / dt_call, "walk_order": order,
+                                 "note": "hawkes_grad_at per call, host wall clock incl. the ell sync"}
+            pctx.close()
+
     # ---- per-rank pass-kernel time (library CUDA events): the load balance of the plan
     pass_ms = [float(kt["rate_ms"] + kt["grad_ms"]) / max(1, kt["rate_launches"])]
     if world > 1:
@@ -558,6 +587,7 @@ def run_ours(args):
         "hmc": hmc,
         "mh_sweep": mh,
         "shaped": shaped,
+        "paper_sized": paper_sized,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline()

@@ -200,6 +200,8 @@ struct hawkes_ctx {
   cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraph_t g_at = nullptr;                 // kept: its nodes address the exec's params
   cudaGraphNode_t at_pack = nullptr, at_pack32 = nullptr, at_fin2 = nullptr;
+  const double* at_x = nullptr;   // the pointers the exec's nodes hold (no update when unchanged)
+  double* at_out = nullptr;
   bool graphs = false;
   bool capturing = false;
   int64_t graph_launches[4] = {0, 0, 0, 0};

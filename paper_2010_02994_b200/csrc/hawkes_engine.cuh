@@ -87,6 +87,8 @@ void drop_graphs(hawkes_ctx* ctx) {
   if (ctx->g_at) cudaGraphDestroy(ctx->g_at);
   ctx->g_at = nullptr;
   ctx->at_pack = ctx->at_pack32 = ctx->at_fin2 = nullptr;
+  ctx->at_x = nullptr;
+  ctx->at_out = nullptr;
   ctx->evals_same_consts = 0;
   drop_mh_graph(ctx);   // its launches carry the folded constants by value
 }
@@ -294,12 +296,23 @@ int grad_at_graph(hawkes_ctx* ctx, const double* x, double* out_grad, bool* done
   *done = false;
   if (ctx->multi || !ctx->pairs || !ctx->order_decided || !ctx->have_x || !use_graph(ctx))
     return HAWKES_OK;
-  if (!ctx->gexec[3]) TRY(capture(ctx, 3));
+  if (!ctx->gexec[3]) {
+    TRY(capture(ctx, 3));
+    ctx->at_x = nullptr;
+    ctx->at_out = nullptr;
+  }
   // k_pack_x(rec, x, N, npad, bad, xcopy); k_pack_x32(rec32, x, N, npad);
-  // k_fin2p(part, sv, N, grad, perm, counters, W, grad2)
-  TRY(set_node_ptr(ctx, ctx->at_pack, 1, 6, (const void* const*)&x));
-  if (ctx->at_pack32) TRY(set_node_ptr(ctx, ctx->at_pack32, 1, 4, (const void* const*)&x));
-  TRY(set_node_ptr(ctx, ctx->at_fin2, 7, 8, (const void* const*)&out_grad));
+  // k_fin2p(part, sv, N, grad, perm, counters, W, grad2) -- only when the caller's pointers
+  // changed since the last launch (an MCMC loop usually reuses its buffers)
+  if (x != ctx->at_x) {
+    TRY(set_node_ptr(ctx, ctx->at_pack, 1, 6, (const void* const*)&x));
+    if (ctx->at_pack32) TRY(set_node_ptr(ctx, ctx->at_pack32, 1, 4, (const void* const*)&x));
+    ctx->at_x = x;
+  }
+  if (out_grad != ctx->at_out) {
+    TRY(set_node_ptr(ctx, ctx->at_fin2, 7, 8, (const void* const*)&out_grad));
+    ctx->at_out = out_grad;
+  }
   CU(cudaGraphLaunch(ctx->gexec[3], ctx->stream));
   ctx->launches += ctx->graph_launches[3];
   ctx->mirror_fresh = true;

@@ -24,6 +24,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="500,5000")
 ap.add_argument("--calls", type=int, default=50)
 ap.add_argument("--precision", default="fp64")
+ap.add_argument("--config", default="C4", help="catalog shape (synth.config name)")
+ap.add_argument("--at", action="store_true", help="hawkes_grad_at calls instead of set_locations + grad_locations")
 a = ap.parse_args()
 
 
@@ -33,20 +35,24 @@ def short(name):
 
 
 for N in [int(s) for s in a.sizes.split(",")]:
-    c = synth.unit_square(N, config=4)
+    c = synth.unit_square(N, config=4) if a.config == "C4" else synth.config(a.config, N=N)
     ctx = HawkesContext(N, 2, precision=a.precision)
     x = torch.from_numpy(c.x).cuda()
     ctx.set_times(torch.from_numpy(c.t).cuda())
     ctx.set_params(c.theta)
     g = torch.empty_like(x)
+    def call():
+        if a.at:
+            ctx.grad_at(x, g)
+        else:
+            ctx.set_locations(x)
+            ctx.grad_locations(g)
     for _ in range(10):
-        ctx.set_locations(x)
-        ctx.grad_locations(g)
+        call()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(a.calls):
-            ctx.set_locations(x)
-            ctx.grad_locations(g)
+            call()
         torch.cuda.synchronize()
     ev = []
     for e in prof.events():
@@ -78,7 +84,7 @@ for N in [int(s) for s in a.sizes.split(",")]:
         if k + 1 < len(calls):
             idle.append(calls[k + 1][0][0] - cl[-1][1])
     med = lambda v: sorted(v)[len(v) // 2] if v else None  # noqa: E731
-    out = {"N": N, "precision": a.precision, "calls": len(calls), "device_span_us": med(spans),
+    out = {"N": N, "config": a.config, "grad_at": a.at, "precision": a.precision, "calls": len(calls), "device_span_us": med(spans),
            "host_idle_between_calls_us": med(idle), "activities": []}
     for key in order:
         out["activities"].append({"name": key, "dur_us": med(dur[key]), "gap_before_us": med(gap[key])})
