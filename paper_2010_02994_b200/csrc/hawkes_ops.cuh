@@ -261,8 +261,25 @@ __device__ __forceinline__ double finp_slot_sum(const double* __restrict__ p, lo
   const int c0 = w * per, c1 = min(nslots, c0 + per);
   double acc = 0.0;
   if (live) {
-#pragma unroll 4
-    for (int c = c0; c < c1; ++c) acc += __ldcg(p + c * stride);   // L2: written by other CTAs
+    // loads in batches of 16 ahead of their adds (one L2 round trip per batch instead of one
+    // per 4 slots), the adds in slot order: the same sum, bit for bit
+    constexpr int B = 16;
+    int c = c0;
+    for (; c + B <= c1; c += B) {
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) v[u] = __ldcg(p + (c + u) * stride);   // L2: written by other CTAs
+#pragma unroll
+      for (int u = 0; u < B; ++u) acc += v[u];
+    }
+    if (c < c1) {
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) v[u] = c + u < c1 ? __ldcg(p + (c + u) * stride) : 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (c + u < c1) acc += v[u];
+    }
   }
   __shared__ double sh[FINP_SPLIT][32];
   sh[w][threadIdx.x & 31] = acc;
@@ -319,17 +336,20 @@ __device__ __forceinline__ void fin1p_block(int blk, int nblk, const double* __r
   __syncthreads();
   if (last) {   // CTA-uniform
     __threadfence();
+    // fixed order: thread k sums blocks k, k + 128, ...; a shuffle-down tree in each warp; the
+    // FINP_SPLIT warp sums in warp order (one barrier instead of a 7-level shared-memory tree)
     double s = 0.0;
     for (int b = threadIdx.x; b < nblk; b += FINP_THREADS) s += __ldcg(ell_part + b);
-    red[threadIdx.x] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
-    for (int w = FINP_THREADS / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-      __syncthreads();
-    }
     if (threadIdx.x == 0) {
-      st->ell = red[0];
-      if (!(red[0] > -INFINITY)) st->undefined = 1;
+      double tot = red[0];
+#pragma unroll
+      for (int w = 1; w < FINP_SPLIT; ++w) tot += red[w];
+      st->ell = tot;
+      if (!(tot > -INFINITY)) st->undefined = 1;
       *ticket = 0;
       __threadfence();
     }
