@@ -18,6 +18,17 @@ import numpy as np  # noqa: E402
 import oracle  # noqa: E402
 from tests.gpu_helpers import TOL, gpu_eval  # noqa: E402
 
+def oracle_subnormal_floor(th, D, N):
+    """Reading R23, oracle side: below this rate the oracle's unscaled exp factors (a term is
+    c * exp(.), c = c_b or c_s of P:L98-99) may be subnormal enough to cost ~1e-13 of lambda:
+    max(2^-1022, 1e13 N 2^-1074 max(c_b, c_s))."""
+    lc = max(math.log(th[0]) - 0.5 * (D + 1) * math.log(2 * math.pi) - D * math.log(th[1])
+             - math.log(th[2]) if th[0] > 0 else -math.inf,
+             math.log(th[3] * th[4]) - 0.5 * D * math.log(2 * math.pi) - D * math.log(th[5])
+             if th[3] > 0 else -math.inf)
+    return max(2.2250738585072014e-308, math.exp(min(700.0, lc + math.log(1e13 * N) - 1074 * math.log(2))))
+
+
 def make_case(rng, nmax):
     """One random case: (N, D, x, t, theta, precision, algorithm, emulated W)."""
     N = int(rng.integers(2, nmax))
@@ -103,11 +114,7 @@ if __name__ == "__main__":
             # case 514 (lambda_35 = 5.4e-299 from two terms whose exp factors are ~1e-318:
             # oracle lambda_35 off by 2.6e-10, the GPU's by 3e-15; profiles/r02_fuzz_case45_514_mp.txt)
             if prec == "fp64":
-                lc = max(math.log(th[0]) - 0.5 * (D + 1) * math.log(2 * math.pi) - D * math.log(th[1])
-                         - math.log(th[2]) if th[0] > 0 else -math.inf,
-                         math.log(th[3] * th[4]) - 0.5 * D * math.log(2 * math.pi) - D * math.log(th[5])
-                         if th[3] > 0 else -math.inf)
-                floor = max(2.2250738585072014e-308, math.exp(min(700.0, lc + math.log(1e13 * N) - 1074 * math.log(2))))
+                floor = oracle_subnormal_floor(th, D, N)
                 if float(np.min(lam_r)) < floor:
                     underflow += 1
                     print(json.dumps({**info, "r23_underflow": "oracle exp factors subnormal",
