@@ -476,6 +476,8 @@ PassConst make_pass_const(const hawkes_params& p, int D, double* lnw_b_out, doub
   pc.kt = -0.5 / (p.tau_t * p.tau_t);
   pc.ks = -0.5 / (p.sigma_x * p.sigma_x);
   pc.omega = p.omega;
+  pc.st = sqrt(-pc.kt);
+  pc.oms = -p.omega / pc.st;
   pc.lnc_b = p.mu0 > 0 ? lnw_b + 64.0 * LN2 : -INFINITY;
   pc.lnc_s = p.theta > 0 ? lnw_s + 64.0 * LN2 : -INFINITY;
   pc.lnc_sr = p.theta > 0 ? lnw_s : -INFINITY;

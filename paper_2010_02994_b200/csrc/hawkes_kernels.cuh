@@ -71,6 +71,8 @@ struct PassConst {
   double lnc_s;        // log(theta omega/((2pi)^{D/2} h^D) / h^2 * 2^64)
   double lnc_sr;       // lnc_s - 64 ln 2: the unordered-pair gradient pass folds -ln lambda_j
                        // into the self-excitation exponent (hawkes_kernels_sym.cuh)
+  double st;           // sqrt(-kt) = 1/(sqrt2 tau_t): rebased times u = st (t - T0) (rate pass)
+  double oms;          // -omega / st: -omega dt = oms du
 };
 
 // ---------------------------------------------------------------- table fp64 exp

@@ -41,6 +41,11 @@ constexpr bool SYM_FOLD = true;
 #else
 constexpr bool SYM_FOLD = false;
 #endif
+#ifdef HK_NO_REB1   // A/B: the rate pass without rebased times
+constexpr bool REB1 = false;
+#else
+constexpr bool REB1 = true;
+#endif
 constexpr int K1P = 2;                    // pass-1 partials of the unordered-pair kernels: M', X' 
 // a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
 // treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
@@ -106,6 +111,7 @@ struct SymRow {
   double x[D];
   double t;
   double rho;
+  double u;   // rate pass, REB: st (t - T0), T0 the current column tile's first time
   int g;
 };
 
@@ -113,7 +119,10 @@ struct SymRow {
 // GEN (spatial order, hawkes_plan.h): the column may be earlier or later than the row; the
 // self-excitation term is that of the later event, exponent k_s r^2 - omega |dt|, added to
 // the row's X (row later) or the column's (column later).
-template <int D, bool MASK, bool SELF, int TS, bool GEN = false>
+// REB (time walk, strict tile pairs passing the span test in sym_items): the column's time
+// arrives as u_j = st (t_j - T0) and the row's as u_i, so du = u_j - u_i = st dt and the
+// background exponent's k_t dt^2 = -du^2 needs no multiply (one FP64 instruction less per pair)
+template <int D, bool MASK, bool SELF, int TS, bool GEN = false, bool REB = false>
 __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           bool dead, double& rM, double& rX, double& cM, double& cX,
                                           const PassConst& c, const int2* __restrict__ tab) {
@@ -123,7 +132,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   double r2 = dx[0] * dx[0];
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
-  const double dt = ct - row.t;   // >= 0: the column is the later event
+  const double dt = REB ? ct - row.u : ct - row.t;   // >= 0: the column is the later event
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
   // the exp's k -> double on the conversion pipe (I2F.F64) in pass 1 as well: with the product
   // form's fewer FP64 instructions it pays at D = 2 (N = 100k 8.84 -> 8.81 ms, Alaska-shaped
@@ -141,9 +150,14 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   // instructions per unordered pair instead of 27 (100 + 51.5 other per 4-pair step), measured
   // 9.00 -> 8.85 ms at N = 100k (profiles/r02_ab_expfma.jsonl; -DHK_NO_EXPFMA: the old form)
   double Tb, Pb, Ts = 0.0, Ps = 0.0;
-  fexp_tp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
-  if (SELF)
-    fexp_tp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+  if (REB) {   // dt holds du = u_j - u_i here
+    fexp_tp<TS, I2F1>(fma(c.kx, r2, fma(-dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+    if (SELF) fexp_tp<TS, I2F1>(fma(c.ks, r2, fma(c.oms, dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+  } else {
+    fexp_tp<TS, I2F1>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+    if (SELF)
+      fexp_tp<TS, I2F1>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+  }
   if (MASK) {
     Tb = dead ? 0.0 : Tb;
     Ts = dead ? 0.0 : Ts;
@@ -275,7 +289,8 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 // 32 skewed steps of one warp: its lanes' R rows x its 32-column group.
-template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA, bool GEN, bool PIECE>
+template <int D, int PASS, bool MASK, int SYM_R, bool SELF, int TS, bool SOA, bool GEN, bool PIECE,
+          bool REB = false>
 __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
                                           const double* __restrict__ grp,
                                           const double* __restrict__ lgrp, int cg0, bool cvalid0,
@@ -356,7 +371,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       const bool dead = MASK && (!cv || row[r].g < 0 || cg == row[r].g ||
                                  (diag && cidx0 + src <= ridx0 + 32 * r));
       if (PASS == 1)
-        sym_pair1<D, MASK, SELF, TS, GEN>(row[r], cx, ct, dead, rM[r], rX[r], cacc[0], cacc[1], c, tab);
+        sym_pair1<D, MASK, SELF, TS, GEN, REB>(row[r], cx, ct, dead, rM[r], rX[r], cacc[0], cacc[1], c, tab);
       else
         sym_pair2<D, MASK, SELF, TS, GEN>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
     }
@@ -680,12 +695,28 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         }
         const bool self_live = fma(c.ks, r2min, self_bound - c.omega * dtmin) > CULL_EXPONENT;
         const bool bg_live = fma(c.kx, r2min, fma(c.kt * dtmin, dtmin, c.lnc_b)) > CULL_EXPONENT;
+        // REB (rate pass, time walk, strict tile pairs): times rebased to T0 = the column tile's
+        // first time and scaled by st, u = st (t - T0), where the tile's span keeps the rounding
+        // of u within the fp64 exponents' error class: omega span <= 256, |k_t| span^2 <= 64
+        // (rows precede T0 here, so |u_i| <= st dt and |u_j| <= st span)
+        bool reb = false;
+        if constexpr (PASS == 1 && !GEN && SOA && REB1) {
+          if (strict) {
+            const double span = st[(cnt - 1) * REC + D] - st[D];
+            reb = c.omega * span <= 256.0 && -c.kt * span * span <= 64.0;
+          }
+          if (reb) {
+#pragma unroll
+            for (int r = 0; r < SYM_R; ++r) row[r].u = c.st * (row[r].t - st[D]);
+          }
+        }
         if (SOA) {   // this lane's column record (+ cL) -> the warp's [pair][32] double2 buffer
           const double* rc = grp + lane * REC;
           double2* g2 = reinterpret_cast<double2*>(mysoa);
           double v[SOAW];
 #pragma unroll
           for (int q = 0; q < REC; ++q) v[q] = rc[q];
+          if (reb) v[D] = c.st * (v[D] - st[D]);
           if constexpr (FOLD) v[D + 2] = c.lnc_sr + lgrp[lane];
 #pragma unroll
           for (int q = (FOLD ? D + 3 : REC); q < SOAW; ++q) v[q] = 0.0;
@@ -701,14 +732,25 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
           sym_group<D, PASS, true, SYM_R, true, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid, row0 + lane,
                                                                      jt + warp * 32, diag_tile, w.s0, w.s1,
                                                                      rM, rX, rG, cacc, c, mytab);
-        else if (self_live)
-          sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid, row0 + lane,
-                                                                      jt + warp * 32, false, w.s0, w.s1, rM,
-                                                                      rX, rG, cacc, c, mytab);
-        else if (bg_live)
-          sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid,
-                                                                       row0 + lane, jt + warp * 32, false,
-                                                                       w.s0, w.s1, rM, rX, rG, cacc, c, mytab);
+        else if (self_live) {
+          if (reb)
+            sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN, PIECE, true>(row, grp, lgrp, cg, cvalid,
+                                                                              row0 + lane, jt + warp * 32, false,
+                                                                              w.s0, w.s1, rM, rX, rG, cacc, c, mytab);
+          else
+            sym_group<D, PASS, false, SYM_R, true, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid, row0 + lane,
+                                                                        jt + warp * 32, false, w.s0, w.s1, rM,
+                                                                        rX, rG, cacc, c, mytab);
+        } else if (bg_live) {
+          if (reb)
+            sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN, PIECE, true>(row, grp, lgrp, cg, cvalid,
+                                                                               row0 + lane, jt + warp * 32, false,
+                                                                               w.s0, w.s1, rM, rX, rG, cacc, c, mytab);
+          else
+            sym_group<D, PASS, false, SYM_R, false, TS, SOA, GEN, PIECE>(row, grp, lgrp, cg, cvalid,
+                                                                         row0 + lane, jt + warp * 32, false,
+                                                                         w.s0, w.s1, rM, rX, rG, cacc, c, mytab);
+        }
         // else: nothing survives; lane l still holds column l's sums (no rotation needed)
         if (cvalid) {
           if (PASS == 1) {
