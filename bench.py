@@ -40,7 +40,7 @@ METRIC = "loglik+location-gradient evals/s and pair-interactions/s at N=100k, 1-
 #           pass's (and, D <= 2, the rate pass's) 8 I2F.F64 per step run on the conversion pipe and are not counted.
 #   F_SURVEY SURVEY.md §8(d)'s frozen ordered-pair F_alg (libdevice exp, ordered pairs): context.
 F_ALG = (13.5, 15.5)
-F_PIPE = (11.5, 14.5)   # rate pass: product-form exps (each sum one fma) with I2F k, 23 per unordered pair
+F_PIPE = (11.0, 14.5)   # rate pass: product-form exps (each sum one fma), I2F k, rebased times: 22 per unordered pair
 # fp32 variant: FMA-pipe instructions per ordered pair of sym_kernel_f32's hot loop (packed
 # FFMA2 / FADD2 / FMUL2 = 1 per lane; SASS); its peak is one packed warp-instruction per 2
 # cycles per SMSP = 64 lanes/clk/SM.  MUFU: one ex2 per ordered pair per pass (two per unordered

@@ -46,6 +46,11 @@ constexpr bool REB1 = false;
 #else
 constexpr bool REB1 = true;
 #endif
+#ifdef HK_REB2      // A/B: the gradient pass with rebased times
+constexpr bool REB2 = true;
+#else
+constexpr bool REB2 = false;
+#endif
 constexpr int K1P = 2;                    // pass-1 partials of the unordered-pair kernels: M', X' 
 // a term whose exponent is below this adds nothing (fexp clamps at -707, and the finalize
 // treats sums below N e^-700 as zero): tile pairs whose bound is lower skip the term
@@ -195,7 +200,7 @@ __device__ __forceinline__ void sym_pair1(const SymRow<D>& row, const double (&c
   }
 }
 
-template <int D, bool MASK, bool SELF, int TS, bool GEN = false>
+template <int D, bool MASK, bool SELF, int TS, bool GEN = false, bool REB = false>
 __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&cx)[D], double ct,
                                           double crho, double cL, bool dead, double (&rG)[D],
                                           double (&cG)[D], const PassConst& c,
@@ -206,7 +211,7 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
   double r2 = dx[0] * dx[0];
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = fma(dx[d], dx[d], r2);
-  const double dt = ct - row.t;
+  const double dt = REB ? ct - row.u : ct - row.t;   // REB: du (sym_pair1)
   const int lane_off = TS > 1 ? (int)(threadIdx.x & (TS - 1)) * 8 : 0;
 #ifdef HK_PASS2_NO_I2F
   constexpr bool I2F = false;
@@ -254,12 +259,14 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
     return;
   }
 #endif
-  double eb = fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
+  double eb = REB ? fexp<TS, I2F>(fma(c.kx, r2, fma(-dt, dt, c.lnc_b)), tab, lane_off)
+                  : fexp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off);
 #ifdef HK_SYM_FOLD
   // rho'_j xi' = beta xi_ji / lambda_j: the column's cL = lnc_s - 64 ln 2 - ln lambda_j
   double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, dt, cL)), tab, lane_off) : 0.0;
 #else   // xi' alone, weighted by rho' of the later event below
-  double es = SELF ? fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off)
+  double es = SELF ? (REB ? fexp<TS, I2F>(fma(c.ks, r2, fma(c.oms, dt, c.lnc_s)), tab, lane_off)
+                          : fexp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off))
                    : 0.0;
 #endif
   if (MASK) {
@@ -373,7 +380,7 @@ __device__ __forceinline__ void sym_group(const SymRow<D> (&row)[SYM_R],
       if (PASS == 1)
         sym_pair1<D, MASK, SELF, TS, GEN, REB>(row[r], cx, ct, dead, rM[r], rX[r], cacc[0], cacc[1], c, tab);
       else
-        sym_pair2<D, MASK, SELF, TS, GEN>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
+        sym_pair2<D, MASK, SELF, TS, GEN, REB>(row[r], cx, ct, crho, cL, dead, rG[r], cG, c, tab);
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) cacc[2 + d] = cG[d];
@@ -700,7 +707,7 @@ __device__ __forceinline__ void sym_items(const SymArgs& a, const Sm& sm, int* s
         // of u within the fp64 exponents' error class: omega span <= 256, |k_t| span^2 <= 64
         // (rows precede T0 here, so |u_i| <= st dt and |u_j| <= st span)
         bool reb = false;
-        if constexpr (PASS == 1 && !GEN && SOA && REB1) {
+        if constexpr (!GEN && SOA && !FOLD && (PASS == 1 ? REB1 : REB2)) {
           if (strict) {
             const double span = st[(cnt - 1) * REC + D] - st[D];
             reb = c.omega * span <= 256.0 && -c.kt * span * span <= 64.0;
