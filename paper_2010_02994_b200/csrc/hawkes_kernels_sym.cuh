@@ -235,9 +235,14 @@ __device__ __forceinline__ void sym_pair2(const SymRow<D>& row, const double (&c
     }
 #else
     double Tb, Pb;
-    fexp_tp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
-    if (SELF)
-      fexp_tp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+    if (REB) {
+      fexp_tp<TS, I2F>(fma(c.kx, r2, fma(-dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+      if (SELF) fexp_tp<TS, I2F>(fma(c.ks, r2, fma(c.oms, dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+    } else {
+      fexp_tp<TS, I2F>(fma(c.kx, r2, fma(c.kt * dt, dt, c.lnc_b)), tab, lane_off, Tb, Pb);
+      if (SELF)
+        fexp_tp<TS, I2F>(fma(c.ks, r2, fma(-c.omega, GEN ? fabs(dt) : dt, c.lnc_s)), tab, lane_off, Ts, Ps);
+    }
     if (MASK) {
       Tb = dead ? 0.0 : Tb;
       Ts = dead ? 0.0 : Ts;
