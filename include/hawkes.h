@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define HAWKES_ABI_VERSION 3   /* 3: HMC transition, coarsening regions + MH sweep, get_locations */
+#define HAWKES_ABI_VERSION 4   /* 3: HMC transition, coarsening regions + MH sweep, get_locations; 4: hawkes_grad_at */
 
 typedef struct hawkes_ctx hawkes_ctx; /* opaque; owns all device memory */
 

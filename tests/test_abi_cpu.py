@@ -22,7 +22,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(lib, s)]
     assert not missing, missing
     assert set(declared) == set(_lib.EXPORTS)
-    assert lib.hawkes_abi_version() == 3
+    assert lib.hawkes_abi_version() == 4
 
 
 def test_library_is_sm100a():
