@@ -59,6 +59,21 @@ def test_grad_at_bitwise_equals_two_calls(name, N, kw):
         np.testing.assert_array_equal(at.get_rates()["lambda"], ref.get_rates()["lambda"])
 
 
+@pytest.mark.parametrize("D,N,ties", [(1, 1500, 0), (3, 2100, 0), (5, 900, 0), (2, 1700, 60)])
+def test_grad_at_other_dimensions_and_ties(D, N, ties):
+    """Every D's captured graph (its own packing / finalize node instantiations) and a tie
+    catalog (masked tile pairs): bitwise equal to the two calls."""
+    c = synth.with_ties(N, ties, D=D) if ties else synth.unit_square(N, config=1, D=D)
+    ref, at = _pair(c)
+    xs = _states(c, 4, seed=D)
+    with ref, at:
+        for k, x in enumerate(xs):
+            ref.set_locations(x)
+            g_ref, ell_ref = ref.grad_locations()
+            g_at, ell_at = at.grad_at(x)
+            assert ell_at == ell_ref and torch.equal(g_at, g_ref), f"D={D} call {k}"
+
+
 def test_grad_at_follows_buffer_contents_and_outputs():
     c = synth.config("C4", 3000)
     ref, at = _pair(c)
