@@ -522,6 +522,8 @@ int compute_constants(hawkes_ctx* ctx, const hawkes_params& p, double tN) {
     c32.omega = (float)(p.omega * L2E);
     c32.cb = (float)(l2b - E);
     c32.cs = (float)(l2s - E);
+    c32.st = (float)sqrt(-pc.kt * L2E);
+    c32.oms = (float)(-p.omega * L2E / sqrt(-pc.kt * L2E));
     if (!isfinite(c32.kx) || !isfinite(c32.kt) || !isfinite(c32.ks) || !isfinite(c32.omega) ||
         c32.kx == 0.f || c32.kt == 0.f || c32.ks == 0.f)
       return set_err(ctx, HAWKES_ERR_PARAM, "Theta outside the fp32 path's range");

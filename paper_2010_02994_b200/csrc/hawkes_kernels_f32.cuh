@@ -28,6 +28,7 @@ struct PassConst32 {
   float kx, kt, ks;   // -log2(e)/(2 tau_x^2), -log2(e)/(2 tau_t^2), -log2(e)/(2 h^2)
   float omega;        // omega log2(e)
   float cb, cs;       // log2(alpha w_b) - E, log2(beta w_s) - E
+  float st, oms;      // sqrt(-kt) and -omega / st: rebased times u = st (t - T0) (REB = 1)
 };
 
 __device__ __forceinline__ float ex2f(float a) {
@@ -316,11 +317,13 @@ __device__ __forceinline__ void sym32_pair2(const RowPair32<D>& rp, const float 
   float2 r2 = __fmul2_rn(dx[0], dx[0]);
 #pragma unroll
   for (int d = 1; d < D; ++d) r2 = __ffma2_rn(dx[d], dx[d], r2);
+  // REB = 1: dt holds du = st dt (the times arrive scaled), so k_t dt^2 = -du^2 needs no multiply
   const float2 dt = REB == 1 ? __fadd2_rn(f2(cth), rp.nrt)
                          : __fadd2_rn(__fadd2_rn(f2(cth), rp.nth), __fadd2_rn(f2(ctl), rp.ntl));
-  const float2 ab = __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
+  const float2 ab = REB == 1 ? __ffma2_rn(f2(c.kx), r2, __ffma2_rn(make_float2(-dt.x, -dt.y), dt, f2(c.cb)))
+                             : __ffma2_rn(f2(c.kx), r2, __ffma2_rn(__fmul2_rn(f2(c.kt), dt), dt, f2(c.cb)));
   const float2 adt = GEN ? make_float2(fabsf(dt.x), fabsf(dt.y)) : dt;
-  const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(-c.omega), adt, f2(c.cs)))
+  const float2 as = SELF ? __ffma2_rn(f2(c.ks), r2, __ffma2_rn(f2(REB == 1 ? c.oms : -c.omega), adt, f2(c.cs)))
                          : make_float2(0.f, 0.f);
   float2 eb = make_float2(ex2f(ab.x), ex2f(ab.y));
   float2 es = SELF ? make_float2(ex2f(as.x), ex2f(as.y)) : make_float2(0.f, 0.f);
@@ -704,7 +707,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
           const float T0h = st[L::TH], T0l = st[L::TL];
 #pragma unroll
           for (int h = 0; h < SR / 2; ++h)
-            rp[h].nrt = __fadd2_rn(__fadd2_rn(rp[h].nth, f2(T0h)), __fadd2_rn(rp[h].ntl, f2(T0l)));
+            rp[h].nrt = __fmul2_rn(f2(c.st), __fadd2_rn(__fadd2_rn(rp[h].nth, f2(T0h)), __fadd2_rn(rp[h].ntl, f2(T0l))));
         }
         // XREB (spatial walk: tiles are compact in space): the same for the locations, relative
         // to O = the column tile's first location, where the column tile's extent E around O
@@ -742,7 +745,7 @@ __global__ void __launch_bounds__(THREADS, D <= 2 ? 4 : (D <= 4 ? 3 : 2)) sym_ke
               v[4 * u + 2] = w4.z;
               v[4 * u + 3] = w4.w;
             }
-            if (treb) v[L::TH] = (v[L::TH] - st[L::TH]) + (v[L::TL] - st[L::TL]);
+            if (treb) v[L::TH] = c.st * ((v[L::TH] - st[L::TH]) + (v[L::TL] - st[L::TL]));
             if (xreb) {
 #pragma unroll
               for (int d = 0; d < D; ++d)
