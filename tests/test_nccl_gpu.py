@@ -97,3 +97,26 @@ def test_one_rank_nccl_hmc_and_mh_sweep(algorithm):
     assert np.allclose(res[0][1], res[1][1], rtol=1e-12, atol=1e-12)
     assert [a for a, _ in res[0][2]] == [a for a, _ in res[1][2]]
     assert np.allclose(res[0][3], res[1][3], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("algorithm", ["pairs", "rows"])
+def test_one_rank_nccl_grad_at(algorithm):
+    """hawkes_grad_at on the sharded path (no captured graph there: the two calls) equals
+    set_locations + grad_locations on the same kind of context, bit for bit."""
+    from paper_2010_02994_b200 import HawkesContext, nccl_unique_id
+    c = synth.config("C1", 1200)
+    ctxs = [HawkesContext(c.N, c.D, algorithm=algorithm, nccl_id=nccl_unique_id()) for _ in range(2)]
+    rng = np.random.default_rng(3)
+    try:
+        for ctx in ctxs:
+            ctx.set_times(c.t)
+            ctx.set_params(c.theta)
+        for k in range(4):
+            x = torch.from_numpy(c.x + 1e-3 * rng.normal(size=c.x.shape)).cuda()
+            ctxs[0].set_locations(x)
+            g0, e0 = ctxs[0].grad_locations()
+            g1, e1 = ctxs[1].grad_at(x)
+            assert e0 == e1 and torch.equal(g0, g1), f"call {k}"
+    finally:
+        for ctx in ctxs:
+            ctx.close()
